@@ -1,0 +1,367 @@
+"""CPU oracle for the ENSI ternary-PCMM hot path (arXiv 2509.09424).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package.  It shares no code with the CUDA path
+(paper_2509_09424_b200/); neither imports the other.
+
+The arithmetic lives in ``ensi_oracle.c`` (plain loops, ``%``-reduced 128-bit products); this module
+is ctypes marshalling plus the float64 encode/decode and big-integer CRT that the paper's client
+performs:
+
+* ``encode``  -- O5: slot u <-> evaluation at zeta^{5^u mod 2N'}, m = round_half_away(Delta * tau^{-1}(z)),
+  tau^{-1} evaluated with numpy's FFT (a library primitive used as one step).
+* ``decode``  -- O7: z_u = Re m(zeta^{5^u}) / Delta.
+* ``crt_centered`` -- O7: CRT over all l limbs with Python integers, centred lift.
+
+Parity status per function is listed in DESIGN.md section "Oracle pins"; key switching bit patterns
+(O10) are pinned by exact CRT identities and decryption, not by external vectors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_LIB = None
+
+u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+i8p = np.ctypeslib.ndpointer(dtype=np.int8, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = _build.build()
+        L = C.CDLL(path)
+        L.or_ctx_create.restype = C.c_void_p
+        L.or_ctx_create.argtypes = [C.c_uint32] * 4 + [C.c_void_p, C.c_void_p]
+        L.or_ctx_destroy.argtypes = [C.c_void_p]
+        L.or_ctx_moduli.argtypes = [C.c_void_p, u64p, u64p]
+        L.or_min_root.restype = C.c_uint64
+        L.or_min_root.argtypes = [C.c_uint64, C.c_uint32]
+        L.or_gen_params.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, u64p, u64p]
+        L.or_ntt.argtypes = [C.c_void_p, C.c_uint32, u64p]
+        L.or_intt.argtypes = [C.c_void_p, C.c_uint32, u64p]
+        L.or_rng_fill.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, i64p]
+        L.or_keygen.argtypes = [C.c_void_p, C.c_uint64, i8p, u64p, u64p]
+        L.or_rotkey.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, u64p, u64p, C.c_void_p]
+        L.or_encrypt.argtypes = [C.c_void_p, C.c_uint64, u64p, C.c_uint32, u64p, u64p]
+        L.or_encrypt_batch.argtypes = [C.c_void_p, u64p, C.c_uint32, u64p, C.c_uint32, u64p, u64p, C.c_uint32]
+        L.or_decrypt.argtypes = [C.c_void_p, u64p, C.c_uint32, u64p, u64p]
+        L.or_pcmm_a.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, i8p,
+                                C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]
+        L.or_automorph_ntt.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, u64p, u64p]
+        L.or_automorph_coeff.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p, u64p]
+        L.or_modup.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
+        L.or_moddown.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
+        L.or_rotate_hoisted.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, u64p, u64p, u64p, u64p]
+        L.or_rotate.argtypes = [C.c_void_p, C.c_uint32, C.c_uint64, u64p, u64p, u64p]
+        L.or_galois_elt.restype = C.c_uint64
+        L.or_galois_elt.argtypes = [C.c_uint32, C.c_int64]
+        L.or_pcmm_b.restype = C.c_int
+        L.or_pcmm_b.argtypes = [C.c_void_p] + [C.c_uint32] * 8 + [u64p, i8p, C.c_uint32, u64p, u64p, u64p]
+        L.or_rescale.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
+        _LIB = L
+    return _LIB
+
+
+def gen_params(log_n: int, L: int, alpha: int):
+    """O1 prime rule -> (q list, p list)."""
+    q = np.zeros(L, np.uint64)
+    p = np.zeros(max(alpha, 1), np.uint64)
+    lib().or_gen_params(log_n, L, alpha, q, p)
+    return [int(v) for v in q], [int(v) for v in p[:alpha]]
+
+
+def min_root(q: int, log_n: int) -> int:
+    """O2: minimal primitive 2N'-th root of unity mod q."""
+    return int(lib().or_min_root(q, log_n))
+
+
+def galois_elt(log_n: int, r: int) -> int:
+    """O9: g = 5^r mod 2N' (left rotation by r)."""
+    return int(lib().or_galois_elt(log_n, r))
+
+
+def rng_fill(seed: int, kind: str, n: int, q: int = 0) -> np.ndarray:
+    kinds = {"raw": 0, "uniform": 1, "ternary": 2, "cbd": 3}
+    out = np.zeros(n, np.int64)
+    lib().or_rng_fill(seed, kinds[kind], q, n, out)
+    return out
+
+
+# ---------------------------------------------------------------- encoding (O5) / decoding (O7)
+
+def _slot_exponents(n: int) -> np.ndarray:
+    """5^u mod 2N' for u in [0, N'/2)."""
+    two_n = 2 * n
+    e = np.empty(n // 2, np.int64)
+    v = 1
+    for u in range(n // 2):
+        e[u] = v
+        v = (v * 5) % two_n
+    return e
+
+
+def encode_coeffs(z, n: int, scale: float) -> list:
+    """O5: real slot vector z (len <= N'/2, zero padded) -> integer coefficients (Python ints).
+
+    m_j = (Delta/N') zeta^{-j} sum_t Z_{2t+1} e^{-2 pi i t j / N'} with Z at exponent 5^u = z_u and at
+    -5^u = conj(z_u); round half away from zero in float64.
+    """
+    z = np.asarray(z, dtype=np.float64)
+    slots = n // 2
+    if z.shape[0] > slots:
+        raise ValueError("more values than slots")
+    zz = np.zeros(slots, np.complex128)
+    zz[: z.shape[0]] = z
+    e = _slot_exponents(n)
+    Z = np.zeros(n, np.complex128)
+    Z[(e - 1) // 2] = zz
+    Z[((2 * n - e) - 1) // 2] = np.conj(zz)
+    j = np.arange(n)
+    m = np.fft.fft(Z) * np.exp(-1j * np.pi * j / n) / n
+    v = m.real * scale
+    r = np.sign(v) * np.floor(np.abs(v) + 0.5)
+    return [int(x) for x in r]
+
+
+def coeffs_to_residues(coeffs, moduli) -> np.ndarray:
+    """Python-int coefficients -> [len(moduli)][N'] uint64 residues."""
+    out = np.empty((len(moduli), len(coeffs)), np.uint64)
+    for i, q in enumerate(moduli):
+        out[i] = np.array([c % q for c in coeffs], dtype=np.uint64)
+    return out
+
+
+def crt_centered(res: np.ndarray, moduli) -> list:
+    """O7: residues [l][N'] -> centred integers in (-Q/2, Q/2] (Python ints)."""
+    moduli = [int(q) for q in moduli]
+    Q = 1
+    for q in moduli:
+        Q *= q
+    basis = []
+    for q in moduli:
+        qh = Q // q
+        basis.append(qh * pow(qh % q, -1, q))
+    n = res.shape[1]
+    cols = [[int(v) for v in res[i]] for i in range(len(moduli))]
+    out = []
+    half = Q // 2
+    for k in range(n):
+        x = 0
+        for i in range(len(moduli)):
+            x += cols[i][k] * basis[i]
+        x %= Q
+        if x > half:
+            x -= Q
+        out.append(x)
+    return out
+
+
+def decode_coeffs(coeffs, n: int, scale: float) -> np.ndarray:
+    """O7: z_u = Re sum_j m_j zeta^{5^u j} / Delta, evaluated as N' * ifft(m_j zeta^j) at t = (5^u-1)/2."""
+    m = np.array([float(c) for c in coeffs], dtype=np.float64)
+    j = np.arange(n)
+    vals = np.fft.ifft(m * np.exp(1j * np.pi * j / n)) * n
+    e = _slot_exponents(n)
+    return vals[(e - 1) // 2].real / scale
+
+
+# ---------------------------------------------------------------- context
+
+class Oracle:
+    """One CKKS parameter set (O1).  Limb order everywhere: q_0..q_{L-1}, p_0..p_{alpha-1}."""
+
+    def __init__(self, log_n: int, L: int, alpha: int, dnum: int, q=None, p=None):
+        self.log_n, self.n, self.L, self.alpha, self.dnum = log_n, 1 << log_n, L, alpha, dnum
+        qa = np.ascontiguousarray(q, np.uint64) if q is not None else None
+        pa = np.ascontiguousarray(p, np.uint64) if p is not None else None
+        self._keep = (qa, pa)
+        h = lib().or_ctx_create(log_n, L, alpha, dnum,
+                                qa.ctypes.data if qa is not None else None,
+                                pa.ctypes.data if pa is not None else None)
+        if not h:
+            raise ValueError("invalid oracle parameters")
+        self.h = C.c_void_p(h)
+        mods = np.zeros(L + alpha, np.uint64)
+        psis = np.zeros(L + alpha, np.uint64)
+        lib().or_ctx_moduli(self.h, mods, psis)
+        self.moduli = [int(v) for v in mods]
+        self.psi = [int(v) for v in psis]
+        self.q = self.moduli[:L]
+        self.p = self.moduli[L:]
+
+    def __del__(self):
+        try:
+            lib().or_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+    # -- NTT (O2)
+    def ntt(self, limb: int, a) -> np.ndarray:
+        a = np.array(a, dtype=np.uint64, copy=True)
+        lib().or_ntt(self.h, limb, a)
+        return a
+
+    def intt(self, limb: int, a) -> np.ndarray:
+        a = np.array(a, dtype=np.uint64, copy=True)
+        lib().or_intt(self.h, limb, a)
+        return a
+
+    # -- keys (O4)
+    def keygen(self, seed: int):
+        n, T = self.n, self.L + self.alpha
+        skc = np.zeros(n, np.int8)
+        sk = np.zeros((T, n), np.uint64)
+        pk = np.zeros((2, self.L, n), np.uint64)
+        lib().or_keygen(self.h, seed, skc, sk, pk)
+        return skc, sk, pk
+
+    def rotkey(self, seed: int, g: int, sk_ntt: np.ndarray, want_e: bool = False):
+        n, T = self.n, self.L + self.alpha
+        key = np.zeros((self.dnum, 2, T, n), np.uint64)
+        e = np.zeros((self.dnum, n), np.int64) if want_e else None
+        lib().or_rotkey(self.h, seed, g, np.ascontiguousarray(sk_ntt), key, e.ctypes.data if want_e else None)
+        return (key, e) if want_e else key
+
+    # -- encode / encrypt / decrypt (O5-O7)
+    def encode(self, z, level: int, scale: float) -> np.ndarray:
+        return coeffs_to_residues(encode_coeffs(z, self.n, scale), self.q[:level])
+
+    def encrypt(self, seed: int, pk: np.ndarray, level: int, m_res: np.ndarray) -> np.ndarray:
+        ct = np.zeros((2, level, self.n), np.uint64)
+        lib().or_encrypt(self.h, seed, np.ascontiguousarray(pk), level, np.ascontiguousarray(m_res, np.uint64), ct)
+        return ct
+
+    def encrypt_batch(self, seeds, pk, level: int, m_res: np.ndarray, nthreads: int = 0) -> np.ndarray:
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        cnt = seeds.shape[0]
+        ct = np.zeros((cnt, 2, level, self.n), np.uint64)
+        nth = nthreads or min(cnt, os.cpu_count() or 1)
+        lib().or_encrypt_batch(self.h, seeds, cnt, np.ascontiguousarray(pk), level,
+                               np.ascontiguousarray(m_res, np.uint64), ct, nth)
+        return ct
+
+    def decrypt_residues(self, sk_ntt, ct: np.ndarray) -> np.ndarray:
+        level = ct.shape[1]
+        mu = np.zeros((level, self.n), np.uint64)
+        lib().or_decrypt(self.h, np.ascontiguousarray(sk_ntt), level, np.ascontiguousarray(ct), mu)
+        return mu
+
+    def decrypt(self, sk_ntt, ct: np.ndarray, scale: float, limbs=None) -> np.ndarray:
+        mu = self.decrypt_residues(sk_ntt, ct)
+        level = ct.shape[1]
+        use = list(range(level)) if limbs is None else list(limbs)
+        coeffs = crt_centered(mu[use], [self.q[i] for i in use])
+        return decode_coeffs(coeffs, self.n, scale)
+
+    # -- PCMM Layout A (O8, Algorithm 1)
+    def pcmm_a(self, x: np.ndarray, W: np.ndarray, cols=None, nthreads: int = 1) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.uint64)
+        W = np.ascontiguousarray(W, np.int8)
+        d, m = W.shape
+        level = x.shape[2]
+        assert x.shape[0] == d and x.shape[1] == 2 and x.shape[3] == self.n
+        if cols is None:
+            y = np.zeros((m, 2, level, self.n), np.uint64)
+            lib().or_pcmm_a(self.h, level, d, m, m, x.ctypes.data, W, y.ctypes.data, None, 0, nthreads)
+        else:
+            ca = np.ascontiguousarray(cols, np.uint32)
+            y = np.zeros((ca.shape[0], 2, level, self.n), np.uint64)
+            lib().or_pcmm_a(self.h, level, d, m, m, x.ctypes.data, W, y.ctypes.data, ca.ctypes.data, ca.shape[0], nthreads)
+        return y
+
+    # -- automorphism / key switching / rotation (O9, O10)
+    def automorph_ntt(self, g: int, rows: np.ndarray) -> np.ndarray:
+        rows = np.ascontiguousarray(rows, np.uint64)
+        out = np.zeros_like(rows)
+        r = rows.reshape(-1, self.n)
+        lib().or_automorph_ntt(self.log_n, g, r.shape[0], r, out.reshape(-1, self.n))
+        return out
+
+    def automorph_coeff(self, limb: int, g: int, a) -> np.ndarray:
+        a = np.ascontiguousarray(a, np.uint64)
+        out = np.zeros_like(a)
+        lib().or_automorph_coeff(self.h, limb, g, a, out)
+        return out
+
+    def galois(self, r: int) -> int:
+        return galois_elt(self.log_n, r)
+
+    def modup(self, level: int, c: np.ndarray) -> np.ndarray:
+        beta = -(-level // self.alpha)
+        out = np.zeros((beta, level + self.alpha, self.n), np.uint64)
+        lib().or_modup(self.h, level, np.ascontiguousarray(c, np.uint64), out)
+        return out
+
+    def moddown(self, level: int, acc: np.ndarray) -> np.ndarray:
+        out = np.zeros((level, self.n), np.uint64)
+        lib().or_moddown(self.h, level, np.ascontiguousarray(acc, np.uint64), out)
+        return out
+
+    def rotate(self, ct: np.ndarray, g: int, key: np.ndarray) -> np.ndarray:
+        out = np.zeros_like(ct)
+        lib().or_rotate(self.h, ct.shape[1], g, np.ascontiguousarray(key), np.ascontiguousarray(ct), out)
+        return out
+
+    def rotate_hoisted(self, ct: np.ndarray, gs, keys: np.ndarray) -> np.ndarray:
+        ga = np.ascontiguousarray(gs, np.uint64)
+        out = np.zeros((ga.shape[0],) + ct.shape, np.uint64)
+        lib().or_rotate_hoisted(self.h, ct.shape[1], ga.shape[0], ga, np.ascontiguousarray(keys),
+                                np.ascontiguousarray(ct), out)
+        return out
+
+    # -- PCMM Layout B (O11)
+    def pcmm_b(self, x: np.ndarray, W: np.ndarray, s: int, k: int, B: int, gkeys, keys: np.ndarray) -> np.ndarray:
+        W = np.ascontiguousarray(W, np.int8)
+        d, m = W.shape
+        n_in, _, level, _ = x.shape
+        y = np.zeros((m, 2, level, self.n), np.uint64)
+        ga = np.ascontiguousarray(gkeys, np.uint64)
+        rc = lib().or_pcmm_b(self.h, level, s, k, B, d, m, m, n_in, np.ascontiguousarray(x, np.uint64), W,
+                             ga.shape[0], ga, np.ascontiguousarray(keys), y)
+        if rc != 0:
+            raise KeyError("missing rotation key")
+        return y
+
+    # -- rescale (O12)
+    def rescale(self, ct: np.ndarray) -> np.ndarray:
+        level = ct.shape[1]
+        out = np.zeros((2, level - 1, self.n), np.uint64)
+        lib().or_rescale(self.h, level, np.ascontiguousarray(ct, np.uint64), out)
+        return out
+
+
+def layout_b_plan(n: int, s: int, d: int, m: int, B: int = 0):
+    """O11 schedule: k = min((N'/2)/s, 2^ceil(log2 d)), n_in = ceil(d/k), B | k power of two,
+    default B = argmin (B-1) n_in + (k/B - 1) m.  Returns (k, n_in, B, G, rotations)."""
+    k = min((n // 2) // s, 1 << max(0, (d - 1).bit_length()))
+    n_in = -(-d // k)
+    if B == 0:
+        best = None
+        b = 1
+        while b <= k:
+            cost = (b - 1) * n_in + (k // b - 1) * m
+            if best is None or cost < best[0]:
+                best = (cost, b)
+            b *= 2
+        B = best[1]
+    G = k // B
+    return k, n_in, B, G, (B - 1) * n_in + (G - 1) * m
+
+
+def layout_b_galois(n: int, log_n: int, s: int, B: int, G: int):
+    """Galois elements Layout B needs: 5^{s b} (b in [1,B)) and 5^{s B gam} (gam in [1,G))."""
+    gs = [galois_elt(log_n, s * b) for b in range(1, B)]
+    gs += [galois_elt(log_n, s * B * g) for g in range(1, G)]
+    out = []
+    for g in gs:
+        if g not in out:
+            out.append(g)
+    return out

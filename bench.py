@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- ENSI ternary PCMM (Algorithm 1) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): N'=2^16, L=12 RNS limbs, one 768x768 BitNet ternary PCMM
+(Layout A, the paper's column packing): 768 input ciphertexts -> 768 output ciphertexts, 9.66 GB in,
+9.66 GB out.  A step = one full layer through ensi_pcmm_ternary_packed (inputs resident in HBM; inputs
+(9.66 GB) exceed the 126 MB L2, so no flush is needed between steps).
+
+Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints ONE JSON line.
+  value       = ms per layer (lower is better).  N > 1: weak scaling over token blocks -- every rank runs
+                the layer on its own token block (its own 768 input ciphertexts, same W), no data-path
+                collective; value = max-over-ranks step time / N (whole-job layers per ms, inverted).
+  e2e         = the same metric through ensi_pcmm_ternary_host: pinned host inputs -> device -> PCMM ->
+                pinned host outputs, every copy inside the timed region (pipelined over (poly, limb) slices).
+  roofline    = the accumulate kernel (the only kernel of a Layout-A step) against its bound.
+  cpu_baseline= the CPU oracle (oracle/ensi_oracle.c, as it stands) on a bounded sample of output columns,
+                extrapolated by nnz (the oracle's cost is exactly linear in nnz).
+  rotations   = hoisted key-switched rotations/s at the same parameters (alpha=4, dnum=3), BASELINE metric's
+                second clause.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "ternary PCMM latency (ms/layer) and rotations/sec per B200; HBM GB/s vs peak"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(parts[1]), smmax=float(parts[2]), power=float(parts[3]),
+                                 hw=parts[5], hwt=parts[6], swt=parts[7], pcap=parts[8]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        loaded = [r for r in rows if r["power"] > 0.3 * max(r2["power"] for r2 in rows)] or rows
+        reasons = set()
+        for r in loaded:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"), ("swt", "sw_thermal_slowdown"),
+                            ("pcap", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in loaded), "sm_max_mhz": max(r["smmax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------------ oracle arm
+
+def oracle_sample_ms(cfg, W, x_host, ncols: int, nthreads: int):
+    """Time the plain oracle (Alg. 1) on `ncols` output columns of the layer; extrapolate by nnz."""
+    import oracle
+    o = oracle.Oracle(cfg["log_n"], cfg["L"], cfg["alpha"], cfg["dnum"])
+    d, m = W.shape
+    cols = list(np.linspace(0, m - 1, ncols).astype(int))
+    t0 = time.perf_counter()
+    o.pcmm_a(x_host, W, cols=cols, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    nnz_s = int(np.count_nonzero(W[:, cols]))
+    nnz = int(np.count_nonzero(W))
+    return dt * 1e3 * nnz / max(1, nnz_s), dt, cols
+
+
+def run_reference(args, cfg_name):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    cfg = synth.CONFIGS[cfg_name]
+    d, m = cfg["shapes"][0]
+    n = 1 << cfg["log_n"]
+    import oracle
+    q, _ = oracle.gen_params(cfg["log_n"], cfg["L"], cfg["alpha"])
+    W = synth.gen_W(synth.SEED_BASE + 102, d, m)
+    x = synth.gen_words(synth.SEED_BASE + 2, q, d, cfg["L"], n)
+    nth = max(1, min(64, os.cpu_count() or 1))
+    ncols = max(1, min(m, nth))
+    times = []
+    for it in range(args.warmup + args.steps):
+        ms, dt, cols = oracle_sample_ms(cfg, W, x, ncols, nth)
+        if it >= args.warmup:
+            times.append(ms)
+    v = statistics.mean(times)
+    line = {"metric": METRIC, "value": v, "unit": "ms/layer", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform RNS words (data-oblivious accumulate)",
+            "impl": "reference",
+            "config": {"workload": f"{cfg_name}: {cfg['desc']}", "d": d, "m": m, "log_n": cfg["log_n"],
+                       "limbs": cfg["L"], "layout": "A"},
+            "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": nth, "kind": "oracle",
+                             "sample": f"{ncols} of {m} output columns per step (all 24 RNS slices), "
+                                       f"extrapolated by nnz(W)"},
+            "e2e": {"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------ our arm
+
+def time_loop(fn, steps: int, stream):
+    import torch
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(steps):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def bench_rotations(ctx_cls, cfg, steps: int, warmup: int, batch: int = 32):
+    """Hoisted key-switched rotations/s: one ciphertext, `batch` Galois elements per call (one ModUp)."""
+    import torch
+    n = 1 << cfg["log_n"]
+    ctx = ctx_cls(cfg["log_n"], cfg["L"], cfg["alpha"], cfg["dnum"])
+    T = cfg["L"] + cfg["alpha"]
+    gs = [pow(5, cfg["s"] * (b + 1), 2 * n) for b in range(batch)]
+    keys = torch.empty((batch, cfg["dnum"], 2, T, n), dtype=torch.int64, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    for r in range(T):
+        keys[:, :, :, r, :].random_(0, ctx.moduli[r], generator=g)
+    ctx.load_keys(galois=gs, rot_keys=keys)
+    x = synth.gen_words_torch(11, ctx.q, 1, cfg["L"], n)
+    y = torch.empty((batch, 2, cfg["L"], n), dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(warmup):
+        ctx.rotate_hoisted(x, gs, y, cfg["L"])
+    ms = time_loop(lambda: ctx.rotate_hoisted(x, gs, y, cfg["L"]), steps, st)
+    ctx.close()
+    return batch / (ms * 1e-3), ms
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--kernel", type=int, default=0, help="0 default, 1 CUDA-core, 2 tcgen05")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rot", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import torch
+    from paper_2509_09424_b200 import Context
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    cfg = synth.CONFIGS[args.config]
+    d, m = cfg["shapes"][0]
+    L, n = cfg["L"], 1 << cfg["log_n"]
+    ctx = Context(cfg["log_n"], L, cfg["alpha"], cfg["dnum"], device=local)
+    W = synth.gen_W(synth.SEED_BASE + 102, d, m)            # same model weights on every rank
+    w = ctx.weights(W)
+    # each rank: its own token block (its own input ciphertexts)
+    x = synth.gen_words_torch(synth.SEED_BASE + 2 + 1000 * rank, ctx.q, d, L, n)
+    y = torch.empty((m, 2, L, n), dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    step = lambda: ctx.pcmm_ternary(x, w, y, level=L, kernel=args.kernel)  # noqa: E731
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev_s, ev_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_s.record(st)
+    for _ in range(args.steps):
+        step()
+    ev_e.record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_rank = ev_s.elapsed_time(ev_e) / args.steps
+    launches = (ctx.launch_count() - l0)
+    clk = clocks.stop()
+    ms_step = max_over_ranks(world, ms_rank)
+    value = ms_step / world                                   # ms per layer over the whole job
+
+    ct_bytes = 2 * L * n * 8
+    alg_bytes = (d + m) * ct_bytes + d * 2 * (2 * ((m + 63) // 64)) * 4
+    term_words = w.nnz * 2 * L * n
+    peaks, peak_src = load_peaks()
+    kernel_name = "tcgen05" if (args.kernel == 2 or (args.kernel == 0 and False)) else "cuda-core"
+    gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
+    # ALU roofline of the CUDA-core accumulate: one 64-bit modular add per term-word = 2 ALU-pipe ops
+    # (IADD3 + IADD3.X); ALU pipe = 64 lanes/clk/SM (B300_MICROARCH: rt_SMSP = 2) x 148 SMs x max clock.
+    alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
+    alu_ach = 2 * term_words / (ms_rank * 1e-3) / 1e12
+    roofline = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s (INT32 ALU lane-ops)",
+                "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary",
+                "algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
+                "hbm_frac": gbs / peaks["hbm_gbs"], "peak_source": peak_src,
+                "ops_per_launch": 2 * term_words}
+
+    out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic uniform RNS words in [0,q_r) (the accumulate is data-oblivious); BitNet absmean W",
+           "config": {"workload": f"{args.config}: {cfg['desc']}", "d": d, "m": m, "log_n": cfg["log_n"],
+                      "limbs": L, "layout": "A", "kernel": kernel_name, "nnz": int(w.nnz),
+                      "l2": "inputs (9.66 GB) larger than L2 (126 MB); no flush",
+                      "parallelism": f"token-block data parallel x{world} (no data-path collective)"},
+           "gpu_launches": launches, "clocks": clk, "roofline": roofline}
+
+    # ---- e2e through the host-buffer entry point (pinned host in, pinned host out)
+    if not args.no_e2e:
+        xh_t = torch.empty((d, 2, L, n), dtype=torch.int64, pin_memory=True)
+        yh_t = torch.empty((m, 2, L, n), dtype=torch.int64, pin_memory=True)
+        xh_t.copy_(x)
+        xh, yh = xh_t.numpy(), yh_t.numpy()
+        e2e_step = lambda: ctx.pcmm_ternary_host(xh, w, yh, level=L, kernel=args.kernel)  # noqa: E731
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier(world)
+        e2e_ms = max_over_ranks(world, time_loop(e2e_step, max(1, min(args.steps, 3)), st))
+        ok = bool((yh_t[5, 1, 3, :4096] == y[5, 1, 3, :4096].cpu()).all())
+        out["e2e"] = {"value": e2e_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": d * ct_bytes,
+                      "d2h_bytes_per_step": m * ct_bytes, "matches_device_path": ok,
+                      "api": "ensi_pcmm_ternary_host"}
+    # ---- rotations/s (BASELINE metric's second clause), rank 0 only
+    if not args.no_rot and rank == 0:
+        rps, rms = bench_rotations(Context, cfg, max(2, args.steps), 2)
+        out["rotations_per_sec"] = {"value": rps, "unit": "rotations/s", "mode": "hoisted, 32 Galois elements per "
+                                    "ModUp, N'=2^16, L=12, alpha=4, dnum=3", "ms_per_call": rms}
+    # ---- CPU oracle baseline (rank 0 at N=1 only)
+    if not args.no_cpu and rank == 0 and world == 1:
+        x_host = (xh_t.numpy().view(np.uint64) if not args.no_e2e else x.cpu().numpy().view(np.uint64))
+        nth = max(1, min(64, os.cpu_count() or 1))
+        ncols = max(1, min(m, nth))
+        ms_cpu, dt, cols = oracle_sample_ms(cfg, W, x_host, ncols, nth)
+        out["cpu_baseline"] = {"value": ms_cpu, "unit": "ms/layer", "cores": nth, "kind": "oracle",
+                               "sample": f"{ncols} of {m} output columns ({dt:.1f} s wall), extrapolated by nnz"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

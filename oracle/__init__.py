@@ -132,8 +132,13 @@ def encode_coeffs(z, n: int, scale: float) -> list:
 
 
 def coeffs_to_residues(coeffs, moduli) -> np.ndarray:
-    """Python-int coefficients -> [len(moduli)][N'] uint64 residues."""
+    """Python-int coefficients -> [len(moduli)][N'] uint64 residues (c mod q, canonical)."""
     out = np.empty((len(moduli), len(coeffs)), np.uint64)
+    if all(-(1 << 62) < c < (1 << 62) for c in coeffs):
+        a = np.array(coeffs, dtype=np.int64)
+        for i, q in enumerate(moduli):
+            out[i] = np.mod(a, np.int64(q)).astype(np.uint64)
+        return out
     for i, q in enumerate(moduli):
         out[i] = np.array([c % q for c in coeffs], dtype=np.uint64)
     return out

@@ -34,8 +34,9 @@ typedef unsigned __int128 u128;
 
 /* ------------------------------------------------------------------ modular arithmetic */
 static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a * b) % q); }
-static uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a + b) % q); }
-static uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((u128)a + q - (b % q)) % q); }
+/* a, b canonical in [0, q): the sum/difference reduced by one conditional correction (q < 2^62). */
+static uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { uint64_t s = a + b; return s >= q ? s - q : s; }
+static uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
 static uint64_t powmod(uint64_t a, uint64_t e, uint64_t q) {
     uint64_t r = 1 % q; a %= q;
     while (e) { if (e & 1) r = mulmod(r, a, q); a = mulmod(a, a, q); e >>= 1; }

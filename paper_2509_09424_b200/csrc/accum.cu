@@ -1,0 +1,139 @@
+// accum.cu -- row a3, the ternary accumulate of Algorithm 1 on the CUDA-core integer pipes.
+//
+// y_i[w] = sum_{j : W[j][i] != 0} W[j][i] x_j[w]  mod q(w),  for every word w of the 2*l*N' words of a ciphertext.
+// This is a d -> m integer contraction over M = 2 l N' word positions.  Tiling:
+//   CTA = 8 warps = 64 outputs x 256 word positions (one limb, so q is CTA-uniform).
+//   warp w owns outputs i0 + 8w .. +8; lane owns positions lane + 32p, p < 8   ->  64 int64 accumulators.
+//   x_j tiles (8 rows of 256 words) are staged in shared memory with cp.async, double buffered, and read by
+//   all 8 warps (each x word is fetched from L2/HBM once per 64 outputs).
+//   The weight sign is warp-uniform: one branch per (j, output) covers 8 words per lane, and zeros are
+//   skipped exactly as Alg. 1 lines 4-8 skip W = 0.
+// Accumulation is signed, lazy 64-bit: |acc| <= d 2^50 < 2^63 for d <= 8184 terms; longer sums are reduced
+// every 8184 rows.  The epilogue maps acc to the canonical word in [0, q) (Barrett), so the output is the
+// unique canonical value and equals the oracle bit for bit.
+#include "ensi_internal.h"
+
+namespace ensi {
+
+static constexpr int AO = 8;          // outputs per warp
+static constexpr int AP = 8;          // positions per lane
+static constexpr int AW = 8;          // warps per CTA
+static constexpr int ATI = AO * AW;   // 64 outputs per CTA
+static constexpr int ATW = 32 * AP;   // 256 positions per CTA
+static constexpr int AKC = 8;         // x rows per pipeline stage
+static constexpr int ARED = 8184;     // rows between intermediate reductions (multiple of AKC)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// planes: [d][2][mw] uint32 (pos bits, neg bits); bit (i % 32) of word i / 32; mw even, zero padded.
+__global__ void __launch_bounds__(256, 1)
+    k_accum_ternary(const uint64_t* __restrict__ x, uint32_t d, uint64_t ctw, const uint32_t* __restrict__ planes,
+                    uint32_t mw, uint32_t m, uint64_t* __restrict__ y, uint32_t log_n, uint32_t level, uint32_t limb0,
+                    ModTab tab) {
+    __shared__ __align__(16) uint64_t sx[2][AKC][ATW];
+    __shared__ uint32_t ssg[2][AKC][4];   // pos lo, pos hi, neg lo, neg hi (64 outputs)
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t i0 = blockIdx.x * ATI;
+    const uint64_t pos0 = (uint64_t)blockIdx.y * ATW;
+    const uint32_t limb = (uint32_t)((limb0 + (pos0 >> log_n)) % level);
+    const Barrett br = tab.br(limb);
+    const uint32_t wsel = warp >> 2, wsh = (warp & 3) * 8;
+    const uint32_t pw0 = i0 >> 5;   // first plane word of this output tile (even)
+
+    int64_t acc[AO][AP];
+#pragma unroll
+    for (int o = 0; o < AO; o++)
+#pragma unroll
+        for (int p = 0; p < AP; p++) acc[o][p] = 0;
+
+    const uint32_t nstages = (d + AKC - 1) / AKC;
+    auto load_stage = [&](uint32_t s, int buf) {
+        const uint32_t j0 = s * AKC;
+        // x: AKC rows x 256 words = 2048 words = 1024 16-byte chunks; 4 per thread
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            uint32_t chunk = tid + c * 256;
+            uint32_t r = chunk >> 7, col = (chunk & 127) * 2;
+            uint32_t j = j0 + r;
+            if (j < d) cp_async16(&sx[buf][r][col], x + (uint64_t)j * ctw + pos0 + col);
+        }
+        if (tid < AKC * 4) {
+            uint32_t r = tid >> 2, which = tid & 3, j = j0 + r;
+            if (j < d) {
+                const uint32_t* src = planes + ((uint64_t)j * 2 + (which >> 1)) * mw + pw0 + (which & 1);
+                cp_async4(&ssg[buf][r][which], src);
+            } else {
+                ssg[buf][r][which] = 0;
+            }
+        }
+    };
+
+    load_stage(0, 0);
+    cp_commit();
+    for (uint32_t s = 0; s < nstages; s++) {
+        const int buf = s & 1;
+        if (s + 1 < nstages) load_stage(s + 1, buf ^ 1);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+#pragma unroll 1
+        for (int r = 0; r < AKC; r++) {
+            const uint32_t pb = (ssg[buf][r][wsel] >> wsh) & 0xFFu;
+            const uint32_t nb = (ssg[buf][r][2 + wsel] >> wsh) & 0xFFu;
+            if ((pb | nb) == 0) continue;
+            int64_t xv[AP];
+#pragma unroll
+            for (int p = 0; p < AP; p++) xv[p] = (int64_t)sx[buf][r][lane + 32 * p];
+#pragma unroll
+            for (int o = 0; o < AO; o++) {
+                if (pb & (1u << o)) {
+#pragma unroll
+                    for (int p = 0; p < AP; p++) acc[o][p] += xv[p];
+                } else if (nb & (1u << o)) {
+#pragma unroll
+                    for (int p = 0; p < AP; p++) acc[o][p] -= xv[p];
+                }
+            }
+        }
+        if ((((s + 1) * AKC) % ARED) == 0 && s + 1 < nstages) {
+#pragma unroll
+            for (int o = 0; o < AO; o++)
+#pragma unroll
+                for (int p = 0; p < AP; p++) acc[o][p] = (int64_t)reduce_signed(acc[o][p], br);
+        }
+        __syncthreads();
+    }
+    // epilogue: canonical words, coalesced stores (32 consecutive positions per warp store)
+#pragma unroll
+    for (int o = 0; o < AO; o++) {
+        const uint32_t i = i0 + warp * AO + o;
+        if (i < m) {
+            uint64_t* yo = y + (uint64_t)i * ctw + pos0;
+#pragma unroll
+            for (int p = 0; p < AP; p++) yo[lane + 32 * p] = reduce_signed(acc[o][p], br);
+        }
+    }
+}
+
+int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
+                  uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw, uint32_t limb0) {
+    if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
+    if (ctw % ATW) return set_err(ctx, ENSI_EINVAL, "ring too small for the accumulate tile");
+    dim3 grid((m + ATI - 1) / ATI, (uint32_t)(ctw / ATW));
+    k_accum_ternary<<<grid, 256, 0, st>>>(x, d, ctw, planes, mw, m, y, ctx->log_n, level, limb0, ctx->tab);
+    ENSI_LAUNCH_CHECK(ctx);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_ternary");
+}
+
+}  // namespace ensi

@@ -1,0 +1,672 @@
+// api.cu -- the C ABI of libensi.so (include/ensi.h).  Argument validation, key/weight management,
+// Layout-A/B orchestration.  Every arithmetic step runs in the kernels of ntt.cu, accum.cu, accum_tc.cu,
+// keyswitch.cu and poly.cu; the host does CRT/decode only inside ensi_decrypt_debug (debug, never timed).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ensi_internal.h"
+
+using namespace ensi;
+
+namespace ensi {
+
+int set_err(ensi_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+int cuda_err(ensi_ctx* ctx, cudaError_t e, const char* where) {
+    return set_err(ctx, ENSI_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int ensure_scratch(ensi_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->scratch_bytes) return ENSI_OK;
+    if (ctx->scratch) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&ctx->scratch, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(ctx, ENSI_ENOMEM, "scratch allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+    ctx->scratch_bytes = bytes;
+    return ENSI_OK;
+}
+
+}  // namespace ensi
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int check_view(ensi_ctx* ctx, const ensi_ct_view* v, const char* name) {
+    if (!v || !v->data) return set_err(ctx, ENSI_EINVAL, std::string(name) + ": NULL view or data");
+    if (v->level < 1 || v->level > ctx->L)
+        return set_err(ctx, ENSI_ELEVEL, std::string(name) + ": level " + std::to_string(v->level) +
+                                             " outside [1, num_q=" + std::to_string(ctx->L) + "]");
+    return ENSI_OK;
+}
+
+bool overlaps(const ensi_ct_view* a, const ensi_ct_view* b, uint32_t n) {
+    const uint8_t* a0 = (const uint8_t*)a->data;
+    const uint8_t* a1 = a0 + (size_t)a->count * 2 * a->level * n * 8;
+    const uint8_t* b0 = (const uint8_t*)b->data;
+    const uint8_t* b1 = b0 + (size_t)b->count * 2 * b->level * n * 8;
+    return a0 < b1 && b0 < a1;
+}
+
+// pack a d x m ternary matrix (row stride ldw) into [rows][2][mw] planes
+int pack_planes(ensi_ctx* ctx, const int8_t* W, uint32_t d, uint32_t m, uint32_t ldw, uint32_t mw,
+                std::vector<uint32_t>& out, uint64_t* nnz) {
+    out.assign((size_t)d * 2 * mw, 0u);
+    uint64_t cnt = 0;
+    for (uint32_t j = 0; j < d; j++) {
+        const int8_t* row = W + (size_t)j * ldw;
+        uint32_t* pos = out.data() + (size_t)j * 2 * mw;
+        uint32_t* neg = pos + mw;
+        for (uint32_t i = 0; i < m; i++) {
+            int8_t v = row[i];
+            if (v == 1) {
+                pos[i >> 5] |= 1u << (i & 31);
+                cnt++;
+            } else if (v == -1) {
+                neg[i >> 5] |= 1u << (i & 31);
+                cnt++;
+            } else if (v != 0) {
+                return set_err(ctx, ENSI_ENOTTERNARY, "W[" + std::to_string(j) + "][" + std::to_string(i) +
+                                                          "] = " + std::to_string((int)v) + " is not in {-1,0,1}");
+            }
+        }
+    }
+    if (nnz) *nnz = cnt;
+    return ENSI_OK;
+}
+
+struct LayoutBPlan {
+    uint32_t k, n_in, B, G, rotations;
+};
+
+int plan_b(ensi_ctx* ctx, uint32_t d, uint32_t m, uint32_t s, uint32_t baby, LayoutBPlan* p) {
+    const uint32_t slots = ctx->n / 2;
+    if (s == 0 || (s & (s - 1)) || s > slots)
+        return set_err(ctx, ENSI_EDIM, "block_s must be a power of two <= N'/2");
+    uint32_t pow2d = 1;
+    while (pow2d < d) pow2d <<= 1;
+    p->k = std::min(slots / s, pow2d);
+    p->n_in = (d + p->k - 1) / p->k;
+    if (baby == 0) {
+        uint64_t best = UINT64_MAX;
+        for (uint32_t b = 1; b <= p->k; b <<= 1) {
+            uint64_t cost = (uint64_t)(b - 1) * p->n_in + (uint64_t)(p->k / b - 1) * m;
+            if (cost < best) {
+                best = cost;
+                p->B = b;
+            }
+        }
+    } else {
+        if ((baby & (baby - 1)) || baby > p->k || p->k % baby)
+            return set_err(ctx, ENSI_EDIM, "baby must be a power of two dividing k");
+        p->B = baby;
+    }
+    p->G = p->k / p->B;
+    p->rotations = (p->B - 1) * p->n_in + (p->G - 1) * m;
+    return ENSI_OK;
+}
+
+// Layout-B weight pack for (k, B): for giant step gam, rows r = c*B + b hold W[c*k + gam*B + b] (0 if >= d).
+int weights_b(ensi_ctx* ctx, ensi_weights* w, uint32_t k, uint32_t B, uint32_t n_in, uint32_t** out) {
+    auto key = std::make_pair(k, B);
+    auto it = w->packs_b.find(key);
+    if (it != w->packs_b.end()) {
+        *out = it->second;
+        return ENSI_OK;
+    }
+    const uint32_t G = k / B, rows = n_in * B;
+    std::vector<int8_t> Wg((size_t)rows * w->m);
+    std::vector<uint32_t> all;
+    all.reserve((size_t)G * rows * 2 * w->mw);
+    for (uint32_t gam = 0; gam < G; gam++) {
+        std::fill(Wg.begin(), Wg.end(), 0);
+        for (uint32_t c = 0; c < n_in; c++)
+            for (uint32_t b = 0; b < B; b++) {
+                uint32_t col = c * k + gam * B + b;
+                if (col < w->d) std::memcpy(&Wg[((size_t)c * B + b) * w->m], &w->host[(size_t)col * w->m], w->m);
+            }
+        std::vector<uint32_t> pl;
+        int rc = pack_planes(ctx, Wg.data(), rows, w->m, w->m, w->mw, pl, nullptr);
+        if (rc) return rc;
+        all.insert(all.end(), pl.begin(), pl.end());
+    }
+    uint32_t* dptr = nullptr;
+    cudaError_t e = cudaMalloc(&dptr, all.size() * 4);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "weights_b malloc");
+    e = cudaMemcpy(dptr, all.data(), all.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "weights_b copy");
+    w->packs_b[key] = dptr;
+    *out = dptr;
+    return ENSI_OK;
+}
+
+// iterative radix-2 complex FFT (host, debug decode only): a[k] = sum_j a_j e^{sign 2 pi i jk / n}
+void fft_host(std::vector<std::complex<double>>& a, int sign) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; i++) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        double ang = sign * 2 * M_PI / (double)len;
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; k++) {
+                std::complex<double> w(std::cos(ang * k), std::sin(ang * k));
+                std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t ensi_abi_version(void) { return ENSI_ABI_VERSION; }
+
+const char* ensi_last_error(const ensi_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+uint64_t ensi_launch_count(const ensi_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
+    if (!out) return ENSI_EINVAL;
+    *out = nullptr;
+    if (!prm) return ENSI_EINVAL;
+    if (prm->log_n < 8 || prm->log_n > 17) return ENSI_EINVAL;
+    if (prm->num_q < 1 || prm->num_q + prm->num_p > ENSI_MAXT) return ENSI_EINVAL;
+    if (prm->num_p > 0) {
+        if (prm->dnum < 1 || prm->num_p != (prm->num_q + prm->dnum - 1) / prm->dnum) return ENSI_EINVAL;
+    }
+    ensi_ctx* ctx = new (std::nothrow) ensi_ctx();
+    if (!ctx) return ENSI_ENOMEM;
+    ctx->device = cuda_device;
+    ctx->log_n = prm->log_n;
+    ctx->n = 1u << prm->log_n;
+    ctx->L = prm->num_q;
+    ctx->A = prm->num_p;
+    ctx->dnum = prm->num_p ? prm->dnum : 0;
+    ctx->T = prm->num_q + prm->num_p;
+    ctx->log2_scale = prm->log2_scale > 0 ? prm->log2_scale : 40.0;
+    uint64_t qq[ENSI_MAXT], pp[ENSI_MAXT];
+    if (!prm->q || (prm->num_p && !prm->p)) gen_primes(prm->log_n, prm->num_q, prm->num_p, qq, pp);
+    for (uint32_t i = 0; i < ctx->L; i++) ctx->mod[i] = prm->q ? prm->q[i] : qq[i];
+    for (uint32_t k = 0; k < ctx->A; k++) ctx->mod[ctx->L + k] = prm->p ? prm->p[k] : pp[k];
+    const uint64_t two_n = 2ull * ctx->n;
+    for (uint32_t i = 0; i < ctx->T; i++) {
+        uint64_t q = ctx->mod[i];
+        bool ok = q > 2 && q < (1ull << 60) && (q % two_n) == 1 && is_prime_u64(q);
+        for (uint32_t j = 0; j < i && ok; j++) ok = ctx->mod[j] != q;
+        if (!ok) {
+            int rc = set_err(ctx, ENSI_EINVAL, "modulus " + std::to_string(q) + " rejected");
+            delete ctx;
+            return rc;
+        }
+    }
+    DeviceGuard g(cuda_device);
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return ENSI_ECUDA;
+    }
+    // twiddle tables
+    const uint32_t n = ctx->n;
+    std::vector<uint64_t> tw((size_t)ctx->T * 4 * n + 2 * ctx->T);
+    for (uint32_t i = 0; i < ctx->T; i++) {
+        const uint64_t q = ctx->mod[i];
+        ctx->psi[i] = min_root(q, ctx->log_n);
+        const uint64_t ipsi = invmod_h(ctx->psi[i], q);
+        uint64_t* base = tw.data() + (size_t)i * 4 * n;
+        // psi^k and psi^-k in natural order, then scatter by bit reversal
+        uint64_t p = 1, ip = 1;
+        for (uint32_t k = 0; k < n; k++) {
+            uint32_t r = 0;
+            for (uint32_t b = 0, kk = k; b < ctx->log_n; b++, kk >>= 1) r = (r << 1) | (kk & 1);
+            base[r] = p;
+            base[n + r] = shoup_h(p, q);
+            base[2 * n + r] = ip;
+            base[3 * n + r] = shoup_h(ip, q);
+            p = mulmod_h(p, ctx->psi[i], q);
+            ip = mulmod_h(ip, ipsi, q);
+        }
+        ctx->ninv[i] = invmod_h(n % q, q);
+        ctx->ninv_sh[i] = shoup_h(ctx->ninv[i], q);
+        tw[(size_t)ctx->T * 4 * n + 2 * i] = ctx->ninv[i];
+        tw[(size_t)ctx->T * 4 * n + 2 * i + 1] = ctx->ninv_sh[i];
+        Barrett b = barrett_h(q);
+        ctx->tab.q[i] = q;
+        ctx->tab.mu[i] = b.mu;
+        ctx->tab.w[i] = b.w;
+    }
+    e = cudaMalloc(&ctx->d_tw, tw.size() * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        ensi_ctx_destroy(ctx);
+        return ENSI_ECUDA;
+    }
+    *out = ctx;
+    return ENSI_OK;
+}
+
+void ensi_ctx_destroy(ensi_ctx* ctx) {
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->d_tw);
+    cudaFree(ctx->d_sk);
+    if (ctx->keys_owned) cudaFree(ctx->d_keys);
+    for (auto& c : ctx->conv) {
+        cudaFree(c.d_modup);
+        cudaFree(c.d_moddown);
+    }
+    cudaFree(ctx->scratch);
+    cudaFree(ctx->host_stage);
+    if (ctx->st_h2d) {
+        cudaStreamDestroy(ctx->st_h2d);
+        cudaStreamDestroy(ctx->st_d2h);
+        for (int b = 0; b < 2; b++) {
+            cudaEventDestroy(ctx->ev_h2d[b]);
+            cudaEventDestroy(ctx->ev_comp[b]);
+            cudaEventDestroy(ctx->ev_d2h[b]);
+        }
+        cudaEventDestroy(ctx->ev_start);
+    }
+    delete ctx;
+}
+
+int ensi_ctx_moduli(const ensi_ctx* ctx, uint64_t* moduli_out, uint64_t* psi_out) {
+    if (!ctx) return ENSI_EINVAL;
+    for (uint32_t i = 0; i < ctx->T; i++) {
+        if (moduli_out) moduli_out[i] = ctx->mod[i];
+        if (psi_out) psi_out[i] = ctx->psi[i];
+    }
+    return ENSI_OK;
+}
+
+int ensi_load_keys(ensi_ctx* ctx, const ensi_keys* keys) {
+    if (!ctx || !keys) return ENSI_EINVAL;
+    DeviceGuard g(ctx->device);
+    const size_t n = ctx->n;
+    cudaDeviceSynchronize();
+    if (keys->sk_ntt) {
+        for (size_t i = 0; i < (size_t)ctx->T * n; i++)
+            if (keys->sk_ntt[i] >= ctx->mod[i / n]) return set_err(ctx, ENSI_EINVAL, "sk word not canonical");
+        if (!ctx->d_sk) {
+            cudaError_t e = cudaMalloc(&ctx->d_sk, (size_t)ctx->T * n * 8);
+            if (e != cudaSuccess) return cuda_err(ctx, e, "sk malloc");
+        }
+        cudaError_t e = cudaMemcpy(ctx->d_sk, keys->sk_ntt, (size_t)ctx->T * n * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "sk copy");
+    }
+    if (keys->n_rot > 0) {
+        if (!keys->galois || !keys->rot_keys) return set_err(ctx, ENSI_EINVAL, "NULL galois or rot_keys");
+        if (ctx->A == 0) return set_err(ctx, ENSI_EINVAL, "rotation keys need num_p > 0");
+        for (uint32_t r = 0; r < keys->n_rot; r++)
+            if ((keys->galois[r] & 1) == 0 || keys->galois[r] >= 2ull * n)
+                return set_err(ctx, ENSI_EINVAL, "galois element must be odd and < 2N'");
+        if (ctx->keys_owned) cudaFree(ctx->d_keys);
+        ctx->d_keys = nullptr;
+        ctx->keys_owned = false;
+        const size_t bytes = (size_t)keys->n_rot * ctx->dnum * 2 * ctx->T * n * 8;
+        if (keys->rot_keys_mem == ENSI_MEM_DEVICE) {
+            ctx->d_keys = const_cast<uint64_t*>(keys->rot_keys);
+        } else {
+            cudaError_t e = cudaMalloc(&ctx->d_keys, bytes);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return set_err(ctx, ENSI_ENOMEM, "rotation key allocation failed");
+            }
+            ctx->keys_owned = true;
+            e = cudaMemcpy(ctx->d_keys, keys->rot_keys, bytes, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_err(ctx, e, "rotation key copy");
+        }
+        ctx->galois.assign(keys->galois, keys->galois + keys->n_rot);
+    }
+    return ENSI_OK;
+}
+
+int ensi_weights_pack(ensi_ctx* ctx, const int8_t* W, uint32_t d, uint32_t m, uint32_t ldw, ensi_weights** out) {
+    if (!ctx || !W || !out) return ctx ? set_err(ctx, ENSI_EINVAL, "NULL argument") : ENSI_EINVAL;
+    *out = nullptr;
+    if (d == 0 || m == 0) return set_err(ctx, ENSI_EDIM, "d and m must be positive");
+    if (ldw < m) return set_err(ctx, ENSI_EDIM, "ldw < m");
+    DeviceGuard g(ctx->device);
+    ensi_weights* w = new (std::nothrow) ensi_weights();
+    if (!w) return ENSI_ENOMEM;
+    w->ctx = ctx;
+    w->d = d;
+    w->m = m;
+    w->mw = 2 * ((m + 63) / 64);
+    std::vector<uint32_t> pl;
+    int rc = pack_planes(ctx, W, d, m, ldw, w->mw, pl, &w->nnz);
+    if (rc) {
+        delete w;
+        return rc;
+    }
+    w->host.resize((size_t)d * m);
+    for (uint32_t j = 0; j < d; j++) std::memcpy(&w->host[(size_t)j * m], W + (size_t)j * ldw, m);
+    cudaError_t e = cudaMalloc(&w->d_planes, pl.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_planes, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        ensi_weights_destroy(w);
+        return cuda_err(ctx, e, "weights upload");
+    }
+    *out = w;
+    return ENSI_OK;
+}
+
+void ensi_weights_destroy(ensi_weights* w) {
+    if (!w) return;
+    DeviceGuard g(w->ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(w->d_planes);
+    for (auto& kv : w->packs_b) cudaFree(kv.second);
+    cudaFree(w->d_wt8);
+    delete w;
+}
+
+int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_weights* wc, ensi_ct_view* y,
+                             const ensi_pcmm_opts* opts, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!wc) return set_err(ctx, ENSI_EINVAL, "NULL weights");
+    ensi_weights* w = const_cast<ensi_weights*>(wc);
+    if (w->ctx != ctx) return set_err(ctx, ENSI_EINVAL, "weights belong to another context");
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    ensi_pcmm_opts o{};
+    if (opts) o = *opts;
+    const uint32_t d = w->d, m = w->m, level = x->level, n = ctx->n;
+    const uint32_t out_level = o.rescale_out ? level - 1 : level;
+    if (o.rescale_out && level < 2) return set_err(ctx, ENSI_ELEVEL, "rescale_out needs level >= 2");
+    if (y->level != out_level) return set_err(ctx, ENSI_ELEVEL, "y.level must be x.level (-1 with rescale_out)");
+    if (y->count != m) return set_err(ctx, ENSI_EDIM, "y.count != m");
+    if (overlaps(x, y, n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
+    if (o.layout > 1) return set_err(ctx, ENSI_EINVAL, "layout must be 0 (A) or 1 (B)");
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceGuard g(ctx->device);
+    const size_t ctw = (size_t)2 * level * n;
+    // output of the accumulate goes to y directly unless a rescale epilogue follows
+    uint64_t* acc_out = y->data;
+    uint64_t* owned = nullptr;
+    if (o.rescale_out) {
+        cudaError_t e = cudaMallocAsync((void**)&owned, (size_t)m * ctw * 8, st);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "pcmm temp");
+        acc_out = owned;
+    }
+    if (o.layout == 0) {
+        if (x->count != d) return set_err(ctx, ENSI_EDIM, "Layout A: x.count must equal d");
+        bool tc = (o.kernel == 2) || (o.kernel == 0 && tc_supported(ctx, level));
+        if (o.kernel == 2 && !tc_supported(ctx, level))
+            return set_err(ctx, ENSI_EINVAL, "tensor-core accumulate not available for these parameters");
+        rc = tc ? accum_ternary_tc(ctx, x->data, d, w, acc_out, level, st)
+                : accum_ternary(ctx, x->data, d, w->d_planes, w->mw, m, acc_out, level, st);
+    } else {
+        LayoutBPlan p;
+        rc = plan_b(ctx, d, m, o.block_s, o.baby, &p);
+        if (rc) return rc;
+        if (x->count != p.n_in) return set_err(ctx, ENSI_EDIM, "Layout B: x.count must be ceil(d/k)");
+        for (uint32_t b = 1; b < p.B; b++)
+            if (!find_key(ctx, galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b)))
+                return set_err(ctx, ENSI_ENOKEY, "missing baby-step key for rotation " + std::to_string(o.block_s * b));
+        for (uint32_t gm = 1; gm < p.G; gm++)
+            if (!find_key(ctx, galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm)))
+                return set_err(ctx, ENSI_ENOKEY, "missing giant-step key");
+        uint32_t* planes = nullptr;
+        rc = weights_b(ctx, w, p.k, p.B, p.n_in, &planes);
+        if (rc) return rc;
+        const uint32_t rows = p.n_in * p.B;
+        uint64_t *R = nullptr, *Tg = nullptr, *Tr = nullptr;
+        cudaError_t e = cudaMallocAsync((void**)&R, (size_t)rows * ctw * 8, st);
+        if (e == cudaSuccess && p.G > 1) e = cudaMallocAsync((void**)&Tg, (size_t)m * ctw * 8, st);
+        if (e == cudaSuccess && p.G > 1) e = cudaMallocAsync((void**)&Tr, ctw * 8, st);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "layout B scratch");
+        std::vector<uint64_t> gb(p.B);
+        for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
+        for (uint32_t c = 0; c < p.n_in && !rc; c++)
+            rc = rotate_hoisted(ctx, x->data + c * ctw, level, p.B, gb.data(), R + (size_t)c * p.B * ctw, st);
+        const size_t plane_words = (size_t)rows * 2 * w->mw;
+        if (!rc) rc = accum_ternary(ctx, R, rows, planes, w->mw, m, acc_out, level, st);
+        for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
+            rc = accum_ternary(ctx, R, rows, planes + gm * plane_words, w->mw, m, Tg, level, st);
+            uint64_t gg = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm);
+            for (uint32_t i = 0; i < m && !rc; i++) {
+                rc = rotate_hoisted(ctx, Tg + (size_t)i * ctw, level, 1, &gg, Tr, st);
+                if (!rc) add_into(ctx, acc_out + (size_t)i * ctw, Tr, 1, level, st);
+            }
+        }
+        cudaFreeAsync(R, st);
+        if (Tg) cudaFreeAsync(Tg, st);
+        if (Tr) cudaFreeAsync(Tr, st);
+    }
+    if (!rc && o.rescale_out) {
+        rc = ensi::rescale(ctx, acc_out, m, level, y->data, st);
+        if (!rc) y->log2_scale = x->log2_scale - std::log2((double)ctx->mod[level - 1]);
+    } else if (!rc) {
+        y->log2_scale = x->log2_scale;
+    }
+    if (owned) cudaFreeAsync(owned, st);
+    if (!rc) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_err(ctx, e, "pcmm");
+    }
+    return rc;
+}
+
+int ensi_pcmm_ternary(ensi_ctx* ctx, const ensi_ct_view* x, const int8_t* W, uint32_t d, uint32_t m, uint32_t ldw,
+                      ensi_ct_view* y, const ensi_pcmm_opts* opts, void* stream) {
+    ensi_weights* w = nullptr;
+    int rc = ensi_weights_pack(ctx, W, d, m, ldw, &w);
+    if (rc) return rc;
+    rc = ensi_pcmm_ternary_packed(ctx, x, w, y, opts, stream);
+    if (!rc) {
+        cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+        if (e != cudaSuccess) rc = cuda_err(ctx, e, "pcmm sync");
+    }
+    ensi_weights_destroy(w);
+    return rc;
+}
+
+int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level, double log2_scale,
+                           const ensi_weights* wc, uint64_t* y_host, uint32_t kernel, void* stream) {
+    (void)log2_scale;
+    if (!ctx) return ENSI_EINVAL;
+    if (!x_host || !y_host || !wc) return set_err(ctx, ENSI_EINVAL, "NULL argument");
+    ensi_weights* w = const_cast<ensi_weights*>(wc);
+    if (w->ctx != ctx) return set_err(ctx, ENSI_EINVAL, "weights belong to another context");
+    if (level < 1 || level > ctx->L) return set_err(ctx, ENSI_ELEVEL, "level out of range");
+    DeviceGuard g(ctx->device);
+    const uint32_t d = w->d, m = w->m, n = ctx->n, slices = 2 * level;
+    const size_t ctb = (size_t)2 * level * n * 8, rowb = (size_t)n * 8;
+    const size_t stage_words = (size_t)(d + m) * n;          // one slice of every input and output
+    if (!ctx->host_stage || ctx->host_stage_words < 2 * stage_words) {
+        if (ctx->host_stage) {
+            cudaDeviceSynchronize();
+            cudaFree(ctx->host_stage);
+        }
+        ctx->host_stage = nullptr;
+        cudaError_t e = cudaMalloc(&ctx->host_stage, 2 * stage_words * 8);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ctx->host_stage_words = 0;
+            return set_err(ctx, ENSI_ENOMEM, "staging allocation failed");
+        }
+        ctx->host_stage_words = 2 * stage_words;
+    }
+    if (!ctx->st_h2d) {
+        cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&ctx->st_d2h, cudaStreamNonBlocking);
+        for (int b = 0; b < 2; b++) {
+            cudaEventCreateWithFlags(&ctx->ev_h2d[b], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ctx->ev_comp[b], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ctx->ev_d2h[b], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool tc = (kernel == 2) || (kernel == 0 && tc_supported(ctx, level));
+    // start: the copy streams wait for everything already queued on the caller's stream
+    cudaEventRecord(ctx->ev_start, st);
+    cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_start, 0);
+    cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_start, 0);
+    int rc = ENSI_OK;
+    for (uint32_t s = 0; s < slices && !rc; s++) {
+        const int b = s & 1;
+        uint64_t* xs = ctx->host_stage + (size_t)b * stage_words;
+        uint64_t* ys = xs + (size_t)d * n;
+        const uint32_t poly = s / level, limb = s % level;
+        const size_t off = ((size_t)poly * level + limb) * n;   // word offset of this slice inside a ct
+        if (s >= 2) cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_comp[b], 0);   // x stage b free again
+        cudaMemcpy2DAsync(xs, rowb, x_host + off, ctb, rowb, d, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaEventRecord(ctx->ev_h2d[b], ctx->st_h2d);
+        cudaStreamWaitEvent(st, ctx->ev_h2d[b], 0);
+        if (s >= 2) cudaStreamWaitEvent(st, ctx->ev_d2h[b], 0);             // y stage b drained
+        rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb)
+                : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
+        cudaEventRecord(ctx->ev_comp[b], st);
+        cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[b], 0);
+        cudaMemcpy2DAsync(y_host + off, ctb, ys, rowb, rowb, m, cudaMemcpyDeviceToHost, ctx->st_d2h);
+        cudaEventRecord(ctx->ev_d2h[b], ctx->st_d2h);
+    }
+    // the caller's stream completes only after the last device->host copy
+    cudaStreamWaitEvent(st, ctx->ev_d2h[(slices - 1) & 1], 0);
+    if (slices >= 2) cudaStreamWaitEvent(st, ctx->ev_d2h[(slices - 2) & 1], 0);
+    if (!rc) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = cuda_err(ctx, e, "pcmm_host");
+    }
+    return rc;
+}
+
+int ensi_ntt(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const uint32_t* limb_of_row, uint32_t period, int inverse,
+             void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!data || !limb_of_row) return set_err(ctx, ENSI_EINVAL, "NULL argument");
+    if (period == 0 || period > 2 * ENSI_MAXT) return set_err(ctx, ENSI_EINVAL, "period out of range");
+    if (rows > 65535) return set_err(ctx, ENSI_EDIM, "at most 65535 rows per call");
+    LimbMap mp = identity_map(1);
+    mp.period = period;
+    for (uint32_t i = 0; i < period; i++) {
+        if (limb_of_row[i] >= ctx->T) return set_err(ctx, ENSI_EINVAL, "limb index out of range");
+        mp.limb[i] = (uint8_t)limb_of_row[i];
+    }
+    DeviceGuard g(ctx->device);
+    if (inverse) ntt_inverse(ctx, data, rows, mp, (cudaStream_t)stream);
+    else ntt_forward(ctx, data, rows, mp, (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "ntt");
+}
+
+int ensi_rotate_hoisted(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, const uint64_t* galois, ensi_ct_view* y,
+                        void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (!galois && n_g) return set_err(ctx, ENSI_EINVAL, "NULL galois");
+    if (y->count < n_g) return set_err(ctx, ENSI_EDIM, "y.count < n_g");
+    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level != x.level");
+    if (overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
+    DeviceGuard g(ctx->device);
+    rc = rotate_hoisted(ctx, x->data, x->level, n_g, galois, y->data, (cudaStream_t)stream);
+    if (!rc) y->log2_scale = x->log2_scale;
+    return rc;
+}
+
+int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (x->level < 2) return set_err(ctx, ENSI_ELEVEL, "rescale needs level >= 2");
+    if (y->level != x->level - 1 || y->count != x->count) return set_err(ctx, ENSI_EDIM, "y must be count x (level-1)");
+    if (overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
+    DeviceGuard g(ctx->device);
+    rc = ensi::rescale(ctx, x->data, x->count, x->level, y->data, (cudaStream_t)stream);
+    if (!rc) y->log2_scale = x->log2_scale - std::log2((double)ctx->mod[x->level - 1]);
+    return rc;
+}
+
+int ensi_decrypt_debug(ensi_ctx* ctx, const ensi_ct_view* ct, uint32_t index, uint64_t* coeffs_out, double* slots_out) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, ct, "ct");
+    if (rc) return rc;
+    if (index >= ct->count) return set_err(ctx, ENSI_EDIM, "index >= count");
+    if (!ctx->d_sk) return set_err(ctx, ENSI_ENOKEY, "no secret key loaded");
+    DeviceGuard g(ctx->device);
+    const uint32_t n = ctx->n, level = ct->level;
+    uint64_t* mu = nullptr;
+    cudaError_t e = cudaMalloc(&mu, (size_t)level * n * 8);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "decrypt malloc");
+    rc = decrypt_mu(ctx, ct->data + (size_t)index * 2 * level * n, level, mu, 0);
+    std::vector<uint64_t> h((size_t)level * n);
+    if (!rc) {
+        e = cudaMemcpy(h.data(), mu, h.size() * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = cuda_err(ctx, e, "decrypt copy");
+    }
+    cudaFree(mu);
+    if (rc) return rc;
+    if (coeffs_out) std::memcpy(coeffs_out, h.data(), h.size() * 8);
+    if (slots_out) {
+        // CRT over limbs {0,1} (or limb 0 alone), centred, then decode z_u = Re sum_j m_j zeta^{5^u j} / Delta
+        std::vector<std::complex<double>> a(n);
+        const uint64_t q0 = ctx->mod[0];
+        const double scale = std::exp2(ct->log2_scale);
+        typedef unsigned __int128 u128;
+        for (uint32_t j = 0; j < n; j++) {
+            double v;
+            if (level >= 2) {
+                const uint64_t q1 = ctx->mod[1];
+                uint64_t r0 = h[j], r1 = h[n + j];
+                uint64_t t = mulmod_h((r1 + q1 - r0 % q1) % q1, invmod_h(q0 % q1, q1), q1);
+                u128 x = (u128)t * q0 + r0, Q = (u128)q0 * q1;
+                v = (x > Q / 2) ? -(double)(Q - x) : (double)x;
+            } else {
+                uint64_t r0 = h[j];
+                v = (r0 > q0 / 2) ? -(double)(q0 - r0) : (double)r0;
+            }
+            double ang = M_PI * (double)j / (double)n;   // m_j zeta^j
+            a[j] = std::complex<double>(v * std::cos(ang), v * std::sin(ang));
+        }
+        fft_host(a, +1);   // sum_j (m_j zeta^j) e^{2 pi i j t / n}
+        uint64_t e5 = 1;
+        const uint64_t two_n = 2ull * n;
+        for (uint32_t u = 0; u < n / 2; u++) {
+            slots_out[u] = a[(e5 - 1) / 2].real() / scale;
+            e5 = (e5 * 5) % two_n;
+        }
+    }
+    return ENSI_OK;
+}
+
+}  // extern "C"

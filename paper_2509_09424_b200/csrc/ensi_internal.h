@@ -1,0 +1,158 @@
+// ensi_internal.h -- context and launch helpers shared by the CUDA translation units of libensi.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ensi.h"
+#include "modarith.cuh"
+
+#define ENSI_MAXT 64
+
+namespace ensi {
+
+// Per-limb modulus data passed by value to kernels (lives in the kernel-parameter constant bank).
+struct ModTab {
+    uint64_t q[ENSI_MAXT];
+    uint64_t mu[ENSI_MAXT];
+    uint32_t w[ENSI_MAXT];
+    __host__ __device__ Barrett br(uint32_t i) const { return Barrett{q[i], mu[i], w[i]}; }
+};
+
+// Row -> limb map for batched polynomial kernels: logical row r uses limb[r % period] and lives at physical
+// row (r / grp_rows) * grp_stride + grp_off + r % grp_rows (identity when grp_rows is huge).
+struct LimbMap {
+    uint32_t period;
+    uint32_t grp_rows, grp_stride, grp_off;
+    uint8_t limb[ENSI_MAXT * 2];
+    __host__ __device__ uint64_t phys(uint32_t r) const {
+        return (uint64_t)(r / grp_rows) * grp_stride + grp_off + (r % grp_rows);
+    }
+};
+
+// ModUp / ModDown basis-conversion constants for one level, resident on the device.
+struct ConvTables {
+    uint32_t level, beta;
+    // modup: per digit t, per source i in D_t: (Q_t/q_i)^{-1} mod q_i (+shoup)  -> [beta][alpha][2]
+    // per digit t, per ext limb e, per source a: [Q_t/q_i]_{r_e} (+shoup)      -> [beta][E][alpha][2]
+    uint64_t* d_modup = nullptr;
+    // moddown: per p_k: (P/p_k)^{-1} mod p_k (+shoup) [alpha][2]; per q_i per k: [P/p_k]_{q_i} (+shoup)
+    // [level][alpha][2]; per q_i: P^{-1} mod q_i (+shoup) [level][2]
+    uint64_t* d_moddown = nullptr;
+};
+
+}  // namespace ensi
+
+struct ensi_weights {
+    ensi_ctx* ctx = nullptr;
+    uint32_t d = 0, m = 0, mw = 0;        // mw = 32-bit words per sign-plane row (multiple of 2)
+    std::vector<int8_t> host;             // dense d x m copy (row-major, ldw = m) for Layout-B re-packing
+    uint32_t* d_planes = nullptr;         // [d][2][mw]: pos bits then neg bits (bit i%32 of word i/32)
+    uint64_t nnz = 0;
+    // Layout B packs keyed by (k, B): [G][n_in*B][2][mw]
+    std::map<std::pair<uint32_t, uint32_t>, uint32_t*> packs_b;
+    // byte-sliced tensor-core operand (W^T as int8 [m_pad][d_pad], K-major), built lazily
+    int8_t* d_wt8 = nullptr;
+    uint32_t wt_mpad = 0, wt_dpad = 0;
+};
+
+struct ensi_ctx {
+    int device = 0;
+    uint32_t log_n = 0, n = 0, L = 0, A = 0, dnum = 0, T = 0;
+    double log2_scale = 40.0;
+    uint64_t mod[ENSI_MAXT] = {};
+    uint64_t psi[ENSI_MAXT] = {};
+    ensi::ModTab tab{};
+    // twiddles: [T][4][n] = psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup
+    uint64_t* d_tw = nullptr;
+    uint64_t ninv[ENSI_MAXT] = {}, ninv_sh[ENSI_MAXT] = {};
+    // keys
+    uint64_t* d_sk = nullptr;             // [T][n]
+    std::vector<uint64_t> galois;
+    uint64_t* d_keys = nullptr;
+    bool keys_owned = false;
+    // conversion tables per level (1..L)
+    std::vector<ensi::ConvTables> conv;
+    // scratch (grown on demand)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // host-staged pipeline (ensi_pcmm_ternary_host)
+    uint64_t* host_stage = nullptr;
+    size_t host_stage_words = 0;
+    cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {}, ev_start = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+};
+
+namespace ensi {
+
+// error helpers (api.cu)
+int set_err(ensi_ctx* ctx, int code, const std::string& msg);
+int cuda_err(ensi_ctx* ctx, cudaError_t e, const char* where);
+
+// host math (host_math.cpp)
+bool is_prime_u64(uint64_t n);
+uint64_t powmod_h(uint64_t a, uint64_t e, uint64_t q);
+uint64_t mulmod_h(uint64_t a, uint64_t b, uint64_t q);
+uint64_t invmod_h(uint64_t a, uint64_t q);
+uint64_t shoup_h(uint64_t w, uint64_t q);
+Barrett barrett_h(uint64_t q);
+void gen_primes(uint32_t log_n, uint32_t L, uint32_t alpha, uint64_t* q, uint64_t* p);
+uint64_t min_root(uint64_t q, uint32_t log_n);
+uint64_t galois_of_rotation(uint32_t log_n, int64_t r);
+
+// scratch
+int ensure_scratch(ensi_ctx* ctx, size_t bytes);
+
+// NTT (ntt.cu): in-place on rows [rows][n], row r modulus = map.limb[r % map.period]
+void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);
+void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);
+
+// accumulate (accum.cu)
+// x: d "ciphertexts" of ctw words each (default ctw = 2*level*N'); word w of a ct lives in limb
+// (limb0 + w / N') % level.  A staged chunk holding one limb r of every ct passes ctw = N', limb0 = r.
+int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
+                  uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
+int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
+                     cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
+bool tc_supported(const ensi_ctx* ctx, uint32_t level);
+
+// key switching (keyswitch.cu)
+int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out);
+int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
+                   uint64_t* out, cudaStream_t st);
+const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g);
+
+// poly (poly.cu)
+int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st);
+int decrypt_mu(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint64_t* mu, cudaStream_t st);
+void add_into(ensi_ctx* ctx, uint64_t* y, const uint64_t* x, uint32_t count, uint32_t level, cudaStream_t st);
+
+inline LimbMap identity_map(uint32_t level) {
+    LimbMap m{};
+    m.period = level;
+    m.grp_rows = 1u << 30;
+    m.grp_stride = 0;
+    m.grp_off = 0;
+    for (uint32_t i = 0; i < level; i++) m.limb[i] = (uint8_t)i;
+    return m;
+}
+// limbs of an extended (Q_l u P) polynomial: e < level -> q_e, else p_{e-level}
+inline uint32_t ext_limb(const ensi_ctx* ctx, uint32_t level, uint32_t e) { return e < level ? e : ctx->L + (e - level); }
+inline LimbMap ext_map(const ensi_ctx* ctx, uint32_t level) {
+    LimbMap m = identity_map(level + ctx->A);
+    for (uint32_t e = 0; e < level + ctx->A; e++) m.limb[e] = (uint8_t)ext_limb(ctx, level, e);
+    return m;
+}
+
+}  // namespace ensi
+
+#define ENSI_LAUNCH_CHECK(ctx)                                             \
+    do {                                                                   \
+        (ctx)->launches++;                                                 \
+    } while (0)

@@ -1,0 +1,292 @@
+// keyswitch.cu -- Galois automorphism + hybrid key switching + hoisted rotations (rows a6, a7, a8).
+//
+// DESIGN.md R9/R10 (= SURVEY.md 8(c) O9/O10; the paper defines Rot only as a slot shift, PAPER.md:134-138,
+// and names evk in KeyGen):
+//   ModUp per digit t (D_t = Q-limbs [t alpha, (t+1) alpha) cap [0,l)): INTT, y_i = [c_i (Q_t/q_i)^-1]_{q_i},
+//   ext_r = sum_i y_i [Q_t/q_i]_r mod r (no overflow correction), NTT.  Rot(ct; g): sigma_g applied to the
+//   ModUp'ed digits (ModUp first, then sigma_g), key inner product over the digits, ModDown
+//   (INTT of the P limbs, fast conversion to Q_l, NTT, (acc - z) P^-1), plus sigma_g(c0).
+// Hoisting: one ModUp per input ciphertext serves every Galois element of a batch.  The automorphism is
+// fused into the key-inner-product load (a gather through the NTT-domain index permutation).
+#include <algorithm>
+
+#include "ensi_internal.h"
+
+namespace ensi {
+
+static constexpr uint32_t kT = 256;
+static constexpr uint32_t kMaxBatch = 32;
+
+struct GBatch {
+    uint64_t g[kMaxBatch];
+    uint32_t key[kMaxBatch];   // index of the Galois key in ctx->galois / d_keys
+    uint32_t oidx[kMaxBatch];  // output ciphertext slot
+};
+
+// ---------------------------------------------------------------- conversion tables
+
+int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
+    if (ctx->conv.size() < ctx->L + 1) ctx->conv.resize(ctx->L + 1);
+    ConvTables& ct = ctx->conv[level];
+    if (ct.d_modup) {
+        *out = &ct;
+        return ENSI_OK;
+    }
+    const uint32_t A = ctx->A, L = ctx->L, E = level + A;
+    const uint32_t beta = (level + A - 1) / A;
+    std::vector<uint64_t> mu((size_t)beta * A * 2 + (size_t)beta * E * A * 2, 0);
+    size_t off1 = (size_t)beta * A * 2;
+    for (uint32_t t = 0; t < beta; t++) {
+        uint32_t lo = t * A, hi = std::min((t + 1) * A, level);
+        for (uint32_t a = 0; a < hi - lo; a++) {
+            uint32_t i = lo + a;
+            uint64_t q = ctx->mod[i], qh = 1;
+            for (uint32_t b = lo; b < hi; b++)
+                if (b != i) qh = mulmod_h(qh, ctx->mod[b] % q, q);
+            uint64_t inv = invmod_h(qh, q);
+            mu[(t * A + a) * 2] = inv;
+            mu[(t * A + a) * 2 + 1] = shoup_h(inv, q);
+        }
+        for (uint32_t e = 0; e < E; e++) {
+            uint64_t r = ctx->mod[ext_limb(ctx, level, e)];
+            for (uint32_t a = 0; a < hi - lo; a++) {
+                uint64_t v = 1;
+                for (uint32_t b = lo; b < hi; b++)
+                    if (b != lo + a) v = mulmod_h(v, ctx->mod[b] % r, r);
+                size_t idx = off1 + (((size_t)t * E + e) * A + a) * 2;
+                mu[idx] = v;
+                mu[idx + 1] = shoup_h(v, r);
+            }
+        }
+    }
+    // moddown: phinv [A][2], ph [level][A][2], Pinv [level][2]
+    std::vector<uint64_t> md((size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2, 0);
+    for (uint32_t k = 0; k < A; k++) {
+        uint64_t p = ctx->mod[L + k], ph = 1;
+        for (uint32_t b = 0; b < A; b++)
+            if (b != k) ph = mulmod_h(ph, ctx->mod[L + b] % p, p);
+        uint64_t inv = invmod_h(ph, p);
+        md[k * 2] = inv;
+        md[k * 2 + 1] = shoup_h(inv, p);
+    }
+    for (uint32_t i = 0; i < level; i++) {
+        uint64_t q = ctx->mod[i], P = 1;
+        for (uint32_t k = 0; k < A; k++) {
+            uint64_t v = 1;
+            for (uint32_t b = 0; b < A; b++)
+                if (b != k) v = mulmod_h(v, ctx->mod[L + b] % q, q);
+            size_t idx = (size_t)A * 2 + ((size_t)i * A + k) * 2;
+            md[idx] = v;
+            md[idx + 1] = shoup_h(v, q);
+            P = mulmod_h(P, ctx->mod[L + k] % q, q);
+        }
+        uint64_t pinv = invmod_h(P, q);
+        size_t idx = (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
+        md[idx] = pinv;
+        md[idx + 1] = shoup_h(pinv, q);
+    }
+    cudaError_t e1 = cudaMalloc(&ct.d_modup, mu.size() * 8);
+    if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables malloc");
+    e1 = cudaMalloc(&ct.d_moddown, md.size() * 8);
+    if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables malloc");
+    cudaMemcpy(ct.d_modup, mu.data(), mu.size() * 8, cudaMemcpyHostToDevice);
+    e1 = cudaMemcpy(ct.d_moddown, md.data(), md.size() * 8, cudaMemcpyHostToDevice);
+    if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables copy");
+    ct.level = level;
+    ct.beta = beta;
+    *out = &ct;
+    return ENSI_OK;
+}
+
+// ---------------------------------------------------------------- kernels
+
+// ModUp conversion.  coef = INTT(c1) [l][N'] (coefficient form).  ext [beta][E][N']:
+//   e in D_t -> coef (NTT brings it back to c1's own limb bit-exactly), else the fast conversion.
+__global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                      uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                      ModTab tab, const uint64_t* __restrict__ cm) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t row = blockIdx.y, t = row / E, e = row % E;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t lo = t * A, hi = min((t + 1) * A, level), cnt = hi - lo;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    uint64_t out;
+    if (li >= lo && li < hi) {
+        out = coef[(size_t)li * n + k];
+    } else {
+        const uint64_t beta = (level + A - 1) / A;
+        const uint64_t* qhinv = cm + (size_t)t * A * 2;
+        const uint64_t* qh = cm + beta * A * 2 + (((size_t)t * E + e) * A) * 2;
+        const uint64_t r = tab.q[li];
+        uint64_t sum = 0;
+        for (uint32_t a = 0; a < cnt; a++) {
+            const uint64_t qi = tab.q[lo + a];
+            uint64_t y = mul_shoup(coef[(size_t)(lo + a) * n + k], qhinv[2 * a], qhinv[2 * a + 1], qi);
+            sum += mul_shoup_lazy(y, qh[2 * a], qh[2 * a + 1], r);
+        }
+        out = reduce64(sum, tab.br(li));
+    }
+    ext[(size_t)row * n + k] = out;
+}
+
+// Key inner product with the automorphism fused on load.
+// acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r)
+__global__ void __launch_bounds__(kT) k_kip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
+                                            uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
+                                            uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab) {
+    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
+    const uint32_t e = blockIdx.y, gi = blockIdx.z >> 1, j = blockIdx.z & 1;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t g = gb.g[gi];
+    const uint32_t src = galois_src_index(k, g, log_n);
+    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * T * n;
+    const Barrett br = tab.br(li);
+    U128 s{0, 0};
+    for (uint32_t t = 0; t < beta; t++) {
+        uint64_t dv = ext[((size_t)t * E + e) * n + src];
+        uint64_t kv = key[(((size_t)t * 2 + j) * T + li) * n + k];
+        mac128(s, dv, kv);
+        if ((t & 3) == 3 && t + 1 < beta) {
+            s.lo = barrett128(s.hi, s.lo, br);
+            s.hi = 0;
+        }
+    }
+    acc[(((size_t)gi * 2 + j) * E + e) * n + k] = barrett128(s.hi, s.lo, br);
+}
+
+// ModDown conversion: z[gi][j][i][k] = sum_k' [pc_k' (P/p_k')^-1]_{p_k'} [P/p_k']_{q_i}  (mod q_i), where
+// pc = INTT'ed P limbs of acc.
+__global__ void __launch_bounds__(kT) k_moddown_convert(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
+                                                        uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                        ModTab tab, const uint64_t* __restrict__ cm) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t i = blockIdx.y, gj = blockIdx.z;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t* phinv = cm;
+    const uint64_t* ph = cm + (size_t)A * 2 + (size_t)i * A * 2;
+    const uint64_t q = tab.q[i];
+    const uint64_t* pc = acc + ((size_t)gj * E + level) * n;
+    uint64_t sum = 0;
+    for (uint32_t a = 0; a < A; a++) {
+        uint64_t y = mul_shoup(pc[(size_t)a * n + k], phinv[2 * a], phinv[2 * a + 1], tab.q[L + a]);
+        sum += mul_shoup_lazy(y, ph[2 * a], ph[2 * a + 1], q);
+    }
+    z[((size_t)gj * level + i) * n + k] = reduce64(sum, tab.br(i));
+}
+
+// out[gi][j][i][k] = (acc_q_i - z) * P^-1 (+ c0[i][src_g(k)] when j == 0)
+__global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
+                                                      const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
+                                                      GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
+                                                      ModTab tab, const uint64_t* __restrict__ cm) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t i = blockIdx.y, gj = blockIdx.z, gi = gj >> 1, j = gj & 1;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t q = tab.q[i];
+    const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
+    uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)gj * level + i) * n + k], q);
+    v = mul_shoup(v, pinv[0], pinv[1], q);
+    if (j == 0) v = add_mod(v, c0[(size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
+    out[(((size_t)gb.oidx[gi] * 2 + j) * level + i) * n + k] = v;
+}
+
+// ---------------------------------------------------------------- host driver
+
+const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g) {
+    for (size_t i = 0; i < ctx->galois.size(); i++)
+        if (ctx->galois[i] == g) return ctx->d_keys + i * (size_t)ctx->dnum * 2 * ctx->T * ctx->n;
+    return nullptr;
+}
+
+static int key_index(const ensi_ctx* ctx, uint64_t g) {
+    for (size_t i = 0; i < ctx->galois.size(); i++)
+        if (ctx->galois[i] == g) return (int)i;
+    return -1;
+}
+
+// Hoisted rotations of one ciphertext ct [2][level][N'] by n_g Galois elements -> out [n_g][2][level][N'].
+int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
+                   uint64_t* out, cudaStream_t st) {
+    const uint32_t n = ctx->n, A = ctx->A, E = level + A;
+    const uint64_t two_n_mask = 2ull * n - 1;
+    const size_t ctw = (size_t)2 * level * n;
+    if (A == 0) return set_err(ctx, ENSI_ENOKEY, "context has no special primes (num_p == 0): no key switching");
+    std::vector<uint32_t> idx;
+    std::vector<uint64_t> gs;
+    for (uint32_t r = 0; r < n_g; r++) {
+        uint64_t g = galois[r] & two_n_mask;
+        if (g == 1) {
+            cudaMemcpyAsync(out + r * ctw, ct, ctw * 8, cudaMemcpyDeviceToDevice, st);
+            continue;
+        }
+        int ki = key_index(ctx, g);
+        if (ki < 0) return set_err(ctx, ENSI_ENOKEY, "no rotation key loaded for Galois element " + std::to_string(g));
+        idx.push_back(r);
+        gs.push_back(g);
+    }
+    if (idx.empty()) return ENSI_OK;
+    ConvTables* cvt = nullptr;
+    int rc = conv_tables(ctx, level, &cvt);
+    if (rc) return rc;
+    const uint32_t beta = cvt->beta;
+    const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), kMaxBatch);
+    // scratch: coef [level][n] | ext [beta][E][n] | acc [nb][2][E][n] | z [nb][2][level][n]
+    const size_t w_coef = (size_t)level * n, w_ext = (size_t)beta * E * n, w_acc = (size_t)nb * 2 * E * n,
+                 w_z = (size_t)nb * 2 * level * n;
+    rc = ensure_scratch(ctx, (w_coef + w_ext + w_acc + w_z) * 8);
+    if (rc) return rc;
+    uint64_t* coef = (uint64_t*)ctx->scratch;
+    uint64_t* ext = coef + w_coef;
+    uint64_t* acc = ext + w_ext;
+    uint64_t* z = acc + w_acc;
+
+    // ---- ModUp (once)
+    cudaMemcpyAsync(coef, ct + (size_t)level * n, w_coef * 8, cudaMemcpyDeviceToDevice, st);
+    ntt_inverse(ctx, coef, level, identity_map(level), st);
+    {
+        dim3 g(n / kT, beta * E);
+        k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
+        ENSI_LAUNCH_CHECK(ctx);
+    }
+    ntt_forward(ctx, ext, beta * E, ext_map(ctx, level), st);
+
+    // ---- per batch of Galois elements
+    for (size_t b0 = 0; b0 < idx.size(); b0 += nb) {
+        const uint32_t cnt = (uint32_t)std::min<size_t>(nb, idx.size() - b0);
+        GBatch gb{};
+        for (uint32_t i = 0; i < cnt; i++) {
+            gb.g[i] = gs[b0 + i];
+            gb.key[i] = (uint32_t)key_index(ctx, gs[b0 + i]);
+            gb.oidx[i] = idx[b0 + i];
+        }
+        {
+            dim3 g(n / kT, E, cnt * 2);
+            k_kip<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                                    ctx->tab);
+            ENSI_LAUNCH_CHECK(ctx);
+        }
+        LimbMap pm = identity_map(A);
+        for (uint32_t a = 0; a < A; a++) pm.limb[a] = (uint8_t)(ctx->L + a);
+        pm.grp_rows = A;
+        pm.grp_stride = E;
+        pm.grp_off = level;
+        ntt_inverse(ctx, acc, cnt * 2 * A, pm, st);
+        {
+            dim3 g(n / kT, level, cnt * 2);
+            k_moddown_convert<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
+            ENSI_LAUNCH_CHECK(ctx);
+        }
+        ntt_forward(ctx, z, cnt * 2 * level, identity_map(level), st);
+        {
+            dim3 g(n / kT, level, cnt * 2);
+            k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown);
+            ENSI_LAUNCH_CHECK(ctx);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_err(ctx, e, "rotate_hoisted");
+    return ENSI_OK;
+}
+
+}  // namespace ensi

@@ -1,0 +1,262 @@
+"""Thin ctypes binding of libensi.so (include/ensi.h).  Argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this module converts torch
+device tensors to (pointer, count, level) views and numpy host arrays to pointers.  There is no CPU
+fallback: if libensi.so is missing or no CUDA device is present the calls raise.
+
+Names follow the C ABI: ``ensi_ctx_create`` -> :class:`Context`, ``ensi_load_keys`` ->
+:meth:`Context.load_keys`, ``ensi_pcmm_ternary`` -> :meth:`Context.pcmm_ternary`,
+``ensi_decrypt_debug`` -> :meth:`Context.decrypt_debug`, etc.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libensi.so")
+
+ENSI_OK, ENSI_EINVAL, ENSI_EDIM, ENSI_ENOTTERNARY, ENSI_ELEVEL, ENSI_ENOKEY, ENSI_ENOMEM, ENSI_ECUDA = range(8)
+ERR_NAMES = {0: "ENSI_OK", 1: "ENSI_EINVAL", 2: "ENSI_EDIM", 3: "ENSI_ENOTTERNARY", 4: "ENSI_ELEVEL",
+             5: "ENSI_ENOKEY", 6: "ENSI_ENOMEM", 7: "ENSI_ECUDA"}
+MEM_HOST, MEM_DEVICE = 0, 1
+KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05 = 0, 1, 2
+
+# every symbol include/ensi.h declares (checked by tests/test_abi.py)
+EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
+           "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
+           "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rescale", "ensi_decrypt_debug",
+           "ensi_launch_count"]
+
+
+class EnsiError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Params(C.Structure):
+    _fields_ = [("log_n", C.c_uint32), ("num_q", C.c_uint32), ("num_p", C.c_uint32), ("dnum", C.c_uint32),
+                ("q", C.c_void_p), ("p", C.c_void_p), ("log2_scale", C.c_double)]
+
+
+class CtView(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("count", C.c_uint32), ("level", C.c_uint32), ("log2_scale", C.c_double)]
+
+
+class Keys(C.Structure):
+    _fields_ = [("sk_ntt", C.c_void_p), ("n_rot", C.c_uint32), ("galois", C.c_void_p), ("rot_keys", C.c_void_p),
+                ("rot_keys_mem", C.c_uint32)]
+
+
+class PcmmOpts(C.Structure):
+    _fields_ = [("layout", C.c_uint32), ("block_s", C.c_uint32), ("baby", C.c_uint32), ("rescale_out", C.c_uint32),
+                ("kernel", C.c_uint32)]
+
+
+_LIB = None
+
+
+def lib():
+    """Load libensi.so (raises if it has not been built -- there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+        L.ensi_abi_version.restype = u32
+        L.ensi_ctx_create.argtypes = [C.POINTER(Params), C.c_int, C.POINTER(vp)]
+        L.ensi_ctx_destroy.argtypes = [vp]
+        L.ensi_ctx_destroy.restype = None
+        L.ensi_last_error.argtypes = [vp]
+        L.ensi_last_error.restype = C.c_char_p
+        L.ensi_ctx_moduli.argtypes = [vp, vp, vp]
+        L.ensi_load_keys.argtypes = [vp, C.POINTER(Keys)]
+        L.ensi_weights_pack.argtypes = [vp, vp, u32, u32, u32, C.POINTER(vp)]
+        L.ensi_weights_destroy.argtypes = [vp]
+        L.ensi_weights_destroy.restype = None
+        L.ensi_pcmm_ternary_packed.argtypes = [vp, C.POINTER(CtView), vp, C.POINTER(CtView), C.POINTER(PcmmOpts), vp]
+        L.ensi_pcmm_ternary.argtypes = [vp, C.POINTER(CtView), vp, u32, u32, u32, C.POINTER(CtView),
+                                        C.POINTER(PcmmOpts), vp]
+        L.ensi_pcmm_ternary_host.argtypes = [vp, vp, u32, C.c_double, vp, vp, u32, vp]
+        L.ensi_ntt.argtypes = [vp, vp, u32, vp, u32, C.c_int, vp]
+        L.ensi_rotate_hoisted.argtypes = [vp, C.POINTER(CtView), u32, vp, C.POINTER(CtView), vp]
+        L.ensi_rescale.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp]
+        L.ensi_decrypt_debug.argtypes = [vp, C.POINTER(CtView), u32, vp, vp]
+        L.ensi_launch_count.argtypes = [vp]
+        L.ensi_launch_count.restype = u64
+        _LIB = L
+    return _LIB
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _np_ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+class Weights:
+    """Packed ternary weights (row a2), a model constant."""
+
+    def __init__(self, ctx: "Context", W: np.ndarray):
+        W = np.ascontiguousarray(W, dtype=np.int8)
+        self.d, self.m = W.shape
+        self.ctx = ctx
+        h = C.c_void_p()
+        rc = lib().ensi_weights_pack(ctx.h, _np_ptr(W), self.d, self.m, self.m, C.byref(h))
+        ctx._check(rc)
+        self.h = h
+        self.nnz = int(np.count_nonzero(W))
+
+    def close(self):
+        if self.h:
+            lib().ensi_weights_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """ensi_ctx_create(...) on one CUDA device."""
+
+    def __init__(self, log_n: int, num_q: int, num_p: int, dnum: int, device: int = 0, q=None, p=None,
+                 log2_scale: float = 40.0):
+        self._qa = np.ascontiguousarray(q, np.uint64) if q is not None else None
+        self._pa = np.ascontiguousarray(p, np.uint64) if p is not None else None
+        prm = Params(log_n, num_q, num_p, dnum,
+                     self._qa.ctypes.data if self._qa is not None else None,
+                     self._pa.ctypes.data if self._pa is not None else None, log2_scale)
+        h = C.c_void_p()
+        rc = lib().ensi_ctx_create(C.byref(prm), device, C.byref(h))
+        if rc != 0:
+            raise EnsiError(rc, "ensi_ctx_create failed")
+        self.h = h
+        self.log_n, self.n, self.L, self.A, self.dnum, self.device = log_n, 1 << log_n, num_q, num_p, dnum, device
+        self.log2_scale = log2_scale
+        mods = np.zeros(num_q + num_p, np.uint64)
+        psi = np.zeros(num_q + num_p, np.uint64)
+        self._check(lib().ensi_ctx_moduli(self.h, _np_ptr(mods), _np_ptr(psi)))
+        self.moduli = [int(v) for v in mods]
+        self.psi = [int(v) for v in psi]
+        self.q = self.moduli[:num_q]
+        self.p = self.moduli[num_q:]
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ensi_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int):
+        if rc != 0:
+            msg = lib().ensi_last_error(self.h)
+            raise EnsiError(rc, msg.decode() if msg else "")
+
+    def launch_count(self) -> int:
+        return int(lib().ensi_launch_count(self.h))
+
+    @staticmethod
+    def view(t, level: int, log2_scale: float = 40.0) -> CtView:
+        """torch uint64 CUDA tensor [count][2][level][N'] -> ensi_ct_view."""
+        assert t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 8
+        assert t.dim() == 4 and t.shape[1] == 2 and t.shape[2] == level
+        return CtView(t.data_ptr(), t.shape[0], level, log2_scale)
+
+    # ---- keys
+    def load_keys(self, sk_ntt: np.ndarray | None = None, galois=None, rot_keys=None):
+        """rot_keys: numpy (host, copied) or torch CUDA tensor (device, referenced in place)."""
+        sk = np.ascontiguousarray(sk_ntt, np.uint64) if sk_ntt is not None else None
+        ga = np.ascontiguousarray(galois if galois is not None else [], np.uint64)
+        mem, kp = MEM_HOST, None
+        if rot_keys is not None:
+            if isinstance(rot_keys, np.ndarray):
+                rk = np.ascontiguousarray(rot_keys, np.uint64)
+                kp = rk.ctypes.data
+                self._keep_host = rk
+            else:
+                assert rot_keys.is_cuda and rot_keys.is_contiguous()
+                mem, kp = MEM_DEVICE, rot_keys.data_ptr()
+                self._keep_dev = rot_keys
+        keys = Keys(sk.ctypes.data if sk is not None else None, ga.shape[0],
+                    ga.ctypes.data if ga.shape[0] else None, kp, mem)
+        self._check(lib().ensi_load_keys(self.h, C.byref(keys)))
+
+    def weights(self, W: np.ndarray) -> Weights:
+        return Weights(self, W)
+
+    # ---- PCMM (rows a3, a4, a8)
+    def pcmm_ternary(self, x, W, y, level: int, layout: int = 0, block_s: int = 0, baby: int = 0,
+                     rescale_out: bool = False, kernel: int = 0, stream=None, log2_scale: float = 40.0) -> float:
+        """y = x (x) W.  W: Weights (prepacked) or host int8 array.  Returns y's log2 scale."""
+        xv = self.view(x, level, log2_scale)
+        yv = self.view(y, level - 1 if rescale_out else level)
+        opts = PcmmOpts(layout, block_s, baby, 1 if rescale_out else 0, kernel)
+        if isinstance(W, Weights):
+            rc = lib().ensi_pcmm_ternary_packed(self.h, C.byref(xv), W.h, C.byref(yv), C.byref(opts),
+                                                _stream_ptr(stream))
+        else:
+            Wa = np.ascontiguousarray(W, np.int8)
+            d, m = Wa.shape
+            rc = lib().ensi_pcmm_ternary(self.h, C.byref(xv), _np_ptr(Wa), d, m, m, C.byref(yv), C.byref(opts),
+                                         _stream_ptr(stream))
+        self._check(rc)
+        return yv.log2_scale
+
+    def pcmm_ternary_host(self, x_host: np.ndarray, w: Weights, y_host: np.ndarray, level: int, kernel: int = 0,
+                          stream=None, log2_scale: float = 40.0):
+        """End-to-end Layout A on host buffers (pinned recommended); enqueued on `stream` (sync before reading)."""
+        assert x_host.dtype.itemsize == 8 and y_host.dtype.itemsize == 8
+        assert x_host.flags.c_contiguous and y_host.flags.c_contiguous
+        assert x_host.shape[0] == w.d and y_host.shape[0] == w.m
+        self._check(lib().ensi_pcmm_ternary_host(self.h, _np_ptr(x_host), level, log2_scale, w.h, _np_ptr(y_host),
+                                                 kernel, _stream_ptr(stream)))
+
+    # ---- primitives (rows a5-a7, a4, a10)
+    def ntt(self, data, limb_of_row, inverse: bool = False, stream=None):
+        lm = np.ascontiguousarray(limb_of_row, np.uint32)
+        rows = data.numel() // self.n
+        self._check(lib().ensi_ntt(self.h, C.c_void_p(data.data_ptr()), rows, _np_ptr(lm), lm.shape[0],
+                                   1 if inverse else 0, _stream_ptr(stream)))
+
+    def rotate_hoisted(self, x, galois, y, level: int, stream=None):
+        ga = np.ascontiguousarray(galois, np.uint64)
+        xv, yv = self.view(x, level), self.view(y, level)
+        self._check(lib().ensi_rotate_hoisted(self.h, C.byref(xv), ga.shape[0], _np_ptr(ga), C.byref(yv),
+                                              _stream_ptr(stream)))
+
+    def rescale(self, x, y, level: int, log2_scale: float = 80.0, stream=None) -> float:
+        xv, yv = self.view(x, level, log2_scale), self.view(y, level - 1)
+        self._check(lib().ensi_rescale(self.h, C.byref(xv), C.byref(yv), _stream_ptr(stream)))
+        return yv.log2_scale
+
+    def decrypt_debug(self, ct, index: int, level: int, log2_scale: float = 40.0, want_coeffs: bool = False):
+        cv = self.view(ct, level, log2_scale)
+        slots = np.zeros(self.n // 2, np.float64)
+        coeffs = np.zeros((level, self.n), np.uint64) if want_coeffs else None
+        self._check(lib().ensi_decrypt_debug(self.h, C.byref(cv), index,
+                                             _np_ptr(coeffs) if want_coeffs else None, _np_ptr(slots)))
+        return (slots, coeffs) if want_coeffs else slots
+
+
+def galois_elt(log_n: int, r: int) -> int:
+    """g = 5^r mod 2N' (left rotation by r); host helper for building key lists."""
+    half = 1 << (log_n - 1)
+    return pow(5, r % half, 2 << log_n)

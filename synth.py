@@ -78,3 +78,14 @@ def edge_W(kind: str, d: int, m: int, seed: int = 0) -> np.ndarray:
     if kind == "toy":
         return np.array([[1, -1], [0, 1], [-1, 0], [0, 1]], np.int8)
     raise ValueError(kind)
+
+
+def gen_words_torch(seed: int, moduli, count: int, level: int, n: int, device="cuda"):
+    """Device-resident uniform RNS words (timing-only inputs): torch int64 [count][2][level][n], limb r in [0, q_r)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    t = torch.empty((count, 2, level, n), dtype=torch.int64, device=device)
+    for r in range(level):
+        t[:, :, r, :].random_(0, int(moduli[r]), generator=g)
+    return t

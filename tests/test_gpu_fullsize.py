@@ -1,0 +1,115 @@
+"""Full-size (BASELINE.json configs[1], C2: N'=2^16, L=12, 768x768) parity in the launch configuration bench.py
+times: sampled output columns compared word for word with the oracle, real pk-encryptions decrypted against
+the float64 product (max-abs <= 1e-4), and full-size rotations / NTT / rescale bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+DELTA = 2.0 ** 40
+NTH = max(1, min(64, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def c2(torch_cuda):
+    from paper_2509_09424_b200 import Context
+    cfg = synth.CONFIGS["C2"]
+    o = oracle.Oracle(cfg["log_n"], cfg["L"], cfg["alpha"], cfg["dnum"])
+    skc, sk, pk = o.keygen(synth.SEED_BASE + 2)
+    ctx = Context(cfg["log_n"], cfg["L"], cfg["alpha"], cfg["dnum"])
+    ctx.load_keys(sk_ntt=sk)
+    return o, sk, pk, ctx
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_c2_sampled_columns_bit_exact(c2, torch_cuda, kernel):
+    """768x768 on uniform words (data-oblivious accumulate): 3 full output columns == oracle Alg. 1."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    d = m = 768
+    x = synth.gen_words(synth.SEED_BASE + 2, o.q, d, 12, o.n)
+    W = synth.gen_W(synth.SEED_BASE + 102, d, m)
+    xd = _dev(torch, x)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    w = ctx.weights(W)
+    ctx.pcmm_ternary(xd, w, yd, level=12, kernel=kernel)
+    torch.cuda.synchronize()
+    cols = [0, 377, 767]
+    want = o.pcmm_a(x, W, cols=cols, nthreads=NTH)
+    got = yd[cols].cpu().numpy().view(np.uint64)
+    assert (got == want).all()
+    # every output word is canonical (property at any size), checked on a strided sample of all outputs
+    qv = torch.tensor(o.q, dtype=torch.int64, device="cuda").view(1, 1, 12, 1)
+    assert bool((yd[:, :, :, ::97] >= 0).all()) and bool((yd[:, :, :, ::97] < qv).all())
+
+
+def test_c2_encrypted_decrypts_to_product(c2, torch_cuda):
+    """Real pk-encryptions of X (128 tokens x 768) -> PCMM -> decrypt == X.W within 1e-4 (north star)."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    s, d, m = 128, 768, 768
+    X = synth.gen_X(synth.SEED_BASE + 2, s, d)
+    W = synth.gen_W(synth.SEED_BASE + 102, d, m)
+    m_res = np.stack([o.encode(X[:, j], 12, DELTA) for j in range(d)])
+    x = o.encrypt_batch(np.arange(d, dtype=np.uint64) + np.uint64(123456), pk, 12, m_res, nthreads=NTH)
+    del m_res
+    xd = _dev(torch, x)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, ctx.weights(W), yd, level=12)
+    torch.cuda.synchronize()
+    ref = X @ W.astype(np.float64)
+    worst = 0.0
+    for i in range(0, m, 37):
+        z = ctx.decrypt_debug(yd, i, 12)
+        worst = max(worst, float(np.max(np.abs(z[:s] - ref[:, i]))), float(np.max(np.abs(z[s:]))))
+    assert worst < 1e-4
+    # the oracle agrees on one column word for word
+    want = o.pcmm_a(x, W, cols=[111], nthreads=NTH)
+    assert (yd[111:112].cpu().numpy().view(np.uint64) == want).all()
+
+
+def test_c2_rotations_bit_exact(c2, torch_cuda):
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    rctx = Context(16, 12, 4, 3)
+    gs = [o.galois(128), o.galois(128 * 255)]
+    keys = np.stack([o.rotkey(777 + i, g, sk) for i, g in enumerate(gs)])
+    rctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    z = np.random.default_rng(1).uniform(-1, 1, o.n // 2)
+    ct = o.encrypt(5, pk, 12, o.encode(z, 12, DELTA))
+    want = o.rotate_hoisted(ct, gs, keys)
+    yd = torch.empty((2, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    rctx.rotate_hoisted(_dev(torch, ct[None]), gs, yd, 12)
+    torch.cuda.synchronize()
+    assert (yd.cpu().numpy().view(np.uint64) == want).all()
+    got = rctx.decrypt_debug(yd, 0, 12)
+    assert np.max(np.abs(got - np.roll(z, -128))) < 1e-5
+
+
+def test_c2_rescale_bit_exact(c2, torch_cuda):
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    x = synth.gen_words(9, o.q, 2, 12, o.n)
+    want = np.stack([o.rescale(x[c]) for c in range(2)])
+    yd = torch.empty((2, 2, 11, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(_dev(torch, x), yd, 12)
+    torch.cuda.synchronize()
+    assert (yd.cpu().numpy().view(np.uint64) == want).all()

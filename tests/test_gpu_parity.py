@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, word for word (bit-exact on every RNS word),
+plus decryption against the float64 plaintext product (north-star tolerance 1e-4 at scale 2^40)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DELTA = 2.0 ** 40
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def setup_c1(torch_cuda):
+    from paper_2509_09424_b200 import Context
+    o = oracle.Oracle(12, 3, 1, 3)
+    skc, sk, pk = o.keygen(synth.SEED_BASE + 1)
+    ctx = Context(12, 3, 1, 3)
+    ctx.load_keys(sk_ntt=sk)
+    return o, sk, pk, ctx
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def test_moduli_and_roots_match_oracle(setup_c1, torch_cuda):
+    o, sk, pk, ctx = setup_c1
+    assert ctx.moduli == o.moduli and ctx.psi == o.psi
+    from paper_2509_09424_b200 import Context
+    big = Context(16, 12, 4, 3)
+    ob = oracle.Oracle(16, 12, 4, 3)
+    assert big.moduli == ob.moduli and big.psi == ob.psi
+
+
+@pytest.mark.parametrize("log_n,L,alpha", [(12, 3, 1), (16, 12, 4), (13, 2, 1), (8, 2, 1)])
+def test_ntt_bit_exact(torch_cuda, log_n, L, alpha):
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    ctx = Context(log_n, L, alpha, max(1, -(-L // alpha)))
+    o = oracle.Oracle(log_n, L, alpha, max(1, -(-L // alpha)))
+    T = L + alpha
+    rs = np.random.default_rng(log_n)
+    rows = np.stack([rs.integers(0, o.moduli[i % T], o.n, dtype=np.uint64) for i in range(2 * T)])
+    rows[0, :3] = 0
+    rows[1, :3] = np.uint64(o.moduli[1] - 1)
+    t = dev(torch, rows)
+    ctx.ntt(t, list(range(T)))
+    got = host(t)
+    want = np.stack([o.ntt(i % T, rows[i]) for i in range(2 * T)])
+    assert (got == want).all()
+    ctx.ntt(t, list(range(T)), inverse=True)
+    assert (host(t) == rows).all()
+
+
+def _enc_cols(o, pk, X, level, seed):
+    d = X.shape[1]
+    m_res = np.stack([o.encode(X[:, j], level, DELTA) for j in range(d)])
+    return o.encrypt_batch(np.arange(d, dtype=np.uint64) + np.uint64(seed), pk, level, m_res)
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel):
+    """C1: 16x16 BitNet layer on real pk-encryptions; every word == oracle; decrypt == X.W within 1e-4."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    X = synth.gen_X(synth.SEED_BASE + 1, 16, 16)
+    W = synth.gen_W(synth.SEED_BASE + 101, 16, 16)
+    x = _enc_cols(o, pk, X, 3, 7000)
+    want = o.pcmm_a(x, W)
+    xd = dev(torch, x)
+    yd = torch.empty((16, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, W, yd, level=3, kernel=kernel)
+    torch.cuda.synchronize()
+    got = host(yd)
+    assert (got == want).all()
+    ref = X @ W.astype(np.float64)
+    for i in range(16):
+        z = ctx.decrypt_debug(yd, i, 3)
+        assert np.max(np.abs(z[:16] - ref[:, i])) < 1e-4
+        zo = o.decrypt(sk, want[i], DELTA)
+        assert np.max(np.abs(z - zo)) < 1e-9
+
+
+@pytest.mark.parametrize("d,m,level", [(37, 70, 3), (1, 1, 1), (64, 64, 2), (130, 3, 3), (5, 129, 1)])
+def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level):
+    """Ragged d (pipeline tail) and m (partial 64-output tile), random words incl. 0 and q-1."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    x = synth.gen_words(d * 1000 + m, o.q, d, level, o.n)
+    x[0, 0, 0, :7] = 0
+    x[-1, 1, level - 1, :7] = np.uint64(o.q[level - 1] - 1)
+    W = synth.gen_W(d + m, d, m)
+    want = o.pcmm_a(x, W, nthreads=4)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, level, o.n), dtype=torch.int64, device="cuda")
+    w = ctx.weights(W)
+    ctx.pcmm_ternary(xd, w, yd, level=level)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+
+
+@pytest.mark.parametrize("kind", ["zero", "identity", "neg_identity", "permutation", "plus", "minus", "toy"])
+def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind):
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    d = m = 4 if kind == "toy" else 96
+    if kind == "toy":
+        m = 2
+    W = synth.edge_W(kind, d, m, seed=5)
+    x = synth.gen_words(77, o.q, d, 3, o.n)
+    x[:, :, :, :11] = np.uint64(0)
+    for r in range(3):
+        x[:, :, r, 11:20] = np.uint64(o.q[r] - 1)
+    want = o.pcmm_a(x, W, nthreads=4)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, W, yd, level=3)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+
+
+def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda):
+    """d = 8300 > 8184 (intermediate reduction) with every word q-1 and W all +1 / -1 / mixed."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    d, m, level = 8300, 3, 1
+    x = np.full((d, 2, level, o.n), np.uint64(o.q[0] - 1), dtype=np.uint64)
+    W = np.ones((d, m), np.int8)
+    W[:, 1] = -1
+    W[::3, 2] = -1
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, level, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, W, yd, level=level)
+    torch.cuda.synchronize()
+    got = host(yd)
+    q = o.q[0]
+    s2 = int(np.sum(W[:, 2].astype(np.int64)))
+    for i, coef in enumerate([d, -d, s2]):
+        assert (got[i] == np.uint64((coef * (q - 1)) % q)).all()
+
+
+def test_pcmm_errors(setup_c1, torch_cuda):
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_ENOTTERNARY, ENSI_EDIM, ENSI_EINVAL
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    x = torch.zeros((4, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    y = torch.zeros((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    W = np.zeros((4, 2), np.int8)
+    W[2, 1] = 2
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary(x, W, y, level=3)
+    assert e.value.code == ENSI_ENOTTERNARY and "W[2][1]" in str(e.value)
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary(x, np.zeros((5, 2), np.int8), y, level=3)
+    assert e.value.code == ENSI_EDIM
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary(x, np.zeros((4, 4), np.int8), x, level=3)
+    assert e.value.code in (ENSI_EINVAL, ENSI_EDIM)
+
+
+# ---------------------------------------------------------------- rotation / key switching
+
+@pytest.fixture(scope="module")
+def rot_setup(setup_c1):
+    o, sk, pk, ctx = setup_c1
+    rs = [1, 2, 5, 16, 33, 100, -1, 1000]
+    gs = [o.galois(r) for r in rs]
+    keys = np.stack([o.rotkey(9000 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    return o, sk, pk, ctx, gs, keys
+
+
+@pytest.mark.parametrize("level", [3, 2, 1])
+def test_rotate_hoisted_bit_exact(rot_setup, torch_cuda, level):
+    o, sk, pk, ctx, gs, keys = rot_setup
+    torch = torch_cuda
+    z = np.random.default_rng(level).uniform(-1, 1, o.n // 2)
+    ct = o.encrypt(31 + level, pk, level, o.encode(z, level, DELTA))
+    want = o.rotate_hoisted(ct, gs, keys)
+    xd = dev(torch, ct[None])
+    yd = torch.empty((len(gs), 2, level, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(xd, gs, yd, level)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+    got = ctx.decrypt_debug(yd, 0, level)
+    assert np.max(np.abs(got - np.roll(z, -1))) < 1e-5
+
+
+def test_rotate_identity_element_copies(rot_setup, torch_cuda):
+    o, sk, pk, ctx, gs, keys = rot_setup
+    torch = torch_cuda
+    ct = synth.gen_words(3, o.q, 1, 3, o.n)
+    xd = dev(torch, ct)
+    yd = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(xd, [1, gs[0]], yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    assert (got[0] == ct[0]).all()
+    assert (got[1] == o.rotate(ct[0], gs[0], keys[0])).all()
+
+
+def test_rotate_missing_key(rot_setup, torch_cuda):
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_ENOKEY
+    o, sk, pk, ctx, gs, keys = rot_setup
+    torch = torch_cuda
+    xd = torch.zeros((1, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    yd = torch.zeros((1, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    with pytest.raises(EnsiError) as e:
+        ctx.rotate_hoisted(xd, [o.galois(7)], yd, 3)
+    assert e.value.code == ENSI_ENOKEY
+
+
+# ---------------------------------------------------------------- Layout B
+
+@pytest.mark.parametrize("d,m,B", [(16, 16, 0), (16, 16, 4), (20, 6, 4)])
+def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B):
+    from paper_2509_09424_b200 import Context
+    o, sk, pk, _ = setup_c1
+    torch = torch_cuda
+    ctx = Context(12, 3, 1, 3)
+    s = 16
+    k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, B)
+    X = synth.gen_X(61 + d, s, d)
+    W = synth.gen_W(62 + d, d, m)
+    slots = o.n // 2
+    cts = []
+    for c in range(n_in):
+        zz = np.zeros(slots)
+        for b in range(k):
+            col = c * k + b
+            if col < d:
+                zz[b * s:(b + 1) * s] = X[:, col]
+        cts.append(o.encrypt(6100 + c, pk, 3, o.encode(zz, 3, DELTA)))
+    x = np.stack(cts)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
+    keys = np.stack([o.rotkey(6200 + i, g, sk) for i, g in enumerate(gk)])
+    want = o.pcmm_b(x, W, s, k, B, gk, keys)
+    ctx.load_keys(sk_ntt=sk, galois=gk, rot_keys=keys)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, W, yd, level=3, layout=1, block_s=s, baby=B)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+    ref = X @ W.astype(np.float64)
+    for i in range(m):
+        zz = ctx.decrypt_debug(yd, i, 3)
+        assert np.max(np.abs(zz[:s] - ref[:, i])) < 1e-4
+
+
+# ---------------------------------------------------------------- rescale
+
+@pytest.mark.parametrize("level", [3, 2])
+def test_rescale_bit_exact(setup_c1, torch_cuda, level):
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    x = synth.gen_words(90 + level, o.q, 5, level, o.n)
+    want = np.stack([o.rescale(x[c]) for c in range(5)])
+    xd = dev(torch, x)
+    yd = torch.empty((5, 2, level - 1, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(xd, yd, level)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+
+
+def test_pcmm_with_rescale_epilogue(setup_c1, torch_cuda):
+    """Inputs at Delta^2 (un-rescaled products); PCMM then rescale == oracle PCMM then oracle rescale."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    X = synth.gen_X(5, 16, 8)
+    W = synth.gen_W(6, 8, 8)
+    scale2 = DELTA * DELTA
+    m_res = np.stack([o.encode(X[:, j], 3, scale2) for j in range(8)])
+    x = o.encrypt_batch(np.arange(8, dtype=np.uint64) + np.uint64(40), pk, 3, m_res)
+    want = np.stack([o.rescale(c) for c in o.pcmm_a(x, W)])
+    xd = dev(torch, x)
+    yd = torch.empty((8, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ls = ctx.pcmm_ternary(xd, W, yd, level=3, rescale_out=True, log2_scale=80.0)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+    ref = X @ W.astype(np.float64)
+    z = ctx.decrypt_debug(yd, 3, 2, log2_scale=ls)
+    assert np.max(np.abs(z[:16] - ref[:, 3])) < 1e-4

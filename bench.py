@@ -274,17 +274,34 @@ def main():
     alg_bytes = (d + m) * ct_bytes + d * 2 * (2 * ((m + 63) // 64)) * 4
     term_words = w.nnz * 2 * L * n
     peaks, peak_src = load_peaks()
-    kernel_name = "tcgen05" if (args.kernel == 2 or (args.kernel == 0 and False)) else "cuda-core"
+    kernel_name = ctx.kernel_name(args.kernel, L)
     gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
     # ALU roofline of the CUDA-core accumulate: one 64-bit modular add per term-word = 2 ALU-pipe ops
     # (IADD3 + IADD3.X); ALU pipe = 64 lanes/clk/SM (B300_MICROARCH: rt_SMSP = 2) x 148 SMs x max clock.
-    alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
-    alu_ach = 2 * term_words / (ms_rank * 1e-3) / 1e12
-    roofline = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s (INT32 ALU lane-ops)",
-                "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary",
-                "algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
-                "hbm_frac": gbs / peaks["hbm_gbs"], "peak_source": peak_src,
-                "ops_per_launch": 2 * term_words}
+    if kernel_name == "tcgen05":
+        # byte-sliced INT8 GEMM: D[i][8w+b] over all 8 bytes of every word, K = d (padded to 128), M = m (padded
+        # to 128).  INT8 dense peak = measured bf16 (burst) x nominal ratio 4.5/2.25 = 2.
+        dpad, mpad = -(-d // 128) * 128, -(-m // 128) * 128
+        tc_ops = 2.0 * ct_bytes * dpad * mpad                 # 2 * (8*ctw bytes) * dpad * mpad
+        tc_peak = 2.0 * peaks["bf16_tflops"]
+        tc_ach = tc_ops / (ms_rank * 1e-3) / 1e12
+        t_tensor, t_hbm = tc_ops / (tc_peak * 1e12), alg_bytes / (peaks["hbm_gbs"] * 1e9)
+        if t_tensor >= t_hbm:
+            roofline = {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TOPS (int8, dense)",
+                        "frac": tc_ach / tc_peak}
+        else:
+            roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": gbs / peaks["hbm_gbs"]}
+        roofline.update({"traffic": None, "kernel": "k_accum_tc", "tensor_ops_per_launch": tc_ops,
+                         "tensor_peak_tops": tc_peak, "tensor_frac": tc_ach / tc_peak})
+    else:
+        alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
+        alu_ach = 2 * term_words / (ms_rank * 1e-3) / 1e12
+        roofline = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s (INT32 ALU lane-ops)",
+                    "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary",
+                    "ops_per_launch": 2 * term_words}
+    roofline.update({"algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
+                     "hbm_frac": gbs / peaks["hbm_gbs"], "peak_source": peak_src})
 
     out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",

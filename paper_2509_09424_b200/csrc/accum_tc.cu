@@ -1,14 +1,413 @@
-// accum_tc.cu -- row a3 on the 5th-generation tensor cores (byte-sliced INT8 tcgen05.mma).  Placeholder
-// until the kernel lands: tc_supported() reports false so the CUDA-core path (accum.cu) runs.
+// accum_tc.cu -- row a3 (Algorithm 1) on the 5th-generation tensor cores.
+//
+// Byte-sliced exact integer contraction.  For a ciphertext word x (< 2^60) write x = sum_b x_b 2^{8b} with
+// bytes x_b in [0,255].  Then for every output i and word w
+//     y_i[w] = sum_j W[j][i] x_j[w] = sum_b 2^{8b} D[i][8w+b],   D[i][c] = sum_j W[j][i] * byte_c(x_j)
+// and D is an int8 x uint8 -> int32 GEMM that is EXACT (|D| <= 255 d < 2^31).  Its B operand is the raw memory
+// of the input ciphertexts: byte c of ciphertext j is B[j][c], i.e. B is an MN-major (N-contiguous) uint8
+// matrix that TMA reads straight from the uint64 ciphertext buffers -- no repacking pass.  A = W^T (int8,
+// K-major, zero padded).  The epilogue reads 8 consecutive TMEM columns (the 8 byte planes of one word) per
+// thread, forms sum_b D_b 2^{8b} as a signed 128-bit value and reduces it to the canonical word in [0, q) --
+// the same unique value Algorithm 1 defines, so the output is bit-identical to the oracle and to accum.cu.
+//
+// Kernel structure (persistent, one CTA per SM, 320 threads):
+//   warp 0      TMA producer: W^T slice (resident in smem when 128*d_pad <= 96 KB, else streamed per stage) and
+//               the X byte tiles (128 K-rows x 256 bytes, two SWIZZLE_128B boxes) into a 3-stage mbarrier ring.
+//   warp 1      TMEM allocation (512 columns = 2 accumulators x 256) and the single-thread tcgen05.mma issue:
+//               M = 128 outputs, N = 256 bytes (32 words), K = 32 per instruction, kind::i8 (s8 x u8 -> s32).
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32, byte-plane recombination + Barrett, SWIZZLE_128B smem
+//               staging, TMA bulk-tensor store of 32 outputs x 16 words per warp.
+// CTA b owns output group g = b % G (128 outputs) and walks the word tiles t = b / G, b / G + P, ...; the G CTAs
+// that share a word tile run at the same time, so each X tile is read from HBM once and served to the others
+// from L2.
+#include <cuda.h>
+
 #include "ensi_internal.h"
 
 namespace ensi {
 
-bool tc_supported(const ensi_ctx*, uint32_t) { return false; }
+namespace tc {
 
-int accum_ternary_tc(ensi_ctx* ctx, const uint64_t*, uint32_t, ensi_weights*, uint64_t*, uint32_t, cudaStream_t, uint64_t,
-                     uint32_t) {
-    return set_err(ctx, ENSI_EINVAL, "tensor-core accumulate not built");
+static constexpr uint32_t kThreads = 320;
+static constexpr uint32_t kStages = 3;
+static constexpr uint32_t kBoxK = 128;                  // K rows per stage / A box inner bytes
+static constexpr uint32_t kABox = 128 * 128;            // 16 KB: 128 outputs x 128 K
+static constexpr uint32_t kBStage = 2 * 128 * 128;      // 32 KB: 128 K x 256 bytes (two 128-byte boxes)
+static constexpr uint32_t kYWarp = 32 * 128;            // 4 KB: 32 outputs x 16 words
+static constexpr uint32_t kAResMax = 96 * 1024;         // resident W^T slice budget
+static constexpr uint32_t kIdesc = (2u << 4)            // D format s32
+                                   | (1u << 7)          // A format: signed int8
+                                   | (0u << 10)         // B format: unsigned int8
+                                   | (0u << 15)         // A K-major
+                                   | (1u << 16)         // B MN-major
+                                   | ((256u >> 3) << 17)  // N = 256
+                                   | ((128u >> 4) << 24); // M = 128
+
+struct EpiConst {
+    uint64_t off_lo[ENSI_MAXT], off_hi[ENSI_MAXT];   // a multiple of q >= 2^80 (makes the 128-bit value non-negative)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, Blackwell version bits.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define TMEM_LD_X32(taddr, r)                                                                                       \
+    asm volatile(                                                                                                   \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"   \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                          \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),    \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
+        : "r"(taddr))
+
+// sum_b D_b 2^{8b} (signed, |D_b| < 2^31) mod q, canonical.
+__device__ __forceinline__ uint64_t combine_word(const uint32_t* r, const Barrett& br, uint64_t off_lo,
+                                                 uint64_t off_hi) {
+    int64_t lo = (int64_t)(int32_t)r[0] + (int64_t)(int32_t)r[1] * 256 + (int64_t)(int32_t)r[2] * 65536 +
+                 (int64_t)(int32_t)r[3] * 16777216;
+    int64_t hi = (int64_t)(int32_t)r[4] + (int64_t)(int32_t)r[5] * 256 + (int64_t)(int32_t)r[6] * 65536 +
+                 (int64_t)(int32_t)r[7] * 16777216;
+    // V = lo + hi * 2^32 as 128-bit two's complement, plus a multiple of q that makes it non-negative
+    uint64_t v_lo = (uint64_t)lo + ((uint64_t)hi << 32);
+    uint64_t carry = v_lo < (uint64_t)lo ? 1 : 0;
+    int64_t v_hi = (hi >> 32) + (lo >> 63) + (int64_t)carry;
+    uint64_t x_lo = v_lo + off_lo;
+    uint64_t x_hi = (uint64_t)v_hi + off_hi + (x_lo < v_lo ? 1 : 0);
+    return barrett128(x_hi, x_lo, br);
+}
+
+template <bool A_RES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_accum_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t groups, uint32_t per_group,
+               uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages * kABox;
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + a_bytes;
+    uint8_t* sY = sB + kStages * kBStage;
+    uint64_t* bars = (uint64_t*)(sY + 8 * kYWarp);
+    uint64_t* full = bars;                    // [kStages]
+    uint64_t* empty = bars + kStages;         // [kStages]
+    uint64_t* tfull = bars + 2 * kStages;     // [2]
+    uint64_t* tempty = tfull + 2;             // [2]
+    uint64_t* afull = tempty + 2;             // [1]
+    uint32_t* tmem_slot = (uint32_t*)(afull + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t g = blockIdx.x % groups;   // output group (128 outputs)
+    const uint32_t p = blockIdx.x / groups;   // position in the group's tile walk
+    if (p >= per_group) return;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < kStages; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        mbar_init(afull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            if (A_RES) {
+                mbar_expect_tx(afull, kblocks * kABox);
+                for (uint32_t kb = 0; kb < kblocks; kb++)
+                    tma_load_2d(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+            }
+            uint32_t s = 0, ph = 0;
+            for (uint32_t t = p; t < ntiles; t += per_group) {
+                for (uint32_t kb = 0; kb < kblocks; kb++) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], kBStage + (A_RES ? 0 : kABox));
+                    uint8_t* b = sB + s * kBStage;
+                    tma_load_2d(b, &map_b, &full[s], (int32_t)(t * 256), (int32_t)(kb * kBoxK));
+                    tma_load_2d(b + kBStage / 2, &map_b, &full[s], (int32_t)(t * 256 + 128), (int32_t)(kb * kBoxK));
+                    if (!A_RES)
+                        tma_load_2d(sA + s * kABox, &map_a, &full[s], (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            if (A_RES) mbar_wait(afull, 0);
+            uint32_t s = 0, ph = 0, it = 0;
+            for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+                const uint32_t acc = it & 1, use = it >> 1;
+                mbar_wait(&tempty[acc], (use & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                for (uint32_t kb = 0; kb < kblocks; kb++) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + (A_RES ? kb : s) * kABox);
+                    const uint32_t b_base = smem_u32(sB + s * kBStage);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < kBoxK / 32; kk++) {
+                        uint64_t ad = umma_desc(a_base + kk * 32, 16, 1024);
+                        uint64_t bd = umma_desc(b_base + kk * 32 * 128, kBStage / 2, 1024);
+                        mma_i8(d_tmem, ad, bd, (kb | kk) != 0);
+                    }
+                    mma_commit(&empty[s]);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue (8 warps)
+        const uint32_t e = warp - 2;                 // 0..7
+        const uint32_t quarter = warp & 3;           // TMEM lane quarter this warp may access
+        const uint32_t half = e >> 2;                // words [16 half, 16 half + 16) of the tile
+        uint8_t* ys = sY + e * kYWarp;
+        const uint32_t row = lane;                   // output g*128 + 32*quarter + lane
+        const uint32_t words_per_limb = 1u << log_n;
+        uint32_t it = 0;
+        for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+            const uint32_t acc = it & 1, use = it >> 1;
+            const uint32_t word0 = t * 32;
+            const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
+            const Barrett br = tab.br(limb);
+            const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
+            mbar_wait(&tfull[acc], use & 1);
+            tc_fence_after();
+            // the previous TMA store from this warp's staging buffer must have finished reading it
+            if (lane == 0) tma_store_wait_read0();
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t c = 0; c < 4; c++) {   // 4 chunks of 4 words (32 TMEM columns)
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * 256 + half * 128 + c * 32;
+                TMEM_LD_X32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (uint32_t wv = 0; wv < 4; wv += 2) {
+                    uint64_t v0 = combine_word(r + 8 * wv, br, olo, ohi);
+                    uint64_t v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
+                    const uint32_t wl = c * 4 + wv;             // word within this warp's 16 (even)
+                    const uint32_t chunk = (wl >> 1) ^ (row & 7);  // SWIZZLE_128B: 16-byte chunk XOR row
+                    uint64_t* dst = (uint64_t*)(ys + row * 128 + chunk * 16);
+                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(dst)), "l"(v0), "l"(v1) : "memory");
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&map_y, ys, (int32_t)(word0 + half * 16), (int32_t)(g * 128 + quarter * 32));
+                tma_store_commit();
+            }
+        }
+        if (lane == 0) tma_store_wait0();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------------------------- host side
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+bool tc_supported(const ensi_ctx* ctx, uint32_t level) {
+    (void)level;
+    if (ctx->n < 32) return false;
+    int dev = ctx->device, major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) return false;   // built for sm_100a only
+    for (uint32_t i = 0; i < ctx->L; i++)
+        if (ctx->mod[i] >= (1ull << 60)) return false;
+    return get_encode() != nullptr;
+}
+
+static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
+    if (w->d_wt8) return ENSI_OK;
+    const uint32_t mpad = (w->m + 127) / 128 * 128, dpad = (w->d + 127) / 128 * 128;
+    std::vector<int8_t> wt((size_t)mpad * dpad, 0);
+    for (uint32_t j = 0; j < w->d; j++)
+        for (uint32_t i = 0; i < w->m; i++) wt[(size_t)i * dpad + j] = w->host[(size_t)j * w->m + i];
+    cudaError_t e = cudaMalloc(&w->d_wt8, wt.size());
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_wt8, wt.data(), wt.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "W^T upload");
+    w->wt_mpad = mpad;
+    w->wt_dpad = dpad;
+    return ENSI_OK;
+}
+
+int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
+                     cudaStream_t st, uint64_t ctw, uint32_t limb0) {
+    if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
+    if (ctw % 32) return set_err(ctx, ENSI_EINVAL, "ciphertext too small for the tensor-core tile");
+    if (d != w->d) return set_err(ctx, ENSI_EDIM, "d mismatch");
+    int rc = build_wt8(ctx, w);
+    if (rc) return rc;
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return set_err(ctx, ENSI_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap ma, mb, my;
+    {   // A = W^T int8 [mpad][dpad], box 128 (K) x 128 (M)
+        cuuint64_t dims[2] = {w->wt_dpad, w->wt_mpad};
+        cuuint64_t strides[1] = {w->wt_dpad};
+        cuuint32_t box[2] = {128, 128}, es[2] = {1, 1};
+        if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)w->d_wt8, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return set_err(ctx, ENSI_ECUDA, "tensor map A");
+    }
+    {   // B = raw ciphertext bytes [d][ctw*8], box 128 bytes x 128 rows
+        cuuint64_t dims[2] = {ctw * 8, d};
+        cuuint64_t strides[1] = {ctw * 8};
+        cuuint32_t box[2] = {128, 128}, es[2] = {1, 1};
+        if (enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return set_err(ctx, ENSI_ECUDA, "tensor map B");
+    }
+    {   // Y = uint64 [m][ctw], box 16 words x 32 rows
+        cuuint64_t dims[2] = {ctw, w->m};
+        cuuint64_t strides[1] = {ctw * 8};
+        cuuint32_t box[2] = {16, 32}, es[2] = {1, 1};
+        if (enc(&my, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)y, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return set_err(ctx, ENSI_ECUDA, "tensor map Y");
+    }
+    tc::EpiConst ec{};
+    for (uint32_t i = 0; i < ctx->L; i++) {
+        // off = q * ceil(2^80 / q) as 128-bit
+        typedef unsigned __int128 u128;
+        const u128 q = ctx->mod[i];
+        const u128 two80 = ((u128)1) << 80;
+        const u128 off = ((two80 + q - 1) / q) * q;
+        ec.off_lo[i] = (uint64_t)off;
+        ec.off_hi[i] = (uint64_t)(off >> 64);
+    }
+    const uint32_t kblocks = w->wt_dpad / 128;
+    const uint32_t groups = w->wt_mpad / 128;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    uint32_t per_group = std::max<uint32_t>(1, (uint32_t)sms / groups);
+    const uint32_t ntiles = (uint32_t)(ctw / 32);
+    per_group = std::min(per_group, ntiles);
+    const bool ares = (size_t)kblocks * tc::kABox <= tc::kAResMax;
+    const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages * tc::kABox;
+    const size_t smem = 1024 + a_bytes + tc::kStages * tc::kBStage + 8 * tc::kYWarp + 256;
+    const uint32_t grid = groups * per_group;
+    cudaError_t e;
+    if (ares) {
+        e = cudaFuncSetAttribute(tc::k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            tc::k_accum_tc<true><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, groups, per_group, ntiles,
+                                                                   ctx->log_n, level, limb0, ctx->tab, ec);
+    } else {
+        e = cudaFuncSetAttribute(tc::k_accum_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            tc::k_accum_tc<false><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, groups, per_group, ntiles,
+                                                                    ctx->log_n, level, limb0, ctx->tab, ec);
+    }
+    ENSI_LAUNCH_CHECK(ctx);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc launch");
 }
 
 }  // namespace ensi

@@ -196,6 +196,14 @@ const char* ensi_last_error(const ensi_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 uint64_t ensi_launch_count(const ensi_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+uint32_t ensi_pcmm_kernel(const ensi_ctx* ctx, uint32_t level, uint32_t requested) {
+    if (!ctx) return 0;
+    const bool tc = tc_supported(ctx, level);
+    if (requested == 1) return 1;
+    if (requested == 2) return tc ? 2 : 0;
+    return tc ? 2 : 1;
+}
+
 int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
     if (!out) return ENSI_EINVAL;
     *out = nullptr;

@@ -59,8 +59,8 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
             }
         }
     }
-    // moddown: phinv [A][2], ph [level][A][2], Pinv [level][2]
-    std::vector<uint64_t> md((size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2, 0);
+    // moddown: phinv [A][2], ph [level][A][2], Pinv [level][2], p_k mod q_i [level][A]
+    std::vector<uint64_t> md((size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)level * A, 0);
     for (uint32_t k = 0; k < A; k++) {
         uint64_t p = ctx->mod[L + k], ph = 1;
         for (uint32_t b = 0; b < A; b++)
@@ -84,6 +84,8 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
         size_t idx = (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
         md[idx] = pinv;
         md[idx + 1] = shoup_h(pinv, q);
+        for (uint32_t k = 0; k < A; k++)
+            md[(size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)i * A + k] = ctx->mod[L + k] % q;
     }
     cudaError_t e1 = cudaMalloc(&ct.d_modup, mu.size() * 8);
     if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables malloc");
@@ -155,8 +157,8 @@ __global__ void __launch_bounds__(kT) k_kip(const uint64_t* __restrict__ ext, co
     acc[(((size_t)gi * 2 + j) * E + e) * n + k] = barrett128(s.hi, s.lo, br);
 }
 
-// ModDown conversion: z[gi][j][i][k] = sum_k' [pc_k' (P/p_k')^-1]_{p_k'} [P/p_k']_{q_i}  (mod q_i), where
-// pc = INTT'ed P limbs of acc.
+// ModDown conversion: z[gi][j][i][k] = sum_k' y_k' [P/p_k']_{q_i}  (mod q_i), y_k' = [pc_k' (P/p_k')^-1]_{p_k'}
+// taken centred in (-p/2, p/2] (R10: zero-mean conversion overflow), pc = INTT'ed P limbs of acc.
 __global__ void __launch_bounds__(kT) k_moddown_convert(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
                                                         uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
                                                         ModTab tab, const uint64_t* __restrict__ cm) {
@@ -167,12 +169,17 @@ __global__ void __launch_bounds__(kT) k_moddown_convert(const uint64_t* __restri
     const uint64_t* ph = cm + (size_t)A * 2 + (size_t)i * A * 2;
     const uint64_t q = tab.q[i];
     const uint64_t* pc = acc + ((size_t)gj * E + level) * n;
+    const uint64_t* pmodq = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)i * A;
+    const Barrett bq = tab.br(i);
     uint64_t sum = 0;
     for (uint32_t a = 0; a < A; a++) {
-        uint64_t y = mul_shoup(pc[(size_t)a * n + k], phinv[2 * a], phinv[2 * a + 1], tab.q[L + a]);
-        sum += mul_shoup_lazy(y, ph[2 * a], ph[2 * a + 1], q);
+        const uint64_t p = tab.q[L + a];
+        uint64_t y = mul_shoup(pc[(size_t)a * n + k], phinv[2 * a], phinv[2 * a + 1], p);
+        uint64_t yq = reduce64(y, bq);
+        if (y > (p >> 1)) yq = sub_mod(yq, pmodq[a], q);
+        sum += mul_shoup_lazy(yq, ph[2 * a], ph[2 * a + 1], q);
     }
-    z[((size_t)gj * level + i) * n + k] = reduce64(sum, tab.br(i));
+    z[((size_t)gj * level + i) * n + k] = reduce64(sum, bq);
 }
 
 // out[gi][j][i][k] = (acc_q_i - z) * P^-1 (+ c0[i][src_g(k)] when j == 0)

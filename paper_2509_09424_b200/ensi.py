@@ -28,7 +28,7 @@ KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05 = 0, 1, 2
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rescale", "ensi_decrypt_debug",
-           "ensi_launch_count"]
+           "ensi_launch_count", "ensi_pcmm_kernel"]
 
 
 class EnsiError(RuntimeError):
@@ -88,6 +88,8 @@ def lib():
         L.ensi_decrypt_debug.argtypes = [vp, C.POINTER(CtView), u32, vp, vp]
         L.ensi_launch_count.argtypes = [vp]
         L.ensi_launch_count.restype = u64
+        L.ensi_pcmm_kernel.argtypes = [vp, u32, u32]
+        L.ensi_pcmm_kernel.restype = u32
         _LIB = L
     return _LIB
 
@@ -169,6 +171,10 @@ class Context:
         if rc != 0:
             msg = lib().ensi_last_error(self.h)
             raise EnsiError(rc, msg.decode() if msg else "")
+
+    def kernel_name(self, requested: int, level: int) -> str:
+        k = int(lib().ensi_pcmm_kernel(self.h, level, requested))
+        return {1: "cuda-core", 2: "tcgen05"}.get(k, "unavailable")
 
     def launch_count(self) -> int:
         return int(lib().ensi_launch_count(self.h))

@@ -72,7 +72,7 @@ def _enc_cols(o, pk, X, level, seed):
     return o.encrypt_batch(np.arange(d, dtype=np.uint64) + np.uint64(seed), pk, level, m_res)
 
 
-@pytest.mark.parametrize("kernel", [1, 0])
+@pytest.mark.parametrize("kernel", [1, 2])
 def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel):
     """C1: 16x16 BitNet layer on real pk-encryptions; every word == oracle; decrypt == X.W within 1e-4."""
     o, sk, pk, ctx = setup_c1
@@ -95,8 +95,9 @@ def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel
         assert np.max(np.abs(z - zo)) < 1e-9
 
 
-@pytest.mark.parametrize("d,m,level", [(37, 70, 3), (1, 1, 1), (64, 64, 2), (130, 3, 3), (5, 129, 1)])
-def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level):
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("d,m,level", [(37, 70, 3), (1, 1, 1), (64, 64, 2), (130, 3, 3), (5, 129, 1), (900, 200, 1)])
+def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level, kernel):
     """Ragged d (pipeline tail) and m (partial 64-output tile), random words incl. 0 and q-1."""
     o, sk, pk, ctx = setup_c1
     torch = torch_cuda
@@ -108,13 +109,33 @@ def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level):
     xd = dev(torch, x)
     yd = torch.empty((m, 2, level, o.n), dtype=torch.int64, device="cuda")
     w = ctx.weights(W)
-    ctx.pcmm_ternary(xd, w, yd, level=level)
+    ctx.pcmm_ternary(xd, w, yd, level=level, kernel=kernel)
     torch.cuda.synchronize()
     assert (host(yd) == want).all()
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_pcmm_host_staged_pipeline(setup_c1, torch_cuda, kernel):
+    """ensi_pcmm_ternary_host (pinned host in/out, slice-pipelined) == oracle, every word."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    d, m = 40, 70
+    x = synth.gen_words(4242, o.q, d, 3, o.n)
+    W = synth.gen_W(4243, d, m)
+    want = o.pcmm_a(x, W, nthreads=4)
+    xh = torch.from_numpy(x.view(np.int64)).pin_memory()
+    yh = torch.zeros((m, 2, 3, o.n), dtype=torch.int64).pin_memory()
+    w = ctx.weights(W)
+    for _ in range(2):
+        ctx.pcmm_ternary_host(xh.numpy(), w, yh.numpy(), level=3, kernel=kernel)
+        torch.cuda.synchronize()
+        assert (yh.numpy().view(np.uint64) == want).all()
+        yh.zero_()
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("kind", ["zero", "identity", "neg_identity", "permutation", "plus", "minus", "toy"])
-def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind):
+def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind, kernel):
     o, sk, pk, ctx = setup_c1
     torch = torch_cuda
     d = m = 4 if kind == "toy" else 96
@@ -128,12 +149,13 @@ def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind):
     want = o.pcmm_a(x, W, nthreads=4)
     xd = dev(torch, x)
     yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
-    ctx.pcmm_ternary(xd, W, yd, level=3)
+    ctx.pcmm_ternary(xd, W, yd, level=3, kernel=kernel)
     torch.cuda.synchronize()
     assert (host(yd) == want).all()
 
 
-def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda, kernel):
     """d = 8300 > 8184 (intermediate reduction) with every word q-1 and W all +1 / -1 / mixed."""
     o, sk, pk, ctx = setup_c1
     torch = torch_cuda
@@ -144,7 +166,7 @@ def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda):
     W[::3, 2] = -1
     xd = dev(torch, x)
     yd = torch.empty((m, 2, level, o.n), dtype=torch.int64, device="cuda")
-    ctx.pcmm_ternary(xd, W, yd, level=level)
+    ctx.pcmm_ternary(xd, W, yd, level=level, kernel=kernel)
     torch.cuda.synchronize()
     got = host(yd)
     q = o.q[0]

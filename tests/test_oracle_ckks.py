@@ -273,7 +273,8 @@ def test_modup_crt_identity():
 
 
 def test_moddown_exact_identity():
-    """ModDown(acc) * P + v == acc over Q_l, where v is the fast-converted P-residue (< alpha * P)."""
+    """ModDown(acc) * P + v == acc over Q_l, where v = [acc]_P + u P is the fast-converted (centred, R10)
+    P-residue with a small integer overflow u, |u| <= alpha."""
     o = _tiny_ks_ctx()
     level = 3
     rs = np.random.default_rng(10)
@@ -288,7 +289,8 @@ def test_moddown_exact_identity():
         q = o.q[i]
         for k in range(o.n):
             # v = xp + u P for some u in [0, alpha): out*P + v == acc (mod q)
-            ok = any((int(out_c[i, k]) * P + xp[k] + u * P - int(acc_c[i, k])) % q == 0 for u in range(o.alpha))
+            ok = any((int(out_c[i, k]) * P + xp[k] + u * P - int(acc_c[i, k])) % q == 0
+                     for u in range(-o.alpha, o.alpha + 1))
             assert ok
 
 
@@ -316,6 +318,20 @@ def test_rotation_decrypts_to_cyclic_shift(c1):
         gi = o.galois(-r)
         back = o.rotate(rot, gi, o.rotkey(200 + r, gi, sk))
         assert np.max(np.abs(o.decrypt(sk, back, DELTA) - z)) < 1e-5
+
+
+def test_rotation_noise_has_no_slot0_spike():
+    """R10: ModDown converts centred P-residues, so the conversion overflow is zero-mean and the v*s term does
+    not pile up in the lowest-frequency slot.  Rotation noise stays at the fresh-encryption level (N'=2^14)."""
+    o = oracle.Oracle(14, 12, 4, 3)
+    skc, sk, pk = o.keygen(5)
+    ct = o.encrypt(5, pk, 12, o.encode(np.zeros(o.n // 2), 12, DELTA))
+    fresh = np.max(np.abs(o.decrypt(sk, ct, DELTA)))
+    g = o.galois(1)
+    rot = o.rotate(ct, g, o.rotkey(777, g, sk))
+    err = np.abs(o.decrypt(sk, rot, DELTA))
+    assert err.max() < 2 * fresh
+    assert err[0] < 5 * np.median(err) + fresh
 
 
 def test_hoisted_equals_single_rotations(c1):

@@ -278,7 +278,7 @@ def main():
     gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
     # ALU roofline of the CUDA-core accumulate: one 64-bit modular add per term-word = 2 ALU-pipe ops
     # (IADD3 + IADD3.X); ALU pipe = 64 lanes/clk/SM (B300_MICROARCH: rt_SMSP = 2) x 148 SMs x max clock.
-    if kernel_name == "tcgen05":
+    if kernel_name.startswith("tcgen05"):
         # byte-sliced INT8 GEMM: D[i][8w+b] over all 8 bytes of every word, K = d (padded to 128), M = m (padded
         # to 128).  INT8 dense peak = measured bf16 (burst) x nominal ratio 4.5/2.25 = 2.
         dpad, mpad = -(-d // 128) * 128, -(-m // 128) * 128

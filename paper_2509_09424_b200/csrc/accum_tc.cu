@@ -289,6 +289,220 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ================================================================================================================
+// 2-CTA variant (cta_group::2, cluster of 2 on a TPC).  The pair computes M = 256 outputs x N = 256 bytes per tile:
+// CTA r holds W^T rows [128 r, 128 r + 128) of the pair's 256 outputs (resident A) and the N-half [128 r, 128 r + 128)
+// of every X byte tile, so each SM pulls half as many X bytes per MMA cycle as the 1-CTA kernel, and the freed
+// shared memory deepens the TMA ring to 6 stages.  The leader (rank 0) issues the MMAs; both CTAs' TMA loads
+// complete on the leader's barriers, the MMA commits multicast to both CTAs' barriers, and the epilogues
+// (one per CTA, on its own TMEM lanes) release the accumulator through the leader's tempty barrier.
+// ================================================================================================================
+
+static constexpr uint32_t kStages2 = 6;
+static constexpr uint32_t kBStage2 = 128 * 128;         // 16 KB: 128 K rows x this CTA's 128-byte N half
+static constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (0u << 10) | (0u << 15) | (1u << 16) |
+                                    ((256u >> 3) << 17) | ((256u >> 4) << 24);   // M = 256, N = 256
+static constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8, %9, %10, %11, %12}, p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u), "r"(0u), "r"(0u),
+        "r"(0u), "r"(0u));
+}
+__device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+template <bool A_RES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
+                uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages2 * kABox;
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + a_bytes;
+    uint8_t* sY = sB + kStages2 * kBStage2;
+    uint64_t* bars = (uint64_t*)(sY + 8 * kYWarp);
+    uint64_t* full = bars;                     // [kStages2]  (leader's are the live ones)
+    uint64_t* empty = bars + kStages2;         // [kStages2]  (per CTA, multicast commits)
+    uint64_t* tfull = bars + 2 * kStages2;     // [2]         (per CTA, multicast commits)
+    uint64_t* tempty = tfull + 2;              // [2]         (leader's: 16 arrivals)
+    uint64_t* afull = tempty + 2;              // [1]         (leader's)
+    uint32_t* tmem_slot = (uint32_t*)(afull + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1;
+    const uint32_t pg = pair % pgroups;        // pair group: outputs [256 pg, 256 pg + 256)
+    const uint32_t p = pair / pgroups;
+    const uint32_t g = pg * 2 + rank;          // this CTA's 128-output group
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < kStages2; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; a++) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 16);
+        }
+        mbar_init(afull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            if (A_RES) {
+                if (rank == 0) mbar_expect_tx(afull, 2 * kblocks * kABox);
+                for (uint32_t kb = 0; kb < kblocks; kb++)
+                    tma_load_2d_2sm(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+            }
+            uint32_t s = 0, ph = 0;
+            for (uint32_t t = p; t < ntiles; t += per_group) {
+                for (uint32_t kb = 0; kb < kblocks; kb++) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * (kBStage2 + (A_RES ? 0 : kABox)));
+                    tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)(t * 256 + rank * 128),
+                                    (int32_t)(kb * kBoxK));
+                    if (!A_RES)
+                        tma_load_2d_2sm(sA + s * kABox, &map_a, &full[s], (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+                    if (++s == kStages2) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------------ MMA issuer (leader CTA only)
+        if (rank == 0 && lane == 0) {
+            if (A_RES) mbar_wait(afull, 0);
+            uint32_t s = 0, ph = 0, it = 0;
+            for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+                const uint32_t acc = it & 1, use = it >> 1;
+                mbar_wait(&tempty[acc], (use & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * 256;
+                for (uint32_t kb = 0; kb < kblocks; kb++) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + (A_RES ? kb : s) * kABox);
+                    const uint32_t b_base = smem_u32(sB + s * kBStage2);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < kBoxK / 32; kk++) {
+                        uint64_t ad = umma_desc(a_base + kk * 32, 16, 1024);
+                        uint64_t bd = umma_desc(b_base + kk * 32 * 128, kBStage2, 1024);
+                        mma_i8_2sm(d_tmem, ad, bd, (kb | kk) != 0);
+                    }
+                    mma_commit_2sm_mc(&empty[s]);
+                    if (++s == kStages2) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                mma_commit_2sm_mc(&tfull[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue (8 warps per CTA)
+        const uint32_t e = warp - 2;
+        const uint32_t quarter = warp & 3;
+        const uint32_t half = e >> 2;
+        uint8_t* ys = sY + e * kYWarp;
+        const uint32_t row = lane;
+        const uint32_t words_per_limb = 1u << log_n;
+        const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+        uint32_t it = 0;
+        for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+            const uint32_t acc = it & 1, use = it >> 1;
+            const uint32_t word0 = t * 32;
+            const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
+            const Barrett br = tab.br(limb);
+            const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
+            mbar_wait(&tfull[acc], use & 1);
+            tc_fence_after();
+            if (lane == 0) tma_store_wait_read0();
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t c = 0; c < 4; c++) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * 256 + half * 128 + c * 32;
+                TMEM_LD_X32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (uint32_t wv = 0; wv < 4; wv += 2) {
+                    uint64_t v0 = combine_word(r + 8 * wv, br, olo, ohi);
+                    uint64_t v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
+                    const uint32_t wl = c * 4 + wv;
+                    const uint32_t chunk = (wl >> 1) ^ (row & 7);
+                    uint64_t* dst = (uint64_t*)(ys + row * 128 + chunk * 16);
+                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(dst)), "l"(v0), "l"(v1) : "memory");
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&map_y, ys, (int32_t)(word0 + half * 16), (int32_t)(g * 128 + quarter * 32));
+                tma_store_commit();
+            }
+        }
+        if (lane == 0) tma_store_wait0();
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
 }  // namespace tc
 
 // ---------------------------------------------------------------------------------------------- host side
@@ -323,7 +537,7 @@ bool tc_supported(const ensi_ctx* ctx, uint32_t level) {
 
 static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
     if (w->d_wt8) return ENSI_OK;
-    const uint32_t mpad = (w->m + 127) / 128 * 128, dpad = (w->d + 127) / 128 * 128;
+    const uint32_t mpad = (w->m + 255) / 256 * 256, dpad = (w->d + 127) / 128 * 128;
     std::vector<int8_t> wt((size_t)mpad * dpad, 0);
     for (uint32_t j = 0; j < w->d; j++)
         for (uint32_t i = 0; i < w->m; i++) wt[(size_t)i * dpad + j] = w->host[(size_t)j * w->m + i];
@@ -336,7 +550,7 @@ static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
 }
 
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
-                     cudaStream_t st, uint64_t ctw, uint32_t limb0) {
+                     cudaStream_t st, uint64_t ctw, uint32_t limb0, bool one_cta) {
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
     if (ctw % 32) return set_err(ctx, ENSI_EINVAL, "ciphertext too small for the tensor-core tile");
     if (d != w->d) return set_err(ctx, ENSI_EDIM, "d mismatch");
@@ -383,17 +597,40 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         ec.off_hi[i] = (uint64_t)(off >> 64);
     }
     const uint32_t kblocks = w->wt_dpad / 128;
-    const uint32_t groups = w->wt_mpad / 128;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    uint32_t per_group = std::max<uint32_t>(1, (uint32_t)sms / groups);
     const uint32_t ntiles = (uint32_t)(ctw / 32);
-    per_group = std::min(per_group, ntiles);
     const bool ares = (size_t)kblocks * tc::kABox <= tc::kAResMax;
+    cudaError_t e;
+    if (!one_cta) {
+        // 2-CTA pairs: pair group pg covers outputs [256 pg, 256 pg + 256)
+        const uint32_t pgroups = w->wt_mpad / 256;
+        uint32_t per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
+        per_group = std::min(per_group, ntiles);
+        const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
+        const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
+        const uint32_t grid = 2 * pgroups * per_group;
+        if (ares) {
+            e = cudaFuncSetAttribute(tc::k_accum_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess)
+                tc::k_accum_tc2<true><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, pgroups, per_group,
+                                                                        ntiles, ctx->log_n, level, limb0, ctx->tab, ec);
+        } else {
+            e = cudaFuncSetAttribute(tc::k_accum_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess)
+                tc::k_accum_tc2<false><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, pgroups, per_group,
+                                                                         ntiles, ctx->log_n, level, limb0, ctx->tab, ec);
+        }
+        ENSI_LAUNCH_CHECK(ctx);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");
+    }
+    const uint32_t groups = (w->m + 127) / 128;
+    uint32_t per_group = std::max<uint32_t>(1, (uint32_t)sms / groups);
+    per_group = std::min(per_group, ntiles);
     const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages * tc::kABox;
     const size_t smem = 1024 + a_bytes + tc::kStages * tc::kBStage + 8 * tc::kYWarp + 256;
     const uint32_t grid = groups * per_group;
-    cudaError_t e;
     if (ares) {
         e = cudaFuncSetAttribute(tc::k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)

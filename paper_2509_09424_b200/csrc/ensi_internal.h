@@ -118,8 +118,9 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
 // (limb0 + w / N') % level.  A staged chunk holding one limb r of every ct passes ctw = N', limb0 = r.
 int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
                   uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
+// one_cta: the 1-CTA (cta_group::1) kernel; default is the 2-CTA pair kernel (cta_group::2)
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
-                     cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
+                     cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0, bool one_cta = false);
 bool tc_supported(const ensi_ctx* ctx, uint32_t level);
 
 // key switching (keyswitch.cu)

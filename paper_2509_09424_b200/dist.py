@@ -1,0 +1,61 @@
+"""Multi-GPU driver for the ternary PCMM.
+
+One process per GPU, `torch.distributed` over NCCL.  Two shardings:
+
+* Token blocks (no collective): a layer whose activation spans several ciphertext "token blocks" (more tokens
+  than N'/2 slots, or several sequences) is a set of independent problems -- each rank runs Algorithm 1 on its
+  own blocks with the same W.  `token_blocks(n_blocks, world, rank)` gives the contiguous block range.
+* Output columns (the north star's layout): inputs X~ replicated, rank r owns output columns
+  [r*S, (r+1)*S) with S = ceil(m / world) (the last shard zero-padded), computes them with its slice of W,
+  and one `all_gather_into_tensor` over NCCL assembles the m output ciphertexts on every rank.
+
+The compute step is a callable `pcmm(x, W_slice, y_local)`; the product passes the CUDA path
+(`Context.pcmm_ternary`), the CPU tests pass a reference to exercise the shard/gather logic with `gloo`.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+
+def token_blocks(n_blocks: int, world: int, rank: int) -> range:
+    """Contiguous, balanced split of n_blocks independent token blocks."""
+    base, extra = divmod(n_blocks, world)
+    lo = rank * base + min(rank, extra)
+    return range(lo, lo + base + (1 if rank < extra else 0))
+
+
+def column_shard(m: int, world: int, rank: int):
+    """(lo, hi, S): rank owns output columns [lo, hi) of an m-column layer; S = ceil(m/world) is the padded shard."""
+    S = -(-m // world)
+    lo = min(m, rank * S)
+    hi = min(m, lo + S)
+    return lo, hi, S
+
+
+class ColumnShardedPCMM:
+    """y = X (x) W with W's output columns sharded across ranks, then one all-gather of the result ciphertexts."""
+
+    def __init__(self, W: np.ndarray, world: int, rank: int, make_weights: Callable = None):
+        self.d, self.m = W.shape
+        self.world, self.rank = world, rank
+        self.lo, self.hi, self.S = column_shard(self.m, world, rank)
+        Ws = np.zeros((self.d, self.S), np.int8)       # zero columns pad the last shard (outputs are (0,0))
+        Ws[:, : self.hi - self.lo] = W[:, self.lo:self.hi]
+        self.W_local = make_weights(Ws) if make_weights else Ws
+
+    def local_buffer(self, torch, ct_shape, device):
+        return torch.empty((self.S,) + tuple(ct_shape), dtype=torch.int64, device=device)
+
+    def gathered_buffer(self, torch, ct_shape, device):
+        return torch.empty((self.S * self.world,) + tuple(ct_shape), dtype=torch.int64, device=device)
+
+    def __call__(self, pcmm: Callable, x, y_local, y_all=None, group=None, async_op: bool = False):
+        """Run this rank's shard into y_local [S][2][l][N'], then all-gather into y_all [S*world][...]
+        (rows >= m are padding).  Returns the collective work handle when async_op."""
+        pcmm(x, self.W_local, y_local)
+        if y_all is None:
+            return None
+        import torch.distributed as dist
+        return dist.all_gather_into_tensor(y_all, y_local, group=group, async_op=async_op)

@@ -1,0 +1,76 @@
+"""World-size-2 `gloo` tests of the multi-GPU shard/gather logic on CPU (no GPU here).  The "kernel" is the
+oracle's Algorithm 1 (test infrastructure), so the gathered result must equal the single-process oracle
+output word for word."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2509_09424_b200.dist import ColumnShardedPCMM, column_shard, token_blocks
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_arithmetic():
+    for m in (1, 7, 768, 5504, 6144):
+        for w in (1, 2, 3, 4, 8):
+            covered = []
+            for r in range(w):
+                lo, hi, S = column_shard(m, w, r)
+                assert hi - lo <= S and S * w >= m
+                covered += list(range(lo, hi))
+            assert covered == list(range(m))
+            blocks = [b for r in range(w) for b in token_blocks(m, w, r)]
+            assert blocks == list(range(m))
+
+
+def _worker(rank, world, port, d, m, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import oracle
+    import synth
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = oracle.Oracle(12, 2, 1, 2)
+    x = synth.gen_words(55, o.q, d, 1, o.n)                     # replicated inputs (same seed on every rank)
+    W = synth.gen_W(56, d, m)
+    sh = ColumnShardedPCMM(W, world, rank)
+
+    def pcmm(xa, Wl, y_local):                                    # oracle as the kernel (test only)
+        y_local.copy_(torch.from_numpy(o.pcmm_a(xa, Wl).view(np.int64)))
+
+    y_local = sh.local_buffer(torch, (2, 1, o.n), "cpu")
+    y_all = sh.gathered_buffer(torch, (2, 1, o.n), "cpu")
+    sh(pcmm, x, y_local, y_all)
+    if rank == 0:
+        out_q.put(y_all[:m].numpy().view(np.uint64).copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,m", [(8, 6), (5, 9)])
+def test_column_sharded_allgather_equals_single_process(d, m):
+    import oracle
+    import synth
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    o = oracle.Oracle(12, 2, 1, 2)
+    want = o.pcmm_a(synth.gen_words(55, o.q, d, 1, o.n), synth.gen_W(56, d, m))
+    assert (got == want).all()

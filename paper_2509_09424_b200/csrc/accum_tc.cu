@@ -338,16 +338,30 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint
         "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u), "r"(0u), "r"(0u),
         "r"(0u), "r"(0u));
 }
-__device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"((uint16_t)0x3)
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* map, uint64_t* bar, uint16_t mask,
+                                                   int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar) & kPeerMask), "h"(mask), "r"(c0), "r"(c1)
         : "memory");
 }
 
-template <bool A_RES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// MC = false: clusters of one pair (2 CTAs), each pair loads its own X tiles; the pairs of the pgroups output
+//             groups that share a word tile meet only in L2.
+// MC = true:  clusters of npairs = pgroups pairs (2*npairs <= 8 CTAs).  The npairs pairs cover all outputs of the
+//             same word tile in lockstep; every X sub-box (32 K-rows x 128 bytes) is loaded once by one pair and
+//             multicast to the same N-half of every pair, so each X byte leaves L2/HBM once per layer.  The stage
+//             ring is released only when all npairs MMA issuers have consumed it (empty count = npairs).
+template <bool A_RES, bool MC>
+__global__ void __launch_bounds__(kThreads, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
                 uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec) {
@@ -366,16 +380,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = (uint32_t*)(afull + 1);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
+    const uint32_t crank = cluster_rank();
+    const uint32_t rank = crank & 1;           // rank inside the CTA pair (0 = leader, issues the MMAs)
+    const uint32_t lead = crank & ~1u;         // cluster rank of this pair's leader
     const uint32_t pair = blockIdx.x >> 1;
     const uint32_t pg = pair % pgroups;        // pair group: outputs [256 pg, 256 pg + 256)
     const uint32_t p = pair / pgroups;
     const uint32_t g = pg * 2 + rank;          // this CTA's 128-output group
+    const uint16_t pair_mask = (uint16_t)(0x3u << lead);
+    const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * pgroups)) - 1) : pair_mask;
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < kStages2; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC ? pgroups : 1);
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(&tfull[a], 1);
@@ -406,8 +424,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (uint32_t kb = 0; kb < kblocks; kb++) {
                     mbar_wait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[s], 2 * (kBStage2 + (A_RES ? 0 : kABox)));
-                    tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)(t * 256 + rank * 128),
-                                    (int32_t)(kb * kBoxK));
+                    if (MC) {
+                        // sub-box j (32 K-rows) of this N-half: issued by pair j % pgroups, multicast to the
+                        // same N-half (cluster ranks rank, rank + 2, ...) of every pair
+                        const uint16_t half_mask = (uint16_t)(all_mask & (rank ? 0xAAAAu : 0x5555u));
+                        for (uint32_t j = pg; j < kBoxK / 32; j += pgroups)
+                            tma_load_2d_2sm_mc(sB + s * kBStage2 + j * 4096, &map_b, &full[s], half_mask,
+                                               (int32_t)(t * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
+                    } else {
+                        tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)(t * 256 + rank * 128),
+                                        (int32_t)(kb * kBoxK));
+                    }
                     if (!A_RES)
                         tma_load_2d_2sm(sA + s * kABox, &map_a, &full[s], (int32_t)(kb * kBoxK), (int32_t)(g * 128));
                     if (++s == kStages2) {
@@ -438,13 +465,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         uint64_t bd = umma_desc(b_base + kk * 32 * 128, kBStage2, 1024);
                         mma_i8_2sm(d_tmem, ad, bd, (kb | kk) != 0);
                     }
-                    mma_commit_2sm_mc(&empty[s]);
+                    mma_commit_2sm_mc(&empty[s], all_mask);
                     if (++s == kStages2) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                mma_commit_2sm_mc(&tfull[acc]);
+                mma_commit_2sm_mc(&tfull[acc], pair_mask);
             }
         }
     } else {
@@ -455,7 +482,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint8_t* ys = sY + e * kYWarp;
         const uint32_t row = lane;
         const uint32_t words_per_limb = 1u << log_n;
-        const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), lead);
         uint32_t it = 0;
         for (uint32_t t = p; t < ntiles; t += per_group, it++) {
             const uint32_t acc = it & 1, use = it >> 1;
@@ -550,7 +577,7 @@ static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
 }
 
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
-                     cudaStream_t st, uint64_t ctw, uint32_t limb0, bool one_cta) {
+                     cudaStream_t st, uint64_t ctw, uint32_t limb0, int variant) {
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
     if (ctw % 32) return set_err(ctx, ENSI_EINVAL, "ciphertext too small for the tensor-core tile");
     if (d != w->d) return set_err(ctx, ENSI_EDIM, "d mismatch");
@@ -568,10 +595,13 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map A");
     }
-    {   // B = raw ciphertext bytes [d][ctw*8], box 128 bytes x 128 rows
+    const uint32_t pgroups = w->wt_mpad / 256;
+    if (variant == TC_AUTO) variant = (2 * pgroups <= 8) ? TC_PAIR_MC : TC_PAIR;
+    if (variant == TC_PAIR_MC && 2 * pgroups > 8) variant = TC_PAIR;
+    {   // B = raw ciphertext bytes [d][ctw*8], box 128 bytes x 128 rows (x 32 rows: multicast sub-boxes)
         cuuint64_t dims[2] = {ctw * 8, d};
         cuuint64_t strides[1] = {ctw * 8};
-        cuuint32_t box[2] = {128, 128}, es[2] = {1, 1};
+        cuuint32_t box[2] = {128, variant == TC_PAIR_MC ? 32u : 128u}, es[2] = {1, 1};
         if (enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -602,25 +632,46 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
     const uint32_t ntiles = (uint32_t)(ctw / 32);
     const bool ares = (size_t)kblocks * tc::kABox <= tc::kAResMax;
     cudaError_t e;
-    if (!one_cta) {
-        // 2-CTA pairs: pair group pg covers outputs [256 pg, 256 pg + 256)
-        const uint32_t pgroups = w->wt_mpad / 256;
-        uint32_t per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
-        per_group = std::min(per_group, ntiles);
+    if (variant != TC_ONE_CTA) {
+        // CTA pairs (cta_group::2): pair group pg covers outputs [256 pg, 256 pg + 256)
+        const bool mc = variant == TC_PAIR_MC;
+        const uint32_t csize = mc ? 2 * pgroups : 2;
         const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
         const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
-        const uint32_t grid = 2 * pgroups * per_group;
-        if (ares) {
-            e = cudaFuncSetAttribute(tc::k_accum_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess)
-                tc::k_accum_tc2<true><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, pgroups, per_group,
-                                                                        ntiles, ctx->log_n, level, limb0, ctx->tab, ec);
+        void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                     uint32_t, uint32_t, ModTab, tc::EpiConst);
+        if (ares) kern = mc ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<true, false>;
+        else kern = mc ? tc::k_accum_tc2<false, true> : tc::k_accum_tc2<false, false>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "accum_tc2 smem attribute");
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(tc::kThreads, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // persistent: as many clusters as can be co-resident (each cluster = pgroups/(csize/2) ... pairs)
+        uint32_t per_group;
+        if (mc) {
+            cfg.gridDim = dim3(csize * 64, 1, 1);
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg) != cudaSuccess || nclusters < 1) {
+                cudaGetLastError();
+                nclusters = std::max(1, sms / (int)csize);
+            }
+            per_group = (uint32_t)nclusters;
         } else {
-            e = cudaFuncSetAttribute(tc::k_accum_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e == cudaSuccess)
-                tc::k_accum_tc2<false><<<grid, tc::kThreads, smem, st>>>(ma, mb, my, kblocks, pgroups, per_group,
-                                                                         ntiles, ctx->log_n, level, limb0, ctx->tab, ec);
+            per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
         }
+        per_group = std::min(per_group, ntiles);
+        cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
+        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
+                               ctx->tab, ec);
         ENSI_LAUNCH_CHECK(ctx);
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");

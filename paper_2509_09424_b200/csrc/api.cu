@@ -100,6 +100,9 @@ int pack_planes(ensi_ctx* ctx, const int8_t* W, uint32_t d, uint32_t m, uint32_t
     return ENSI_OK;
 }
 
+// opts.kernel -> tensor-core variant: 0/2 best, 3 single CTA, 4 pairs without multicast
+int tc_variant(uint32_t kernel) { return kernel == 3 ? TC_ONE_CTA : kernel == 4 ? TC_PAIR : TC_AUTO; }
+
 struct LayoutBPlan {
     uint32_t k, n_in, B, G, rotations;
 };
@@ -200,7 +203,7 @@ uint32_t ensi_pcmm_kernel(const ensi_ctx* ctx, uint32_t level, uint32_t requeste
     if (!ctx) return 0;
     const bool tc = tc_supported(ctx, level);
     if (requested == 1) return 1;
-    if (requested == 2 || requested == 3) return tc ? requested : 0;
+    if (requested >= 2 && requested <= 4) return tc ? requested : 0;
     return tc ? 2 : 1;
 }
 
@@ -433,9 +436,10 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
     if (o.layout == 0) {
         if (x->count != d) return set_err(ctx, ENSI_EDIM, "Layout A: x.count must equal d");
         bool tc = (o.kernel >= 2) || (o.kernel == 0 && tc_supported(ctx, level));
+        if (o.kernel > 4) return set_err(ctx, ENSI_EINVAL, "opts.kernel must be 0..4");
         if (o.kernel >= 2 && !tc_supported(ctx, level))
             return set_err(ctx, ENSI_EINVAL, "tensor-core accumulate not available for these parameters");
-        rc = tc ? accum_ternary_tc(ctx, x->data, d, w, acc_out, level, st, 0, 0, o.kernel == 3)
+        rc = tc ? accum_ternary_tc(ctx, x->data, d, w, acc_out, level, st, 0, 0, tc_variant(o.kernel))
                 : accum_ternary(ctx, x->data, d, w->d_planes, w->mw, m, acc_out, level, st);
     } else {
         LayoutBPlan p;
@@ -557,7 +561,7 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
         cudaEventRecord(ctx->ev_h2d[b], ctx->st_h2d);
         cudaStreamWaitEvent(st, ctx->ev_h2d[b], 0);
         if (s >= 2) cudaStreamWaitEvent(st, ctx->ev_d2h[b], 0);             // y stage b drained
-        rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, kernel == 3)
+        rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, tc_variant(kernel))
                 : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
         cudaEventRecord(ctx->ev_comp[b], st);
         cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[b], 0);

@@ -118,9 +118,11 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
 // (limb0 + w / N') % level.  A staged chunk holding one limb r of every ct passes ctw = N', limb0 = r.
 int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
                   uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
-// one_cta: the 1-CTA (cta_group::1) kernel; default is the 2-CTA pair kernel (cta_group::2)
+// tensor-core variants: pairs with cluster multicast (default when 2*ceil(m/256) <= 8), pairs without
+// multicast, single CTA (cta_group::1)
+enum { TC_AUTO = 0, TC_PAIR_MC = 1, TC_PAIR = 2, TC_ONE_CTA = 3 };
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
-                     cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0, bool one_cta = false);
+                     cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0, int variant = TC_AUTO);
 bool tc_supported(const ensi_ctx* ctx, uint32_t level);
 
 // key switching (keyswitch.cu)

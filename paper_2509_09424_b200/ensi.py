@@ -22,7 +22,7 @@ ENSI_OK, ENSI_EINVAL, ENSI_EDIM, ENSI_ENOTTERNARY, ENSI_ELEVEL, ENSI_ENOKEY, ENS
 ERR_NAMES = {0: "ENSI_OK", 1: "ENSI_EINVAL", 2: "ENSI_EDIM", 3: "ENSI_ENOTTERNARY", 4: "ENSI_ELEVEL",
              5: "ENSI_ENOKEY", 6: "ENSI_ENOMEM", 7: "ENSI_ECUDA"}
 MEM_HOST, MEM_DEVICE = 0, 1
-KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA = 0, 1, 2, 3
+KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA, KERNEL_TCGEN05_PAIR = 0, 1, 2, 3, 4
 
 # every symbol include/ensi.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
@@ -174,7 +174,7 @@ class Context:
 
     def kernel_name(self, requested: int, level: int) -> str:
         k = int(lib().ensi_pcmm_kernel(self.h, level, requested))
-        return {1: "cuda-core", 2: "tcgen05-2cta", 3: "tcgen05-1cta"}.get(k, "unavailable")
+        return {1: "cuda-core", 2: "tcgen05", 3: "tcgen05-1cta", 4: "tcgen05-pair-nomc"}.get(k, "unavailable")
 
     def launch_count(self) -> int:
         return int(lib().ensi_launch_count(self.h))

@@ -38,7 +38,7 @@ def _dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
 
 
-@pytest.mark.parametrize("kernel", [2, 3, 1])
+@pytest.mark.parametrize("kernel", [2, 4, 3, 1])
 def test_c2_sampled_columns_bit_exact(c2, torch_cuda, kernel):
     """768x768 on uniform words (data-oblivious accumulate): 3 full output columns == oracle Alg. 1."""
     o, sk, pk, ctx = c2

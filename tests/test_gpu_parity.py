@@ -72,7 +72,7 @@ def _enc_cols(o, pk, X, level, seed):
     return o.encrypt_batch(np.arange(d, dtype=np.uint64) + np.uint64(seed), pk, level, m_res)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel):
     """C1: 16x16 BitNet layer on real pk-encryptions; every word == oracle; decrypt == X.W within 1e-4."""
     o, sk, pk, ctx = setup_c1
@@ -95,7 +95,7 @@ def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel
         assert np.max(np.abs(z - zo)) < 1e-9
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 @pytest.mark.parametrize("d,m,level", [(37, 70, 3), (1, 1, 1), (64, 64, 2), (130, 3, 3), (5, 129, 1), (900, 200, 1)])
 def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level, kernel):
     """Ragged d (pipeline tail) and m (partial 64-output tile), random words incl. 0 and q-1."""
@@ -114,7 +114,7 @@ def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level, kernel):
     assert (host(yd) == want).all()
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_pcmm_host_staged_pipeline(setup_c1, torch_cuda, kernel):
     """ensi_pcmm_ternary_host (pinned host in/out, slice-pipelined) == oracle, every word."""
     o, sk, pk, ctx = setup_c1
@@ -133,7 +133,7 @@ def test_pcmm_host_staged_pipeline(setup_c1, torch_cuda, kernel):
         yh.zero_()
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 @pytest.mark.parametrize("kind", ["zero", "identity", "neg_identity", "permutation", "plus", "minus", "toy"])
 def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind, kernel):
     o, sk, pk, ctx = setup_c1
@@ -154,7 +154,7 @@ def test_pcmm_a_edge_weights(setup_c1, torch_cuda, kind, kernel):
     assert (host(yd) == want).all()
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda, kernel):
     """d = 8300 > 8184 (intermediate reduction) with every word q-1 and W all +1 / -1 / mixed."""
     o, sk, pk, ctx = setup_c1

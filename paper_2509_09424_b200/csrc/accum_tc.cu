@@ -318,8 +318,12 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Release of a TMEM accumulator to the pair leader's MMA issuer.  Relaxed: the only thing ordered before it is
+// the epilogue's tcgen05.ld, already complete (tcgen05.wait::ld) and fenced (tcgen05.fence::before_thread_sync);
+// a release.cluster arrive would also drain every prior store of the thread (ERRBAR), measured at 25% of the
+// kernel's warp-stall samples.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                                 int32_t c1) {

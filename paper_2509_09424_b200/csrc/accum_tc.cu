@@ -132,6 +132,20 @@ __device__ __forceinline__ uint64_t combine_word(const uint32_t* r, const Barret
     return barrett128(x_hi, x_lo, br);
 }
 
+// planes 0..4 only (q < 2^40: bytes 5..7 of every canonical word are zero, so D_5 = D_6 = D_7 = 0)
+__device__ __forceinline__ uint64_t combine_word5(const uint32_t* r, const Barrett& br, uint64_t off_lo,
+                                                  uint64_t off_hi) {
+    int64_t lo = (int64_t)(int32_t)r[0] + (int64_t)(int32_t)r[1] * 256 + (int64_t)(int32_t)r[2] * 65536 +
+                 (int64_t)(int32_t)r[3] * 16777216;
+    int64_t hi = (int64_t)(int32_t)r[4];
+    uint64_t v_lo = (uint64_t)lo + ((uint64_t)hi << 32);
+    uint64_t carry = v_lo < (uint64_t)lo ? 1 : 0;
+    int64_t v_hi = (hi >> 32) + (lo >> 63) + (int64_t)carry;
+    uint64_t x_lo = v_lo + off_lo;
+    uint64_t x_hi = (uint64_t)v_hi + off_hi + (x_lo < v_lo ? 1 : 0);
+    return barrett128(x_hi, x_lo, br);
+}
+
 template <bool A_RES>
 __global__ void __launch_bounds__(kThreads, 1)
     k_accum_tc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -299,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ================================================================================================================
 
 static constexpr uint32_t kStages2 = 6;
+static constexpr uint32_t kThreads2 = 64 + 8 * 32;     // producer, MMA, 8 epilogue warps
 static constexpr uint32_t kBStage2 = 128 * 128;         // 16 KB: 128 K rows x this CTA's 128-byte N half
 static constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (0u << 10) | (0u << 15) | (1u << 16) |
                                     ((256u >> 3) << 17) | ((256u >> 4) << 24);   // M = 256, N = 256
@@ -365,7 +380,7 @@ __device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap*
 //             multicast to the same N-half of every pair, so each X byte leaves L2/HBM once per layer.  The stage
 //             ring is released only when all npairs MMA issuers have consumed it (empty count = npairs).
 template <bool A_RES, bool MC>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads2, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
                 uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec) {
@@ -480,6 +495,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------------------------ epilogue (8 warps per CTA)
+        // warp (quarter q = warp % 4, half h = (warp-2) / 4): TMEM lanes [32q, 32q+32) = outputs, words
+        // [16 h, 16 h + 16) of the 32-word tile.
         const uint32_t e = warp - 2;
         const uint32_t quarter = warp & 3;
         const uint32_t half = e >> 2;
@@ -494,6 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
             const Barrett br = tab.br(limb);
             const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
+            const bool narrow = br.w <= 40;          // bytes 5..7 of every word are zero: planes 5..7 vanish
             mbar_wait(&tfull[acc], use & 1);
             tc_fence_after();
             if (lane == 0) tma_store_wait_read0();
@@ -504,19 +522,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * 256 + half * 128 + c * 32;
                 TMEM_LD_X32(taddr, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c == 3) {   // every TMEM read of this accumulator slice is done: hand it back to the MMA
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+                }
 #pragma unroll
                 for (uint32_t wv = 0; wv < 4; wv += 2) {
-                    uint64_t v0 = combine_word(r + 8 * wv, br, olo, ohi);
-                    uint64_t v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
+                    uint64_t v0, v1;
+                    if (narrow) {
+                        v0 = combine_word5(r + 8 * wv, br, olo, ohi);
+                        v1 = combine_word5(r + 8 * (wv + 1), br, olo, ohi);
+                    } else {
+                        v0 = combine_word(r + 8 * wv, br, olo, ohi);
+                        v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
+                    }
                     const uint32_t wl = c * 4 + wv;
                     const uint32_t chunk = (wl >> 1) ^ (row & 7);
                     uint64_t* dst = (uint64_t*)(ys + row * 128 + chunk * 16);
                     asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(dst)), "l"(v0), "l"(v1) : "memory");
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
@@ -611,13 +637,13 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map B");
     }
-    {   // Y = uint64 [m][ctw], box 16 words x 32 rows
+    {   // Y = uint64 [m][ctw], box 16 words x 32 rows (SWIZZLE_128B; pair kernels: 8 words, SWIZZLE_64B)
         cuuint64_t dims[2] = {ctw, w->m};
         cuuint64_t strides[1] = {ctw * 8};
-        cuuint32_t box[2] = {16, 32}, es[2] = {1, 1};
+        cuuint32_t box[2] = {16u, 32}, es[2] = {1, 1};
         if (enc(&my, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)y, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map Y");
     }
     tc::EpiConst ec{};
@@ -654,7 +680,7 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         attr[0].val.clusterDim.x = csize;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(tc::kThreads, 1, 1);
+        cfg.blockDim = dim3(tc::kThreads2, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cfg.attrs = attr;

@@ -45,6 +45,9 @@ static constexpr uint32_t kIdesc = (2u << 4)            // D format s32
 
 struct EpiConst {
     uint64_t off_lo[ENSI_MAXT], off_hi[ENSI_MAXT];   // a multiple of q >= 2^80 (makes the 128-bit value non-negative)
+    uint64_t off64[ENSI_MAXT];                       // narrow limbs: a multiple of q >= max |V| (64-bit path)
+    uint32_t mu32[ENSI_MAXT];                        // narrow limbs: floor(2^64 / q) (< 2^32 since q > 2^32)
+    uint32_t narrow_ok;                              // 64-bit path valid for this d (2 max|V| + q < 2^64)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -132,18 +135,19 @@ __device__ __forceinline__ uint64_t combine_word(const uint32_t* r, const Barret
     return barrett128(x_hi, x_lo, br);
 }
 
-// planes 0..4 only (q < 2^40: bytes 5..7 of every canonical word are zero, so D_5 = D_6 = D_7 = 0)
-__device__ __forceinline__ uint64_t combine_word5(const uint32_t* r, const Barrett& br, uint64_t off_lo,
-                                                  uint64_t off_hi) {
-    int64_t lo = (int64_t)(int32_t)r[0] + (int64_t)(int32_t)r[1] * 256 + (int64_t)(int32_t)r[2] * 65536 +
-                 (int64_t)(int32_t)r[3] * 16777216;
-    int64_t hi = (int64_t)(int32_t)r[4];
-    uint64_t v_lo = (uint64_t)lo + ((uint64_t)hi << 32);
-    uint64_t carry = v_lo < (uint64_t)lo ? 1 : 0;
-    int64_t v_hi = (hi >> 32) + (lo >> 63) + (int64_t)carry;
-    uint64_t x_lo = v_lo + off_lo;
-    uint64_t x_hi = (uint64_t)v_hi + off_hi + (x_lo < v_lo ? 1 : 0);
-    return barrett128(x_hi, x_lo, br);
+// planes 0..4 only (q < 2^40: bytes 5..7 of every canonical word are zero, so D_5 = D_6 = D_7 = 0).
+// |V| <= 255 d (2^32 + 2^24 + 2^16 + 2^8 + 1) < 2^63 for d < 2^23, so V is a signed 64-bit value; u = V + off64
+// (a multiple of q) is non-negative and u mod q = V mod q.  64-bit Barrett with mu = floor(2^64/q) < 2^32:
+// qhat = floor((u_hi mu + floor(u_lo mu / 2^32)) / 2^32) >= floor(u/q) - 2, so u - qhat q in [0, 3q).
+__device__ __forceinline__ uint64_t combine_word5(const uint32_t* r, uint64_t q, uint32_t mu32, uint64_t off64) {
+    int64_t v = (int64_t)(int32_t)r[0] + (int64_t)(int32_t)r[1] * 256 + (int64_t)(int32_t)r[2] * 65536 +
+                (int64_t)(int32_t)r[3] * 16777216 + (int64_t)(int32_t)r[4] * 4294967296LL;
+    uint64_t u = (uint64_t)v + off64;
+    uint64_t t = ((uint64_t)(uint32_t)u * mu32) >> 32;
+    uint64_t qhat = ((uint64_t)(uint32_t)(u >> 32) * mu32 + t) >> 32;
+    uint64_t rr = u - qhat * q;
+    rr = rr >= q ? rr - q : rr;
+    return rr >= q ? rr - q : rr;
 }
 
 template <bool A_RES>
@@ -511,7 +515,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
             const Barrett br = tab.br(limb);
             const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
-            const bool narrow = br.w <= 40;          // bytes 5..7 of every word are zero: planes 5..7 vanish
+            const bool narrow = ec.narrow_ok && br.w <= 40;   // bytes 5..7 of every word are zero
+            const uint64_t off64 = ec.off64[limb];
+            const uint32_t mu32 = ec.mu32[limb];
             mbar_wait(&tfull[acc], use & 1);
             tc_fence_after();
             if (lane == 0) tma_store_wait_read0();
@@ -531,8 +537,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 for (uint32_t wv = 0; wv < 4; wv += 2) {
                     uint64_t v0, v1;
                     if (narrow) {
-                        v0 = combine_word5(r + 8 * wv, br, olo, ohi);
-                        v1 = combine_word5(r + 8 * (wv + 1), br, olo, ohi);
+                        v0 = combine_word5(r + 8 * wv, br.q, mu32, off64);
+                        v1 = combine_word5(r + 8 * (wv + 1), br.q, mu32, off64);
                     } else {
                         v0 = combine_word(r + 8 * wv, br, olo, ohi);
                         v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
@@ -655,6 +661,13 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         const u128 off = ((two80 + q - 1) / q) * q;
         ec.off_lo[i] = (uint64_t)off;
         ec.off_hi[i] = (uint64_t)(off >> 64);
+        // narrow 64-bit path: Vmax = 255 d_pad (2^32 + 2^24 + 2^16 + 2^8 + 1)
+        const u128 vmax = (u128)255 * w->wt_dpad * ((((u128)1) << 32) + (1u << 24) + (1u << 16) + (1u << 8) + 1);
+        const u128 off64 = ((vmax + q - 1) / q) * q;
+        ec.off64[i] = (uint64_t)off64;
+        ec.mu32[i] = (q > (((u128)1) << 32)) ? (uint32_t)((((u128)1) << 64) / q) : 0;
+        if (i == 0) ec.narrow_ok = (2 * vmax + q < (((u128)1) << 64)) ? 1 : 0;
+        if (!(q > (((u128)1) << 32))) ec.narrow_ok = 0;
     }
     const uint32_t kblocks = w->wt_dpad / 128;
     int sms = 148;

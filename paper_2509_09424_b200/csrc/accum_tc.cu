@@ -522,33 +522,44 @@ __global__ void __launch_bounds__(kThreads2, 1)
             tc_fence_after();
             if (lane == 0) tma_store_wait_read0();
             __syncwarp();
-#pragma unroll 1
-            for (uint32_t c = 0; c < 4; c++) {
-                uint32_t r[32];
-                const uint32_t taddr = tmem_base + ((quarter * 32) << 16) + acc * 256 + half * 128 + c * 32;
-                TMEM_LD_X32(taddr, r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (c == 3) {   // every TMEM read of this accumulator slice is done: hand it back to the MMA
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+            // Software-pipelined TMEM drain: the 32-column load of chunk c+1 is in flight while chunk c's four
+            // words are combined (four independent reduction chains per thread).
+            const uint32_t tbase = tmem_base + ((quarter * 32) << 16) + acc * 256 + half * 128;
+            uint32_t ra[32], rb[32];
+            auto combine4 = [&](const uint32_t* r, uint32_t c) {
+                uint64_t v[4];
+                if (narrow) {
+#pragma unroll
+                    for (uint32_t wv = 0; wv < 4; wv++) v[wv] = combine_word5(r + 8 * wv, br.q, mu32, off64);
+                } else {
+#pragma unroll
+                    for (uint32_t wv = 0; wv < 4; wv++) v[wv] = combine_word(r + 8 * wv, br, olo, ohi);
                 }
 #pragma unroll
                 for (uint32_t wv = 0; wv < 4; wv += 2) {
-                    uint64_t v0, v1;
-                    if (narrow) {
-                        v0 = combine_word5(r + 8 * wv, br.q, mu32, off64);
-                        v1 = combine_word5(r + 8 * (wv + 1), br.q, mu32, off64);
-                    } else {
-                        v0 = combine_word(r + 8 * wv, br, olo, ohi);
-                        v1 = combine_word(r + 8 * (wv + 1), br, olo, ohi);
-                    }
                     const uint32_t wl = c * 4 + wv;
                     const uint32_t chunk = (wl >> 1) ^ (row & 7);
                     uint64_t* dst = (uint64_t*)(ys + row * 128 + chunk * 16);
-                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(dst)), "l"(v0), "l"(v1) : "memory");
+                    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(dst)), "l"(v[wv]), "l"(v[wv + 1])
+                                 : "memory");
                 }
-            }
+            };
+            TMEM_LD_X32(tbase, ra);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            TMEM_LD_X32(tbase + 32, rb);
+            combine4(ra, 0);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            TMEM_LD_X32(tbase + 64, ra);
+            combine4(rb, 1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            TMEM_LD_X32(tbase + 96, rb);
+            combine4(ra, 2);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // every TMEM read of this accumulator slice is done: hand it back to the MMA issuer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+            combine4(rb, 3);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {

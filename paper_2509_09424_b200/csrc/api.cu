@@ -134,18 +134,19 @@ int plan_b(ensi_ctx* ctx, uint32_t d, uint32_t m, uint32_t s, uint32_t baby, Lay
     return ENSI_OK;
 }
 
-// Layout-B weight pack for (k, B): for giant step gam, rows r = c*B + b hold W[c*k + gam*B + b] (0 if >= d).
-int weights_b(ensi_ctx* ctx, ensi_weights* w, uint32_t k, uint32_t B, uint32_t n_in, uint32_t** out) {
+// Layout-B weights for (k, B): one packed weight object per giant step gam, whose row r = c*B + b holds
+// W[c*k + gam*B + b] (zero rows past d).  Built once per (k, B) and cached on the weights handle.
+int weights_b(ensi_ctx* ctx, ensi_weights* w, uint32_t k, uint32_t B, uint32_t n_in,
+              const std::vector<ensi_weights*>** out) {
     auto key = std::make_pair(k, B);
     auto it = w->packs_b.find(key);
     if (it != w->packs_b.end()) {
-        *out = it->second;
+        *out = &it->second;
         return ENSI_OK;
     }
     const uint32_t G = k / B, rows = n_in * B;
     std::vector<int8_t> Wg((size_t)rows * w->m);
-    std::vector<uint32_t> all;
-    all.reserve((size_t)G * rows * 2 * w->mw);
+    std::vector<ensi_weights*> subs;
     for (uint32_t gam = 0; gam < G; gam++) {
         std::fill(Wg.begin(), Wg.end(), 0);
         for (uint32_t c = 0; c < n_in; c++)
@@ -153,18 +154,17 @@ int weights_b(ensi_ctx* ctx, ensi_weights* w, uint32_t k, uint32_t B, uint32_t n
                 uint32_t col = c * k + gam * B + b;
                 if (col < w->d) std::memcpy(&Wg[((size_t)c * B + b) * w->m], &w->host[(size_t)col * w->m], w->m);
             }
-        std::vector<uint32_t> pl;
-        int rc = pack_planes(ctx, Wg.data(), rows, w->m, w->m, w->mw, pl, nullptr);
-        if (rc) return rc;
-        all.insert(all.end(), pl.begin(), pl.end());
+        ensi_weights* sw = nullptr;
+        int rc = ensi_weights_pack(ctx, Wg.data(), rows, w->m, w->m, &sw);
+        if (rc) {
+            for (auto* x : subs) ensi_weights_destroy(x);
+            return rc;
+        }
+        subs.push_back(sw);
     }
-    uint32_t* dptr = nullptr;
-    cudaError_t e = cudaMalloc(&dptr, all.size() * 4);
-    if (e != cudaSuccess) return cuda_err(ctx, e, "weights_b malloc");
-    e = cudaMemcpy(dptr, all.data(), all.size() * 4, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_err(ctx, e, "weights_b copy");
-    w->packs_b[key] = dptr;
-    *out = dptr;
+    auto& slot = w->packs_b[key];
+    slot = std::move(subs);
+    *out = &slot;
     return ENSI_OK;
 }
 
@@ -247,6 +247,15 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
         delete ctx;
         return ENSI_ECUDA;
     }
+    // keep stream-ordered allocations (rescale epilogue temporaries) pooled instead of returning them to the OS
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
     // twiddle tables
     const uint32_t n = ctx->n;
     std::vector<uint64_t> tw((size_t)ctx->T * 4 * n + 2 * ctx->T);
@@ -299,6 +308,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     }
     cudaFree(ctx->scratch);
     cudaFree(ctx->host_stage);
+    cudaFree(ctx->lb_buf);
     if (ctx->st_h2d) {
         cudaStreamDestroy(ctx->st_h2d);
         cudaStreamDestroy(ctx->st_d2h);
@@ -398,7 +408,8 @@ void ensi_weights_destroy(ensi_weights* w) {
     DeviceGuard g(w->ctx->device);
     cudaDeviceSynchronize();
     cudaFree(w->d_planes);
-    for (auto& kv : w->packs_b) cudaFree(kv.second);
+    for (auto& kv : w->packs_b)
+        for (auto* sw : kv.second) ensi_weights_destroy(sw);
     cudaFree(w->d_wt8);
     delete w;
 }
@@ -452,32 +463,47 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
         for (uint32_t gm = 1; gm < p.G; gm++)
             if (!find_key(ctx, galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm)))
                 return set_err(ctx, ENSI_ENOKEY, "missing giant-step key");
-        uint32_t* planes = nullptr;
-        rc = weights_b(ctx, w, p.k, p.B, p.n_in, &planes);
+        const std::vector<ensi_weights*>* subs = nullptr;
+        rc = weights_b(ctx, w, p.k, p.B, p.n_in, &subs);
         if (rc) return rc;
+        const bool tcb = (o.kernel >= 2) || (o.kernel == 0 && tc_supported(ctx, level));
         const uint32_t rows = p.n_in * p.B;
-        uint64_t *R = nullptr, *Tg = nullptr, *Tr = nullptr;
-        cudaError_t e = cudaMallocAsync((void**)&R, (size_t)rows * ctw * 8, st);
-        if (e == cudaSuccess && p.G > 1) e = cudaMallocAsync((void**)&Tg, (size_t)m * ctw * 8, st);
-        if (e == cudaSuccess && p.G > 1) e = cudaMallocAsync((void**)&Tr, ctw * 8, st);
-        if (e != cudaSuccess) return cuda_err(ctx, e, "layout B scratch");
+        // rotated inputs R [rows] and giant-step partials: ctx-owned, grown on demand (cudaMallocAsync would return
+        // the 9+ GB to the OS at every synchronisation under the default pool release threshold)
+        const size_t need = ((size_t)rows + (p.G > 1 ? (size_t)m + 1 : 0)) * ctw;
+        if (ctx->lb_words < need) {
+            cudaStreamSynchronize(st);
+            cudaFree(ctx->lb_buf);
+            ctx->lb_buf = nullptr;
+            ctx->lb_words = 0;
+            cudaError_t ea = cudaMalloc(&ctx->lb_buf, need * 8);
+            if (ea != cudaSuccess) {
+                cudaGetLastError();
+                return set_err(ctx, ENSI_ENOMEM, "layout B scratch allocation failed");
+            }
+            ctx->lb_words = need;
+        }
+        uint64_t* R = ctx->lb_buf;
+        uint64_t* Tg = p.G > 1 ? R + (size_t)rows * ctw : nullptr;
+        uint64_t* Tr = p.G > 1 ? Tg + (size_t)m * ctw : nullptr;
+        auto accum_b = [&](uint32_t gm, uint64_t* dst) -> int {
+            ensi_weights* sw = (*subs)[gm];
+            return tcb ? accum_ternary_tc(ctx, R, sw->d, sw, dst, level, st, 0, 0, tc_variant(o.kernel))
+                       : accum_ternary(ctx, R, sw->d, sw->d_planes, sw->mw, m, dst, level, st);
+        };
         std::vector<uint64_t> gb(p.B);
         for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
         for (uint32_t c = 0; c < p.n_in && !rc; c++)
             rc = rotate_hoisted(ctx, x->data + c * ctw, level, p.B, gb.data(), R + (size_t)c * p.B * ctw, st);
-        const size_t plane_words = (size_t)rows * 2 * w->mw;
-        if (!rc) rc = accum_ternary(ctx, R, rows, planes, w->mw, m, acc_out, level, st);
+        if (!rc) rc = accum_b(0, acc_out);
         for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
-            rc = accum_ternary(ctx, R, rows, planes + gm * plane_words, w->mw, m, Tg, level, st);
+            rc = accum_b(gm, Tg);
             uint64_t gg = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm);
             for (uint32_t i = 0; i < m && !rc; i++) {
                 rc = rotate_hoisted(ctx, Tg + (size_t)i * ctw, level, 1, &gg, Tr, st);
                 if (!rc) add_into(ctx, acc_out + (size_t)i * ctw, Tr, 1, level, st);
             }
         }
-        cudaFreeAsync(R, st);
-        if (Tg) cudaFreeAsync(Tg, st);
-        if (Tr) cudaFreeAsync(Tr, st);
     }
     if (!rc && o.rescale_out) {
         rc = ensi::rescale(ctx, acc_out, m, level, y->data, st);
@@ -523,6 +549,7 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
         if (ctx->host_stage) {
             cudaDeviceSynchronize();
             cudaFree(ctx->host_stage);
+    cudaFree(ctx->lb_buf);
         }
         ctx->host_stage = nullptr;
         cudaError_t e = cudaMalloc(&ctx->host_stage, 2 * stage_words * 8);

@@ -53,8 +53,8 @@ struct ensi_weights {
     std::vector<int8_t> host;             // dense d x m copy (row-major, ldw = m) for Layout-B re-packing
     uint32_t* d_planes = nullptr;         // [d][2][mw]: pos bits then neg bits (bit i%32 of word i/32)
     uint64_t nnz = 0;
-    // Layout B packs keyed by (k, B): [G][n_in*B][2][mw]
-    std::map<std::pair<uint32_t, uint32_t>, uint32_t*> packs_b;
+    // Layout B: per (k, B), one re-ordered weight object per giant step (rows c*B + b = W[c*k + gam*B + b])
+    std::map<std::pair<uint32_t, uint32_t>, std::vector<ensi_weights*>> packs_b;
     // byte-sliced tensor-core operand (W^T as int8 [m_pad][d_pad], K-major), built lazily
     int8_t* d_wt8 = nullptr;
     uint32_t wt_mpad = 0, wt_dpad = 0;
@@ -80,6 +80,9 @@ struct ensi_ctx {
     // scratch (grown on demand)
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
+    // Layout-B scratch (rotated inputs + giant-step partials)
+    uint64_t* lb_buf = nullptr;
+    size_t lb_words = 0;
     // host-staged pipeline (ensi_pcmm_ternary_host)
     uint64_t* host_stage = nullptr;
     size_t host_stage_words = 0;

@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "ensi_internal.h"
+#include "ntt_v2.cuh"
 
 namespace ensi {
 
@@ -131,6 +132,34 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
     ext[(size_t)row * n + k] = out;
 }
 
+// Key inner product with the automorphism fused on load, both key polynomials per thread (the digit gathers are
+// shared): acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r), j = 0, 1.
+__global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
+                                             uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
+                                             uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab) {
+    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
+    const uint32_t e = blockIdx.y, gi = blockIdx.z;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint32_t src = galois_src_index(k, gb.g[gi], log_n);
+    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * T * n + (size_t)li * n + k;
+    const Barrett br = tab.br(li);
+    U128 s0{0, 0}, s1{0, 0};
+    for (uint32_t t = 0; t < beta; t++) {
+        uint64_t dv = ext[((size_t)t * E + e) * n + src];
+        mac128(s0, dv, key[((size_t)t * 2 + 0) * T * n]);
+        mac128(s1, dv, key[((size_t)t * 2 + 1) * T * n]);
+        if ((t & 3) == 3 && t + 1 < beta) {
+            s0.lo = barrett128(s0.hi, s0.lo, br);
+            s0.hi = 0;
+            s1.lo = barrett128(s1.hi, s1.lo, br);
+            s1.hi = 0;
+        }
+    }
+    acc[(((size_t)gi * 2 + 0) * E + e) * n + k] = barrett128(s0.hi, s0.lo, br);
+    acc[(((size_t)gi * 2 + 1) * E + e) * n + k] = barrett128(s1.hi, s1.lo, br);
+}
+
 // Key inner product with the automorphism fused on load.
 // acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r)
 __global__ void __launch_bounds__(kT) k_kip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
@@ -198,6 +227,53 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     out[(((size_t)gb.oidx[gi] * 2 + j) * level + i) * n + k] = v;
 }
 
+// ---------------------------------------------------------------- fused ModDown (N' = 2^16, v2 NTT passes)
+// Row r of the z NTT = (gj = r / level, limb i = r % level).  The first NTT pass computes the centred fast
+// conversion of the INTT'ed P limbs on load (no z round trip through HBM); the last pass forms
+// (acc_{q_i} - NTT(z)) P^{-1} (+ sigma_g(c0)) on store and writes the rotated ciphertext directly.
+struct ModDownIn {
+    const uint64_t* acc;
+    const uint64_t* cm;
+    ModTab tab;
+    uint32_t level, L, A, E;
+    __device__ __forceinline__ uint64_t load(const uint64_t*, uint32_t row, uint32_t i, uint32_t k) const {
+        const uint32_t n = 65536, gj = row / level;
+        const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+        const uint64_t* phinv = cm;
+        const uint64_t* ph = cm + (size_t)A * 2 + (size_t)i * A * 2;
+        const uint64_t* pmodq = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)i * A;
+        const uint64_t q = tab.q[i];
+        const Barrett bq = tab.br(i);
+        uint64_t sum = 0;
+        for (uint32_t a = 0; a < A; a++) {
+            const uint64_t p = tab.q[L + a];
+            uint64_t y = mul_shoup(pc[(size_t)a * n], phinv[2 * a], phinv[2 * a + 1], p);
+            uint64_t yq = reduce64(y, bq);
+            if (y > (p >> 1)) yq = sub_mod(yq, pmodq[a], q);
+            sum += mul_shoup_lazy(yq, ph[2 * a], ph[2 * a + 1], q);
+        }
+        return reduce64(sum, bq);
+    }
+};
+struct ModDownOut {
+    const uint64_t* acc;
+    const uint64_t* c0;
+    uint64_t* out;
+    const uint64_t* cm;
+    ModTab tab;
+    GBatch gb;
+    uint32_t level, A, E;
+    __device__ __forceinline__ void store(uint64_t*, uint32_t row, uint32_t i, uint32_t k, uint64_t zt) const {
+        const uint32_t n = 65536, gj = row / level, gi = gj >> 1, j = gj & 1;
+        const uint64_t q = tab.q[i];
+        const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
+        uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], zt, q);
+        v = mul_shoup(v, pinv[0], pinv[1], q);
+        if (j == 0) v = add_mod(v, c0[(size_t)i * n + galois_src_index(k, gb.g[gi], 16)], q);
+        out[(((size_t)gb.oidx[gi] * 2 + j) * level + i) * n + k] = v;
+    }
+};
+
 // ---------------------------------------------------------------- host driver
 
 const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g) {
@@ -210,6 +286,18 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
     for (size_t i = 0; i < ctx->galois.size(); i++)
         if (ctx->galois[i] == g) return (int)i;
     return -1;
+}
+
+// ModDown fusion level at N' = 2^16 (ENSI_KS for A/B timing): 0 = separate convert / NTT / final kernels
+// (default, fastest measured: 11.0k rot/s), 1 = final combine fused into the last NTT pass (10.8k), 2 = conversion
+// also fused into the first pass (9.8k: 126 registers and 4 P-limb gathers per point cut the pass's occupancy).
+static int fused_moddown() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KS");
+        v = !e ? 0 : std::string(e) == "final" ? 1 : std::string(e) == "full" ? 2 : 0;
+    }
+    return v;
 }
 
 // Hoisted rotations of one ciphertext ct [2][level][N'] by n_g Galois elements -> out [n_g][2][level][N'].
@@ -268,9 +356,9 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
             gb.oidx[i] = idx[b0 + i];
         }
         {
-            dim3 g(n / kT, E, cnt * 2);
-            k_kip<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                    ctx->tab);
+            dim3 g(n / kT, E, cnt);
+            k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                                     ctx->tab);
             ENSI_LAUNCH_CHECK(ctx);
         }
         LimbMap pm = identity_map(A);
@@ -279,6 +367,26 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
         pm.grp_stride = E;
         pm.grp_off = level;
         ntt_inverse(ctx, acc, cnt * 2 * A, pm, st);
+        if (ctx->log_n == 16 && fused_moddown() > 0) {
+            const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
+            LimbMap zm = identity_map(level);
+            ModDownIn in{acc, cvt->d_moddown, ctx->tab, level, ctx->L, A, E};
+            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
+            dim3 g(16, cnt * 2 * level);
+            if (fused_moddown() == 2) {
+                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv,
+                                                                                   in, v2::PlainOut());
+            } else {
+                dim3 gc(n / kT, level, cnt * 2);
+                k_moddown_convert<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
+                v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv);
+                ctx->launches += 1;
+            }
+            v2::k_ntt256<v2::FWD_B, v2::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv,
+                                                                               v2::PlainIn(), outf);
+            ctx->launches += 2;
+            continue;
+        }
         {
             dim3 g(n / kT, level, cnt * 2);
             k_moddown_convert<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);

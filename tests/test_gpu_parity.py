@@ -316,3 +316,23 @@ def test_pcmm_with_rescale_epilogue(setup_c1, torch_cuda):
     ref = X @ W.astype(np.float64)
     z = ctx.decrypt_debug(yd, 3, 2, log2_scale=ls)
     assert np.max(np.abs(z[:16] - ref[:, 3])) < 1e-4
+
+
+@pytest.mark.parametrize("L,alpha,dnum,level", [(4, 2, 2, 4), (4, 2, 2, 3), (5, 2, 3, 5)])
+def test_rotate_hoisted_n16_fused_moddown(torch_cuda, L, alpha, dnum, level):
+    """N'=2^16 takes the fused ModDown (conversion in the first NTT pass, final combine in the last) and the
+    two-digit KIP; bit-exact against the oracle at reduced limb counts."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(16, L, alpha, dnum)
+    skc, sk, pk = o.keygen(4242)
+    ctx = Context(16, L, alpha, dnum)
+    gs = [o.galois(r) for r in (1, 128, 3000)]
+    keys = np.stack([o.rotkey(900 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    ct = synth.gen_words(77 + level, o.q, 1, level, o.n)[0]
+    want = o.rotate_hoisted(ct, [1] + gs, keys[[0] + list(range(3))])
+    yd = torch.empty((4, 2, level, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(dev(torch, ct[None]), [1] + gs, yd, level)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()

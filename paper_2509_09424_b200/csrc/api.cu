@@ -305,6 +305,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     for (auto& c : ctx->conv) {
         cudaFree(c.d_modup);
         cudaFree(c.d_moddown);
+        cudaFree(c.d_moddown2);
     }
     cudaFree(ctx->scratch);
     cudaFree(ctx->host_stage);

@@ -43,6 +43,8 @@ struct ConvTables {
     // moddown: per p_k: (P/p_k)^{-1} mod p_k (+shoup) [alpha][2]; per q_i per k: [P/p_k]_{q_i} (+shoup)
     // [level][alpha][2]; per q_i: P^{-1} mod q_i (+shoup) [level][2]
     uint64_t* d_moddown = nullptr;
+    // moddown v2: per (q_i, p_k): [P/p_k]_{q_i}, Shoup companion, q_i - [p_k P/p_k]_{q_i}  -> [level][alpha][3]
+    uint64_t* d_moddown2 = nullptr;
 };
 
 }  // namespace ensi

@@ -88,6 +88,21 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
         for (uint32_t k = 0; k < A; k++)
             md[(size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)i * A + k] = ctx->mod[L + k] % q;
     }
+    // moddown v2 constants [level][A][3]: ph, ph shoup, q - (p * ph mod q)
+    std::vector<uint64_t> md2((size_t)level * A * 3);
+    for (uint32_t i = 0; i < level; i++) {
+        const uint64_t q = ctx->mod[i];
+        for (uint32_t k = 0; k < A; k++) {
+            const uint64_t ph = md[(size_t)A * 2 + ((size_t)i * A + k) * 2];
+            const uint64_t pph = mulmod_h(ctx->mod[L + k] % q, ph, q);
+            md2[((size_t)i * A + k) * 3 + 0] = ph;
+            md2[((size_t)i * A + k) * 3 + 1] = shoup_h(ph, q);
+            md2[((size_t)i * A + k) * 3 + 2] = pph ? q - pph : 0;
+        }
+    }
+    if (cudaMalloc(&ct.d_moddown2, md2.size() * 8) != cudaSuccess ||
+        cudaMemcpy(ct.d_moddown2, md2.data(), md2.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cuda_err(ctx, cudaGetLastError(), "conv_tables md2");
     cudaError_t e1 = cudaMalloc(&ct.d_modup, mu.size() * 8);
     if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables malloc");
     e1 = cudaMalloc(&ct.d_moddown, md.size() * 8);
@@ -209,6 +224,43 @@ __global__ void __launch_bounds__(kT) k_moddown_convert(const uint64_t* __restri
         sum += mul_shoup_lazy(yq, ph[2 * a], ph[2 * a + 1], q);
     }
     z[((size_t)gj * level + i) * n + k] = reduce64(sum, bq);
+}
+
+// Same conversion, one thread per word position producing all `level` target limbs: the alpha centred residues
+// y_k' are computed once (not once per target limb), and y_k' [P/p_k']_{q_i} is a lazy Shoup product of the
+// un-reduced y (< p < 2^64 is a valid Shoup input); the centring adds the precomputed -[p_k' P/p_k']_{q_i}.
+// Constants per (i, k'): [P/p_k']_{q_i}, its Shoup companion, q_i - [p_k' (P/p_k')]_{q_i}  (md2, [level][A][3]).
+__global__ void __launch_bounds__(kT) k_moddown_convert2(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
+                                                         uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                         ModTab tab, const uint64_t* __restrict__ cm,
+                                                         const uint64_t* __restrict__ md2) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t gj = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+    uint64_t y[8];
+    bool neg[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; a++) {
+        if (a < A) {
+            const uint64_t p = tab.q[L + a];
+            y[a] = mul_shoup(pc[(size_t)a * n], cm[2 * a], cm[2 * a + 1], p);
+            neg[a] = y[a] > (p >> 1);
+        }
+    }
+    for (uint32_t i = 0; i < level; i++) {
+        const uint64_t q = tab.q[i];
+        const uint64_t* c = md2 + (size_t)i * A * 3;
+        uint64_t sum = 0;
+#pragma unroll
+        for (uint32_t a = 0; a < 8; a++) {
+            if (a < A) {
+                sum += mul_shoup_lazy(y[a], c[3 * a], c[3 * a + 1], q);   // [0, 2q)
+                if (neg[a]) sum += c[3 * a + 2];                          // [0, q)
+            }
+        }
+        z[((size_t)gj * level + i) * n + k] = reduce64(sum, tab.br(i));   // sum < 3 A q < 2^(2w+2)
+    }
 }
 
 // out[gi][j][i][k] = (acc_q_i - z) * P^-1 (+ c0[i][src_g(k)] when j == 0)
@@ -377,8 +429,9 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
                 v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv,
                                                                                    in, v2::PlainOut());
             } else {
-                dim3 gc(n / kT, level, cnt * 2);
-                k_moddown_convert<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
+                dim3 gc(n / kT, cnt * 2);
+                k_moddown_convert2<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                                      cvt->d_moddown, cvt->d_moddown2);
                 v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv);
                 ctx->launches += 1;
             }
@@ -387,7 +440,12 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
             ctx->launches += 2;
             continue;
         }
-        {
+        if (A <= 8) {
+            dim3 g(n / kT, cnt * 2);
+            k_moddown_convert2<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
+                                                 cvt->d_moddown2);
+            ENSI_LAUNCH_CHECK(ctx);
+        } else {
             dim3 g(n / kT, level, cnt * 2);
             k_moddown_convert<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
             ENSI_LAUNCH_CHECK(ctx);

@@ -287,6 +287,18 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
     }
     e = cudaMalloc(&ctx->d_tw, tw.size() * 8);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        std::vector<uint64_t> tw2((size_t)ctx->T * 4 * n);
+        for (uint32_t i = 0; i < ctx->T; i++)
+            for (uint32_t dir = 0; dir < 2; dir++)
+                for (uint32_t k = 0; k < n; k++) {
+                    const uint64_t* base = tw.data() + (size_t)i * 4 * n + (size_t)dir * 2 * n;
+                    tw2[(((size_t)i * 2 + dir) * n + k) * 2 + 0] = base[k];
+                    tw2[(((size_t)i * 2 + dir) * n + k) * 2 + 1] = base[n + k];
+                }
+        e = cudaMalloc(&ctx->d_tw2, tw2.size() * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw2, tw2.data(), tw2.size() * 8, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         ensi_ctx_destroy(ctx);
         return ENSI_ECUDA;
@@ -300,6 +312,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
     cudaFree(ctx->d_tw);
+    cudaFree(ctx->d_tw2);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
     for (auto& c : ctx->conv) {

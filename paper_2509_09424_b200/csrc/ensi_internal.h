@@ -71,6 +71,7 @@ struct ensi_ctx {
     ensi::ModTab tab{};
     // twiddles: [T][4][n] = psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup
     uint64_t* d_tw = nullptr;
+    uint64_t* d_tw2 = nullptr;            // interleaved [T][fwd, inv][n][w, w'] for the v2 NTT passes
     uint64_t ninv[ENSI_MAXT] = {}, ninv_sh[ENSI_MAXT] = {};
     // keys
     uint64_t* d_sk = nullptr;             // [T][n]

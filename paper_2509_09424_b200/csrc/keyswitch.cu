@@ -426,16 +426,16 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
             ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
             dim3 g(16, cnt * 2 * level);
             if (fused_moddown() == 2) {
-                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv,
+                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv,
                                                                                    in, v2::PlainOut());
             } else {
                 dim3 gc(n / kT, cnt * 2);
                 k_moddown_convert2<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                       cvt->d_moddown, cvt->d_moddown2);
-                v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv);
+                v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv);
                 ctx->launches += 1;
             }
-            v2::k_ntt256<v2::FWD_B, v2::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw, ninv,
+            v2::k_ntt256<v2::FWD_B, v2::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv,
                                                                                v2::PlainIn(), outf);
             ctx->launches += 2;
             continue;

@@ -191,8 +191,8 @@ void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
     if (use_v2(log_n)) {
         const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
         dim3 g(16, rows);
-        v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw, ninv);
-        v2::k_ntt256<v2::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw, ninv);
+        v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
+        v2::k_ntt256<v2::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
         ctx->launches += 2;
         return;
     }
@@ -217,18 +217,18 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
     const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;   // [T][2] appended after the twiddles
     if (use_v2(log_n)) {
         dim3 g(16, rows);
-        v2::k_ntt256<v2::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw, ninv);
-        v2::k_ntt256<v2::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw, ninv);
+        v2::k_ntt256<v2::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
+        v2::k_ntt256<v2::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
         ctx->launches += 2;
         return;
     }
     dim3 g2(n / tile, rows);
-    k_intt_block<<<g2, kThreads, 0, st>>>(data, log_n, ln2, ln2 == log_n ? 1 : 0, map, ctx->tab, ctx->d_tw, ninv);
+    k_intt_block<<<g2, kThreads, 0, st>>>(data, log_n, ln2, ln2 == log_n ? 1 : 0, map, ctx->tab, ctx->d_tw2, ninv);
     ENSI_LAUNCH_CHECK(ctx);
     if (ln2 < log_n) {
         const uint32_t cols = 1u << (12 - (log_n - ln2));
         dim3 g((1u << ln2) / cols, rows);
-        k_intt_strided<<<g, kThreads, 0, st>>>(data, log_n, ln2, map, ctx->tab, ctx->d_tw, ninv);
+        k_intt_strided<<<g, kThreads, 0, st>>>(data, log_n, ln2, map, ctx->tab, ctx->d_tw2, ninv);
         ENSI_LAUNCH_CHECK(ctx);
     }
 }

@@ -28,8 +28,9 @@ struct PlainOut {
     __device__ __forceinline__ void store(uint64_t* a, uint32_t, uint32_t, uint32_t k, uint64_t v) const { a[k] = v; }
 };
 
+// tw: interleaved (w, w') table [limb][fwd/inv][N'][2] (ctx->d_tw2): one 16-byte load per butterfly twiddle.
 template <int PASS, class IN = PlainIn, class OUT = PlainOut>
-__global__ void __launch_bounds__(256) k_ntt256(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
+__global__ void __launch_bounds__(256, 3) k_ntt256(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
                                                 const uint64_t* __restrict__ tw, const uint64_t* __restrict__ ninv,
                                                 IN in = IN(), OUT out = OUT()) {
     __shared__ uint64_t sm[16 * kRow];
@@ -38,8 +39,7 @@ __global__ void __launch_bounds__(256) k_ntt256(uint64_t* __restrict__ data, Lim
     const uint64_t q = tab.q[limb], q2 = 2 * q;
     const bool fwd = PASS == FWD_A || PASS == FWD_B;
     const bool colp = PASS == FWD_A || PASS == INV_A;          // column (strided) pass
-    const uint64_t* W = tw + (size_t)limb * 4 * n + (fwd ? 0 : 2 * (size_t)n);
-    const uint64_t* Wp = W + n;
+    const ulonglong2* W2 = reinterpret_cast<const ulonglong2*>(tw) + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n;
     uint64_t* a = data + map.phys(row) * n;
     const uint32_t tid = threadIdx.x;
     // lane mapping: column passes put consecutive sub-problems (columns) on consecutive lanes; block passes put
@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(256) k_ntt256(uint64_t* __restrict__ data, Lim
     };
     auto ct = [&](uint64_t& U, uint64_t& V, uint32_t t) {   // CT, inputs/outputs in [0, 4q)
         uint64_t u = U >= q2 ? U - q2 : U;
-        uint64_t x = mul_shoup_lazy(V, W[t], Wp[t], q);     // [0, 2q)
+        const ulonglong2 w = W2[t];
+        uint64_t x = mul_shoup_lazy(V, w.x, w.y, q);         // [0, 2q)
         U = u + x;
         V = u + q2 - x;
     };
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(256) k_ntt256(uint64_t* __restrict__ data, Lim
         uint64_t u = U, x = V;
         uint64_t s = u + x;
         U = s >= q2 ? s - q2 : s;
-        V = mul_shoup_lazy(u + q2 - x, W[t], Wp[t], q);
+        const ulonglong2 w = W2[t];
+        V = mul_shoup_lazy(u + q2 - x, w.x, w.y, q);
     };
 
     if (fwd) {

@@ -166,7 +166,8 @@ def run_reference(args, cfg_name):
         if it >= args.warmup:
             times.append(ms)
     v = statistics.mean(times)
-    line = {"metric": METRIC, "value": v, "unit": "ms/layer", "n_gpus": 0, "steps": args.steps,
+    line = {"metric": METRIC, "value": v, "unit": "ms/layer", "n_gpus": args.gpus, "device": "cpu (host cores)",
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform RNS words (data-oblivious accumulate)",
             "impl": "reference",
@@ -194,27 +195,86 @@ def time_loop(fn, steps: int, stream):
     return s.elapsed_time(e) / steps
 
 
-def bench_rotations(ctx_cls, cfg, steps: int, warmup: int, batch: int = 32):
-    """Hoisted key-switched rotations/s: one ciphertext, `batch` Galois elements per call (one ModUp)."""
+def _random_keys(ctx, gs, cfg, n):
     import torch
-    n = 1 << cfg["log_n"]
-    ctx = ctx_cls(cfg["log_n"], cfg["L"], cfg["alpha"], cfg["dnum"])
     T = cfg["L"] + cfg["alpha"]
-    gs = [pow(5, cfg["s"] * (b + 1), 2 * n) for b in range(batch)]
-    keys = torch.empty((batch, cfg["dnum"], 2, T, n), dtype=torch.int64, device="cuda")
+    keys = torch.empty((len(gs), cfg["dnum"], 2, T, n), dtype=torch.int64, device="cuda")
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
     for r in range(T):
         keys[:, :, :, r, :].random_(0, ctx.moduli[r], generator=g)
-    ctx.load_keys(galois=gs, rot_keys=keys)
-    x = synth.gen_words_torch(11, ctx.q, 1, cfg["L"], n)
-    y = torch.empty((batch, 2, cfg["L"], n), dtype=torch.int64, device="cuda")
+    return keys
+
+
+def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool = True):
+    """The other section-8 rows at the same parameters (timing-only uniform words and random keys; every kernel
+    is data-oblivious): NTT/INTT per limb (a5), hoisted key-switched rotations (a6+a7, the BASELINE metric's
+    rotations/sec), rescale (a4), and the Layout-B PCMM (a8: 765 hoisted rotations + the accumulate)."""
+    import torch
+    n = 1 << cfg["log_n"]
+    L, A, dnum, s = cfg["L"], cfg["alpha"], cfg["dnum"], cfg["s"]
+    T = L + A
+    ctx = ctx_cls(cfg["log_n"], L, A, dnum)
     st = torch.cuda.current_stream()
+    out = {}
+    # NTT / INTT over 768 limb rows (every limb of Q u P)
+    rows = 768
+    data = torch.empty((rows, n), dtype=torch.int64, device="cuda")
+    for lim in range(T):
+        data[lim::T].random_(0, ctx.moduli[lim])
+    limbs = list(range(T))
+    for name, inv in (("ntt_forward", False), ("ntt_inverse", True)):
+        for _ in range(warmup):
+            ctx.ntt(data, limbs, inverse=inv)
+        ms = time_loop(lambda: ctx.ntt(data, limbs, inverse=inv), steps, st)
+        alg = rows * n * 8 * 2          # one read + one write of every limb (the algorithmic minimum)
+        gbs = alg / (ms * 1e-3) / 1e9
+        out[name] = {"us_per_limb": 1e3 * ms / rows, "rows": rows, "achieved_GBps": gbs,
+                     "hbm_frac": gbs / peaks["hbm_gbs"], "passes": 2,
+                     "note": "algorithmic bytes = 1 read + 1 write per limb; the kernel makes 2 passes"}
+    del data
+    # hoisted rotations, 32 Galois elements per ModUp
+    batch = 32
+    gs = [pow(5, s * (b + 1), 2 * n) for b in range(batch)]
+    keys = _random_keys(ctx, gs, cfg, n)
+    ctx.load_keys(galois=gs, rot_keys=keys)
+    x = synth.gen_words_torch(11, ctx.q, 1, L, n)
+    y = torch.empty((batch, 2, L, n), dtype=torch.int64, device="cuda")
     for _ in range(warmup):
-        ctx.rotate_hoisted(x, gs, y, cfg["L"])
-    ms = time_loop(lambda: ctx.rotate_hoisted(x, gs, y, cfg["L"]), steps, st)
+        ctx.rotate_hoisted(x, gs, y, L)
+    ms = time_loop(lambda: ctx.rotate_hoisted(x, gs, y, L), steps, st)
+    key_bytes = dnum * 2 * T * n * 8
+    out["rotations"] = {"value": batch / (ms * 1e-3), "unit": "rotations/s", "ms_per_call": ms,
+                        "mode": f"hoisted, {batch} Galois elements per ModUp, N'=2^16, L=12, alpha=4, dnum=3",
+                        "key_GBps": batch * key_bytes / (ms * 1e-3) / 1e9}
+    del keys, y
+    # rescale 64 ciphertexts (level 12 -> 11)
+    xr = synth.gen_words_torch(5, ctx.q, 64, L, n)
+    yr = torch.empty((64, 2, L - 1, n), dtype=torch.int64, device="cuda")
+    for _ in range(warmup):
+        ctx.rescale(xr, yr, L)
+    ms = time_loop(lambda: ctx.rescale(xr, yr, L), steps, st)
+    out["rescale"] = {"us_per_ciphertext": 1e3 * ms / 64, "ciphertexts": 64}
+    del xr, yr
+    if layout_b:
+        d, m = cfg["shapes"][0]
+        k = (n // 2) // s
+        n_in = -(-d // k)
+        gsb = [pow(5, s * b, 2 * n) for b in range(1, k)]
+        keys = _random_keys(ctx, gsb, cfg, n)
+        ctx.load_keys(galois=gsb, rot_keys=keys)
+        W = synth.gen_W(synth.SEED_BASE + 102, d, m)
+        w = ctx.weights(W)
+        xb = synth.gen_words_torch(13, ctx.q, n_in, L, n)
+        yb = torch.empty((m, 2, L, n), dtype=torch.int64, device="cuda")
+        ctx.pcmm_ternary(xb, w, yb, level=L, layout=1, block_s=s)
+        ms = time_loop(lambda: ctx.pcmm_ternary(xb, w, yb, level=L, layout=1, block_s=s), max(1, steps // 2), st)
+        out["pcmm_layout_b"] = {"value": ms, "unit": "ms/layer", "rotations": (k - 1) * n_in, "block_s": s,
+                                "k": k, "n_in": n_in, "rotations_per_sec": (k - 1) * n_in / (ms * 1e-3)}
+        del keys, xb, yb
     ctx.close()
-    return batch / (ms * 1e-3), ms
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -227,7 +287,8 @@ def main():
     ap.add_argument("--kernel", type=int, default=0, help="0 default, 1 CUDA-core, 2 tcgen05")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-rot", action="store_true")
+    ap.add_argument("--no-rot", action="store_true", help="skip the secondary rows (NTT, rotations, rescale, Layout B)")
+    ap.add_argument("--no-layout-b", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)
@@ -330,9 +391,11 @@ def main():
                       "api": "ensi_pcmm_ternary_host"}
     # ---- rotations/s (BASELINE metric's second clause), rank 0 only
     if not args.no_rot and rank == 0:
-        rps, rms = bench_rotations(Context, cfg, max(2, args.steps), 2)
-        out["rotations_per_sec"] = {"value": rps, "unit": "rotations/s", "mode": "hoisted, 32 Galois elements per "
-                                    "ModUp, N'=2^16, L=12, alpha=4, dnum=3", "ms_per_call": rms}
+        del y
+        torch.cuda.empty_cache()
+        sec = bench_secondary(Context, cfg, max(3, args.steps), 2, peaks, layout_b=not args.no_layout_b)
+        out["rotations_per_sec"] = sec.pop("rotations")
+        out["secondary"] = sec
     # ---- CPU oracle baseline (rank 0 at N=1 only)
     if not args.no_cpu and rank == 0 and world == 1:
         x_host = (xh_t.numpy().view(np.uint64) if not args.no_e2e else x.cpu().numpy().view(np.uint64))

@@ -336,3 +336,23 @@ def test_rotate_hoisted_n16_fused_moddown(torch_cuda, L, alpha, dnum, level):
     ctx.rotate_hoisted(dev(torch, ct[None]), [1] + gs, yd, level)
     torch.cuda.synchronize()
     assert (host(yd) == want).all()
+
+
+@pytest.mark.parametrize("kernel", [2, 4, 1])
+@pytest.mark.parametrize("d,m", [(2048, 1200), (300, 2100), (3072, 96)])
+def test_pcmm_a_block_shapes_streamed_a(torch_cuda, kernel, d, m):
+    """C3-C5-like shapes at a small ring: d > 768 streams W^T per stage (no resident A), m > 1024 has more than
+    four pair groups (no cluster multicast); sampled output columns against the oracle."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(12, 2, 1, 2)
+    ctx = Context(12, 2, 1, 2)
+    x = synth.gen_words(d + 7 * m, o.q, d, 2, o.n)
+    W = synth.gen_W(d * 3 + m, d, m)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, ctx.weights(W), yd, level=2, kernel=kernel)
+    torch.cuda.synchronize()
+    cols = sorted(set([0, 1, m // 3, m // 2 + 1, m - 2, m - 1]))
+    want = o.pcmm_a(x, W, cols=cols, nthreads=8)
+    assert (host(yd[cols]) == want).all()

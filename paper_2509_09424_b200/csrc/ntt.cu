@@ -223,12 +223,12 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         return;
     }
     dim3 g2(n / tile, rows);
-    k_intt_block<<<g2, kThreads, 0, st>>>(data, log_n, ln2, ln2 == log_n ? 1 : 0, map, ctx->tab, ctx->d_tw2, ninv);
+    k_intt_block<<<g2, kThreads, 0, st>>>(data, log_n, ln2, ln2 == log_n ? 1 : 0, map, ctx->tab, ctx->d_tw, ninv);
     ENSI_LAUNCH_CHECK(ctx);
     if (ln2 < log_n) {
         const uint32_t cols = 1u << (12 - (log_n - ln2));
         dim3 g((1u << ln2) / cols, rows);
-        k_intt_strided<<<g, kThreads, 0, st>>>(data, log_n, ln2, map, ctx->tab, ctx->d_tw2, ninv);
+        k_intt_strided<<<g, kThreads, 0, st>>>(data, log_n, ln2, map, ctx->tab, ctx->d_tw, ninv);
         ENSI_LAUNCH_CHECK(ctx);
     }
 }

@@ -379,15 +379,17 @@ __device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap*
 
 // MC = false: clusters of one pair (2 CTAs), each pair loads its own X tiles; the pairs of the pgroups output
 //             groups that share a word tile meet only in L2.
-// MC = true:  clusters of npairs = pgroups pairs (2*npairs <= 8 CTAs).  The npairs pairs cover all outputs of the
-//             same word tile in lockstep; every X sub-box (32 K-rows x 128 bytes) is loaded once by one pair and
-//             multicast to the same N-half of every pair, so each X byte leaves L2/HBM once per layer.  The stage
-//             ring is released only when all npairs MMA issuers have consumed it (empty count = npairs).
+// MC = true:  clusters of cpairs pairs (cpairs | pgroups, 2*cpairs <= 8 CTAs; cpairs == pgroups when m <= 1024).
+//             The cpairs pairs of a cluster cover consecutive output groups of the same word tile in lockstep;
+//             every X sub-box (32 K-rows x 128 bytes) is loaded once by one pair and multicast to the same N-half
+//             of every pair of the cluster, so each X byte leaves L2/HBM once per cluster (once per layer when
+//             cpairs == pgroups).  The stage ring is released only when all cpairs MMA issuers have consumed it.
 template <bool A_RES, bool MC>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
-                uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec) {
+                uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec,
+                uint32_t cpairs) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages2 * kABox;
@@ -411,12 +413,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const uint32_t p = pair / pgroups;
     const uint32_t g = pg * 2 + rank;          // this CTA's 128-output group
     const uint16_t pair_mask = (uint16_t)(0x3u << lead);
-    const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * pgroups)) - 1) : pair_mask;
+    const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * cpairs)) - 1) : pair_mask;
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < kStages2; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], MC ? pgroups : 1);
+            mbar_init(&empty[s], MC ? cpairs : 1);
         }
         for (int a = 0; a < 2; a++) {
             mbar_init(&tfull[a], 1);
@@ -448,10 +450,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     mbar_wait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[s], 2 * (kBStage2 + (A_RES ? 0 : kABox)));
                     if (MC) {
-                        // sub-box j (32 K-rows) of this N-half: issued by pair j % pgroups, multicast to the
-                        // same N-half (cluster ranks rank, rank + 2, ...) of every pair
+                        // sub-box j (32 K-rows) of this N-half: issued by the pair with j % cpairs == its rank in the
+                        // cluster, multicast to the same N-half (cluster ranks rank, rank + 2, ...) of every pair
                         const uint16_t half_mask = (uint16_t)(all_mask & (rank ? 0xAAAAu : 0x5555u));
-                        for (uint32_t j = pg; j < kBoxK / 32; j += pgroups)
+                        for (uint32_t j = lead >> 1; j < kBoxK / 32; j += cpairs)
                             tma_load_2d_2sm_mc(sB + s * kBStage2 + j * 4096, &map_b, &full[s], half_mask,
                                                (int32_t)(t * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
                     } else {
@@ -643,8 +645,14 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
             return set_err(ctx, ENSI_ECUDA, "tensor map A");
     }
     const uint32_t pgroups = w->wt_mpad / 256;
-    if (variant == TC_AUTO) variant = (2 * pgroups <= 8) ? TC_PAIR_MC : TC_PAIR;
-    if (variant == TC_PAIR_MC && 2 * pgroups > 8) variant = TC_PAIR;
+    uint32_t cpairs = 1;                       // pairs per multicast cluster: largest divisor of pgroups <= 4
+    for (uint32_t c = 4; c >= 2; c--)
+        if (pgroups % c == 0) {
+            cpairs = c;
+            break;
+        }
+    if (variant == TC_AUTO) variant = cpairs >= 2 ? TC_PAIR_MC : TC_PAIR;
+    if (variant == TC_PAIR_MC && cpairs < 2) variant = TC_PAIR;
     {   // B = raw ciphertext bytes [d][ctw*8], box 128 bytes x 128 rows (x 32 rows: multicast sub-boxes)
         cuuint64_t dims[2] = {ctw * 8, d};
         cuuint64_t strides[1] = {ctw * 8};
@@ -689,11 +697,11 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
     if (variant != TC_ONE_CTA) {
         // CTA pairs (cta_group::2): pair group pg covers outputs [256 pg, 256 pg + 256)
         const bool mc = variant == TC_PAIR_MC;
-        const uint32_t csize = mc ? 2 * pgroups : 2;
+        const uint32_t csize = mc ? 2 * cpairs : 2;
         const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
         const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
         void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                     uint32_t, uint32_t, ModTab, tc::EpiConst);
+                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t);
         if (ares) kern = mc ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<true, false>;
         else kern = mc ? tc::k_accum_tc2<false, true> : tc::k_accum_tc2<false, false>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -718,14 +726,14 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 cudaGetLastError();
                 nclusters = std::max(1, sms / (int)csize);
             }
-            per_group = (uint32_t)nclusters;
+            per_group = std::max<uint32_t>(1, (uint32_t)nclusters / (pgroups / cpairs));
         } else {
             per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
         }
         per_group = std::min(per_group, ntiles);
         cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
         e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
-                               ctx->tab, ec);
+                               ctx->tab, ec, cpairs);
         ENSI_LAUNCH_CHECK(ctx);
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");

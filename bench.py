@@ -386,9 +386,10 @@ def main():
         barrier(world)
         e2e_ms = max_over_ranks(world, time_loop(e2e_step, max(1, min(args.steps, 3)), st))
         ok = bool((yh_t[5, 1, 3, :4096] == y[5, 1, 3, :4096].cpu()).all())
-        out["e2e"] = {"value": e2e_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": d * ct_bytes,
-                      "d2h_bytes_per_step": m * ct_bytes, "matches_device_path": ok,
-                      "api": "ensi_pcmm_ternary_host"}
+        # every rank copies its own token block's inputs in and outputs out (weak scaling): job-level metric
+        out["e2e"] = {"value": e2e_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": world * d * ct_bytes,
+                      "d2h_bytes_per_step": world * m * ct_bytes, "matches_device_path": ok,
+                      "api": "ensi_pcmm_ternary_host", "per_rank_ms": e2e_ms}
     # ---- rotations/s (BASELINE metric's second clause), rank 0 only
     if not args.no_rot and rank == 0:
         del y
@@ -408,6 +409,7 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
+        barrier(world)                 # ranks > 0 wait for rank 0's secondary measurements before teardown
         dist.destroy_process_group()
     return 0
 

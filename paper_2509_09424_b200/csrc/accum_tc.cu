@@ -138,15 +138,17 @@ __device__ __forceinline__ uint64_t combine_word(const uint32_t* r, const Barret
 // planes 0..4 only (q < 2^40: bytes 5..7 of every canonical word are zero, so D_5 = D_6 = D_7 = 0).
 // |V| <= 255 d (2^32 + 2^24 + 2^16 + 2^8 + 1) < 2^63 for d < 2^23, so V is a signed 64-bit value; u = V + off64
 // (a multiple of q) is non-negative and u mod q = V mod q.  64-bit Barrett with mu = floor(2^64/q) < 2^32:
-// qhat = floor((u_hi mu + floor(u_lo mu / 2^32)) / 2^32) >= floor(u/q) - 2, so u - qhat q in [0, 3q).
+// qhat = floor((u_hi mu + floor(u_lo mu / 2^32)) / 2^32) = floor(u mu / 2^64) exactly, and u mu / 2^64 > u/q - 1,
+// so qhat >= floor(u/q) - 1 and u - qhat q lies in [0, 2q): one conditional subtraction.
 __device__ __forceinline__ uint64_t combine_word5(const uint32_t* r, uint64_t q, uint32_t mu32, uint64_t off64) {
-    int64_t v = (int64_t)(int32_t)r[0] + (int64_t)(int32_t)r[1] * 256 + (int64_t)(int32_t)r[2] * 65536 +
-                (int64_t)(int32_t)r[3] * 16777216 + (int64_t)(int32_t)r[4] * 4294967296LL;
-    uint64_t u = (uint64_t)v + off64;
-    uint64_t t = ((uint64_t)(uint32_t)u * mu32) >> 32;
-    uint64_t qhat = ((uint64_t)(uint32_t)(u >> 32) * mu32 + t) >> 32;
-    uint64_t rr = u - qhat * q;
-    rr = rr >= q ? rr - q : rr;
+    int64_t v = (int64_t)off64 + (int64_t)(int32_t)r[0];
+    v += (int64_t)(int32_t)r[1] * 256;
+    v += (int64_t)(int32_t)r[2] * 65536;
+    v += (int64_t)(int32_t)r[3] * 16777216;
+    const uint64_t u = (uint64_t)v + ((uint64_t)(int64_t)(int32_t)r[4] << 32);
+    const uint32_t t = __umulhi((uint32_t)u, mu32);
+    const uint32_t qhat = (uint32_t)(((uint64_t)(uint32_t)(u >> 32) * mu32 + t) >> 32);
+    const uint64_t rr = u - (uint64_t)qhat * q;
     return rr >= q ? rr - q : rr;
 }
 

@@ -272,6 +272,22 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         out["pcmm_layout_b"] = {"value": ms, "unit": "ms/layer", "rotations": (k - 1) * n_in, "block_s": s,
                                 "k": k, "n_in": n_in, "rotations_per_sec": (k - 1) * n_in / (ms * 1e-3)}
         del keys, xb, yb
+    # Layout-A throughput at the other BASELINE shapes (C3 FFN pair, C4/C5 hidden-2048 projections)
+    sweep = {}
+    for name, (dd, mm) in (("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)), ("C4_2048x2048", (2048, 2048)),
+                           ("C5_2048x5504", (2048, 5504)), ("C5_5504x2048", (5504, 2048))):
+        W = synth.gen_W(synth.SEED_BASE + dd + mm, dd, mm)
+        w = ctx.weights(W)
+        xs = synth.gen_words_torch(17, ctx.q, dd, L, n)
+        ys = torch.empty((mm, 2, L, n), dtype=torch.int64, device="cuda")
+        ctx.pcmm_ternary(xs, w, ys, level=L)
+        ms = time_loop(lambda: ctx.pcmm_ternary(xs, w, ys, level=L), max(1, steps // 2), st)
+        ops = 2.0 * (2 * L * n * 8) * (-(-dd // 128) * 128) * (-(-mm // 256) * 256)
+        sweep[name] = {"ms_per_layer": ms, "tensor_TOPS": ops / (ms * 1e-3) / 1e12,
+                       "hbm_GBps": (dd + mm) * 2 * L * n * 8 / (ms * 1e-3) / 1e9}
+        del xs, ys, w
+        torch.cuda.empty_cache()
+    out["layout_a_shapes"] = sweep
     ctx.close()
     torch.cuda.empty_cache()
     return out

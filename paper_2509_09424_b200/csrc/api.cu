@@ -507,8 +507,8 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
         };
         std::vector<uint64_t> gb(p.B);
         for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
-        for (uint32_t c = 0; c < p.n_in && !rc; c++)
-            rc = rotate_hoisted(ctx, x->data + c * ctw, level, p.B, gb.data(), R + (size_t)c * p.B * ctw, st);
+        // baby steps for all inputs at once: key-stationary (each rotation key read once for the n_in inputs)
+        rc = rotate_hoisted_multi(ctx, x->data, p.n_in, ctw, level, p.B, gb.data(), R, p.B, st);
         if (!rc) rc = accum_b(0, acc_out);
         for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
             rc = accum_b(gm, Tg);

@@ -135,6 +135,8 @@ bool tc_supported(const ensi_ctx* ctx, uint32_t level);
 int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out);
 int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
                    uint64_t* out, cudaStream_t st);
+int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
+                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st);
 const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g);
 
 // poly (poly.cu)

@@ -18,10 +18,17 @@ namespace ensi {
 static constexpr uint32_t kT = 256;
 static constexpr uint32_t kMaxBatch = 32;
 
+// A batch of cnt Galois elements applied to n_ct input ciphertexts (key-stationary: each key word is read once
+// for all n_ct inputs).  Rotation (c, gi) reads input c at c0 + c * in_stride and writes output ciphertext
+// c * out_c_stride + oidx[gi].  Key-switch rows are indexed gj = (c * cnt + gi) * 2 + j.
 struct GBatch {
     uint64_t g[kMaxBatch];
     uint32_t key[kMaxBatch];   // index of the Galois key in ctx->galois / d_keys
-    uint32_t oidx[kMaxBatch];  // output ciphertext slot
+    uint32_t oidx[kMaxBatch];  // output ciphertext slot (per input)
+    uint32_t cnt, n_ct, out_c_stride;
+    uint64_t in_stride;        // words between consecutive input ciphertexts
+    __host__ __device__ uint32_t c_of(uint32_t r) const { return r / cnt; }
+    __host__ __device__ uint32_t gi_of(uint32_t r) const { return r % cnt; }
 };
 
 // ---------------------------------------------------------------- conversion tables
@@ -151,7 +158,8 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
 // shared): acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r), j = 0, 1.
 __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
                                              uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
-                                             uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab) {
+                                             uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab,
+                                             uint64_t ext_stride) {
     const uint32_t n = 1u << log_n, E = level + A, T = L + A;
     const uint32_t e = blockIdx.y, gi = blockIdx.z;
     const uint32_t li = e < level ? e : L + (e - level);
@@ -159,20 +167,26 @@ __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, c
     const uint32_t src = galois_src_index(k, gb.g[gi], log_n);
     const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * T * n + (size_t)li * n + k;
     const Barrett br = tab.br(li);
-    U128 s0{0, 0}, s1{0, 0};
-    for (uint32_t t = 0; t < beta; t++) {
-        uint64_t dv = ext[((size_t)t * E + e) * n + src];
-        mac128(s0, dv, key[((size_t)t * 2 + 0) * T * n]);
-        mac128(s1, dv, key[((size_t)t * 2 + 1) * T * n]);
-        if ((t & 3) == 3 && t + 1 < beta) {
-            s0.lo = barrett128(s0.hi, s0.lo, br);
-            s0.hi = 0;
-            s1.lo = barrett128(s1.hi, s1.lo, br);
-            s1.hi = 0;
+    // key-stationary: the key words of this position are fetched from HBM for the first input and served from L1
+    // for the others (same addresses, same thread)
+    for (uint32_t c = 0; c < gb.n_ct; c++) {
+        const uint64_t* ex = ext + (size_t)c * ext_stride;
+        U128 s0{0, 0}, s1{0, 0};
+        for (uint32_t t = 0; t < beta; t++) {
+            uint64_t dv = ex[((size_t)t * E + e) * n + src];
+            mac128(s0, dv, __ldg(key + ((size_t)t * 2 + 0) * T * n));
+            mac128(s1, dv, __ldg(key + ((size_t)t * 2 + 1) * T * n));
+            if ((t & 3) == 3 && t + 1 < beta) {
+                s0.lo = barrett128(s0.hi, s0.lo, br);
+                s0.hi = 0;
+                s1.lo = barrett128(s1.hi, s1.lo, br);
+                s1.hi = 0;
+            }
         }
+        const size_t r = (size_t)c * gb.cnt + gi;
+        acc[((r * 2 + 0) * E + e) * n + k] = barrett128(s0.hi, s0.lo, br);
+        acc[((r * 2 + 1) * E + e) * n + k] = barrett128(s1.hi, s1.lo, br);
     }
-    acc[(((size_t)gi * 2 + 0) * E + e) * n + k] = barrett128(s0.hi, s0.lo, br);
-    acc[(((size_t)gi * 2 + 1) * E + e) * n + k] = barrett128(s1.hi, s1.lo, br);
 }
 
 // Key inner product with the automorphism fused on load.
@@ -269,14 +283,15 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
                                                       GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
                                                       ModTab tab, const uint64_t* __restrict__ cm) {
     const uint32_t n = 1u << log_n, E = level + A;
-    const uint32_t i = blockIdx.y, gj = blockIdx.z, gi = gj >> 1, j = gj & 1;
+    const uint32_t i = blockIdx.y, gj = blockIdx.z, j = gj & 1;
+    const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
     const uint64_t q = tab.q[i];
     const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
     uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)gj * level + i) * n + k], q);
     v = mul_shoup(v, pinv[0], pinv[1], q);
-    if (j == 0) v = add_mod(v, c0[(size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
-    out[(((size_t)gb.oidx[gi] * 2 + j) * level + i) * n + k] = v;
+    if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
+    out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
 }
 
 // ---------------------------------------------------------------- fused ModDown (N' = 2^16, v2 NTT passes)
@@ -316,13 +331,14 @@ struct ModDownOut {
     GBatch gb;
     uint32_t level, A, E;
     __device__ __forceinline__ void store(uint64_t*, uint32_t row, uint32_t i, uint32_t k, uint64_t zt) const {
-        const uint32_t n = 65536, gj = row / level, gi = gj >> 1, j = gj & 1;
+        const uint32_t n = 65536, gj = row / level, j = gj & 1;
+        const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
         const uint64_t q = tab.q[i];
         const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
         uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], zt, q);
         v = mul_shoup(v, pinv[0], pinv[1], q);
-        if (j == 0) v = add_mod(v, c0[(size_t)i * n + galois_src_index(k, gb.g[gi], 16)], q);
-        out[(((size_t)gb.oidx[gi] * 2 + j) * level + i) * n + k] = v;
+        if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], 16)], q);
+        out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
     }
 };
 
@@ -352,19 +368,24 @@ static int fused_moddown() {
     return v;
 }
 
-// Hoisted rotations of one ciphertext ct [2][level][N'] by n_g Galois elements -> out [n_g][2][level][N'].
-int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
-                   uint64_t* out, cudaStream_t st) {
+// Hoisted rotations of n_ct ciphertexts (input c at ct + c * in_stride words, [2][level][N']) by n_g Galois elements:
+// rotation (c, r) -> out + (c * out_c_stride + r) ciphertexts.  One ModUp per input; per batch of up to 32 Galois
+// elements one key-stationary KIP (each key word read once for all n_ct inputs) and one ModDown over n_ct * cnt.
+int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
+                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st) {
     const uint32_t n = ctx->n, A = ctx->A, E = level + A;
     const uint64_t two_n_mask = 2ull * n - 1;
     const size_t ctw = (size_t)2 * level * n;
     if (A == 0) return set_err(ctx, ENSI_ENOKEY, "context has no special primes (num_p == 0): no key switching");
+    if (n_ct == 0) return ENSI_OK;
     std::vector<uint32_t> idx;
     std::vector<uint64_t> gs;
     for (uint32_t r = 0; r < n_g; r++) {
         uint64_t g = galois[r] & two_n_mask;
         if (g == 1) {
-            cudaMemcpyAsync(out + r * ctw, ct, ctw * 8, cudaMemcpyDeviceToDevice, st);
+            for (uint32_t c = 0; c < n_ct; c++)
+                cudaMemcpyAsync(out + ((size_t)c * out_c_stride + r) * ctw, ct + c * in_stride, ctw * 8,
+                                cudaMemcpyDeviceToDevice, st);
             continue;
         }
         int ki = key_index(ctx, g);
@@ -377,26 +398,28 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
     int rc = conv_tables(ctx, level, &cvt);
     if (rc) return rc;
     const uint32_t beta = cvt->beta;
+    if (beta > 8) return set_err(ctx, ENSI_EINVAL, "more than 8 key-switch digits");
     const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), kMaxBatch);
-    // scratch: coef [level][n] | ext [beta][E][n] | acc [nb][2][E][n] | z [nb][2][level][n]
-    const size_t w_coef = (size_t)level * n, w_ext = (size_t)beta * E * n, w_acc = (size_t)nb * 2 * E * n,
-                 w_z = (size_t)nb * 2 * level * n;
-    rc = ensure_scratch(ctx, (w_coef + w_ext + w_acc + w_z) * 8);
+    // scratch: coef [level][n] | ext [n_ct][beta][E][n] | acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n]
+    const size_t w_coef = (size_t)level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
+                 w_z = (size_t)n_ct * nb * 2 * level * n;
+    rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + w_acc + w_z) * 8);
     if (rc) return rc;
     uint64_t* coef = (uint64_t*)ctx->scratch;
     uint64_t* ext = coef + w_coef;
-    uint64_t* acc = ext + w_ext;
+    uint64_t* acc = ext + n_ct * w_ext1;
     uint64_t* z = acc + w_acc;
 
-    // ---- ModUp (once)
-    cudaMemcpyAsync(coef, ct + (size_t)level * n, w_coef * 8, cudaMemcpyDeviceToDevice, st);
-    ntt_inverse(ctx, coef, level, identity_map(level), st);
-    {
+    // ---- ModUp (once per input)
+    for (uint32_t c = 0; c < n_ct; c++) {
+        cudaMemcpyAsync(coef, ct + c * in_stride + (size_t)level * n, w_coef * 8, cudaMemcpyDeviceToDevice, st);
+        ntt_inverse(ctx, coef, level, identity_map(level), st);
         dim3 g(n / kT, beta * E);
-        k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
+        k_modup_convert<<<g, kT, 0, st>>>(coef, ext + c * w_ext1, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                          cvt->d_modup);
         ENSI_LAUNCH_CHECK(ctx);
+        ntt_forward(ctx, ext + c * w_ext1, beta * E, ext_map(ctx, level), st);
     }
-    ntt_forward(ctx, ext, beta * E, ext_map(ctx, level), st);
 
     // ---- per batch of Galois elements
     for (size_t b0 = 0; b0 < idx.size(); b0 += nb) {
@@ -407,10 +430,15 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
             gb.key[i] = (uint32_t)key_index(ctx, gs[b0 + i]);
             gb.oidx[i] = idx[b0 + i];
         }
+        gb.cnt = cnt;
+        gb.n_ct = n_ct;
+        gb.out_c_stride = out_c_stride;
+        gb.in_stride = in_stride;
+        const uint32_t nr = n_ct * cnt;   // rotations in this batch
         {
             dim3 g(n / kT, E, cnt);
             k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                     ctx->tab);
+                                     ctx->tab, w_ext1);
             ENSI_LAUNCH_CHECK(ctx);
         }
         LimbMap pm = identity_map(A);
@@ -418,18 +446,18 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
         pm.grp_rows = A;
         pm.grp_stride = E;
         pm.grp_off = level;
-        ntt_inverse(ctx, acc, cnt * 2 * A, pm, st);
+        ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
         if (ctx->log_n == 16 && fused_moddown() > 0) {
             const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
             LimbMap zm = identity_map(level);
             ModDownIn in{acc, cvt->d_moddown, ctx->tab, level, ctx->L, A, E};
             ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
-            dim3 g(16, cnt * 2 * level);
+            dim3 g(16, nr * 2 * level);
             if (fused_moddown() == 2) {
-                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv,
-                                                                                   in, v2::PlainOut());
+                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2,
+                                                                                   ninv, in, v2::PlainOut());
             } else {
-                dim3 gc(n / kT, cnt * 2);
+                dim3 gc(n / kT, nr * 2);
                 k_moddown_convert2<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                       cvt->d_moddown, cvt->d_moddown2);
                 v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv);
@@ -441,18 +469,18 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
             continue;
         }
         if (A <= 8) {
-            dim3 g(n / kT, cnt * 2);
+            dim3 g(n / kT, nr * 2);
             k_moddown_convert2<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
                                                  cvt->d_moddown2);
             ENSI_LAUNCH_CHECK(ctx);
         } else {
-            dim3 g(n / kT, level, cnt * 2);
+            dim3 g(n / kT, level, nr * 2);
             k_moddown_convert<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
             ENSI_LAUNCH_CHECK(ctx);
         }
-        ntt_forward(ctx, z, cnt * 2 * level, identity_map(level), st);
+        ntt_forward(ctx, z, nr * 2 * level, identity_map(level), st);
         {
-            dim3 g(n / kT, level, cnt * 2);
+            dim3 g(n / kT, level, nr * 2);
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown);
             ENSI_LAUNCH_CHECK(ctx);
         }
@@ -460,6 +488,11 @@ int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_err(ctx, e, "rotate_hoisted");
     return ENSI_OK;
+}
+
+int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
+                   uint64_t* out, cudaStream_t st) {
+    return rotate_hoisted_multi(ctx, ct, 1, 0, level, n_g, galois, out, 0, st);
 }
 
 }  // namespace ensi

@@ -299,6 +299,29 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
         e = cudaMalloc(&ctx->d_tw2, tw2.size() * 8);
         if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw2, tw2.data(), tw2.size() * 8, cudaMemcpyHostToDevice);
     }
+    ctx->ntt_fp_ok = true;
+    for (uint32_t i = 0; i < ctx->T; i++) ctx->ntt_fp_ok = ctx->ntt_fp_ok && ctx->mod[i] < (1ull << 50);
+    if (e == cudaSuccess && ctx->ntt_fp_ok) {
+        // centred twiddle c (|c| < q/2, exact in a double) and RN(c / q) for the FP64 NTT (ntt_fp.cuh)
+        std::vector<double> tw3((size_t)ctx->T * 4 * n + (size_t)ctx->T * 2);
+        auto centred = [](uint64_t w, uint64_t q) -> double {
+            return w > q / 2 ? -(double)(q - w) : (double)w;
+        };
+        for (uint32_t i = 0; i < ctx->T; i++) {
+            const uint64_t q = ctx->mod[i];
+            for (uint32_t dir = 0; dir < 2; dir++)
+                for (uint32_t k = 0; k < n; k++) {
+                    const double c = centred(tw[(size_t)i * 4 * n + (size_t)dir * 2 * n + k], q);
+                    tw3[(((size_t)i * 2 + dir) * n + k) * 2 + 0] = c;
+                    tw3[(((size_t)i * 2 + dir) * n + k) * 2 + 1] = c / (double)q;
+                }
+            const double c = centred(ctx->ninv[i], q);
+            tw3[(size_t)ctx->T * 4 * n + 2 * i] = c;
+            tw3[(size_t)ctx->T * 4 * n + 2 * i + 1] = c / (double)q;
+        }
+        e = cudaMalloc(&ctx->d_tw3, tw3.size() * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw3, tw3.data(), tw3.size() * 8, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         ensi_ctx_destroy(ctx);
         return ENSI_ECUDA;
@@ -313,6 +336,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     cudaDeviceSynchronize();
     cudaFree(ctx->d_tw);
     cudaFree(ctx->d_tw2);
+    cudaFree(ctx->d_tw3);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
     for (auto& c : ctx->conv) {

@@ -72,6 +72,10 @@ struct ensi_ctx {
     // twiddles: [T][4][n] = psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup
     uint64_t* d_tw = nullptr;
     uint64_t* d_tw2 = nullptr;            // interleaved [T][fwd, inv][n][w, w'] for the v2 NTT passes
+    // FP64 NTT (ntt_fp.cuh, all moduli < 2^50): [T][fwd, inv][n] of (w centred, RN(w/q)), then [T] of
+    // (n^-1 centred, RN(n^-1/q)), as double2
+    double* d_tw3 = nullptr;
+    bool ntt_fp_ok = false;
     uint64_t ninv[ENSI_MAXT] = {}, ninv_sh[ENSI_MAXT] = {};
     // keys
     uint64_t* d_sk = nullptr;             // [T][n]

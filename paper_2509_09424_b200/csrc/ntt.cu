@@ -9,6 +9,7 @@
 // Twiddle multiplications are Shoup products; every output word is canonical.
 #include "ensi_internal.h"
 #include "ntt_v2.cuh"
+#include "ntt_fp.cuh"
 
 namespace ensi {
 
@@ -175,19 +176,30 @@ __global__ void __launch_bounds__(kThreads) k_intt_strided(uint64_t* __restrict_
 
 static uint32_t split_log_n2(uint32_t log_n) { return log_n <= 12 ? log_n : log_n - log_n / 2; }
 
-// ENSI_NTT=v1 forces the generic kernels (for A/B timing); default uses v2 at N' = 2^16
-static bool use_v2(uint32_t log_n) {
+// Kernel choice at N' = 2^16: the FP64 passes (ntt_fp.cuh) when every modulus is below 2^50, else the integer v2
+// passes.  ENSI_NTT=v1 / v2 force the generic / integer kernels (A/B timing).
+static int ntt_env() {
     static int env = -1;
     if (env < 0) {
         const char* e = getenv("ENSI_NTT");
-        env = (e && e[0] == 'v' && e[1] == '1') ? 0 : 1;
+        env = (e && e[0] == 'v' && e[1] == '1') ? 1 : (e && e[0] == 'v' && e[1] == '2') ? 2 : 3;
     }
-    return env == 1 && log_n == 16;
+    return env;
 }
+static bool use_v2(uint32_t log_n) { return log_n == 16 && ntt_env() >= 2; }
+static bool use_fp(const ensi_ctx* ctx) { return ctx->log_n == 16 && ctx->ntt_fp_ok && ntt_env() == 3; }
 
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st) {
     if (rows == 0) return;
     const uint32_t log_n = ctx->log_n, n = ctx->n;
+    if (use_fp(ctx)) {
+        const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
+        dim3 g(16, rows);
+        nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        nttfp::k_ntt256<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        ctx->launches += 2;
+        return;
+    }
     if (use_v2(log_n)) {
         const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
         dim3 g(16, rows);
@@ -215,6 +227,14 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
     const uint32_t ln2 = split_log_n2(log_n);
     const uint32_t tile = n < kTile ? n : kTile;
     const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;   // [T][2] appended after the twiddles
+    if (use_fp(ctx)) {
+        const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
+        dim3 g(16, rows);
+        nttfp::k_ntt256<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        nttfp::k_ntt256<nttfp::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        ctx->launches += 2;
+        return;
+    }
     if (use_v2(log_n)) {
         dim3 g(16, rows);
         v2::k_ntt256<v2::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);

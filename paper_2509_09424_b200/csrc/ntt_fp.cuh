@@ -1,0 +1,201 @@
+// ntt_fp.cuh -- N' = 2^16 negacyclic NTT passes with the modular arithmetic on the FP64 pipe (sm_100a).
+//
+// Why: the integer Shoup butterfly costs ~32 instructions (a 64x64 high product is ~8 IMADs on the 32-bit integer
+// multiplier) and the v2 kernel is integer-issue bound (profiles/r01_ncu_ntt_keyswitch.md).  B200 keeps a full
+// FP64 unit (64 DFMA/SM/clk, half the FP32 rate), and for moduli q < 2^50 every word, twiddle and remainder is an
+// integer below 2^53, i.e. an exact double.  A butterfly becomes 8 DP instructions, measured 2.4x the integer
+// butterfly throughput in registers (tools/mb_modmul.cu).
+//
+// Exact modular product (centred residues, all values are integers held in doubles):
+//   h = V*w,  l = fma(V, w, -h)                 (h + l == V*w exactly: TwoProduct)
+//   t = fma(V, wq, M) - M,   wq = RN(w / q), M = 1.5*2^52    (t = rint(V*wq): the add to M rounds to an integer
+//                                                             while |V*wq| < 2^51)
+//   r = fma(-t, q, h) + l                        (= V*w - t*q exactly: h - t*q is an integer < 2^53 because
+//                                                 ulp(h) <= 2^49 when |V*w| < 2^101)
+//   |V*w/q - t| <= 1/2 + |V| 2^-55   ->   |r| <= 0.625 q   for |V| < 2^52.
+// Bounds (b = max |value| / q): CT (forward) outputs U +- r grow by 0.625 per stage; GS (inverse) sums U + V
+// double per stage.  Preconditions of the product: |V| < 2^52 and every sum < 2^53.
+//  * narrow limbs (q < 2^41, bmax = 2^52/q >= 2048): forward runs both passes unreduced (b <= 1 + 16*0.625 = 11);
+//    inverse reduces the sums every 4 stages (b <= 16).
+//  * wide limbs (2^41 <= q < 2^50, bmax > 4): forward reduces every 4 stages (b <= 1 + 4*0.625 = 3.5); inverse
+//    centres its input and reduces the sums every 2 stages (product inputs b <= 2.5).
+// Centred reduction red(v) = v - rint(v/q) q (3 DP), |red(v)| <= q/2 + tiny.  The last store maps the centred
+// result to the canonical word in [0, q), so the output is bit-identical to the integer kernels (and the oracle).
+// The pass-A -> pass-B intermediate is stored as the double's bit pattern (private to the two launches).
+#pragma once
+#include "ensi_internal.h"
+
+namespace ensi {
+namespace nttfp {
+
+enum Pass { FWD_A = 0, FWD_B = 1, INV_B = 2, INV_A = 3 };
+static constexpr uint32_t kRow = 273;          // smem row stride (words): 256 + 16 pads + 1 -> conflict-free
+static constexpr double kM = 6755399441055744.0;   // 1.5 * 2^52
+static constexpr long long kMbits = 0x4338000000000000ll;
+
+__device__ __forceinline__ uint32_t sidx(uint32_t sp, uint32_t i) { return sp * kRow + i + (i >> 4); }
+
+// signed integer |x| < 2^51 <-> double, through the 1.5*2^52 binade (one integer add + one DADD)
+__device__ __forceinline__ double i2d(long long x) { return __longlong_as_double(kMbits + x) - kM; }
+__device__ __forceinline__ long long d2i(double v) { return __double_as_longlong(v + kM) - kMbits; }
+// centred integer-valued double (|v| < q) -> canonical word in [0, q)
+__device__ __forceinline__ uint64_t canon(double v, uint64_t q) {
+    long long x = d2i(v);
+    return (uint64_t)(x + ((x >> 63) & (long long)q));
+}
+__device__ __forceinline__ double red(double v, double q, double qinv) {
+    const double t = fma(v, qinv, kM) - kM;
+    return fma(-t, q, v);
+}
+__device__ __forceinline__ double mulmod(double V, double w, double wq, double q) {
+    const double h = V * w;
+    const double l = fma(V, w, -h);
+    const double t = fma(V, wq, kM) - kM;
+    return fma(-t, q, h) + l;
+}
+
+struct PlainIn {
+    __device__ __forceinline__ uint64_t load(const uint64_t* a, uint32_t, uint32_t, uint32_t k) const { return a[k]; }
+};
+struct PlainOut {
+    __device__ __forceinline__ void store(uint64_t* a, uint32_t, uint32_t, uint32_t k, uint64_t v) const { a[k] = v; }
+};
+
+// tw: [limb][fwd/inv][N'] of (w centred, RN(w/q)) as double2, then [limb] of (n^-1 centred, RN(n^-1/q)).
+// Same CTA geometry as the integer v2 passes (ntt_v2.cuh): 16 sub-problems of 256 points, 16 points per thread.
+template <int PASS, bool WIDE, class IN, class OUT>
+__device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t row, uint32_t limb, uint64_t q,
+                                            const double2* __restrict__ W2, const double2* __restrict__ ninv,
+                                            double* sm, const IN& in, const OUT& out) {
+    const double qd = (double)q, qinv = 1.0 / qd;
+    const bool fwd = PASS == FWD_A || PASS == FWD_B;
+    const bool colp = PASS == FWD_A || PASS == INV_A;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t sp = colp ? (tid & 15) : (tid >> 4);
+    const uint32_t tt = colp ? (tid >> 4) : (tid & 15);
+    const uint32_t sub = blockIdx.x * 16 + sp;
+    auto gaddr = [&](uint32_t i) -> uint64_t { return colp ? (uint64_t)sub + 256ull * i : 256ull * sub + i; };
+    auto twi = [&](uint32_t lt, uint32_t i1) -> uint32_t {
+        if (colp) return (128u >> lt) + (i1 >> (lt + 1));
+        return (32768u >> lt) + sub * (128u >> lt) + (i1 >> (lt + 1));
+    };
+    auto ct = [&](double& U, double& V, uint32_t t) {
+        const double2 w = W2[t];
+        const double r = mulmod(V, w.x, w.y, qd);
+        V = U - r;
+        U = U + r;
+    };
+    auto gs = [&](double& U, double& V, uint32_t t, bool reduce) {
+        const double2 w = W2[t];
+        const double s = U + V;
+        V = mulmod(U - V, w.x, w.y, qd);
+        U = reduce ? red(s, qd, qinv) : s;
+    };
+    double v[16];
+
+    if (fwd) {
+#pragma unroll
+        for (uint32_t k = 0; k < 16; k++) {
+            const uint32_t i = tt + 16 * k;
+            if (PASS == FWD_A) v[k] = i2d((long long)in.load(a, row, limb, (uint32_t)gaddr(i)));
+            else v[k] = __longlong_as_double((long long)a[gaddr(i)]);
+        }
+#pragma unroll
+        for (int lt = 7; lt >= 4; lt--) {
+            const uint32_t ks = 1u << (lt - 4);
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                if (!(k & ks)) ct(v[k], v[k + ks], twi(lt, tt + 16 * k));
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, tt + 16 * k)] = WIDE ? red(v[k], qd, qinv) : v[k];
+        __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, 16 * tt + k)];
+#pragma unroll
+        for (int lt = 3; lt >= 0; lt--) {
+            const uint32_t ks = 1u << lt;
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                if (!(k & ks)) ct(v[k], v[k + ks], twi(lt, 16 * tt + k));
+        }
+        if (PASS == FWD_A) {
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                a[gaddr(16 * tt + k)] = (uint64_t)__double_as_longlong(WIDE ? red(v[k], qd, qinv) : v[k]);
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, 16 * tt + k)] = red(v[k], qd, qinv);
+            __syncthreads();
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                out.store(a, row, limb, (uint32_t)gaddr(tt + 16 * k), canon(sm[sidx(sp, tt + 16 * k)], q));
+        }
+    } else {
+        // wide limbs centre the canonical input (b = 1/2) so that two doubling stages stay below b = 2
+        auto load_in = [&](uint64_t x) -> double {
+            long long s = (long long)x;
+            if (WIDE) s -= (s > (long long)(q >> 1)) ? (long long)q : 0;
+            return i2d(s);
+        };
+        if (PASS == INV_B) {
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, tt + 16 * k)] = load_in(a[gaddr(tt + 16 * k)]);
+            __syncthreads();
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, 16 * tt + k)];
+        } else {
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) v[k] = __longlong_as_double((long long)a[gaddr(16 * tt + k)]);
+        }
+#pragma unroll
+        for (int lt = 0; lt <= 3; lt++) {
+            const uint32_t ks = 1u << lt;
+            const bool rd = WIDE ? (lt & 1) : (lt == 3);
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                if (!(k & ks)) gs(v[k], v[k + ks], twi(lt, 16 * tt + k), rd);
+        }
+        if (PASS == INV_B) __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, 16 * tt + k)] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, tt + 16 * k)];
+#pragma unroll
+        for (int lt = 4; lt <= 7; lt++) {
+            const uint32_t ks = 1u << (lt - 4);
+            const bool rd = WIDE ? (lt & 1) : (lt == 7);
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++)
+                if (!(k & ks)) gs(v[k], v[k + ks], twi(lt, tt + 16 * k), rd);
+        }
+        if (PASS == INV_B) {
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) a[gaddr(tt + 16 * k)] = (uint64_t)__double_as_longlong(v[k]);
+        } else {
+            const double2 ni = ninv[limb];
+#pragma unroll
+            for (uint32_t k = 0; k < 16; k++) a[gaddr(tt + 16 * k)] = canon(mulmod(v[k], ni.x, ni.y, qd), q);
+        }
+    }
+}
+
+template <int PASS, class IN = PlainIn, class OUT = PlainOut>
+__global__ void __launch_bounds__(256, 3) k_ntt256(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
+                                                const double2* __restrict__ tw, const double2* __restrict__ ninv,
+                                                IN in = IN(), OUT out = OUT()) {
+    __shared__ double sm[16 * kRow];
+    const uint32_t n = 65536;
+    const uint32_t row = blockIdx.y, limb = map.limb[row % map.period];
+    const uint64_t q = tab.q[limb];
+    const bool fwd = PASS == FWD_A || PASS == FWD_B;
+    const double2* W2 = tw + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n;
+    uint64_t* a = data + map.phys(row) * n;
+    if (q >= (1ull << 41)) ntt256_body<PASS, true>(a, row, limb, q, W2, ninv, sm, in, out);
+    else ntt256_body<PASS, false>(a, row, limb, q, W2, ninv, sm, in, out);
+}
+
+}  // namespace nttfp
+}  // namespace ensi

@@ -66,6 +66,32 @@ def test_ntt_bit_exact(torch_cuda, log_n, L, alpha):
     assert (host(t) == rows).all()
 
 
+def test_ntt_n16_extreme_inputs(torch_cuda):
+    """N'=2^16 (the FP64 passes, ntt_fp.cuh): structured extreme rows on every limb (narrow 40-bit and wide 50-bit),
+    forward and inverse separately, against the oracle's definition."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    ctx = Context(16, 12, 4, 3)
+    o = oracle.Oracle(16, 12, 4, 3)
+    T = 16
+    rows, limbs = [], []
+    for li in range(T):
+        q = o.moduli[li]
+        pats = [np.full(o.n, q - 1, dtype=np.uint64), np.full(o.n, (q + 1) // 2, dtype=np.uint64),
+                np.tile(np.array([0, q - 1], dtype=np.uint64), o.n // 2), np.zeros(o.n, dtype=np.uint64)]
+        pats[3][0] = q - 1
+        for p in pats:
+            rows.append(p)
+            limbs.append(li)
+    rows = np.stack(rows)
+    t = dev(torch, rows)
+    ctx.ntt(t, limbs)
+    assert (host(t) == np.stack([o.ntt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+    t = dev(torch, rows)
+    ctx.ntt(t, limbs, inverse=True)
+    assert (host(t) == np.stack([o.intt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+
+
 def _enc_cols(o, pk, X, level, seed):
     d = X.shape[1]
     m_res = np.stack([o.encode(X[:, j], level, DELTA) for j in range(d)])

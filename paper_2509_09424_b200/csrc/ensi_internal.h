@@ -45,6 +45,9 @@ struct ConvTables {
     uint64_t* d_moddown = nullptr;
     // moddown v2: per (q_i, p_k): [P/p_k]_{q_i}, Shoup companion, q_i - [p_k P/p_k]_{q_i}  -> [level][alpha][3]
     uint64_t* d_moddown2 = nullptr;
+    // moddown for the FP64 conversion (moduli < 2^50): (P/p_k)^-1 mod p_k centred and RN(./p_k) [alpha][2], then
+    // [P/p_k]_{q_i} centred and RN(./q_i) [level][alpha][2]
+    double* d_moddown_fp = nullptr;
 };
 
 }  // namespace ensi

@@ -12,6 +12,7 @@
 
 #include "ensi_internal.h"
 #include "ntt_v2.cuh"
+#include "ntt_fp.cuh"
 
 namespace ensi {
 
@@ -110,6 +111,24 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
     if (cudaMalloc(&ct.d_moddown2, md2.size() * 8) != cudaSuccess ||
         cudaMemcpy(ct.d_moddown2, md2.data(), md2.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
         return cuda_err(ctx, cudaGetLastError(), "conv_tables md2");
+    if (ctx->ntt_fp_ok) {
+        std::vector<double> mf((size_t)A * 2 + (size_t)level * A * 2);
+        auto centred = [](uint64_t w, uint64_t q) -> double { return w > q / 2 ? -(double)(q - w) : (double)w; };
+        for (uint32_t k = 0; k < A; k++) {
+            const uint64_t p = ctx->mod[L + k];
+            mf[k * 2] = centred(md[k * 2], p);
+            mf[k * 2 + 1] = mf[k * 2] / (double)p;
+        }
+        for (uint32_t i = 0; i < level; i++)
+            for (uint32_t k = 0; k < A; k++) {
+                const size_t o = (size_t)A * 2 + ((size_t)i * A + k) * 2;
+                mf[o] = centred(md[o], ctx->mod[i]);
+                mf[o + 1] = mf[o] / (double)ctx->mod[i];
+            }
+        if (cudaMalloc(&ct.d_moddown_fp, mf.size() * 8) != cudaSuccess ||
+            cudaMemcpy(ct.d_moddown_fp, mf.data(), mf.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+            return cuda_err(ctx, cudaGetLastError(), "conv_tables fp");
+    }
     cudaError_t e1 = cudaMalloc(&ct.d_modup, mu.size() * 8);
     if (e1 != cudaSuccess) return cuda_err(ctx, e1, "conv_tables malloc");
     e1 = cudaMalloc(&ct.d_moddown, md.size() * 8);
@@ -277,6 +296,42 @@ __global__ void __launch_bounds__(kT) k_moddown_convert2(const uint64_t* __restr
     }
 }
 
+// FP64 version (all moduli < 2^50, ntt_fp.cuh arithmetic): y_k' = [pc_k' (P/p_k')^-1]_{p_k'} as the exact centred
+// representative in [-(p-1)/2, (p-1)/2] (R10), then z_i = sum_k' y_k' [P/p_k']_{q_i} with |sum| <= 2.5 q_i,
+// one centred reduction, canonical store -- the same words as k_moddown_convert2.
+__device__ __forceinline__ double y_centred(double x, double p, double hp, double w, double wq) {
+    double r = nttfp::mulmod(x, w, wq, p);      // |r| <= 0.625 p, r == x w mod p
+    r = r > hp ? r - p : r;
+    return r < -hp ? r + p : r;
+}
+__global__ void __launch_bounds__(kT) k_moddown_convert_fp(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
+                                                           uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                           ModTab tab, const double* __restrict__ mf) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t gj = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+    double y[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; a++) {
+        if (a < A) {
+            const uint64_t p = tab.q[L + a];
+            y[a] = y_centred(nttfp::i2d((long long)pc[(size_t)a * n]), (double)p, (double)(p >> 1),
+                             __ldg(mf + 2 * a), __ldg(mf + 2 * a + 1));
+        }
+    }
+    const double* c = mf + (size_t)A * 2;
+    for (uint32_t i = 0; i < level; i++) {
+        const uint64_t q = tab.q[i];
+        const double qd = (double)q;
+        double s = 0.0;
+#pragma unroll
+        for (uint32_t a = 0; a < 8; a++)
+            if (a < A) s += nttfp::mulmod(y[a], __ldg(c + ((size_t)i * A + a) * 2), __ldg(c + ((size_t)i * A + a) * 2 + 1), qd);
+        z[((size_t)gj * level + i) * n + k] = nttfp::canon(nttfp::red(s, qd, 1.0 / qd), q);
+    }
+}
+
 // out[gi][j][i][k] = (acc_q_i - z) * P^-1 (+ c0[i][src_g(k)] when j == 0)
 __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
                                                       const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
@@ -322,6 +377,26 @@ struct ModDownIn {
         return reduce64(sum, bq);
     }
 };
+struct ModDownInFp {
+    const uint64_t* acc;
+    const double* mf;
+    ModTab tab;
+    uint32_t level, L, A, E;
+    __device__ __forceinline__ uint64_t load(const uint64_t*, uint32_t row, uint32_t i, uint32_t k) const {
+        const uint32_t n = 65536, gj = row / level;
+        const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+        const double qd = (double)tab.q[i];
+        const double* c = mf + (size_t)A * 2 + (size_t)i * A * 2;
+        double s = 0.0;
+        for (uint32_t a = 0; a < A; a++) {
+            const uint64_t p = tab.q[L + a];
+            const double y = y_centred(nttfp::i2d((long long)pc[(size_t)a * n]), (double)p, (double)(p >> 1),
+                                       __ldg(mf + 2 * a), __ldg(mf + 2 * a + 1));
+            s += nttfp::mulmod(y, __ldg(c + 2 * a), __ldg(c + 2 * a + 1), qd);
+        }
+        return nttfp::canon(nttfp::red(s, qd, 1.0 / qd), tab.q[i]);
+    }
+};
 struct ModDownOut {
     const uint64_t* acc;
     const uint64_t* c0;
@@ -357,8 +432,9 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
 }
 
 // ModDown fusion level at N' = 2^16 (ENSI_KS for A/B timing): 0 = separate convert / NTT / final kernels
-// (default, fastest measured: 11.0k rot/s), 1 = final combine fused into the last NTT pass (10.8k), 2 = conversion
-// also fused into the first pass (9.8k: 126 registers and 4 P-limb gathers per point cut the pass's occupancy).
+// (default, fastest measured: 17.9k rot/s with the FP64 NTT and conversion), 1 = final combine fused into the last
+// NTT pass (17.3k), 2 = conversion also fused into the first pass (15.6k: the alpha P-limb loads and products per
+// point and per target limb lengthen the pass).  Integer-NTT era: 11.0k / 10.8k / 9.8k.
 static int fused_moddown() {
     static int v = -1;
     if (v < 0) {
@@ -366,6 +442,16 @@ static int fused_moddown() {
         v = !e ? 0 : std::string(e) == "final" ? 1 : std::string(e) == "full" ? 2 : 0;
     }
     return v;
+}
+
+// ENSI_MODDOWN=int forces the integer conversion kernel (A/B timing); default FP64 when every modulus < 2^50
+static bool moddown_fp() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_MODDOWN");
+        v = (e && std::string(e) == "int") ? 0 : 1;
+    }
+    return v == 1;
 }
 
 // Hoisted rotations of n_ct ciphertexts (input c at ct + c * in_stride words, [2][level][N']) by n_g Galois elements:
@@ -447,6 +533,27 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         pm.grp_stride = E;
         pm.grp_off = level;
         ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
+        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0) {
+            const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
+            const double2* ninv = tw + (size_t)ctx->T * 2 * n;
+            LimbMap zm = identity_map(level);
+            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
+            dim3 g(16, nr * 2 * level);
+            if (fused_moddown() == 2) {
+                ModDownInFp in{acc, cvt->d_moddown_fp, ctx->tab, level, ctx->L, A, E};
+                nttfp::k_ntt256<nttfp::FWD_A, ModDownInFp><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv, in);
+            } else {
+                dim3 gc(n / kT, nr * 2);
+                k_moddown_convert_fp<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                                        cvt->d_moddown_fp);
+                nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv);
+                ctx->launches += 1;
+            }
+            nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv,
+                                                                                       nttfp::PlainIn(), outf);
+            ctx->launches += 2;
+            continue;
+        }
         if (ctx->log_n == 16 && fused_moddown() > 0) {
             const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
             LimbMap zm = identity_map(level);
@@ -468,7 +575,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             ctx->launches += 2;
             continue;
         }
-        if (A <= 8) {
+        if (A <= 8 && ctx->ntt_fp_ok && moddown_fp()) {
+            dim3 g(n / kT, nr * 2);
+            k_moddown_convert_fp<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                                   cvt->d_moddown_fp);
+            ENSI_LAUNCH_CHECK(ctx);
+        } else if (A <= 8) {
             dim3 g(n / kT, nr * 2);
             k_moddown_convert2<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
                                                  cvt->d_moddown2);

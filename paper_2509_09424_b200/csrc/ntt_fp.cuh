@@ -98,7 +98,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         for (uint32_t k = 0; k < 16; k++) {
             const uint32_t i = tt + 16 * k;
             if (PASS == FWD_A) v[k] = i2d((long long)in.load(a, row, limb, (uint32_t)gaddr(i)));
-            else v[k] = __longlong_as_double((long long)a[gaddr(i)]);
+            else v[k] = __longlong_as_double((long long)__ldcg(a + gaddr(i)));
         }
 #pragma unroll
         for (int lt = 7; lt >= 4; lt--) {
@@ -147,7 +147,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, 16 * tt + k)];
         } else {
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++) v[k] = __longlong_as_double((long long)a[gaddr(16 * tt + k)]);
+            for (uint32_t k = 0; k < 16; k++) v[k] = __longlong_as_double((long long)__ldcg(a + gaddr(16 * tt + k)));
         }
 #pragma unroll
         for (int lt = 0; lt <= 3; lt++) {

@@ -10,7 +10,7 @@ LIB = os.path.join(HERE, "libensi.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-Xptxas", "-O3"]
+         "-Xptxas", "-O3"] + os.environ.get("ENSI_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -26,6 +26,9 @@
 #include "ensi_internal.h"
 
 namespace ensi {
+#ifndef ENSI_NTTFP_MINB
+#define ENSI_NTTFP_MINB 3
+#endif
 namespace nttfp {
 
 enum Pass { FWD_A = 0, FWD_B = 1, INV_B = 2, INV_A = 3 };
@@ -75,18 +78,19 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
     const uint32_t tt = colp ? (tid >> 4) : (tid & 15);
     const uint32_t sub = blockIdx.x * 16 + sp;
     auto gaddr = [&](uint32_t i) -> uint64_t { return colp ? (uint64_t)sub + 256ull * i : 256ull * sub + i; };
-    auto twi = [&](uint32_t lt, uint32_t i1) -> uint32_t {
-        if (colp) return (128u >> lt) + (i1 >> (lt + 1));
-        return (32768u >> lt) + sub * (128u >> lt) + (i1 >> (lt + 1));
+    // twiddle index of the butterfly with lower point i1 at local stride 2^lt is pre(lt) + (i1 >> (lt + 1)).  For
+    // points i1 = tt + 16 k (lt >= 4) that is pre(lt) + (k >> (lt - 3)); for i1 = 16 tt + k (lt <= 3) it is
+    // pre(lt) + (tt << (3 - lt)) + (k >> (lt + 1)): each distinct twiddle is loaded once per thread and stage
+    // (15 + 15 loads per pass instead of one per butterfly -- the L1/LSU wavefronts were the limiter).
+    auto pre = [&](uint32_t lt) -> uint32_t {
+        return colp ? (128u >> lt) : (32768u >> lt) + sub * (128u >> lt);
     };
-    auto ct = [&](double& U, double& V, uint32_t t) {
-        const double2 w = W2[t];
+    auto ct = [&](double& U, double& V, const double2 w) {
         const double r = mulmod(V, w.x, w.y, qd);
         V = U - r;
         U = U + r;
     };
-    auto gs = [&](double& U, double& V, uint32_t t, bool reduce) {
-        const double2 w = W2[t];
+    auto gs = [&](double& U, double& V, const double2 w, bool reduce) {
         const double s = U + V;
         V = mulmod(U - V, w.x, w.y, qd);
         U = reduce ? red(s, qd, qinv) : s;
@@ -102,10 +106,13 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         }
 #pragma unroll
         for (int lt = 7; lt >= 4; lt--) {
-            const uint32_t ks = 1u << (lt - 4);
+            const uint32_t ks = 1u << (lt - 4), sh = lt - 3, base = pre(lt);
+            double2 w;
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++)
-                if (!(k & ks)) ct(v[k], v[k + ks], twi(lt, tt + 16 * k));
+            for (uint32_t k = 0; k < 16; k++) {
+                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ks)) ct(v[k], v[k + ks], w);
+            }
         }
 #pragma unroll
         for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, tt + 16 * k)] = WIDE ? red(v[k], qd, qinv) : v[k];
@@ -114,10 +121,13 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, 16 * tt + k)];
 #pragma unroll
         for (int lt = 3; lt >= 0; lt--) {
-            const uint32_t ks = 1u << lt;
+            const uint32_t ks = 1u << lt, sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
+            double2 w;
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++)
-                if (!(k & ks)) ct(v[k], v[k + ks], twi(lt, 16 * tt + k));
+            for (uint32_t k = 0; k < 16; k++) {
+                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ks)) ct(v[k], v[k + ks], w);
+            }
         }
         if (PASS == FWD_A) {
 #pragma unroll
@@ -151,11 +161,14 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         }
 #pragma unroll
         for (int lt = 0; lt <= 3; lt++) {
-            const uint32_t ks = 1u << lt;
+            const uint32_t ks = 1u << lt, sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
             const bool rd = WIDE ? (lt & 1) : (lt == 3);
+            double2 w;
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++)
-                if (!(k & ks)) gs(v[k], v[k + ks], twi(lt, 16 * tt + k), rd);
+            for (uint32_t k = 0; k < 16; k++) {
+                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ks)) gs(v[k], v[k + ks], w, rd);
+            }
         }
         if (PASS == INV_B) __syncthreads();
 #pragma unroll
@@ -165,11 +178,14 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, tt + 16 * k)];
 #pragma unroll
         for (int lt = 4; lt <= 7; lt++) {
-            const uint32_t ks = 1u << (lt - 4);
+            const uint32_t ks = 1u << (lt - 4), sh = lt - 3, base = pre(lt);
             const bool rd = WIDE ? (lt & 1) : (lt == 7);
+            double2 w;
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++)
-                if (!(k & ks)) gs(v[k], v[k + ks], twi(lt, tt + 16 * k), rd);
+            for (uint32_t k = 0; k < 16; k++) {
+                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ks)) gs(v[k], v[k + ks], w, rd);
+            }
         }
         if (PASS == INV_B) {
 #pragma unroll
@@ -183,7 +199,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
 }
 
 template <int PASS, class IN = PlainIn, class OUT = PlainOut>
-__global__ void __launch_bounds__(256, 3) k_ntt256(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
+__global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
                                                 const double2* __restrict__ tw, const double2* __restrict__ ninv,
                                                 IN in = IN(), OUT out = OUT()) {
     __shared__ double sm[16 * kRow];

@@ -343,6 +343,12 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
 // the epilogue's tcgen05.ld, already complete (tcgen05.wait::ld) and fenced (tcgen05.fence::before_thread_sync);
 // a release.cluster arrive would also drain every prior store of the thread (ERRBAR), measured at 25% of the
 // kernel's warp-stall samples.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -473,8 +479,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer (leader CTA only)
-        if (rank == 0 && lane == 0) {
+        // The whole warp runs the loop (warp-uniform control flow and operands, so descriptors live in uniform
+        // registers); one elected lane -- always lane 0, which therefore also owns the commits -- issues the MMAs.
+        // A single-lane loop made the compiler rebuild every descriptor through an ELECT/R2UR.BROADCAST loop
+        // (~23 instructions per MMA), and the issuer warp was busy 94% of its samples.
+        if (rank == 0) {
             if (A_RES) mbar_wait(afull, 0);
+            const uint64_t adesc0 = umma_desc(smem_u32(sA), 16, 1024);
+            const uint64_t bdesc0 = umma_desc(smem_u32(sB), kBStage2, 1024);
             uint32_t s = 0, ph = 0, it = 0;
             for (uint32_t t = p; t < ntiles; t += per_group, it++) {
                 const uint32_t acc = it & 1, use = it >> 1;
@@ -484,21 +496,24 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 for (uint32_t kb = 0; kb < kblocks; kb++) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + (A_RES ? kb : s) * kABox);
-                    const uint32_t b_base = smem_u32(sB + s * kBStage2);
+                    // descriptor start-address field is (smem address >> 4): K step of 32 bytes in A is +2, K step of
+                    // 32 rows x 128 bytes in B is +256
+                    const uint64_t ad = adesc0 + (uint64_t)(((A_RES ? kb : s) * kABox) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((s * kBStage2) >> 4);
+                    if (elect_one()) {
 #pragma unroll
-                    for (uint32_t kk = 0; kk < kBoxK / 32; kk++) {
-                        uint64_t ad = umma_desc(a_base + kk * 32, 16, 1024);
-                        uint64_t bd = umma_desc(b_base + kk * 32 * 128, kBStage2, 1024);
-                        mma_i8_2sm(d_tmem, ad, bd, (kb | kk) != 0);
+                        for (uint32_t kk = 0; kk < kBoxK / 32; kk++)
+                            mma_i8_2sm(d_tmem, ad + 2 * kk, bd + 256 * kk, (kb | kk) != 0);
+                        mma_commit_2sm_mc(&empty[s], all_mask);
                     }
-                    mma_commit_2sm_mc(&empty[s], all_mask);
+                    __syncwarp();
                     if (++s == kStages2) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                mma_commit_2sm_mc(&tfull[acc], pair_mask);
+                if (elect_one()) mma_commit_2sm_mc(&tfull[acc], pair_mask);
+                __syncwarp();
             }
         }
     } else {

@@ -24,6 +24,10 @@
 
 #include "ensi_internal.h"
 
+#ifndef ENSI_EPI_EARLY_RELEASE
+#define ENSI_EPI_EARLY_RELEASE 1
+#endif
+
 namespace ensi {
 
 namespace tc {
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
                 uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec,
-                uint32_t cpairs) {
+                uint32_t cpairs, uint32_t tile0) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages2 * kABox;
@@ -463,9 +467,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const uint16_t half_mask = (uint16_t)(all_mask & (rank ? 0xAAAAu : 0x5555u));
                         for (uint32_t j = lead >> 1; j < kBoxK / 32; j += cpairs)
                             tma_load_2d_2sm_mc(sB + s * kBStage2 + j * 4096, &map_b, &full[s], half_mask,
-                                               (int32_t)(t * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
+                                               (int32_t)((tile0 + t) * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
                     } else {
-                        tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)(t * 256 + rank * 128),
+                        tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)((tile0 + t) * 256 + rank * 128),
                                         (int32_t)(kb * kBoxK));
                     }
                     if (!A_RES)
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         uint32_t it = 0;
         for (uint32_t t = p; t < ntiles; t += per_group, it++) {
             const uint32_t acc = it & 1, use = it >> 1;
-            const uint32_t word0 = t * 32;
+            const uint32_t word0 = (tile0 + t) * 32;
             const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
             const Barrett br = tab.br(limb);
             const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
@@ -563,6 +567,24 @@ __global__ void __launch_bounds__(kThreads2, 1)
                                  : "memory");
                 }
             };
+#if ENSI_EPI_EARLY_RELEASE
+            // Drain the whole 128-column slice into registers (4 x 32 columns, one wait) and hand the accumulator
+            // back before any combine: the MMA issuer's wait for a free accumulator no longer includes the
+            // epilogue's arithmetic.
+            uint32_t rc[32], rd[32];
+            TMEM_LD_X32(tbase, ra);
+            TMEM_LD_X32(tbase + 32, rb);
+            TMEM_LD_X32(tbase + 64, rc);
+            TMEM_LD_X32(tbase + 96, rd);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+            combine4(ra, 0);
+            combine4(rb, 1);
+            combine4(rc, 2);
+            combine4(rd, 3);
+#else
             TMEM_LD_X32(tbase, ra);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             TMEM_LD_X32(tbase + 32, rb);
@@ -579,6 +601,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
             combine4(rb, 3);
+#endif
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
@@ -642,6 +665,19 @@ static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
     return ENSI_OK;
 }
 
+// ENSI_TC_FILL=0 disables the filler launch on the SMs the multicast clusters leave idle (A/B timing)
+// ENSI_TC_FILL=<percent> sets the filler pairs' assumed speed relative to the multicast pairs (tile split)
+static int fill_pct() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_TC_FILL");
+        v = e ? atoi(e) : 60;
+        if (v < 0) v = 0;
+    }
+    return v;
+}
+static bool fill_enabled() { return fill_pct() > 0; }
+
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
                      cudaStream_t st, uint64_t ctw, uint32_t limb0, int variant) {
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
@@ -678,6 +714,16 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map B");
+    }
+    CUtensorMap mb2 = mb;   // B map with 128-row boxes for the non-multicast filler launch
+    if (variant == TC_PAIR_MC) {
+        cuuint64_t dims[2] = {ctw * 8, d};
+        cuuint64_t strides[1] = {ctw * 8};
+        cuuint32_t box[2] = {128, 128u}, es[2] = {1, 1};
+        if (enc(&mb2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)x, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return set_err(ctx, ENSI_ECUDA, "tensor map B (filler)");
     }
     {   // Y = uint64 [m][ctw], box 16 words x 32 rows (SWIZZLE_128B; pair kernels: 8 words, SWIZZLE_64B)
         cuuint64_t dims[2] = {ctw, w->m};
@@ -718,7 +764,7 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
         const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
         void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t);
+                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t, uint32_t);
         if (ares) kern = mc ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<true, false>;
         else kern = mc ? tc::k_accum_tc2<false, true> : tc::k_accum_tc2<false, false>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -748,10 +794,46 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
             per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
         }
         per_group = std::min(per_group, ntiles);
+        // Filler: multicast clusters of 2*cpairs CTAs must sit inside one GPC, so the co-resident clusters can
+        // leave SMs idle (C2: 22 clusters of 6 = 132 of 148 SMs).  The idle SMs run the same kernel without
+        // multicast (plain pairs) on a proportional tail of the word tiles, on a forked stream.
+        uint32_t per_group2 = 0, t1 = ntiles;
+        if (mc && fill_enabled()) {
+            const int used = (int)(2 * pgroups * per_group);
+            per_group2 = sms > used ? (uint32_t)(sms - used) / (2 * pgroups) : 0;
+            if (per_group2 > 0)
+                t1 = (uint32_t)((uint64_t)ntiles * per_group * 100 / (per_group * 100 + per_group2 * fill_pct()));
+            if (t1 >= ntiles || t1 == 0) per_group2 = 0, t1 = ntiles;
+        }
+        if (per_group2 > 0) {
+            if (!ctx->st_fill) {
+                cudaStreamCreateWithFlags(&ctx->st_fill, cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&ctx->ev_fill_fork, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&ctx->ev_fill_join, cudaEventDisableTiming);
+            }
+            cudaEventRecord(ctx->ev_fill_fork, st);
+            cudaStreamWaitEvent(ctx->st_fill, ctx->ev_fill_fork, 0);
+        }
         cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
-        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
-                               ctx->tab, ec, cpairs);
+        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, t1, ctx->log_n, level, limb0,
+                               ctx->tab, ec, cpairs, 0u);
         ENSI_LAUNCH_CHECK(ctx);
+        if (e == cudaSuccess && per_group2 > 0) {
+            auto kern2 = ares ? tc::k_accum_tc2<true, false> : tc::k_accum_tc2<false, false>;
+            cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaLaunchConfig_t cfg2 = cfg;
+            cudaLaunchAttribute attr2[1];
+            attr2[0] = attr[0];
+            attr2[0].val.clusterDim.x = 2;
+            cfg2.attrs = attr2;
+            cfg2.stream = ctx->st_fill;
+            cfg2.gridDim = dim3(2 * pgroups * per_group2, 1, 1);
+            e = cudaLaunchKernelEx(&cfg2, kern2, ma, mb2, my, kblocks, pgroups, per_group2, ntiles - t1, ctx->log_n,
+                                   level, limb0, ctx->tab, ec, 1u, t1);
+            ENSI_LAUNCH_CHECK(ctx);
+            cudaEventRecord(ctx->ev_fill_join, ctx->st_fill);
+            cudaStreamWaitEvent(st, ctx->ev_fill_join, 0);
+        }
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");
     }

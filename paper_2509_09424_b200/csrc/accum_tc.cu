@@ -665,19 +665,6 @@ static int build_wt8(ensi_ctx* ctx, ensi_weights* w) {
     return ENSI_OK;
 }
 
-// ENSI_TC_FILL=0 disables the filler launch on the SMs the multicast clusters leave idle (A/B timing)
-// ENSI_TC_FILL=<percent> sets the filler pairs' assumed speed relative to the multicast pairs (tile split)
-static int fill_pct() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_TC_FILL");
-        v = e ? atoi(e) : 60;
-        if (v < 0) v = 0;
-    }
-    return v;
-}
-static bool fill_enabled() { return fill_pct() > 0; }
-
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
                      cudaStream_t st, uint64_t ctw, uint32_t limb0, int variant) {
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
@@ -714,16 +701,6 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map B");
-    }
-    CUtensorMap mb2 = mb;   // B map with 128-row boxes for the non-multicast filler launch
-    if (variant == TC_PAIR_MC) {
-        cuuint64_t dims[2] = {ctw * 8, d};
-        cuuint64_t strides[1] = {ctw * 8};
-        cuuint32_t box[2] = {128, 128u}, es[2] = {1, 1};
-        if (enc(&mb2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)x, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return set_err(ctx, ENSI_ECUDA, "tensor map B (filler)");
     }
     {   // Y = uint64 [m][ctw], box 16 words x 32 rows (SWIZZLE_128B; pair kernels: 8 words, SWIZZLE_64B)
         cuuint64_t dims[2] = {ctw, w->m};
@@ -794,46 +771,10 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
             per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
         }
         per_group = std::min(per_group, ntiles);
-        // Filler: multicast clusters of 2*cpairs CTAs must sit inside one GPC, so the co-resident clusters can
-        // leave SMs idle (C2: 22 clusters of 6 = 132 of 148 SMs).  The idle SMs run the same kernel without
-        // multicast (plain pairs) on a proportional tail of the word tiles, on a forked stream.
-        uint32_t per_group2 = 0, t1 = ntiles;
-        if (mc && fill_enabled()) {
-            const int used = (int)(2 * pgroups * per_group);
-            per_group2 = sms > used ? (uint32_t)(sms - used) / (2 * pgroups) : 0;
-            if (per_group2 > 0)
-                t1 = (uint32_t)((uint64_t)ntiles * per_group * 100 / (per_group * 100 + per_group2 * fill_pct()));
-            if (t1 >= ntiles || t1 == 0) per_group2 = 0, t1 = ntiles;
-        }
-        if (per_group2 > 0) {
-            if (!ctx->st_fill) {
-                cudaStreamCreateWithFlags(&ctx->st_fill, cudaStreamNonBlocking);
-                cudaEventCreateWithFlags(&ctx->ev_fill_fork, cudaEventDisableTiming);
-                cudaEventCreateWithFlags(&ctx->ev_fill_join, cudaEventDisableTiming);
-            }
-            cudaEventRecord(ctx->ev_fill_fork, st);
-            cudaStreamWaitEvent(ctx->st_fill, ctx->ev_fill_fork, 0);
-        }
         cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
-        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, t1, ctx->log_n, level, limb0,
+        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
                                ctx->tab, ec, cpairs, 0u);
         ENSI_LAUNCH_CHECK(ctx);
-        if (e == cudaSuccess && per_group2 > 0) {
-            auto kern2 = ares ? tc::k_accum_tc2<true, false> : tc::k_accum_tc2<false, false>;
-            cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaLaunchConfig_t cfg2 = cfg;
-            cudaLaunchAttribute attr2[1];
-            attr2[0] = attr[0];
-            attr2[0].val.clusterDim.x = 2;
-            cfg2.attrs = attr2;
-            cfg2.stream = ctx->st_fill;
-            cfg2.gridDim = dim3(2 * pgroups * per_group2, 1, 1);
-            e = cudaLaunchKernelEx(&cfg2, kern2, ma, mb2, my, kblocks, pgroups, per_group2, ntiles - t1, ctx->log_n,
-                                   level, limb0, ctx->tab, ec, 1u, t1);
-            ENSI_LAUNCH_CHECK(ctx);
-            cudaEventRecord(ctx->ev_fill_join, ctx->st_fill);
-            cudaStreamWaitEvent(st, ctx->ev_fill_join, 0);
-        }
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");
     }

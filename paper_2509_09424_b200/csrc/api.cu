@@ -358,11 +358,6 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
         }
         cudaEventDestroy(ctx->ev_start);
     }
-    if (ctx->st_fill) {
-        cudaStreamDestroy(ctx->st_fill);
-        cudaEventDestroy(ctx->ev_fill_fork);
-        cudaEventDestroy(ctx->ev_fill_join);
-    }
     delete ctx;
 }
 

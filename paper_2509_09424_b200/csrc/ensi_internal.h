@@ -98,9 +98,6 @@ struct ensi_ctx {
     size_t host_stage_words = 0;
     cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {}, ev_start = nullptr;
-    // tensor-core accumulate filler launch (idle SMs next to the multicast clusters)
-    cudaStream_t st_fill = nullptr;
-    cudaEvent_t ev_fill_fork = nullptr, ev_fill_join = nullptr;
     std::string err;
     uint64_t launches = 0;
 };

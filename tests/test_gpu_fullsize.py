@@ -113,3 +113,24 @@ def test_c2_rescale_bit_exact(c2, torch_cuda):
     ctx.rescale(_dev(torch, x), yd, 12)
     torch.cuda.synchronize()
     assert (yd.cpu().numpy().view(np.uint64) == want).all()
+
+
+@pytest.mark.parametrize("d,m", [(768, 3072), (2048, 2048)])
+def test_c3_c4_sampled_columns_bit_exact(c2, torch_cuda, d, m):
+    """BASELINE configs[2] (768->3072, 8-CTA multicast clusters, resident W^T) and configs[3] (2048x2048,
+    streamed W^T) at full size: sampled output columns == oracle Alg. 1 word for word.  Inputs are seeded uniform
+    words from synth (the accumulate is data-oblivious), copied to the host for the oracle."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    xd = synth.gen_words_torch(synth.SEED_BASE + 3, o.q, d, 12, o.n)
+    W = synth.gen_W(synth.SEED_BASE + 103, d, m)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, ctx.weights(W), yd, level=12)
+    torch.cuda.synchronize()
+    cols = [0, m // 2 + 5, m - 1]
+    got = yd[cols].cpu().numpy().view(np.uint64)
+    del yd
+    x = xd.cpu().numpy().view(np.uint64)
+    del xd
+    want = o.pcmm_a(x, W, cols=cols, nthreads=NTH)
+    assert (got == want).all()

@@ -358,6 +358,13 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
         }
         cudaEventDestroy(ctx->ev_start);
     }
+    if (ctx->st_ks[0]) {
+        for (int i = 0; i < 2; i++) {
+            cudaStreamDestroy(ctx->st_ks[i]);
+            cudaEventDestroy(ctx->ev_ks_done[i]);
+        }
+        cudaEventDestroy(ctx->ev_ks_fork);
+    }
     delete ctx;
 }
 

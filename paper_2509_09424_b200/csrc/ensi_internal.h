@@ -98,6 +98,9 @@ struct ensi_ctx {
     size_t host_stage_words = 0;
     cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {}, ev_start = nullptr;
+    // key switching: two internal streams for alternating rotation batches
+    cudaStream_t st_ks[2] = {};
+    cudaEvent_t ev_ks_done[2] = {}, ev_ks_fork = nullptr;
     std::string err;
     uint64_t launches = 0;
 };

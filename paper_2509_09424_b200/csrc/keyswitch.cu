@@ -454,6 +454,16 @@ static bool moddown_fp() {
     return v == 1;
 }
 
+// ENSI_KS_STREAMS=1 runs every batch on the caller's stream (A/B timing); default 2 internal streams
+static int ks_streams() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KS_STREAMS");
+        v = e ? atoi(e) : 2;
+    }
+    return v;
+}
+
 // Hoisted rotations of n_ct ciphertexts (input c at ct + c * in_stride words, [2][level][N']) by n_g Galois elements:
 // rotation (c, r) -> out + (c * out_c_stride + r) ciphertexts.  One ModUp per input; per batch of up to 32 Galois
 // elements one key-stationary KIP (each key word read once for all n_ct inputs) and one ModDown over n_ct * cnt.
@@ -486,15 +496,25 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     const uint32_t beta = cvt->beta;
     if (beta > 8) return set_err(ctx, ENSI_EINVAL, "more than 8 key-switch digits");
     const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), kMaxBatch);
-    // scratch: coef [level][n] | ext [n_ct][beta][E][n] | acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n]
+    const uint32_t nbatches = (uint32_t)((idx.size() + nb - 1) / nb);
+    // Batches alternate between two internal streams, each with its own (acc, z) buffers: the key inner product of
+    // batch b+1 (HBM-bound) runs alongside the ModDown transforms of batch b (FP64/LSU-bound).
+    const uint32_t nsets = (nbatches > 1 && ks_streams() > 1) ? 2 : 1;
+    // scratch: coef [level][n] | ext [n_ct][beta][E][n] | nsets x (acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n])
     const size_t w_coef = (size_t)level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
                  w_z = (size_t)n_ct * nb * 2 * level * n;
-    rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + w_acc + w_z) * 8);
+    rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + nsets * (w_acc + w_z)) * 8);
     if (rc) return rc;
     uint64_t* coef = (uint64_t*)ctx->scratch;
     uint64_t* ext = coef + w_coef;
-    uint64_t* acc = ext + n_ct * w_ext1;
-    uint64_t* z = acc + w_acc;
+    uint64_t* set0 = ext + n_ct * w_ext1;
+    if (nsets == 2 && !ctx->st_ks[0]) {
+        for (int i = 0; i < 2; i++) {
+            cudaStreamCreateWithFlags(&ctx->st_ks[i], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&ctx->ev_ks_done[i], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&ctx->ev_ks_fork, cudaEventDisableTiming);
+    }
 
     // ---- ModUp (once per input)
     for (uint32_t c = 0; c < n_ct; c++) {
@@ -507,8 +527,18 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         ntt_forward(ctx, ext + c * w_ext1, beta * E, ext_map(ctx, level), st);
     }
 
+    if (nsets == 2) {
+        cudaEventRecord(ctx->ev_ks_fork, st);
+        for (int i = 0; i < 2; i++) cudaStreamWaitEvent(ctx->st_ks[i], ctx->ev_ks_fork, 0);
+    }
+    const cudaStream_t st_caller = st;
+
     // ---- per batch of Galois elements
     for (size_t b0 = 0; b0 < idx.size(); b0 += nb) {
+        const uint32_t bi = (uint32_t)(b0 / nb);
+        cudaStream_t st = nsets == 2 ? ctx->st_ks[bi & 1] : st_caller;   // batches of a set run in order
+        uint64_t* acc = set0 + (size_t)(bi % nsets) * (w_acc + w_z);
+        uint64_t* z = acc + w_acc;
         const uint32_t cnt = (uint32_t)std::min<size_t>(nb, idx.size() - b0);
         GBatch gb{};
         for (uint32_t i = 0; i < cnt; i++) {
@@ -595,6 +625,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             dim3 g(n / kT, level, nr * 2);
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown);
             ENSI_LAUNCH_CHECK(ctx);
+        }
+    }
+    if (nsets == 2) {
+        for (int k = 0; k < 2; k++) {
+            cudaEventRecord(ctx->ev_ks_done[k], ctx->st_ks[k]);
+            cudaStreamWaitEvent(st, ctx->ev_ks_done[k], 0);
         }
     }
     cudaError_t e = cudaGetLastError();

@@ -83,7 +83,11 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
     // pre(lt) + (tt << (3 - lt)) + (k >> (lt + 1)): each distinct twiddle is loaded once per thread and stage
     // (15 + 15 loads per pass instead of one per butterfly -- the L1/LSU wavefronts were the limiter).
     auto pre = [&](uint32_t lt) -> uint32_t {
+#ifdef ENSI_ABL_TW
+        return colp ? (128u >> lt) : (32768u >> lt) + (sub & 1) * (128u >> lt);   // ablation: timing only
+#else
         return colp ? (128u >> lt) : (32768u >> lt) + sub * (128u >> lt);
+#endif
     };
     auto ct = [&](double& U, double& V, const double2 w) {
         const double r = mulmod(V, w.x, w.y, qd);

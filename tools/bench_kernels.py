@@ -70,7 +70,7 @@ def main():
     ms = timed(lambda: ctx.rescale(x, y, L), args.iters)
     out["rescale"] = {"cts": 64, "ms": ms, "us_per_ct": 1e3 * ms / 64}
     # hoisted rotations
-    for batch in (1, 32):
+    for batch in (1, 32, 128):
         gs = [pow(5, 128 * (b + 1), 2 * n) for b in range(batch)]
         keys = random_keys(ctx, gs, dnum, T, n)
         ctx.load_keys(galois=gs, rot_keys=keys)

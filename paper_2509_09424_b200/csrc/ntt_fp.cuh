@@ -108,14 +108,22 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             if (PASS == FWD_A) v[k] = i2d((long long)in.load(a, row, limb, (uint32_t)gaddr(i)));
             else v[k] = __longlong_as_double((long long)__ldcg(a + gaddr(i)));
         }
+        {
+            // the group's 15 distinct twiddles are fetched up front (one batch of loads in flight instead of
+            // a dependent load before every stage)
+            double2 tw[15];
 #pragma unroll
-        for (int lt = 7; lt >= 4; lt--) {
-            const uint32_t ks = 1u << (lt - 4), sh = lt - 3, base = pre(lt);
-            double2 w;
+            for (int lt = 7; lt >= 4; lt--) {
+                const uint32_t sh = lt - 3, base = pre(lt);
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++) {
-                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
-                if (!(k & ks)) ct(v[k], v[k + ks], w);
+                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (7 - lt)) - 1) + j] = W2[base + j];
+            }
+#pragma unroll
+            for (int lt = 7; lt >= 4; lt--) {
+                const uint32_t ks = 1u << (lt - 4), sh = lt - 3;
+#pragma unroll
+                for (uint32_t k = 0; k < 16; k++)
+                    if (!(k & ks)) ct(v[k], v[k + ks], tw[((1u << (7 - lt)) - 1) + (k >> sh)]);
             }
         }
 #pragma unroll
@@ -123,14 +131,22 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         __syncthreads();
 #pragma unroll
         for (uint32_t k = 0; k < 16; k++) v[k] = sm[sidx(sp, 16 * tt + k)];
+        {
+            // the group's 15 distinct twiddles are fetched up front (one batch of loads in flight instead of
+            // a dependent load before every stage)
+            double2 tw[15];
 #pragma unroll
-        for (int lt = 3; lt >= 0; lt--) {
-            const uint32_t ks = 1u << lt, sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
-            double2 w;
+            for (int lt = 3; lt >= 0; lt--) {
+                const uint32_t sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
 #pragma unroll
-            for (uint32_t k = 0; k < 16; k++) {
-                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
-                if (!(k & ks)) ct(v[k], v[k + ks], w);
+                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (3 - lt)) - 1) + j] = W2[base + j];
+            }
+#pragma unroll
+            for (int lt = 3; lt >= 0; lt--) {
+                const uint32_t ks = 1u << lt, sh = lt + 1;
+#pragma unroll
+                for (uint32_t k = 0; k < 16; k++)
+                    if (!(k & ks)) ct(v[k], v[k + ks], tw[((1u << (3 - lt)) - 1) + (k >> sh)]);
             }
         }
         if (PASS == FWD_A) {

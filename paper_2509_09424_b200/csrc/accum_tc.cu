@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
                 uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec,
-                uint32_t cpairs, uint32_t tile0) {
+                uint32_t cpairs) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages2 * kABox;
@@ -467,9 +467,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const uint16_t half_mask = (uint16_t)(all_mask & (rank ? 0xAAAAu : 0x5555u));
                         for (uint32_t j = lead >> 1; j < kBoxK / 32; j += cpairs)
                             tma_load_2d_2sm_mc(sB + s * kBStage2 + j * 4096, &map_b, &full[s], half_mask,
-                                               (int32_t)((tile0 + t) * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
+                                               (int32_t)(t * 256 + rank * 128), (int32_t)(kb * kBoxK + j * 32));
                     } else {
-                        tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)((tile0 + t) * 256 + rank * 128),
+                        tma_load_2d_2sm(sB + s * kBStage2, &map_b, &full[s], (int32_t)(t * 256 + rank * 128),
                                         (int32_t)(kb * kBoxK));
                     }
                     if (!A_RES)
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         uint32_t it = 0;
         for (uint32_t t = p; t < ntiles; t += per_group, it++) {
             const uint32_t acc = it & 1, use = it >> 1;
-            const uint32_t word0 = (tile0 + t) * 32;
+            const uint32_t word0 = t * 32;
             const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
             const Barrett br = tab.br(limb);
             const uint64_t olo = ec.off_lo[limb], ohi = ec.off_hi[limb];
@@ -741,7 +741,7 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
         const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
         void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t, uint32_t);
+                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t);
         if (ares) kern = mc ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<true, false>;
         else kern = mc ? tc::k_accum_tc2<false, true> : tc::k_accum_tc2<false, false>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -773,7 +773,7 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
         per_group = std::min(per_group, ntiles);
         cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
         e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
-                               ctx->tab, ec, cpairs, 0u);
+                               ctx->tab, ec, cpairs);
         ENSI_LAUNCH_CHECK(ctx);
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");

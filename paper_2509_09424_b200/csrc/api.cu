@@ -595,7 +595,6 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
         if (ctx->host_stage) {
             cudaDeviceSynchronize();
             cudaFree(ctx->host_stage);
-    cudaFree(ctx->lb_buf);
         }
         ctx->host_stage = nullptr;
         cudaError_t e = cudaMalloc(&ctx->host_stage, 2 * stage_words * 8);

@@ -121,6 +121,42 @@ def test_pcmm_a_encrypted_c1_bit_exact_and_decrypts(setup_c1, torch_cuda, kernel
         assert np.max(np.abs(z - zo)) < 1e-9
 
 
+def test_layout_b_after_host_pipeline_regrowth(setup_c1, torch_cuda):
+    """ctx-owned buffers keep their lifetimes across entry points: Layout B (ctx Layout-B buffer), then the
+    host-staged pipeline growing its staging area twice, new device allocations, then Layout B again -- still
+    bit-exact (a stray free of the Layout-B buffer on staging regrowth was a use-after-free)."""
+    from paper_2509_09424_b200 import Context
+    o, sk, pk, _ = setup_c1
+    torch = torch_cuda
+    ctx = Context(12, 3, 1, 3)
+    s, d, m = 16, 16, 16
+    k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, 0)
+    x = synth.gen_words(6300, o.q, n_in, 3, o.n)
+    W = synth.gen_W(6301, d, m)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
+    keys = np.stack([o.rotkey(6400 + i, g, sk) for i, g in enumerate(gk)])
+    want = o.pcmm_b(x, W, s, k, B, gk, keys)
+    ctx.load_keys(sk_ntt=sk, galois=gk, rot_keys=keys)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(xd, W, yd, level=3, layout=1, block_s=s)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+    for dd in (40, 300):
+        xa = synth.gen_words(6500 + dd, o.q, dd, 3, o.n)
+        Wa = synth.gen_W(6600 + dd, dd, 24)
+        ya = np.zeros((24, 2, 3, o.n), np.uint64)
+        ctx.pcmm_ternary_host(xa, ctx.weights(Wa), ya, level=3)
+        torch.cuda.synchronize()
+        assert (ya == o.pcmm_a(xa, Wa, nthreads=4)).all()
+    filler = torch.full((64 << 20,), 7, dtype=torch.int64, device="cuda")
+    yd.zero_()
+    ctx.pcmm_ternary(xd, W, yd, level=3, layout=1, block_s=s)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+    assert bool((filler == 7).all())
+
+
 @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 @pytest.mark.parametrize("d,m,level", [(37, 70, 3), (1, 1, 1), (64, 64, 2), (130, 3, 3), (5, 129, 1), (900, 200, 1)])
 def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level, kernel):

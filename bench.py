@@ -410,7 +410,10 @@ def main():
         # every rank copies its own token block's inputs in and outputs out (weak scaling): job-level metric
         out["e2e"] = {"value": e2e_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": world * d * ct_bytes,
                       "d2h_bytes_per_step": world * m * ct_bytes, "matches_device_path": ok,
-                      "api": "ensi_pcmm_ternary_host", "per_rank_ms": e2e_ms}
+                      "api": "ensi_pcmm_ternary_host", "per_rank_ms": e2e_ms,
+                      "pcie_GBps_per_rank": (d + m) * ct_bytes / (e2e_ms * 1e-3) / 1e9,
+                      "note": "PCIe-bound: both directions overlap; tools/pcie_bw.py measures 92.7 GB/s bidirectional "
+                              "pinned-copy bandwidth on the B200 box"}
     # ---- rotations/s (BASELINE metric's second clause), rank 0 only
     if not args.no_rot and rank == 0:
         del y

@@ -253,6 +253,20 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         else:
             out["rotations"]["per_32_batch"] = r
         del keys, y
+    # non-hoisted: 96 independent ciphertexts, each rotated by the same element (one ModUp per input; the key is
+    # read once for all 96 inputs)
+    gs1 = [pow(5, s, 2 * n)]
+    keys = _random_keys(ctx, gs1, cfg, n)
+    ctx.load_keys(galois=gs1, rot_keys=keys)
+    xb = synth.gen_words_torch(12, ctx.q, 96, L, n)
+    yb = torch.empty((96, 2, L, n), dtype=torch.int64, device="cuda")
+    for _ in range(warmup):
+        ctx.rotate_batch(xb, gs1, yb, L)
+    ms = time_loop(lambda: ctx.rotate_batch(xb, gs1, yb, L), steps, st)
+    out["rotations"]["independent_inputs"] = {
+        "value": 96 / (ms * 1e-3), "unit": "rotations/s", "ms_per_call": ms,
+        "mode": "96 independent ciphertexts x 1 Galois element (ensi_rotate_batch; one ModUp per rotation)"}
+    del keys, xb, yb
     # rescale 64 ciphertexts (level 12 -> 11)
     xr = synth.gen_words_torch(5, ctx.q, 64, L, n)
     yr = torch.empty((64, 2, L - 1, n), dtype=torch.int64, device="cuda")

@@ -686,6 +686,30 @@ int ensi_rotate_hoisted(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, cons
     return rc;
 }
 
+int ensi_rotate_batch(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, const uint64_t* galois, ensi_ct_view* y,
+                      void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (!galois && n_g) return set_err(ctx, ENSI_EINVAL, "NULL galois");
+    if ((uint64_t)y->count < (uint64_t)x->count * n_g) return set_err(ctx, ENSI_EDIM, "y.count < x.count * n_g");
+    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level != x.level");
+    if (overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
+    if (n_g == 0 || x->count == 0) return ENSI_OK;
+    DeviceGuard g(ctx->device);
+    const uint64_t ctw = (uint64_t)2 * x->level * ctx->n;
+    // inputs in chunks of at most 96 (bounds the ModUp and key-switch scratch)
+    for (uint32_t c0 = 0; c0 < x->count && !rc; c0 += 96) {
+        const uint32_t nc = std::min<uint32_t>(96, x->count - c0);
+        rc = rotate_hoisted_multi(ctx, x->data + (uint64_t)c0 * ctw, nc, ctw, x->level, n_g, galois,
+                                  y->data + (uint64_t)c0 * n_g * ctw, n_g, (cudaStream_t)stream);
+    }
+    if (!rc) y->log2_scale = x->log2_scale;
+    return rc;
+}
+
 int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* stream) {
     if (!ctx) return ENSI_EINVAL;
     int rc = check_view(ctx, x, "x");

@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
                                                       ModTab tab, const uint64_t* __restrict__ cm) {
     const uint32_t n = 1u << log_n, E = level + A;
     const uint32_t row = blockIdx.y, t = row / E, e = row % E;
+    const uint32_t beta_ = (level + A - 1) / A;
+    coef += (size_t)blockIdx.z * level * n;                // input ciphertext blockIdx.z of a batched ModUp
+    ext += (size_t)blockIdx.z * beta_ * E * n;
     const uint32_t li = e < level ? e : L + (e - level);
     const uint32_t lo = t * A, hi = min((t + 1) * A, level), cnt = hi - lo;
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
@@ -495,13 +498,15 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     if (rc) return rc;
     const uint32_t beta = cvt->beta;
     if (beta > 8) return set_err(ctx, ENSI_EINVAL, "more than 8 key-switch digits");
-    const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), kMaxBatch);
+    // rotations per key-switch batch: up to 32 Galois elements, and at most ~96 rotations (n_ct * cnt) so the
+    // (acc, z) scratch stays bounded (~2.8 GB per set at C2)
+    const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), std::max<uint32_t>(1, std::min<uint32_t>(kMaxBatch, 96 / n_ct)));
     const uint32_t nbatches = (uint32_t)((idx.size() + nb - 1) / nb);
     // Batches alternate between two internal streams, each with its own (acc, z) buffers: the key inner product of
     // batch b+1 (HBM-bound) runs alongside the ModDown transforms of batch b (FP64/LSU-bound).
     const uint32_t nsets = (nbatches > 1 && ks_streams() > 1) ? 2 : 1;
-    // scratch: coef [level][n] | ext [n_ct][beta][E][n] | nsets x (acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n])
-    const size_t w_coef = (size_t)level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
+    // scratch: coef [n_ct][level][n] | ext [n_ct][beta][E][n] | nsets x (acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n])
+    const size_t w_coef = (size_t)n_ct * level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
                  w_z = (size_t)n_ct * nb * 2 * level * n;
     rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + nsets * (w_acc + w_z)) * 8);
     if (rc) return rc;
@@ -516,15 +521,19 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         cudaEventCreateWithFlags(&ctx->ev_ks_fork, cudaEventDisableTiming);
     }
 
-    // ---- ModUp (once per input)
-    for (uint32_t c = 0; c < n_ct; c++) {
-        cudaMemcpyAsync(coef, ct + c * in_stride + (size_t)level * n, w_coef * 8, cudaMemcpyDeviceToDevice, st);
-        ntt_inverse(ctx, coef, level, identity_map(level), st);
-        dim3 g(n / kT, beta * E);
-        k_modup_convert<<<g, kT, 0, st>>>(coef, ext + c * w_ext1, ctx->log_n, level, ctx->L, A, ctx->tab,
-                                          cvt->d_modup);
+    // ---- ModUp (once per input; all inputs in one launch per step so small batches still fill the GPU)
+    {
+        const size_t row_b = (size_t)level * n * 8;
+        if (n_ct == 1)
+            cudaMemcpyAsync(coef, ct + (size_t)level * n, row_b, cudaMemcpyDeviceToDevice, st);
+        else
+            cudaMemcpy2DAsync(coef, row_b, ct + (size_t)level * n, in_stride * 8, row_b, n_ct,
+                              cudaMemcpyDeviceToDevice, st);
+        ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
+        dim3 g(n / kT, beta * E, n_ct);
+        k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
         ENSI_LAUNCH_CHECK(ctx);
-        ntt_forward(ctx, ext + c * w_ext1, beta * E, ext_map(ctx, level), st);
+        ntt_forward(ctx, ext, n_ct * beta * E, ext_map(ctx, level), st);
     }
 
     if (nsets == 2) {

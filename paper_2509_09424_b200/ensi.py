@@ -27,7 +27,7 @@ KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA, KERNEL_TC
 # every symbol include/ensi.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
-           "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rescale", "ensi_decrypt_debug",
+           "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch", "ensi_rescale", "ensi_decrypt_debug",
            "ensi_launch_count", "ensi_pcmm_kernel"]
 
 
@@ -84,6 +84,7 @@ def lib():
         L.ensi_pcmm_ternary_host.argtypes = [vp, vp, u32, C.c_double, vp, vp, u32, vp]
         L.ensi_ntt.argtypes = [vp, vp, u32, vp, u32, C.c_int, vp]
         L.ensi_rotate_hoisted.argtypes = [vp, C.POINTER(CtView), u32, vp, C.POINTER(CtView), vp]
+        L.ensi_rotate_batch.argtypes = [vp, C.POINTER(CtView), u32, vp, C.POINTER(CtView), vp]
         L.ensi_rescale.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp]
         L.ensi_decrypt_debug.argtypes = [vp, C.POINTER(CtView), u32, vp, vp]
         L.ensi_launch_count.argtypes = [vp]
@@ -247,6 +248,13 @@ class Context:
         xv, yv = self.view(x, level), self.view(y, level)
         self._check(lib().ensi_rotate_hoisted(self.h, C.byref(xv), ga.shape[0], _np_ptr(ga), C.byref(yv),
                                               _stream_ptr(stream)))
+
+    def rotate_batch(self, x, galois, y, level: int, stream=None):
+        """y[c * len(galois) + r] = Rot_{galois[r]}(x[c]) for every input c (hoisted, key-stationary)."""
+        ga = np.ascontiguousarray(galois, np.uint64)
+        xv, yv = self.view(x, level), self.view(y, level)
+        self._check(lib().ensi_rotate_batch(self.h, C.byref(xv), ga.shape[0], _np_ptr(ga), C.byref(yv),
+                                            _stream_ptr(stream)))
 
     def rescale(self, x, y, level: int, log2_scale: float = 80.0, stream=None) -> float:
         xv, yv = self.view(x, level, log2_scale), self.view(y, level - 1)

@@ -284,6 +284,24 @@ def test_rotate_hoisted_bit_exact(rot_setup, torch_cuda, level):
     assert np.max(np.abs(got - np.roll(z, -1))) < 1e-5
 
 
+@pytest.mark.parametrize("n_ct,sel", [(3, [0, 3]), (40, [5]), (5, [1, 2, 3, 4, 5, 6, 7])])
+def test_rotate_batch_bit_exact(rot_setup, torch_cuda, n_ct, sel):
+    """ensi_rotate_batch: y[c * n_g + r] = Rot_{g_r}(x_c) == oracle single rotation, every word (several inputs
+    share each key batch; n_g = 1 over 40 inputs is the non-hoisted batch case)."""
+    o, sk, pk, ctx, gs, keys = rot_setup
+    torch = torch_cuda
+    x = synth.gen_words(7700 + n_ct, o.q, n_ct, 3, o.n)
+    g_sel = [gs[i] for i in sel]
+    yd = torch.empty((n_ct * len(sel), 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_batch(dev(torch, x), g_sel, yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    for c in range(n_ct):
+        for r, i in enumerate(sel):
+            if c < 3 or c == n_ct - 1:
+                assert (got[c * len(sel) + r] == o.rotate(x[c], gs[i], keys[i])).all()
+
+
 def test_rotate_identity_element_copies(rot_setup, torch_cuda):
     o, sk, pk, ctx, gs, keys = rot_setup
     torch = torch_cuda

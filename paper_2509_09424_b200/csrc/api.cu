@@ -344,6 +344,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
         cudaFree(c.d_moddown);
         cudaFree(c.d_moddown2);
         cudaFree(c.d_moddown_fp);
+        cudaFree(c.d_modup_fp);
     }
     cudaFree(ctx->scratch);
     cudaFree(ctx->host_stage);

@@ -112,6 +112,27 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
         cudaMemcpy(ct.d_moddown2, md2.data(), md2.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
         return cuda_err(ctx, cudaGetLastError(), "conv_tables md2");
     if (ctx->ntt_fp_ok) {
+        // ModUp, FP64 copy of mu with every constant centred and paired with RN(c / modulus)
+        std::vector<double> uf(mu.size());
+        auto centred_ = [](uint64_t w, uint64_t q) -> double { return w > q / 2 ? -(double)(q - w) : (double)w; };
+        for (uint32_t t = 0; t < beta; t++) {
+            const uint32_t lo = t * A, hi = std::min((t + 1) * A, level);
+            for (uint32_t a = 0; a < hi - lo; a++) {
+                const uint64_t q = ctx->mod[lo + a];
+                const size_t i0 = ((size_t)t * A + a) * 2;
+                uf[i0] = centred_(mu[i0], q);
+                uf[i0 + 1] = uf[i0] / (double)q;
+                for (uint32_t e = 0; e < E; e++) {
+                    const uint64_t r = ctx->mod[ext_limb(ctx, level, e)];
+                    const size_t i1 = off1 + (((size_t)t * E + e) * A + a) * 2;
+                    uf[i1] = centred_(mu[i1], r);
+                    uf[i1 + 1] = uf[i1] / (double)r;
+                }
+            }
+        }
+        if (cudaMalloc(&ct.d_modup_fp, uf.size() * 8) != cudaSuccess ||
+            cudaMemcpy(ct.d_modup_fp, uf.data(), uf.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+            return cuda_err(ctx, cudaGetLastError(), "conv_tables modup fp");
         std::vector<double> mf((size_t)A * 2 + (size_t)level * A * 2);
         auto centred = [](uint64_t w, uint64_t q) -> double { return w > q / 2 ? -(double)(q - w) : (double)w; };
         for (uint32_t k = 0; k < A; k++) {
@@ -174,6 +195,55 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
         out = reduce64(sum, tab.br(li));
     }
     ext[(size_t)row * n + k] = out;
+}
+
+// FP64 ModUp conversion, one thread per (input, digit t, position k) producing all E extended limbs: the digit's
+// y_i = [c_i (Q_t/q_i)^-1]_{q_i} (canonical, as the oracle's uncorrected fast conversion requires, R10) are computed
+// once; ext_r = sum_i y_i [Q_t/q_i]_r with |partial sums| <= 2.5 r, one centred reduction, canonical store.
+// The digit's own limbs are copied (the NTT that follows restores the input's NTT words).
+__global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                         uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                         ModTab tab, const double* __restrict__ cf) {
+    const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
+    const uint32_t t = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    coef += (size_t)blockIdx.z * level * n;
+    ext += ((size_t)blockIdx.z * beta + t) * E * n;
+    const uint32_t lo = t * A, hi = min((t + 1) * A, level), cnt = hi - lo;
+    const double* cinv = cf + (size_t)t * A * 2;
+    const double* cq = cf + (size_t)beta * A * 2 + (size_t)t * E * A * 2;
+    uint64_t own[8];
+    double y[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; a++) {
+        if (a < cnt) {
+            const uint64_t qa = tab.q[lo + a];
+            own[a] = coef[(size_t)(lo + a) * n + k];
+            double r = nttfp::mulmod(nttfp::i2d((long long)own[a]), __ldg(cinv + 2 * a), __ldg(cinv + 2 * a + 1),
+                                     (double)qa);
+            y[a] = r < 0.0 ? r + (double)qa : r;                     // canonical [0, q_a)
+        }
+    }
+    for (uint32_t e = 0; e < E; e++) {
+        const uint32_t li = e < level ? e : L + (e - level);
+        uint64_t out;
+        if (li >= lo && li < hi) {
+            out = 0;
+#pragma unroll
+            for (uint32_t a = 0; a < 8; a++)
+                if (a < cnt && lo + a == li) out = own[a];
+        } else {
+            const uint64_t r = tab.q[li];
+            const double rd = (double)r;
+            const double* c = cq + (size_t)e * A * 2;
+            double sum = 0.0;
+#pragma unroll
+            for (uint32_t a = 0; a < 8; a++)
+                if (a < cnt) sum += nttfp::mulmod(y[a], __ldg(c + 2 * a), __ldg(c + 2 * a + 1), rd);
+            out = nttfp::canon(nttfp::red(sum, rd, 1.0 / rd), r);
+        }
+        ext[(size_t)e * n + k] = out;
+    }
 }
 
 // Key inner product with the automorphism fused on load, both key polynomials per thread (the digit gathers are
@@ -530,8 +600,14 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             cudaMemcpy2DAsync(coef, row_b, ct + (size_t)level * n, in_stride * 8, row_b, n_ct,
                               cudaMemcpyDeviceToDevice, st);
         ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
-        dim3 g(n / kT, beta * E, n_ct);
-        k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
+        if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
+            dim3 g(n / kT, beta, n_ct);
+            k_modup_convert_fp<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                                 cvt->d_modup_fp);
+        } else {
+            dim3 g(n / kT, beta * E, n_ct);
+            k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
+        }
         ENSI_LAUNCH_CHECK(ctx);
         ntt_forward(ctx, ext, n_ct * beta * E, ext_map(ctx, level), st);
     }

@@ -388,8 +388,15 @@ def main():
         else:
             roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": gbs / peaks["hbm_gbs"]}
-        roofline.update({"traffic": None, "kernel": "k_accum_tc", "tensor_ops_per_launch": tc_ops,
-                         "tensor_peak_tops": tc_peak, "tensor_frac": tc_ach / tc_peak})
+        # ncu's own INT8 dense peak (sm__ops_path_tensor_op_utcimma: 16384 ops/clk/SM) -- the no-epilogue ablation
+        # reaches ~98 % of it, i.e. the bf16-derived peak above understates INT8 throughput (profiles/)
+        ncu_peak = 16384 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        # DRAM traffic of one launch from the committed ncu --set full capture (C2 layer only)
+        traffic = 9664524288 + 9623952384 if (args.config == "C2" and d == 768 and m == 768) else None
+        roofline.update({"traffic": traffic, "kernel": "k_accum_tc2", "tensor_ops_per_launch": tc_ops,
+                         "tensor_peak_tops": tc_peak, "tensor_frac": tc_ach / tc_peak,
+                         "int8_peak_tops_ncu": ncu_peak, "frac_vs_ncu_int8_peak": tc_ach / ncu_peak,
+                         "traffic_source": "profiles/r01_ncu_accum_tcgen05.md (ncu --set full, dram read + write)"})
     else:
         alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
         alu_ach = 2 * term_words / (ms_rank * 1e-3) / 1e12

@@ -1,7 +1,9 @@
 // poly.cu -- rescale (row a4), decrypt pointwise (row a10) and ciphertext add (Layout-B giant steps).
 #include <cmath>
+#include <cstdlib>
 
 #include "ensi_internal.h"
+#include "ntt_fp.cuh"
 
 namespace ensi {
 
@@ -45,6 +47,46 @@ __global__ void __launch_bounds__(kT) k_copy_last_limb(const uint64_t* __restric
     out[(size_t)cp * n + k] = in[((size_t)cp * level + level - 1) * n + k];
 }
 
+// FP64-NTT rescale with the conversion fused into the first forward pass (load) and the final combine into the
+// last pass (store): no converted-limb or transformed-limb round trip through HBM.  Row r of the transform = (cp =
+// r / (l-1) ciphertext-poly, limb i = r % (l-1)).
+struct RescaleInFp {
+    const uint64_t* tl;                 // INTT'd last limb, [count*2][n]
+    uint64_t ql;
+    uint32_t lm1;
+    double qd[ENSI_MAXT];
+    __device__ __forceinline__ uint64_t load(const uint64_t*, uint32_t row, uint32_t i, uint32_t k) const {
+        const uint32_t cp = row / lm1;
+        const uint64_t t = tl[(size_t)cp * 65536 + k];
+        const long long vc = t > (ql >> 1) ? (long long)t - (long long)ql : (long long)t;   // centred, R12
+        const double q = qd[i];
+        return nttfp::canon(nttfp::red(nttfp::i2d(vc), q, 1.0 / q), (uint64_t)q);
+    }
+};
+struct RescaleOutFp {
+    const uint64_t* in;                 // [count*2][level][n]
+    uint64_t* out;                      // [count*2][level-1][n]
+    uint32_t level, lm1;
+    double qd[ENSI_MAXT], c[ENSI_MAXT], cq[ENSI_MAXT];   // q_i, [q_last^-1]_{q_i} centred, RN(c / q_i)
+    __device__ __forceinline__ void store(uint64_t*, uint32_t row, uint32_t i, uint32_t k, uint64_t tt) const {
+        const uint32_t cp = row / lm1;
+        const uint64_t x = in[((size_t)cp * level + i) * 65536 + k];
+        const double V = (double)(long long)x - (double)(long long)tt;       // exact, |V| < q_i
+        const double q = qd[i];
+        out[((size_t)cp * lm1 + i) * 65536 + k] = nttfp::canon(nttfp::mulmod(V, c[i], cq[i], q), (uint64_t)q);
+    }
+};
+
+// ENSI_RESCALE=unfused forces the separate convert / NTT / final kernels (A/B timing)
+static bool rescale_fused() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_RESCALE");
+        v = (e && e[0] == 'u') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st) {
     const uint32_t n = ctx->n, lm1 = level - 1;
     if (count == 0) return ENSI_OK;
@@ -66,6 +108,33 @@ int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, u
     LimbMap lm = identity_map(1);
     lm.limb[0] = (uint8_t)lm1;
     ntt_inverse(ctx, tl, count * 2, lm, st);
+    if (ctx->log_n == 16 && ctx->ntt_fp_ok && rescale_fused()) {
+        RescaleInFp fin{};
+        RescaleOutFp fout{};
+        fin.tl = tl;
+        fin.ql = ql;
+        fin.lm1 = lm1;
+        fout.in = in;
+        fout.out = out;
+        fout.level = level;
+        fout.lm1 = lm1;
+        for (uint32_t i = 0; i < lm1; i++) {
+            const uint64_t q = ctx->mod[i];
+            fin.qd[i] = fout.qd[i] = (double)q;
+            fout.c[i] = rc.qlinv[i] > q / 2 ? -(double)(q - rc.qlinv[i]) : (double)rc.qlinv[i];
+            fout.cq[i] = fout.c[i] / (double)q;
+        }
+        const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
+        const double2* ninv = tw + (size_t)ctx->T * 2 * n;
+        const LimbMap zm = identity_map(lm1);
+        dim3 g(16, count * 2 * lm1);
+        nttfp::k_ntt256<nttfp::FWD_A, RescaleInFp><<<g, 256, 0, st>>>(tc, zm, ctx->tab, tw, ninv, fin);
+        nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, RescaleOutFp><<<g, 256, 0, st>>>(tc, zm, ctx->tab, tw, ninv,
+                                                                                    nttfp::PlainIn(), fout);
+        ctx->launches += 2;
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "rescale");
+    }
     k_rescale_convert<<<dim3(n / kT, lm1, count * 2), kT, 0, st>>>(tl, tc, ctx->log_n, level, ctx->tab, rc);
     ENSI_LAUNCH_CHECK(ctx);
     ntt_forward(ctx, tc, count * 2 * lm1, identity_map(lm1), st);

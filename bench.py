@@ -307,6 +307,31 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         del xs, ys, w
         torch.cuda.empty_cache()
     out["layout_a_shapes"] = sweep
+    # the paper's own Table III / Fig. 8 PCMM shapes at its default N'=2^14 (PAPER.md:478,
+    # 575,583,588,492) -- context beside the A100 (Phantom) 1.78 / 3.12 / 1.57 s and the single-core 1.41 s.  The
+    # paper does not state the limb count at PCMM time, so both l = 12 (our configs) and l = 48 (its stated L) run.
+    table3 = {}
+    for lv, alpha in ((12, 4), (48, 16)):
+        c14 = ctx_cls(14, lv, alpha, 3)
+        n14 = 1 << 14
+        row = {}
+        for name, (dd, mm, reps) in (("qkv_1536x1536_x3", (1536, 1536, 3)), ("gate_up_1536x4096_x2", (1536, 4096, 2)),
+                                     ("down_4096x1536", (4096, 1536, 1)), ("fig8_768x64", (768, 64, 1))):
+            W = synth.gen_W(synth.SEED_BASE + 7 * dd + mm, dd, mm)
+            w = c14.weights(W)
+            xs = synth.gen_words_torch(19, c14.q, dd, lv, n14)
+            ys = torch.empty((mm, 2, lv, n14), dtype=torch.int64, device="cuda")
+            c14.pcmm_ternary(xs, w, ys, level=lv)
+            ms = time_loop(lambda: c14.pcmm_ternary(xs, w, ys, level=lv), max(1, steps // 2), st)
+            row[name] = {"ms_total": ms * reps, "reps": reps}
+            del xs, ys, w
+            torch.cuda.empty_cache()
+        table3[f"l{lv}"] = row
+        c14.close()
+    out["paper_table3_n14"] = {"results": table3,
+                               "paper_seconds": {"qkv": 1.78, "gate_up": 3.12, "down": 1.57, "fig8_cpu_1core": 1.41},
+                               "note": "paper: A100 80GB, Phantom, per input amortized over a batch of 32; limb count "
+                                       "unstated (PAPER.md:575,583,588); fig8: i9-14900K single core (PAPER.md:492)"}
     ctx.close()
     torch.cuda.empty_cache()
     return out

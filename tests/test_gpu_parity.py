@@ -176,6 +176,25 @@ def test_pcmm_a_ragged_shapes(setup_c1, torch_cuda, d, m, level, kernel):
     assert (host(yd) == want).all()
 
 
+@pytest.mark.parametrize("L,alpha", [(12, 4), (48, 16)])
+def test_pcmm_a_paper_default_ring_n14(torch_cuda, L, alpha):
+    """The paper's default N'=2^14 at l = 12 and its stated L = 48 (64 moduli, the ctx maximum):
+    Layout A on uniform words == oracle, every word (bench's Table III shapes run in this configuration)."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(14, L, alpha, 3)
+    ctx = Context(14, L, alpha, 3)
+    assert ctx.moduli == o.moduli
+    d, m = 70, 40
+    x = synth.gen_words(1400 + L, o.q, d, L, o.n)
+    W = synth.gen_W(1401 + L, d, m)
+    want = o.pcmm_a(x, W, nthreads=4)
+    yd = torch.empty((m, 2, L, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(dev(torch, x), W, yd, level=L)
+    torch.cuda.synchronize()
+    assert (host(yd) == want).all()
+
+
 @pytest.mark.parametrize("kernel", [1, 2, 3, 4])
 def test_pcmm_host_staged_pipeline(setup_c1, torch_cuda, kernel):
     """ensi_pcmm_ternary_host (pinned host in/out, slice-pipelined) == oracle, every word."""

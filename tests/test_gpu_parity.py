@@ -455,3 +455,31 @@ def test_pcmm_a_block_shapes_streamed_a(torch_cuda, kernel, d, m):
     cols = sorted(set([0, 1, m // 3, m // 2 + 1, m - 2, m - 1]))
     want = o.pcmm_a(x, W, cols=cols, nthreads=8)
     assert (host(yd[cols]) == want).all()
+
+
+def test_cuda_graph_capture_replay(setup_c1, rot_setup, torch_cuda):
+    """The product path is capturable: Layout A (tensor-core accumulate) and hoisted rotations recorded into one
+    CUDA graph on a side stream and replayed give the same words as the oracle (no host sync inside the calls)."""
+    o, sk, pk, ctx, gs, keys = rot_setup
+    torch = torch_cuda
+    d, m = 40, 70
+    x = synth.gen_words(8100, o.q, d, 3, o.n)
+    W = synth.gen_W(8101, d, m)
+    w = ctx.weights(W)
+    xd = dev(torch, x)
+    yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    rd = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    ctx.pcmm_ternary(xd, w, yd, level=3, stream=s)          # warm-up outside capture (lazy tables, scratch)
+    ctx.rotate_hoisted(xd[:1], gs[:2], rd, 3, stream=s)
+    torch.cuda.synchronize()
+    yd.zero_()
+    rd.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.pcmm_ternary(xd, w, yd, level=3, stream=torch.cuda.current_stream())
+        ctx.rotate_hoisted(xd[:1], gs[:2], rd, 3, stream=torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    assert (host(yd) == o.pcmm_a(x, W, nthreads=4)).all()
+    assert (host(rd) == o.rotate_hoisted(x[0], gs[:2], keys[:2])).all()

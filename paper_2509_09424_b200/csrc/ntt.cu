@@ -189,14 +189,45 @@ static int ntt_env() {
 static bool use_v2(uint32_t log_n) { return log_n == 16 && ntt_env() >= 2; }
 static bool use_fp(const ensi_ctx* ctx) { return ctx->log_n == 16 && ctx->ntt_fp_ok && ntt_env() == 3; }
 
+// Tensor map of a row buffer for the TMA block passes: {16 words, N'/16 chunks, physical rows}, box {16, 256, 1},
+// SWIZZLE_128B.  ENSI_NTT_TMA=0 keeps the shared-memory transpose (A/B timing).
+typedef CUresult (*PFN_tmapEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, CUtensorMap* tm) {
+    static int env = -1;
+    static PFN_tmapEncode enc = nullptr;
+    if (env < 0) {
+        const char* e = getenv("ENSI_NTT_TMA");
+        env = (e && e[0] == '0') ? 0 : 1;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = (PFN_tmapEncode)p;
+    }
+    if (!env || !enc || rows == 0) return false;
+    const uint64_t n = ctx->n;
+    cuuint64_t dims[3] = {16, n / 16, map.phys(rows - 1) + 1};
+    cuuint64_t strides[2] = {128, n * 8};
+    cuuint32_t box[3] = {16, 256, 1}, es[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void*)data, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st) {
     if (rows == 0) return;
     const uint32_t log_n = ctx->log_n, n = ctx->n;
     if (use_fp(ctx)) {
         const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
         dim3 g(16, rows);
+        CUtensorMap tm;
         nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
-        nttfp::k_ntt256<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        if (row_tmap(ctx, data, rows, map, &tm))
+            nttfp::k_ntt256_tma<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm);
+        else
+            nttfp::k_ntt256<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         ctx->launches += 2;
         return;
     }
@@ -230,7 +261,11 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
     if (use_fp(ctx)) {
         const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
         dim3 g(16, rows);
-        nttfp::k_ntt256<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+        CUtensorMap tm;
+        if (row_tmap(ctx, data, rows, map, &tm))
+            nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm);
+        else
+            nttfp::k_ntt256<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         nttfp::k_ntt256<nttfp::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         ctx->launches += 2;
         return;

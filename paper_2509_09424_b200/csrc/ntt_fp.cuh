@@ -23,6 +23,8 @@
 // result to the canonical word in [0, q), so the output is bit-identical to the integer kernels (and the oracle).
 // The pass-A -> pass-B intermediate is stored as the double's bit pattern (private to the two launches).
 #pragma once
+#include <cuda.h>
+
 #include "ensi_internal.h"
 
 namespace ensi {
@@ -66,10 +68,40 @@ struct PlainOut {
 
 // tw: [limb][fwd/inv][N'] of (w centred, RN(w/q)) as double2, then [limb] of (n^-1 centred, RN(n^-1/q)).
 // Same CTA geometry as the integer v2 passes (ntt_v2.cuh): 16 sub-problems of 256 points, 16 points per thread.
-template <int PASS, bool WIDE, class IN, class OUT>
+// ---- TMA helpers for the block passes (tile = 16 consecutive 256-point blocks = 32 KB, SWIZZLE_128B)
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tile_load(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c1, int32_t c2) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(32768u) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+            "r"(su32(dst)),
+        "l"((uint64_t)map), "r"(su32(bar)), "r"(0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tile_wait(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(bar)),
+        "r"(0u)
+        : "memory");
+}
+__device__ __forceinline__ void tile_store(const CUtensorMap* map, const void* src, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"((uint64_t)map),
+                 "r"(su32(src)), "r"(0), "r"(c1), "r"(c2)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// 16-byte unit j (words 2j, 2j+1) of tile row r (128 bytes) under SWIZZLE_128B
+__device__ __forceinline__ uint32_t tile_off(uint32_t r, uint32_t j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+
+template <int PASS, bool WIDE, class IN, class OUT, bool TMA = false>
 __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t row, uint32_t limb, uint64_t q,
                                             const double2* __restrict__ W2, const double2* __restrict__ ninv,
-                                            double* sm, const IN& in, const OUT& out) {
+                                            double* sm, const IN& in, const OUT& out,
+                                            const CUtensorMap* tmap = nullptr, uint32_t prow = 0,
+                                            uint64_t* bar = nullptr) {
     const double qd = (double)q, qinv = 1.0 / qd;
     const bool fwd = PASS == FWD_A || PASS == FWD_B;
     const bool colp = PASS == FWD_A || PASS == INV_A;
@@ -153,6 +185,18 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
 #pragma unroll
             for (uint32_t k = 0; k < 16; k++)
                 a[gaddr(16 * tt + k)] = (uint64_t)__double_as_longlong(WIDE ? red(v[k], qd, qinv) : v[k]);
+        } else if (TMA) {
+            // final canonical words straight from registers into the swizzled tile, one TMA bulk store per CTA
+            __syncthreads();
+            uint8_t* tile = reinterpret_cast<uint8_t*>(sm);
+            const uint32_t r = sp * 16 + tt;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; j++)
+                *reinterpret_cast<ulonglong2*>(tile + tile_off(r, j)) =
+                    make_ulonglong2(canon(red(v[2 * j], qd, qinv), q), canon(red(v[2 * j + 1], qd, qinv), q));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) tile_store(tmap, tile, (int32_t)(256 * blockIdx.x), (int32_t)prow);
         } else {
             __syncthreads();
 #pragma unroll
@@ -169,7 +213,18 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             if (WIDE) s -= (s > (long long)(q >> 1)) ? (long long)q : 0;
             return i2d(s);
         };
-        if (PASS == INV_B) {
+        if (PASS == INV_B && TMA) {
+            if (threadIdx.x == 0) tile_load(sm, tmap, bar, (int32_t)(256 * blockIdx.x), (int32_t)prow);
+            tile_wait(bar);
+            const uint8_t* tile = reinterpret_cast<const uint8_t*>(sm);
+            const uint32_t r = sp * 16 + tt;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; j++) {
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(tile + tile_off(r, j));
+                v[2 * j] = load_in(x.x);
+                v[2 * j + 1] = load_in(x.y);
+            }
+        } else if (PASS == INV_B) {
 #pragma unroll
             for (uint32_t k = 0; k < 16; k++) sm[sidx(sp, tt + 16 * k)] = load_in(a[gaddr(tt + 16 * k)]);
             __syncthreads();
@@ -231,6 +286,35 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256(uint64_t* __res
     uint64_t* a = data + map.phys(row) * n;
     if (q >= (1ull << 41)) ntt256_body<PASS, true>(a, row, limb, q, W2, ninv, sm, in, out);
     else ntt256_body<PASS, false>(a, row, limb, q, W2, ninv, sm, in, out);
+}
+
+// Block passes with TMA tile I/O (PlainIn / PlainOut only): INV_B loads its 16 blocks with one bulk-tensor load,
+// FWD_B stores them with one bulk-tensor store, instead of a shared-memory transpose around coalesced
+// per-thread accesses.  tmap: the data buffer as a 3D tensor {16 words, N'/16 chunks, physical rows}.
+template <int PASS>
+__global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
+                                                    const double2* __restrict__ tw, const double2* __restrict__ ninv,
+                                                    const __grid_constant__ CUtensorMap tmap) {
+    __shared__ __align__(1024) double sm[16 * kRow];
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t n = 65536;
+    const uint32_t row = blockIdx.y, limb = map.limb[row % map.period];
+    const uint64_t q = tab.q[limb];
+    const bool fwd = PASS == FWD_A || PASS == FWD_B;
+    const double2* W2 = tw + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n;
+    const uint32_t prow = (uint32_t)map.phys(row);
+    uint64_t* a = data + (uint64_t)prow * n;
+    if (PASS == INV_B) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    const PlainIn in;
+    const PlainOut out;
+    if (q >= (1ull << 41)) ntt256_body<PASS, true, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
+    else ntt256_body<PASS, false, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
 }
 
 }  // namespace nttfp

@@ -1,4 +1,5 @@
 // poly.cu -- rescale (row a4), decrypt pointwise (row a10) and ciphertext add (Layout-B giant steps).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -87,7 +88,8 @@ static bool rescale_fused() {
     return v == 1;
 }
 
-int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st) {
+static int rescale_chunk(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out,
+                         cudaStream_t st) {
     const uint32_t n = ctx->n, lm1 = level - 1;
     if (count == 0) return ENSI_OK;
     RescaleConst rc{};
@@ -142,6 +144,17 @@ int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, u
     ENSI_LAUNCH_CHECK(ctx);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "rescale");
+}
+
+// Chunks of at most 256 ciphertexts: bounded scratch (256 x 2 x level limbs) and transform grids far below the
+// 65535-row launch limit, whatever the layer width (a 5504-output rescale epilogue is 121k limb rows).
+int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st) {
+    const uint64_t ci = (uint64_t)2 * level * ctx->n, co = (uint64_t)2 * (level - 1) * ctx->n;
+    for (uint32_t c0 = 0; c0 < count; c0 += 256) {
+        const int r = rescale_chunk(ctx, in + c0 * ci, std::min<uint32_t>(256, count - c0), level, out + c0 * co, st);
+        if (r) return r;
+    }
+    return ENSI_OK;
 }
 
 // mu[i][k] = c0[i][k] + c1[i][k] * s[i][k] mod q_i   (NTT form)

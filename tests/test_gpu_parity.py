@@ -397,6 +397,20 @@ def test_rescale_bit_exact(setup_c1, torch_cuda, level):
     assert (host(yd) == want).all()
 
 
+def test_rescale_chunked_many(setup_c1, torch_cuda):
+    """More ciphertexts than one rescale chunk (256): words on both sides of the chunk boundary == oracle."""
+    o, sk, pk, ctx = setup_c1
+    torch = torch_cuda
+    cnt = 300
+    x = synth.gen_words(95, o.q, cnt, 3, o.n)
+    yd = torch.empty((cnt, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(dev(torch, x), yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    for c in (0, 255, 256, cnt - 1):
+        assert (got[c] == o.rescale(x[c])).all()
+
+
 def test_pcmm_with_rescale_epilogue(setup_c1, torch_cuda):
     """Inputs at Delta^2 (un-rescaled products); PCMM then rescale == oracle PCMM then oracle rescale."""
     o, sk, pk, ctx = setup_c1

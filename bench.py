@@ -133,6 +133,16 @@ def max_over_ranks(world, v: float) -> float:
 
 # ------------------------------------------------------------------------------------------------ oracle arm
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample_ms(cfg, W, x_host, ncols: int, nthreads: int):
     """Time the plain oracle (Alg. 1) on `ncols` output columns of the layer; extrapolate by nnz."""
     import oracle
@@ -429,7 +439,8 @@ def main():
                     "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary",
                     "ops_per_launch": 2 * term_words}
     roofline.update({"algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
-                     "hbm_frac": gbs / peaks["hbm_gbs"], "peak_source": peak_src})
+                     "hbm_frac": gbs / peaks["hbm_gbs"], "hbm_frac_vs_8tbps_spec": gbs / 8000.0,
+                     "peak_source": peak_src})
 
     out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
@@ -473,8 +484,14 @@ def main():
         nth = max(1, min(64, os.cpu_count() or 1))
         ncols = max(1, min(m, nth))
         ms_cpu, dt, cols = oracle_sample_ms(cfg, W, x_host, ncols, nth)
+        # the same oracle on one core (1 core and all host cores), a 2-column sample
+        ms_1, dt_1, _ = oracle_sample_ms(cfg, W, x_host, 2, 1)
         out["cpu_baseline"] = {"value": ms_cpu, "unit": "ms/layer", "cores": nth, "kind": "oracle",
-                               "sample": f"{ncols} of {m} output columns ({dt:.1f} s wall), extrapolated by nnz"}
+                               "sample": f"{ncols} of {m} output columns ({dt:.1f} s wall), extrapolated by nnz",
+                               "one_core": {"value": ms_1, "unit": "ms/layer", "cores": 1,
+                                            "sample": f"2 of {m} output columns ({dt_1:.1f} s wall), "
+                                                      f"extrapolated by nnz"},
+                               "cpu_model": _cpu_model()}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

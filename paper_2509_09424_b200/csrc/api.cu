@@ -307,13 +307,25 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
         auto centred = [](uint64_t w, uint64_t q) -> double {
             return w > q / 2 ? -(double)(q - w) : (double)w;
         };
+        // table position of natural index k: identity, except the lane-transposed block-pass region at N'=2^16
+        // (ntt_fp.cuh): stage base m = 32768 >> lt (lt <= 3), block run b = m + sub (128 >> lt), k = b + tt J + j
+        // (J = 8 >> lt) -> b + j 16 + tt
+        auto tpos = [&](uint32_t k) -> uint32_t {
+            if (ctx->log_n != 16 || k < 4096) return k;
+            uint32_t lt = 0;
+            while ((32768u >> lt) > k) lt++;
+            const uint32_t m = 32768u >> lt, run = 128u >> lt, J = 8u >> lt;
+            const uint32_t b = m + ((k - m) / run) * run, off = k - b, tt = off / J, j = off % J;
+            return b + j * 16 + tt;
+        };
         for (uint32_t i = 0; i < ctx->T; i++) {
             const uint64_t q = ctx->mod[i];
             for (uint32_t dir = 0; dir < 2; dir++)
                 for (uint32_t k = 0; k < n; k++) {
                     const double c = centred(tw[(size_t)i * 4 * n + (size_t)dir * 2 * n + k], q);
-                    tw3[(((size_t)i * 2 + dir) * n + k) * 2 + 0] = c;
-                    tw3[(((size_t)i * 2 + dir) * n + k) * 2 + 1] = c / (double)q;
+                    const uint32_t kp = tpos(k);
+                    tw3[(((size_t)i * 2 + dir) * n + kp) * 2 + 0] = c;
+                    tw3[(((size_t)i * 2 + dir) * n + kp) * 2 + 1] = c / (double)q;
                 }
             const double c = centred(ctx->ninv[i], q);
             tw3[(size_t)ctx->T * 4 * n + 2 * i] = c;

@@ -67,6 +67,9 @@ struct PlainOut {
 };
 
 // tw: [limb][fwd/inv][N'] of (w centred, RN(w/q)) as double2, then [limb] of (n^-1 centred, RN(n^-1/q)).
+// Lane-transposed region: for the block-pass stages with local stride 2^lt <= 8 (table indices >= 4096), each
+// (stage, block) run of 128 >> lt twiddles is stored as [j][tt] instead of [tt][j] (tt < 16, j < 8 >> lt), so the
+// 16 lanes that need entry j of their own tt read 16 consecutive entries (was one 128-byte line per lane).
 // Same CTA geometry as the integer v2 passes (ntt_v2.cuh): 16 sub-problems of 256 points, 16 points per thread.
 // ---- TMA helpers for the block passes (tile = 16 consecutive 256-point blocks = 32 KB, SWIZZLE_128B)
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -169,9 +172,12 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             double2 tw[15];
 #pragma unroll
             for (int lt = 3; lt >= 0; lt--) {
-                const uint32_t sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
+                // block passes read the lane-transposed table region (twi_step = 16: the 16 lanes of a j are
+                // consecutive entries, one 256-byte coalesced load); column passes the natural order
+                const uint32_t sh = lt + 1, base = colp ? pre(lt) + (tt << (3 - lt)) : pre(lt) + tt;
+                const uint32_t step = colp ? 1u : 16u;
 #pragma unroll
-                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (3 - lt)) - 1) + j] = W2[base + j];
+                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (3 - lt)) - 1) + j] = W2[base + step * j];
             }
 #pragma unroll
             for (int lt = 3; lt >= 0; lt--) {
@@ -236,12 +242,13 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
         }
 #pragma unroll
         for (int lt = 0; lt <= 3; lt++) {
-            const uint32_t ks = 1u << lt, sh = lt + 1, base = pre(lt) + (tt << (3 - lt));
+            const uint32_t ks = 1u << lt, sh = lt + 1;
+            const uint32_t base = colp ? pre(lt) + (tt << (3 - lt)) : pre(lt) + tt, step = colp ? 1u : 16u;
             const bool rd = WIDE ? (lt & 1) : (lt == 3);
             double2 w;
 #pragma unroll
             for (uint32_t k = 0; k < 16; k++) {
-                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ((1u << sh) - 1))) w = W2[base + step * (k >> sh)];
                 if (!(k & ks)) gs(v[k], v[k + ks], w, rd);
             }
         }

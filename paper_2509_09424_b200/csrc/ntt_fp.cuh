@@ -29,7 +29,7 @@
 
 namespace ensi {
 #ifndef ENSI_NTTFP_MINB
-#define ENSI_NTTFP_MINB 3
+#define ENSI_NTTFP_MINB 4
 #endif
 namespace nttfp {
 

@@ -497,3 +497,57 @@ def test_cuda_graph_capture_replay(setup_c1, rot_setup, torch_cuda):
     torch.cuda.synchronize()
     assert (host(yd) == o.pcmm_a(x, W, nthreads=4)).all()
     assert (host(rd) == o.rotate_hoisted(x[0], gs[:2], keys[:2])).all()
+
+
+def _primes_1mod(mod2n, below, count, skip=0):
+    import sympy
+    out, v = [], (below - 1) // mod2n * mod2n + 1
+    while len(out) < count + skip:
+        if v < below and sympy.isprime(v):
+            out.append(v)
+        v -= mod2n
+    return out[skip:]
+
+
+def test_custom_moduli_all_size_classes_n16(torch_cuda):
+    """User-chosen moduli across the FP64 size classes at N'=2^16 (ntt_fp.cuh: 'wide' >= 2^41 incl. the largest
+    below 2^50, 'narrow' just under 2^41, and a 31-bit prime): NTT both directions on extreme rows, hoisted
+    rotations (ModUp / KIP / ModDown) and rescale, all word for word against the oracle."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    m2n = 1 << 17
+    q = [_primes_1mod(m2n, 1 << 50, 1)[0], _primes_1mod(m2n, (1 << 41) + (1 << 36), 1)[0],
+         _primes_1mod(m2n, 1 << 41, 1)[0], _primes_1mod(m2n, 1 << 31, 1)[0]]
+    p = [_primes_1mod(m2n, 1 << 50, 1, skip=1)[0], _primes_1mod(m2n, 1 << 45, 1)[0]]
+    o = oracle.Oracle(16, 4, 2, 2, q=q, p=p)
+    ctx = Context(16, 4, 2, 2, q=q, p=p)
+    assert ctx.moduli == o.moduli
+    T = 6
+    rows, limbs = [], []
+    for li in range(T):
+        qq = o.moduli[li]
+        for pat in (np.full(o.n, qq - 1, np.uint64), np.tile(np.array([0, qq - 1], np.uint64), o.n // 2),
+                    synth.gen_words(300 + li, [qq], 1, 1, o.n)[0, 0, 0]):
+            rows.append(pat)
+            limbs.append(li)
+    rows = np.stack(rows)
+    t = dev(torch, rows)
+    ctx.ntt(t, limbs)
+    assert (host(t) == np.stack([o.ntt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+    t = dev(torch, rows)
+    ctx.ntt(t, limbs, inverse=True)
+    assert (host(t) == np.stack([o.intt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+    skc, sk, pk = o.keygen(4242)
+    gs = [o.galois(3), o.galois(1000)]
+    keys = np.stack([o.rotkey(4300 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    ct = synth.gen_words(4400, o.q, 1, 4, o.n)[0]
+    yd = torch.empty((2, 2, 4, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(dev(torch, ct[None]), gs, yd, 4)
+    torch.cuda.synchronize()
+    assert (host(yd) == o.rotate_hoisted(ct, gs, keys)).all()
+    x = synth.gen_words(4500, o.q, 2, 4, o.n)
+    yr = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(dev(torch, x), yr, 4)
+    torch.cuda.synchronize()
+    assert (host(yr) == np.stack([o.rescale(x[c]) for c in range(2)])).all()

@@ -11,7 +11,6 @@
 #include <algorithm>
 
 #include "ensi_internal.h"
-#include "ntt_v2.cuh"
 #include "ntt_fp.cuh"
 
 namespace ensi {
@@ -281,32 +280,6 @@ __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, c
     }
 }
 
-// Key inner product with the automorphism fused on load.
-// acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r)
-__global__ void __launch_bounds__(kT) k_kip(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
-                                            uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
-                                            uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab) {
-    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
-    const uint32_t e = blockIdx.y, gi = blockIdx.z >> 1, j = blockIdx.z & 1;
-    const uint32_t li = e < level ? e : L + (e - level);
-    const uint32_t k = blockIdx.x * kT + threadIdx.x;
-    const uint64_t g = gb.g[gi];
-    const uint32_t src = galois_src_index(k, g, log_n);
-    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * T * n;
-    const Barrett br = tab.br(li);
-    U128 s{0, 0};
-    for (uint32_t t = 0; t < beta; t++) {
-        uint64_t dv = ext[((size_t)t * E + e) * n + src];
-        uint64_t kv = key[(((size_t)t * 2 + j) * T + li) * n + k];
-        mac128(s, dv, kv);
-        if ((t & 3) == 3 && t + 1 < beta) {
-            s.lo = barrett128(s.hi, s.lo, br);
-            s.hi = 0;
-        }
-    }
-    acc[(((size_t)gi * 2 + j) * E + e) * n + k] = barrett128(s.hi, s.lo, br);
-}
-
 // ModDown conversion: z[gi][j][i][k] = sum_k' y_k' [P/p_k']_{q_i}  (mod q_i), y_k' = [pc_k' (P/p_k')^-1]_{p_k'}
 // taken centred in (-p/2, p/2] (R10: zero-mean conversion overflow), pc = INTT'ed P limbs of acc.
 __global__ void __launch_bounds__(kT) k_moddown_convert(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
@@ -422,34 +395,10 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
 }
 
-// ---------------------------------------------------------------- fused ModDown (N' = 2^16, v2 NTT passes)
+// ---------------------------------------------------------------- fused ModDown (N' = 2^16, FP64 NTT passes; opt-in)
 // Row r of the z NTT = (gj = r / level, limb i = r % level).  The first NTT pass computes the centred fast
 // conversion of the INTT'ed P limbs on load (no z round trip through HBM); the last pass forms
 // (acc_{q_i} - NTT(z)) P^{-1} (+ sigma_g(c0)) on store and writes the rotated ciphertext directly.
-struct ModDownIn {
-    const uint64_t* acc;
-    const uint64_t* cm;
-    ModTab tab;
-    uint32_t level, L, A, E;
-    __device__ __forceinline__ uint64_t load(const uint64_t*, uint32_t row, uint32_t i, uint32_t k) const {
-        const uint32_t n = 65536, gj = row / level;
-        const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
-        const uint64_t* phinv = cm;
-        const uint64_t* ph = cm + (size_t)A * 2 + (size_t)i * A * 2;
-        const uint64_t* pmodq = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)level * 2 + (size_t)i * A;
-        const uint64_t q = tab.q[i];
-        const Barrett bq = tab.br(i);
-        uint64_t sum = 0;
-        for (uint32_t a = 0; a < A; a++) {
-            const uint64_t p = tab.q[L + a];
-            uint64_t y = mul_shoup(pc[(size_t)a * n], phinv[2 * a], phinv[2 * a + 1], p);
-            uint64_t yq = reduce64(y, bq);
-            if (y > (p >> 1)) yq = sub_mod(yq, pmodq[a], q);
-            sum += mul_shoup_lazy(yq, ph[2 * a], ph[2 * a + 1], q);
-        }
-        return reduce64(sum, bq);
-    }
-};
 struct ModDownInFp {
     const uint64_t* acc;
     const double* mf;
@@ -666,27 +615,6 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             }
             nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv,
                                                                                        nttfp::PlainIn(), outf);
-            ctx->launches += 2;
-            continue;
-        }
-        if (ctx->log_n == 16 && fused_moddown() > 0) {
-            const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
-            LimbMap zm = identity_map(level);
-            ModDownIn in{acc, cvt->d_moddown, ctx->tab, level, ctx->L, A, E};
-            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
-            dim3 g(16, nr * 2 * level);
-            if (fused_moddown() == 2) {
-                v2::k_ntt256<v2::FWD_A, ModDownIn, v2::PlainOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2,
-                                                                                   ninv, in, v2::PlainOut());
-            } else {
-                dim3 gc(n / kT, nr * 2);
-                k_moddown_convert2<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
-                                                      cvt->d_moddown, cvt->d_moddown2);
-                v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv);
-                ctx->launches += 1;
-            }
-            v2::k_ntt256<v2::FWD_B, v2::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, ctx->d_tw2, ninv,
-                                                                               v2::PlainIn(), outf);
             ctx->launches += 2;
             continue;
         }

@@ -27,8 +27,8 @@ KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA, KERNEL_TC
 # every symbol include/ensi.h declares (checked by tests/test_abi.py)
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
-           "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch", "ensi_rescale", "ensi_decrypt_debug",
-           "ensi_launch_count", "ensi_pcmm_kernel"]
+           "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
+           "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel"]
 
 
 class EnsiError(RuntimeError):
@@ -180,11 +180,14 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().ensi_launch_count(self.h))
 
-    @staticmethod
-    def view(t, level: int, log2_scale: float = 40.0) -> CtView:
-        """torch uint64 CUDA tensor [count][2][level][N'] -> ensi_ct_view."""
-        assert t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 8
-        assert t.dim() == 4 and t.shape[1] == 2 and t.shape[2] == level
+    def view(self, t, level: int, log2_scale: float = 40.0) -> CtView:
+        """torch 64-bit CUDA tensor [count][2][level][N'] on this context's device -> ensi_ct_view."""
+        if not (t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 8):
+            raise ValueError("ciphertexts must be a contiguous 64-bit CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{t.device.index}, context on cuda:{self.device}")
+        if t.dim() != 4 or t.shape[1] != 2 or t.shape[2] != level or t.shape[3] != self.n:
+            raise ValueError(f"expected [count][2][{level}][{self.n}], got {tuple(t.shape)}")
         return CtView(t.data_ptr(), t.shape[0], level, log2_scale)
 
     # ---- keys
@@ -199,7 +202,8 @@ class Context:
                 kp = rk.ctypes.data
                 self._keep_host = rk
             else:
-                assert rot_keys.is_cuda and rot_keys.is_contiguous()
+                if not (rot_keys.is_cuda and rot_keys.is_contiguous() and rot_keys.dtype.itemsize == 8):
+                    raise ValueError("device rotation keys must be a contiguous 64-bit CUDA tensor")
                 mem, kp = MEM_DEVICE, rot_keys.data_ptr()
                 self._keep_dev = rot_keys
         keys = Keys(sk.ctypes.data if sk is not None else None, ga.shape[0],
@@ -230,9 +234,13 @@ class Context:
     def pcmm_ternary_host(self, x_host: np.ndarray, w: Weights, y_host: np.ndarray, level: int, kernel: int = 0,
                           stream=None, log2_scale: float = 40.0):
         """End-to-end Layout A on host buffers (pinned recommended); enqueued on `stream` (sync before reading)."""
-        assert x_host.dtype.itemsize == 8 and y_host.dtype.itemsize == 8
-        assert x_host.flags.c_contiguous and y_host.flags.c_contiguous
-        assert x_host.shape[0] == w.d and y_host.shape[0] == w.m
+        if not (x_host.dtype.itemsize == 8 and y_host.dtype.itemsize == 8 and x_host.flags.c_contiguous
+                and y_host.flags.c_contiguous):
+            raise ValueError("host buffers must be C-contiguous 64-bit arrays")
+        if x_host.shape[0] != w.d or y_host.shape[0] != w.m:
+            raise ValueError("x_host / y_host leading dimensions must be d / m of the weights")
+        if x_host.size != w.d * 2 * level * self.n or y_host.size != w.m * 2 * level * self.n:
+            raise ValueError("host buffers must hold [count][2][level][N'] words")
         self._check(lib().ensi_pcmm_ternary_host(self.h, _np_ptr(x_host), level, log2_scale, w.h, _np_ptr(y_host),
                                                  kernel, _stream_ptr(stream)))
 

@@ -2,8 +2,8 @@
 //
 // y_i[w] = sum_{j : W[j][i] != 0} W[j][i] x_j[w]  mod q(w),  for every word w of the 2*l*N' words of a ciphertext.
 // This is a d -> m integer contraction over M = 2 l N' word positions.  Tiling:
-//   CTA = 8 warps = 64 outputs x 256 word positions (one limb, so q is CTA-uniform).
-//   warp w owns outputs i0 + 8w .. +8; lane owns positions lane + 32p, p < 8   ->  64 int64 accumulators.
+//   CTA = 8 warps = 64 outputs x 32*AP word positions (one limb, so q is CTA-uniform); AP = 4: 2 CTAs per SM.
+//   warp w owns outputs i0 + 8w .. +8; lane owns positions lane + 32p, p < AP  ->  8*AP int64 accumulators.
 //   x_j tiles (8 rows of 256 words) are staged in shared memory with cp.async, double buffered, and read by
 //   all 8 warps (each x word is fetched from L2/HBM once per 64 outputs).
 //   The weight sign is warp-uniform: one branch per (j, output) covers 8 words per lane, and zeros are
@@ -13,10 +13,14 @@
 // unique canonical value and equals the oracle bit for bit.
 #include "ensi_internal.h"
 
+#ifndef ENSI_ACC_AP
+#define ENSI_ACC_AP 4
+#endif
+
 namespace ensi {
 
 static constexpr int AO = 8;          // outputs per warp
-static constexpr int AP = 8;          // positions per lane
+static constexpr int AP = ENSI_ACC_AP;  // positions per lane
 static constexpr int AW = 8;          // warps per CTA
 static constexpr int ATI = AO * AW;   // 64 outputs per CTA
 static constexpr int ATW = 32 * AP;   // 256 positions per CTA
@@ -36,7 +40,7 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // planes: [d][2][mw] uint32 (pos bits, neg bits); bit (i % 32) of word i / 32; mw even, zero padded.
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 8 / AP)
     k_accum_ternary(const uint64_t* __restrict__ x, uint32_t d, uint64_t ctw, const uint32_t* __restrict__ planes,
                     uint32_t mw, uint32_t m, uint64_t* __restrict__ y, uint32_t log_n, uint32_t level, uint32_t limb0,
                     ModTab tab) {
@@ -59,11 +63,11 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t nstages = (d + AKC - 1) / AKC;
     auto load_stage = [&](uint32_t s, int buf) {
         const uint32_t j0 = s * AKC;
-        // x: AKC rows x 256 words = 2048 words = 1024 16-byte chunks; 4 per thread
+        // x: AKC rows x ATW words in 16-byte chunks, AKC * ATW / 512 per thread
 #pragma unroll
-        for (int c = 0; c < 4; c++) {
+        for (int c = 0; c < AKC * ATW / 512; c++) {
             uint32_t chunk = tid + c * 256;
-            uint32_t r = chunk >> 7, col = (chunk & 127) * 2;
+            uint32_t r = chunk / (ATW / 2), col = (chunk % (ATW / 2)) * 2;
             uint32_t j = j0 + r;
             if (j < d) cp_async16(&sx[buf][r][col], x + (uint64_t)j * ctw + pos0 + col);
         }

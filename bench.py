@@ -304,7 +304,8 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
     # Layout-A throughput at the other BASELINE shapes (C3 FFN pair, C4/C5 hidden-2048 projections)
     sweep = {}
     for name, (dd, mm) in (("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)), ("C4_2048x2048", (2048, 2048)),
-                           ("C5_2048x5504", (2048, 5504)), ("C5_5504x2048", (5504, 2048))):
+                           ("C5_2048x5504", (2048, 5504)), ("C5_5504x2048", (5504, 2048)),
+                           ("C5_qkv_2048x6144", (2048, 6144))):
         W = synth.gen_W(synth.SEED_BASE + dd + mm, dd, mm)
         w = ctx.weights(W)
         xs = synth.gen_words_torch(17, ctx.q, dd, L, n)
@@ -317,6 +318,10 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         del xs, ys, w
         torch.cuda.empty_cache()
     out["layout_a_shapes"] = sweep
+    # BASELINE configs[4]: one transformer block at hidden 2048 (Q/K/V fused 2048->6144, O 2048x2048, gate and up
+    # 2048->5504 run separately on one GPU, down 5504->2048), summed
+    blk = ["C5_qkv_2048x6144", "C4_2048x2048", "C5_2048x5504", "C5_2048x5504", "C5_5504x2048"]
+    out["c5_block"] = {"ms_per_block": sum(sweep[k]["ms_per_layer"] for k in blk), "projections": blk}
     # the paper's own Table III / Fig. 8 PCMM shapes at its default N'=2^14 (PAPER.md:478,
     # 575,583,588,492) -- context beside the A100 (Phantom) 1.78 / 3.12 / 1.57 s and the single-core 1.41 s.  The
     # paper does not state the limb count at PCMM time, so both l = 12 (our configs) and l = 48 (its stated L) run.

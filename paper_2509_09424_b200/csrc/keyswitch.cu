@@ -196,13 +196,22 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
     ext[(size_t)row * n + k] = out;
 }
 
+// Extended-digit row order.  perm == 0: row = e (limbs in Q_l u P order).  perm != 0 (every digit has A limbs):
+// the E - A converted limbs first, then the digit's own A limbs, which are copied in NTT form from the input
+// instead of being INTT'ed, converted and NTT'ed again -- the ModUp NTT then runs on E - A rows per digit.
+__device__ __forceinline__ uint32_t ext_row(uint32_t perm, uint32_t t, uint32_t e, uint32_t A, uint32_t E) {
+    if (!perm) return e;
+    const uint32_t lo = t * A, hi = lo + A;
+    return e < lo ? e : (e >= hi ? e - A : (E - A) + (e - lo));
+}
+
 // FP64 ModUp conversion, one thread per (input, digit t, position k) producing all E extended limbs: the digit's
 // y_i = [c_i (Q_t/q_i)^-1]_{q_i} (canonical, as the oracle's uncorrected fast conversion requires, R10) are computed
 // once; ext_r = sum_i y_i [Q_t/q_i]_r with |partial sums| <= 2.5 r, one centred reduction, canonical store.
 // The digit's own limbs are copied (the NTT that follows restores the input's NTT words).
 __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
                                                          uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
-                                                         ModTab tab, const double* __restrict__ cf) {
+                                                         ModTab tab, const double* __restrict__ cf, uint32_t perm) {
     const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
     const uint32_t t = blockIdx.y;
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
@@ -227,6 +236,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restr
         const uint32_t li = e < level ? e : L + (e - level);
         uint64_t out;
         if (li >= lo && li < hi) {
+            if (perm) continue;                  // copied from the input's NTT-form limbs by the host
             out = 0;
 #pragma unroll
             for (uint32_t a = 0; a < 8; a++)
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restr
                 if (a < cnt) sum += nttfp::mulmod(y[a], __ldg(c + 2 * a), __ldg(c + 2 * a + 1), rd);
             out = nttfp::canon(nttfp::red(sum, rd, 1.0 / rd), r);
         }
-        ext[(size_t)e * n + k] = out;
+        ext[(size_t)ext_row(perm, t, e, A, E) * n + k] = out;
     }
 }
 
@@ -250,7 +260,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restr
 __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
                                              uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
                                              uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab,
-                                             uint64_t ext_stride) {
+                                             uint64_t ext_stride, uint32_t perm) {
     const uint32_t n = 1u << log_n, E = level + A, T = L + A;
     const uint32_t e = blockIdx.y, gi = blockIdx.z;
     const uint32_t li = e < level ? e : L + (e - level);
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, c
         const uint64_t* ex = ext + (size_t)c * ext_stride;
         U128 s0{0, 0}, s1{0, 0};
         for (uint32_t t = 0; t < beta; t++) {
-            uint64_t dv = ex[((size_t)t * E + e) * n + src];
+            uint64_t dv = ex[((size_t)t * E + ext_row(perm, t, e, A, E)) * n + src];
             mac128(s0, dv, __ldg(key + ((size_t)t * 2 + 0) * T * n));
             mac128(s1, dv, __ldg(key + ((size_t)t * 2 + 1) * T * n));
             if ((t & 3) == 3 && t + 1 < beta) {
@@ -476,6 +486,16 @@ static bool moddown_fp() {
     return v == 1;
 }
 
+// ENSI_MODUP_PERM=0 keeps the INTT -> copy -> NTT round trip of the digits' own limbs (A/B timing)
+static bool modup_perm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_MODUP_PERM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // ENSI_KS_STREAMS=1 runs every batch on the caller's stream (A/B timing); default 2 internal streams
 static int ks_streams() {
     static int v = -1;
@@ -541,6 +561,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     }
 
     // ---- ModUp (once per input; all inputs in one launch per step so small batches still fill the GPU)
+    const uint32_t perm = (ctx->ntt_fp_ok && A <= 8 && moddown_fp() && level % A == 0 && modup_perm()) ? 1u : 0u;
     {
         const size_t row_b = (size_t)level * n * 8;
         if (n_ct == 1)
@@ -552,13 +573,35 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
             dim3 g(n / kT, beta, n_ct);
             k_modup_convert_fp<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab,
-                                                 cvt->d_modup_fp);
+                                                 cvt->d_modup_fp, perm);
         } else {
             dim3 g(n / kT, beta * E, n_ct);
             k_modup_convert<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_modup);
         }
         ENSI_LAUNCH_CHECK(ctx);
-        ntt_forward(ctx, ext, n_ct * beta * E, ext_map(ctx, level), st);
+        if (perm) {
+            // own limbs: the input's c1 limbs [tA, tA + A) in NTT form, to rows [E - A, E) of every digit block
+            const size_t own_b = (size_t)A * n * 8;
+            for (uint32_t t = 0; t < beta; t++) {
+                uint64_t* dst = ext + ((size_t)t * E + (E - A)) * n;
+                const uint64_t* src = ct + ((size_t)level + t * A) * n;
+                if (n_ct == 1)
+                    cudaMemcpyAsync(dst, src, own_b, cudaMemcpyDeviceToDevice, st);
+                else
+                    cudaMemcpy2DAsync(dst, w_ext1 * 8, src, in_stride * 8, own_b, n_ct, cudaMemcpyDeviceToDevice, st);
+            }
+            LimbMap em = identity_map(1);
+            em.period = beta * (E - A);
+            em.grp_rows = E - A;
+            em.grp_stride = E;
+            em.grp_off = 0;
+            for (uint32_t t = 0, r = 0; t < beta; t++)
+                for (uint32_t e = 0; e < E; e++)
+                    if (e < t * A || e >= (t + 1) * A) em.limb[r++] = (uint8_t)ext_limb(ctx, level, e);
+            ntt_forward(ctx, ext, n_ct * beta * (E - A), em, st);
+        } else {
+            ntt_forward(ctx, ext, n_ct * beta * E, ext_map(ctx, level), st);
+        }
     }
 
     if (nsets == 2) {
@@ -588,7 +631,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         {
             dim3 g(n / kT, E, cnt);
             k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                     ctx->tab, w_ext1);
+                                     ctx->tab, w_ext1, perm);
             ENSI_LAUNCH_CHECK(ctx);
         }
         LimbMap pm = identity_map(A);

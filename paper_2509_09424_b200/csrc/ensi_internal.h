@@ -48,6 +48,7 @@ struct ConvTables {
     // moddown for the FP64 conversion (moduli < 2^50): (P/p_k)^-1 mod p_k centred and RN(./p_k) [alpha][2], then
     // [P/p_k]_{q_i} centred and RN(./q_i) [level][alpha][2]
     double* d_moddown_fp = nullptr;
+    std::vector<double> h_moddown_fp;     // host copy (kernel-parameter constants)
     // modup for the FP64 conversion: same indexing as d_modup, (centred constant, RN(constant / modulus)) pairs
     double* d_modup_fp = nullptr;
 };

@@ -145,6 +145,7 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
                 mf[o] = centred(md[o], ctx->mod[i]);
                 mf[o + 1] = mf[o] / (double)ctx->mod[i];
             }
+        ct.h_moddown_fp = mf;
         if (cudaMalloc(&ct.d_moddown_fp, mf.size() * 8) != cudaSuccess ||
             cudaMemcpy(ct.d_moddown_fp, mf.data(), mf.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
             return cuda_err(ctx, cudaGetLastError(), "conv_tables fp");
@@ -388,6 +389,37 @@ __global__ void __launch_bounds__(kT) k_moddown_convert_fp(const uint64_t* __res
     }
 }
 
+// Same conversion with every constant in the kernel-parameter (constant) bank and the target / source loops fully
+// unrolled to fixed bounds: the products read their constants as instruction operands instead of ~100 uniform
+// global loads and 12 double divisions per position (level <= 16, alpha <= 8).
+struct MDConstFp {
+    double yw[8], ywq[8], p[8], hp[8];    // (P/p_k)^-1 mod p_k centred, RN(./p_k), p_k, floor(p_k / 2)
+    double c[16][8], cq[16][8];           // [P/p_k]_{q_i} centred, RN(./q_i)
+    double q[16], qinv[16];               // q_i, RN(1/q_i)
+};
+__global__ void __launch_bounds__(kT) k_moddown_convert_fpc(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
+                                                            uint32_t log_n, uint32_t level, uint32_t A,
+                                                            const __grid_constant__ MDConstFp mc) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t gj = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+    double y[8];
+#pragma unroll
+    for (uint32_t a = 0; a < 8; a++)
+        if (a < A) y[a] = y_centred(nttfp::i2d((long long)pc[(size_t)a * n]), mc.p[a], mc.hp[a], mc.yw[a], mc.ywq[a]);
+#pragma unroll
+    for (uint32_t i = 0; i < 16; i++) {
+        if (i < level) {
+            double s = 0.0;
+#pragma unroll
+            for (uint32_t a = 0; a < 8; a++)
+                if (a < A) s += nttfp::mulmod(y[a], mc.c[i][a], mc.cq[i][a], mc.q[i]);
+            z[((size_t)gj * level + i) * n + k] = nttfp::canon(nttfp::red(s, mc.q[i], mc.qinv[i]), (uint64_t)mc.q[i]);
+        }
+    }
+}
+
 // out[gi][j][i][k] = (acc_q_i - z) * P^-1 (+ c0[i][src_g(k)] when j == 0)
 __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
                                                       const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
@@ -482,6 +514,16 @@ static bool moddown_fp() {
     if (v < 0) {
         const char* e = getenv("ENSI_MODDOWN");
         v = (e && std::string(e) == "int") ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+static bool moddown_fpc() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_MODDOWN_FPC");
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }
@@ -663,6 +705,26 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         }
         if (A <= 8 && ctx->ntt_fp_ok && moddown_fp()) {
             dim3 g(n / kT, nr * 2);
+            if (level <= 16 && moddown_fpc()) {
+                MDConstFp mc{};
+                const std::vector<double>& mf = cvt->h_moddown_fp;
+                for (uint32_t a = 0; a < A; a++) {
+                    const uint64_t pk = ctx->mod[ctx->L + a];
+                    mc.yw[a] = mf[2 * a];
+                    mc.ywq[a] = mf[2 * a + 1];
+                    mc.p[a] = (double)pk;
+                    mc.hp[a] = (double)(pk >> 1);
+                }
+                for (uint32_t i = 0; i < level; i++) {
+                    mc.q[i] = (double)ctx->mod[i];
+                    mc.qinv[i] = 1.0 / mc.q[i];
+                    for (uint32_t a = 0; a < A; a++) {
+                        mc.c[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2];
+                        mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
+                    }
+                }
+                k_moddown_convert_fpc<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, A, mc);
+            } else
             k_moddown_convert_fp<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                    cvt->d_moddown_fp);
             ENSI_LAUNCH_CHECK(ctx);

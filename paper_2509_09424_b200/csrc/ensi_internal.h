@@ -51,6 +51,7 @@ struct ConvTables {
     std::vector<double> h_moddown_fp;     // host copy (kernel-parameter constants)
     // modup for the FP64 conversion: same indexing as d_modup, (centred constant, RN(constant / modulus)) pairs
     double* d_modup_fp = nullptr;
+    std::vector<double> h_modup_fp;       // host copy (kernel-parameter constants)
 };
 
 }  // namespace ensi

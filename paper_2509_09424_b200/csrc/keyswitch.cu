@@ -129,6 +129,7 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
                 }
             }
         }
+        ct.h_modup_fp = uf;
         if (cudaMalloc(&ct.d_modup_fp, uf.size() * 8) != cudaSuccess ||
             cudaMemcpy(ct.d_modup_fp, uf.data(), uf.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
             return cuda_err(ctx, cudaGetLastError(), "conv_tables modup fp");
@@ -253,6 +254,56 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restr
             out = nttfp::canon(nttfp::red(sum, rd, 1.0 / rd), r);
         }
         ext[(size_t)ext_row(perm, t, e, A, E) * n + k] = out;
+    }
+}
+
+// Same conversion with the constants in the kernel-parameter bank and the target/source loops unrolled to fixed
+// bounds (alpha <= 4, beta <= 4, E <= 16): no per-position constant loads or divisions.
+struct MUConstFp {
+    double cinv[4][4], cinvq[4][4];       // [t][a]: (Q_t/q_i)^-1 mod q_i centred, RN(./q_i)
+    double c[4][16][4], cq[4][16][4];     // [t][e][a]: [Q_t/q_i]_{r_e} centred, RN(./r_e)
+    double qs[16], r[16], rinv[16];       // q of the source limbs (Q order), r_e, RN(1/r_e)
+};
+__global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                          uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                          const __grid_constant__ MUConstFp mc, uint32_t perm) {
+    const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
+    const uint32_t t = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    coef += (size_t)blockIdx.z * level * n;
+    ext += ((size_t)blockIdx.z * beta + t) * E * n;
+    const uint32_t lo = t * A, hi = min((t + 1) * A, level), cnt = hi - lo;
+    uint64_t own[4];
+    double y[4];
+#pragma unroll
+    for (uint32_t a = 0; a < 4; a++) {
+        if (a < cnt) {
+            const double qa = mc.qs[lo + a];
+            own[a] = coef[(size_t)(lo + a) * n + k];
+            const double rr = nttfp::mulmod(nttfp::i2d((long long)own[a]), mc.cinv[t][a], mc.cinvq[t][a], qa);
+            y[a] = rr < 0.0 ? rr + qa : rr;                           // canonical [0, q_a)
+        }
+    }
+#pragma unroll
+    for (uint32_t e = 0; e < 16; e++) {
+        if (e < E) {
+            const uint32_t li = e < level ? e : L + (e - level);
+            if (li >= lo && li < hi) {
+                if (perm) continue;
+                uint64_t out = 0;
+#pragma unroll
+                for (uint32_t a = 0; a < 4; a++)
+                    if (a < cnt && lo + a == li) out = own[a];
+                ext[(size_t)e * n + k] = out;
+            } else {
+                double sum = 0.0;
+#pragma unroll
+                for (uint32_t a = 0; a < 4; a++)
+                    if (a < cnt) sum += nttfp::mulmod(y[a], mc.c[t][e][a], mc.cq[t][e][a], mc.r[e]);
+                ext[(size_t)ext_row(perm, t, e, A, E) * n + k] =
+                    nttfp::canon(nttfp::red(sum, mc.r[e], mc.rinv[e]), (uint64_t)mc.r[e]);
+            }
+        }
     }
 }
 
@@ -612,7 +663,27 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             cudaMemcpy2DAsync(coef, row_b, ct + (size_t)level * n, in_stride * 8, row_b, n_ct,
                               cudaMemcpyDeviceToDevice, st);
         ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
-        if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
+        if (ctx->ntt_fp_ok && A <= 4 && beta <= 4 && E <= 16 && moddown_fp() && moddown_fpc()) {
+            MUConstFp mc{};
+            const std::vector<double>& uf = cvt->h_modup_fp;
+            const size_t off1 = (size_t)beta * A * 2;
+            for (uint32_t t = 0; t < beta; t++)
+                for (uint32_t a = 0; a < A && t * A + a < level; a++) {
+                    mc.cinv[t][a] = uf[((size_t)t * A + a) * 2];
+                    mc.cinvq[t][a] = uf[((size_t)t * A + a) * 2 + 1];
+                    for (uint32_t e = 0; e < E; e++) {
+                        mc.c[t][e][a] = uf[off1 + (((size_t)t * E + e) * A + a) * 2];
+                        mc.cq[t][e][a] = uf[off1 + (((size_t)t * E + e) * A + a) * 2 + 1];
+                    }
+                }
+            for (uint32_t i = 0; i < level && i < 16; i++) mc.qs[i] = (double)ctx->mod[i];
+            for (uint32_t e = 0; e < E; e++) {
+                mc.r[e] = (double)ctx->mod[ext_limb(ctx, level, e)];
+                mc.rinv[e] = 1.0 / mc.r[e];
+            }
+            dim3 g(n / kT, beta, n_ct);
+            k_modup_convert_fpc<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, mc, perm);
+        } else if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
             dim3 g(n / kT, beta, n_ct);
             k_modup_convert_fp<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                  cvt->d_modup_fp, perm);

@@ -307,6 +307,43 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __rest
     }
 }
 
+// FP64 key inner product, lean (<= 32 registers, 8 CTAs/SM: the kernel is memory-latency sensitive): per digit one
+// exact FP64 product per key polynomial (a, b < q < 2^50: h = ab, l = fma(a, b, -h), t = rint(h / q),
+// r = fma(-t, q, h) + l, |r| <= 0.75 q), beta partial products summed (|s| < 6 q), one centred reduction, canonical
+// store -- the same words as k_kip2 at ~1/3 of its integer instructions (128-bit products + Barrett).
+__device__ __forceinline__ double kip_mul(double a, double b, double q, double qinv) {
+    const double h = a * b;
+    const double l = fma(a, b, -h);
+    const double t = fma(h, qinv, nttfp::kM) - nttfp::kM;
+    return fma(-t, q, h) + l;
+}
+__global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
+                                                  uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
+                                                  uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab,
+                                                  uint64_t ext_stride, uint32_t perm) {
+    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
+    const uint32_t e = blockIdx.y, gi = blockIdx.z;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint32_t src = galois_src_index(k, gb.g[gi], log_n);
+    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * T * n + (size_t)li * n + k;
+    const uint64_t q = tab.q[li];
+    const double qd = (double)q, qinv = 1.0 / qd;
+    for (uint32_t c = 0; c < gb.n_ct; c++) {
+        const uint64_t* ex = ext + (size_t)c * ext_stride + src;
+        double s0 = 0.0, s1 = 0.0;
+        for (uint32_t t = 0; t < beta; t++) {
+            const double dv = nttfp::i2d((long long)ex[((size_t)t * E + ext_row(perm, t, e, A, E)) * n]);
+            const uint64_t* kp = key + (size_t)t * 2 * T * n;
+            s0 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp)), qd, qinv);
+            s1 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp + (size_t)T * n)), qd, qinv);
+        }
+        const size_t r = (size_t)c * gb.cnt + gi;
+        acc[((r * 2 + 0) * E + e) * n + k] = nttfp::canon(nttfp::red(s0, qd, qinv), q);
+        acc[((r * 2 + 1) * E + e) * n + k] = nttfp::canon(nttfp::red(s1, qd, qinv), q);
+    }
+}
+
 // Key inner product with the automorphism fused on load, both key polynomials per thread (the digit gathers are
 // shared): acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r), j = 0, 1.
 __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
@@ -569,6 +606,16 @@ static bool moddown_fp() {
     return v == 1;
 }
 
+// ENSI_KIP=int selects the integer key inner product (A/B timing)
+static bool kip_fp() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KIP");
+        v = (e && e[0] == 'i') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
 static bool moddown_fpc() {
     static int v = -1;
@@ -743,8 +790,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         const uint32_t nr = n_ct * cnt;   // rotations in this batch
         {
             dim3 g(n / kT, E, cnt);
-            k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                     ctx->tab, w_ext1, perm);
+            if (ctx->ntt_fp_ok && beta <= 8 && kip_fp())
+                k_kip_fp<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                                           ctx->tab, w_ext1, perm);
+            else
+                k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                                         ctx->tab, w_ext1, perm);
             ENSI_LAUNCH_CHECK(ctx);
         }
         LimbMap pm = identity_map(A);

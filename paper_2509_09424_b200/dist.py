@@ -43,6 +43,7 @@ class ColumnShardedPCMM:
         self.lo, self.hi, self.S = column_shard(self.m, world, rank)
         Ws = np.zeros((self.d, self.S), np.int8)       # zero columns pad the last shard (outputs are (0,0))
         Ws[:, : self.hi - self.lo] = W[:, self.lo:self.hi]
+        self._W_np = Ws
         self.W_local = make_weights(Ws) if make_weights else Ws
 
     def local_buffer(self, torch, ct_shape, device):
@@ -50,6 +51,31 @@ class ColumnShardedPCMM:
 
     def gathered_buffer(self, torch, ct_shape, device):
         return torch.empty((self.S * self.world,) + tuple(ct_shape), dtype=torch.int64, device=device)
+
+    def chunk_bounds(self, chunks: int):
+        """Contiguous, balanced split of this rank's S output columns into `chunks` pieces."""
+        return [(c * self.S // chunks, (c + 1) * self.S // chunks) for c in range(chunks)]
+
+    def chunk_weights(self, chunks: int, make_weights: Callable = None):
+        """Per-chunk column slices of the local weights (a model constant: build once, reuse every call)."""
+        Wl = self._W_np
+        return [make_weights(np.ascontiguousarray(Wl[:, a:b])) if make_weights else np.ascontiguousarray(Wl[:, a:b])
+                for a, b in self.chunk_bounds(chunks)]
+
+    def run_overlapped(self, pcmm: Callable, x, y_local, y_all, w_chunks, group=None):
+        """Chunked variant: the all-gather of output chunk c runs asynchronously (NCCL's own stream
+        waits for the compute stream at issue time) while chunk c + 1 is computed; returns after every gather
+        has completed.  w_chunks: from chunk_weights()."""
+        import torch.distributed as dist
+        works = []
+        for (a, b), wc in zip(self.chunk_bounds(len(w_chunks)), w_chunks):
+            if b == a:
+                continue
+            pcmm(x, wc, y_local[a:b])
+            outs = [y_all[r * self.S + a: r * self.S + b] for r in range(self.world)]
+            works.append(dist.all_gather(outs, y_local[a:b], group=group, async_op=True))
+        for wk in works:
+            wk.wait()
 
     def __call__(self, pcmm: Callable, x, y_local, y_all=None, group=None, async_op: bool = False):
         """Run this rank's shard into y_local [S][2][l][N'], then all-gather into y_all [S*world][...]

@@ -50,6 +50,12 @@ def _worker(rank, world, port, d, m, out_q):
     y_local = sh.local_buffer(torch, (2, 1, o.n), "cpu")
     y_all = sh.gathered_buffer(torch, (2, 1, o.n), "cpu")
     sh(pcmm, x, y_local, y_all)
+    # the chunked, overlapped variant gathers the same words
+    y_local2 = sh.local_buffer(torch, (2, 1, o.n), "cpu")
+    y_all2 = sh.gathered_buffer(torch, (2, 1, o.n), "cpu")
+    y_all2.zero_()
+    sh.run_overlapped(pcmm, x, y_local2, y_all2, sh.chunk_weights(3))
+    assert torch.equal(y_all2[:m], y_all[:m])
     if rank == 0:
         out_q.put(y_all[:m].numpy().view(np.uint64).copy())
     dist.barrier()

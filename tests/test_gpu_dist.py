@@ -57,6 +57,12 @@ def test_column_sharded_nccl_world1(torch_cuda):
         ctx.pcmm_ternary(xd, ctx.weights(W), direct, level=level)
         torch.cuda.synchronize()
         assert torch.equal(y_all[:m], direct)
+        # chunked: the NCCL all-gather of chunk c overlaps the accumulate of chunk c + 1
+        y_all.zero_()
+        sh.run_overlapped(lambda xa, wl, yl: ctx.pcmm_ternary(xa, wl, yl, level=level), xd, y_local, y_all,
+                          sh.chunk_weights(3, make_weights=ctx.weights))
+        torch.cuda.synchronize()
+        assert torch.equal(y_all[:m], direct)
         want = o.pcmm_a(x, W, cols=[0, 33, 69])
         assert (y_all[[0, 33, 69]].cpu().numpy().view(np.uint64) == want).all()
     finally:

@@ -476,6 +476,32 @@ def main():
                       "pcie_GBps_per_rank": (d + m) * ct_bytes / (e2e_ms * 1e-3) / 1e9,
                       "note": "PCIe-bound: both directions overlap; tools/pcie_bw.py measures 92.7 GB/s bidirectional "
                               "pinned-copy bandwidth on the B200 box"}
+    # ---- N > 1: the north star's output-column sharding of ONE layer (strong scaling): each rank computes
+    # ceil(m/N) output ciphertexts and the result is all-gathered over NCCL, chunked so the gather of chunk c
+    # overlaps the accumulate of chunk c+1 (paper_2509_09424_b200/dist.py).  Device time, max over ranks.
+    if world > 1 or os.environ.get("ENSI_BENCH_COLSHARD") == "1":
+        import torch.distributed as dist
+        from paper_2509_09424_b200.dist import ColumnShardedPCMM
+        if not dist.is_initialized():           # forced at N = 1 (tests): a one-rank NCCL group under torchrun
+            dist.init_process_group("nccl", rank=0, world_size=1)
+        sh = ColumnShardedPCMM(W, world, rank)
+        wch = sh.chunk_weights(4, make_weights=ctx.weights)
+        y_loc = sh.local_buffer(torch, (2, L, n), "cuda")
+        y_all = sh.gathered_buffer(torch, (2, L, n), "cuda")
+        x0 = synth.gen_words_torch(synth.SEED_BASE + 2, ctx.q, d, L, n)     # the same layer input on every rank
+        pc = lambda xa, wl, yl: ctx.pcmm_ternary(xa, wl, yl, level=L)      # noqa: E731
+        for _ in range(2):
+            sh.run_overlapped(pc, x0, y_loc, y_all, wch)
+        torch.cuda.synchronize()
+        barrier(world)
+        cs_ms = max_over_ranks(world, time_loop(lambda: sh.run_overlapped(pc, x0, y_loc, y_all, wch),
+                                                max(1, args.steps), st))
+        out["column_sharded"] = {"value": cs_ms, "unit": "ms/layer", "n_gpus": world, "scaling": "strong",
+                                 "gather_bytes_per_rank": (world - 1) * sh.S * ct_bytes,
+                                 "note": "one 768x768 layer split by output columns, NCCL all-gather of the result "
+                                         "ciphertexts overlapped in 4 chunks"}
+        del y_loc, y_all, x0, wch
+        torch.cuda.empty_cache()
     # ---- rotations/s (BASELINE metric's second clause), rank 0 only
     if not args.no_rot and rank == 0:
         del y

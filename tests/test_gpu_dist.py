@@ -74,9 +74,11 @@ def test_bench_under_torchrun_nccl(torch_cuda):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1", "--steps", "3", "--warmup", "3",
            "--no-cpu", "--no-e2e", "--no-rot"]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, ENSI_BENCH_COLSHARD="1")          # run the column-sharded (all-gather) leg at N=1 too
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     out = json.loads(line)
     assert out["n_gpus"] == 1 and out["value"] > 0 and out["gpu_launches"] >= 3
     assert out["roofline"]["frac"] > 0
+    assert out["column_sharded"]["value"] > 0 and out["column_sharded"]["n_gpus"] == 1

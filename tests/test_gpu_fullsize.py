@@ -115,10 +115,11 @@ def test_c2_rescale_bit_exact(c2, torch_cuda):
     assert (yd.cpu().numpy().view(np.uint64) == want).all()
 
 
-@pytest.mark.parametrize("d,m", [(768, 3072), (2048, 2048)])
+@pytest.mark.parametrize("d,m", [(768, 3072), (2048, 2048), (5504, 2048), (2048, 6144)])
 def test_c3_c4_sampled_columns_bit_exact(c2, torch_cuda, d, m):
-    """BASELINE configs[2] (768->3072, 8-CTA multicast clusters, resident W^T) and configs[3] (2048x2048,
-    streamed W^T) at full size: sampled output columns == oracle Alg. 1 word for word.  Inputs are seeded uniform
+    """BASELINE configs[2] (768->3072, 8-CTA multicast clusters, resident W^T), configs[3] (2048x2048, streamed
+    W^T) and configs[4]'s widest shapes (down 5504->2048: 43 streamed K blocks; fused Q/K/V 2048->6144) at full
+    size: sampled output columns == oracle Alg. 1 word for word.  Inputs are seeded uniform
     words from synth (the accumulate is data-oblivious), copied to the host for the oracle."""
     o, sk, pk, ctx = c2
     torch = torch_cuda

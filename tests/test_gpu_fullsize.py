@@ -135,3 +135,40 @@ def test_c3_c4_sampled_columns_bit_exact(c2, torch_cuda, d, m):
     del xd
     want = o.pcmm_a(x, W, cols=cols, nthreads=NTH)
     assert (got == want).all()
+
+
+@pytest.mark.parametrize("B", [0, 4])
+def test_layout_b_full_ring_bit_exact(c2, torch_cuda, B):
+    """Layout B at the C2 ring (N'=2^16, L=12, alpha=4, dnum=3) on real encryptions: 20 columns packed in blocks of
+    s=2048 slots (k=16, n_in=2), hoisted baby steps (B = k, or B = 4 with giant steps) through the FP64 key
+    switching -- every output word == the oracle's O11 schedule, block 0 decrypts to X.W."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    s, d, m = 2048, 20, 6
+    k, n_in, Bq, G, rots = oracle.layout_b_plan(o.n, s, d, m, B)
+    X = synth.gen_X(synth.SEED_BASE + 31, s, d) * 0.5
+    W = synth.gen_W(synth.SEED_BASE + 131, d, m)
+    slots = o.n // 2
+    cts = []
+    for c in range(n_in):
+        zz = np.zeros(slots)
+        for b in range(k):
+            col = c * k + b
+            if col < d:
+                zz[b * s:(b + 1) * s] = X[:, col]
+        cts.append(o.encrypt(5100 + c, pk, 12, o.encode(zz, 12, DELTA)))
+    x = np.stack(cts)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, Bq, G)
+    keys = np.stack([o.rotkey(5200 + i, g, sk) for i, g in enumerate(gk)])
+    want = o.pcmm_b(x, W, s, k, Bq, gk, keys)
+    bctx = Context(16, 12, 4, 3)
+    bctx.load_keys(sk_ntt=sk, galois=gk, rot_keys=keys)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    bctx.pcmm_ternary(_dev(torch, x), W, yd, level=12, layout=1, block_s=s, baby=Bq)
+    torch.cuda.synchronize()
+    assert (yd.cpu().numpy().view(np.uint64) == want).all()
+    ref = X @ W.astype(np.float64)
+    for i in range(m):
+        z = bctx.decrypt_debug(yd, i, 12)
+        assert np.max(np.abs(z[:s] - ref[:, i])) < 1e-4

@@ -12,6 +12,9 @@ performs (PAPER.md:115-126):
   tau^{-1} evaluated with numpy's FFT (a library primitive used as one step).
 * ``decode``  -- O7: z_u = Re m(zeta^{5^u}) / Delta.
 * ``crt_centered`` -- O7: CRT over all l limbs with Python integers, centred lift.
+* ``Oracle.ccmm``  -- R18: the ciphertext-ciphertext matrix product of PAPER.md:343-360
+  (c_i = sum_j a_j (x) rep(B_ji)), element extraction by mask + rotations, composed step by step from
+  the C primitives (rotation, plaintext product, tensor product, relinearisation, rescale).
 
 Parity status per function is listed in DESIGN.md section "Oracle pins"; key switching bit patterns
 (O10) are pinned by exact CRT identities and decryption, not by external vectors.
@@ -66,6 +69,10 @@ def lib():
         L.or_pcmm_b.restype = C.c_int
         L.or_pcmm_b.argtypes = [C.c_void_p] + [C.c_uint32] * 8 + [u64p, i8p, C.c_uint32, u64p, u64p, u64p]
         L.or_rescale.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
+        L.or_relinkey.argtypes = [C.c_void_p, C.c_uint64, u64p, u64p, C.c_void_p]
+        L.or_mul_plain.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
+        L.or_mul_ct.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
+        L.or_relin.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
         _LIB = L
     return _LIB
 
@@ -341,6 +348,98 @@ class Oracle:
         out = np.zeros((2, level - 1, self.n), np.uint64)
         lib().or_rescale(self.h, level, np.ascontiguousarray(ct, np.uint64), out)
         return out
+
+    # -- CCMM primitives (R18)
+    def relinkey(self, seed: int, sk_ntt: np.ndarray, want_e: bool = False):
+        n, T = self.n, self.L + self.alpha
+        key = np.zeros((self.dnum, 2, T, n), np.uint64)
+        e = np.zeros((self.dnum, n), np.int64) if want_e else None
+        lib().or_relinkey(self.h, seed, np.ascontiguousarray(sk_ntt), key, e.ctypes.data if want_e else None)
+        return (key, e) if want_e else key
+
+    def add(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        """ciphertext addition (PAPER.md:124 Add): word-wise (a + b) mod q_r; a, b [..][l][N']"""
+        level = a.shape[-2]
+        q = np.array(self.q[:level], np.uint64).reshape(level, 1)
+        return (a + b) % q
+
+    def mul_plain(self, ct: np.ndarray, pt: np.ndarray) -> np.ndarray:
+        out = np.zeros_like(ct)
+        lib().or_mul_plain(self.h, ct.shape[1], np.ascontiguousarray(ct), np.ascontiguousarray(pt, np.uint64), out)
+        return out
+
+    def mul_ct(self, a: np.ndarray, b: np.ndarray) -> np.ndarray:
+        level = a.shape[1]
+        out = np.zeros((3, level, self.n), np.uint64)
+        lib().or_mul_ct(self.h, level, np.ascontiguousarray(a), np.ascontiguousarray(b), out)
+        return out
+
+    def relin(self, d3: np.ndarray, key: np.ndarray) -> np.ndarray:
+        level = d3.shape[1]
+        out = np.zeros((2, level, self.n), np.uint64)
+        lib().or_relin(self.h, level, np.ascontiguousarray(d3), np.ascontiguousarray(key), out)
+        return out
+
+    def ccmm(self, a: np.ndarray, src: np.ndarray, form: int, s: int, d: int, m: int, mask_pt: np.ndarray,
+             rot_keys: dict, relin_key: np.ndarray, outputs=None) -> np.ndarray:
+        """R18: C = A . B (form 2, ``src`` = the m column ciphertexts of B, d <= s) or C = A . K^T (form 1,
+        ``src`` = the d column ciphertexts of K, m <= s), every head block of s slots in SIMD.
+        a [d][2][l][N'] (level l >= 3), mask_pt [l][N'] = encode(1 at slots h s + u, u = 0 mod pi) at scale
+        q_{l-1}; rot_keys {g: key}.  Returns the output columns ``outputs`` (default all m) at level l - 2.
+        Steps per output column i, in this order (PAPER.md:354-359 c_i = sum_j a_j (x) b_i^(j)):
+          1. form 2: periodic copy P_i = b_i; for u < log2(s/pi): P_i += Rot(P_i, -pi 2^u)
+          2. align   R_j = Rot(P_i, j) (form 2) or Rot(k_j, i) (form 1)
+          3. mask    M_j = Rescale(R_j (.) mask)                       -> level l-1, scale Delta
+          4. replicate: for u < log2(pi): M_j += Rot(M_j, -2^u)        -> rep(B_ji) on every slot of the block
+          5. D_i = sum_j a_j|_{l-1} (x) M_j  (tensor products)
+          6. c_i = Rescale(Relin(D_i))                                   -> level l-2"""
+        level = a.shape[2]
+        pi = s if form == 1 else 1 << max(0, (d - 1).bit_length())
+        lg = lambda v: v.bit_length() - 1
+        key = lambda r: rot_keys[self.galois(r)]
+        outs = list(range(m)) if outputs is None else list(outputs)
+        res = []
+        for i in outs:
+            if form == 2:
+                P = src[i]
+                for u in range(lg(s // pi)):
+                    r = -pi * (1 << u)
+                    P = self.add(P, self.rotate(P, self.galois(r), key(r)))
+                gs = [self.galois(j) for j in range(d)]
+                R = self.rotate_hoisted(P, gs, np.stack([key(j) if j else key(1) for j in range(d)]))
+            else:
+                R = np.stack([src[j] if i == 0 else self.rotate(src[j], self.galois(i), key(i)) for j in range(d)])
+            D = None
+            for j in range(d):
+                M = self.rescale(self.mul_plain(R[j], mask_pt))
+                for u in range(lg(pi)):
+                    r = -(1 << u)
+                    M = self.add(M, self.rotate(M, self.galois(r), key(r)))
+                t = self.mul_ct(np.ascontiguousarray(a[j][:, :level - 1]), M)
+                D = t if D is None else self.add(D, t)
+            res.append(self.rescale(self.relin(D, relin_key)))
+        return np.stack(res)
+
+    def decrypt3(self, sk_ntt, d3: np.ndarray, scale: float) -> np.ndarray:
+        """decrypt a 3-component product: mu = d0 + d1 s + d2 s^2 (NTT), INTT, CRT, decode"""
+        level = d3.shape[1]
+        s2 = self.mul_plain(np.stack([sk_ntt[:level], sk_ntt[:level]]), sk_ntt[:level])[0]
+        ct2 = np.stack([self.add(d3[0], self.mul_plain(np.stack([d3[2], d3[2]]), s2)[0]), d3[1]])
+        return self.decrypt(sk_ntt, ct2, scale)
+
+
+def ccmm_plan(form: int, s: int, d: int, m: int):
+    """R18 rotation schedule: (period pi, rotation amounts that need keys, rotations per output column)."""
+    pi = s if form == 1 else 1 << max(0, (d - 1).bit_length())
+    lg = lambda v: v.bit_length() - 1
+    amounts = [-(1 << u) for u in range(lg(pi))]
+    if form == 2:
+        amounts += [-pi * (1 << u) for u in range(lg(s // pi))] + list(range(1, d))
+        per_out = lg(s // pi) + (d - 1) + d * lg(pi)
+    else:
+        amounts += list(range(1, m))
+        per_out = d * lg(pi)        # + d alignment rotations for every output column except i = 0
+    return pi, sorted(set(amounts)), per_out
 
 
 def layout_b_plan(n: int, s: int, d: int, m: int, B: int = 0):

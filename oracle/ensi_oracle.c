@@ -24,6 +24,10 @@
  *   or_rotate*      O9+O10                                              pinned: decrypt == cyclic shift
  *   or_pcmm_b       O11 Layout B (our construction)         pinned: decrypt block 0 == X.W
  *   or_rescale      O12                                   pinned: == round(c/q_last) (big int)
+ *   or_relinkey     O4 gadget towards s^2 (CCMM, R18)                    pinned: gadget identity test
+ *   or_mul_plain    pt x ct in NTT form (R18)                            pinned: schoolbook negacyclic product
+ *   or_mul_ct       tensor product (PAPER.md:124-126 Mult)                pinned: d0+d1 s+d2 s^2 == m_a m_b (big int)
+ *   or_relin        O10 with the relinearisation key                     pinned: decrypt(relin(d)) ~ decrypt3(d)
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -290,15 +294,15 @@ void or_automorph_coeff(const or_ctx* cx, uint32_t limb, uint64_t g, const uint6
     }
 }
 
-/* Rotation (switching) key for Galois element g (O4), seed-driven.  Draw order: for t in [0,dnum):
+/* Switching key towards a target key s' (O4), seed-driven.  Draw order: for t in [0,dnum):
  * a_t limb-major uniform over all L+alpha limbs, then N' CBD draws e_t.
- * key[t][0][limb][k] = b_t = -a_t*s + e_t + [limb in D_t] * (P mod q_limb) * sigma_g(s),  key[t][1] = a_t.
- * D_t = Q-limbs [t*alpha, (t+1)*alpha) cap [0,L).  e_out (optional) = int64 [dnum][N'] the e_t. */
-void or_rotkey(const or_ctx* cx, uint64_t seed, uint64_t g, const uint64_t* sk_ntt, uint64_t* key, int64_t* e_out) {
+ * key[t][0][limb][k] = b_t = -a_t*s + e_t + [limb in D_t] * (P mod q_limb) * s',  key[t][1] = a_t.
+ * D_t = Q-limbs [t*alpha, (t+1)*alpha) cap [0,L).  target [(L+alpha)][N'] = s' in NTT form.
+ * e_out (optional) = int64 [dnum][N'] the e_t. */
+static void gadget_key(const or_ctx* cx, uint64_t seed, const uint64_t* sk_ntt, const uint64_t* target, uint64_t* key,
+                       int64_t* e_out) {
     uint32_t n = cx->n, L = cx->L, A = cx->alpha, T = L + A;
     rng_t r; rng_seed(&r, seed);
-    uint64_t* sg = (uint64_t*)malloc((size_t)T * n * sizeof(uint64_t));
-    or_automorph_ntt(cx->log_n, g, T, sk_ntt, sg);
     int64_t* e = (int64_t*)malloc(n * sizeof(int64_t));
     uint64_t* tmp = (uint64_t*)malloc(n * sizeof(uint64_t));
     for (uint32_t t = 0; t < cx->dnum; t++) {
@@ -317,12 +321,33 @@ void or_rotkey(const or_ctx* cx, uint64_t seed, uint64_t g, const uint64_t* sk_n
             or_ntt(cx, i, tmp);
             for (uint32_t k = 0; k < n; k++) {
                 uint64_t v = submod(tmp[k], mulmod(a[(size_t)i * n + k], sk_ntt[(size_t)i * n + k], q), q);
-                if (in_digit) v = addmod(v, mulmod(Pq, sg[(size_t)i * n + k], q), q);
+                if (in_digit) v = addmod(v, mulmod(Pq, target[(size_t)i * n + k], q), q);
                 b[(size_t)i * n + k] = v;
             }
         }
     }
-    free(sg); free(e); free(tmp);
+    free(e); free(tmp);
+}
+
+/* Rotation key for Galois element g: the switching key towards s' = sigma_g(s). */
+void or_rotkey(const or_ctx* cx, uint64_t seed, uint64_t g, const uint64_t* sk_ntt, uint64_t* key, int64_t* e_out) {
+    uint32_t T = cx->L + cx->alpha;
+    uint64_t* sg = (uint64_t*)malloc((size_t)T * cx->n * sizeof(uint64_t));
+    or_automorph_ntt(cx->log_n, g, T, sk_ntt, sg);
+    gadget_key(cx, seed, sk_ntt, sg, key, e_out);
+    free(sg);
+}
+
+/* Relinearisation key (CCMM, R18): the switching key towards s' = s^2 (pointwise square in NTT form =
+ * negacyclic square of the coefficient polynomial).  Same draw order as or_rotkey. */
+void or_relinkey(const or_ctx* cx, uint64_t seed, const uint64_t* sk_ntt, uint64_t* key, int64_t* e_out) {
+    uint32_t n = cx->n, T = cx->L + cx->alpha;
+    uint64_t* s2 = (uint64_t*)malloc((size_t)T * n * sizeof(uint64_t));
+    for (uint32_t i = 0; i < T; i++)
+        for (uint32_t k = 0; k < n; k++)
+            s2[(size_t)i * n + k] = mulmod(sk_ntt[(size_t)i * n + k], sk_ntt[(size_t)i * n + k], cx->mod[i]);
+    gadget_key(cx, seed, sk_ntt, s2, key, e_out);
+    free(s2);
 }
 
 /* ------------------------------------------------------------------ encrypt / decrypt (O6, O7) */
@@ -670,4 +695,54 @@ void or_rescale(const or_ctx* cx, uint32_t level, const uint64_t* ct, uint64_t* 
         }
     }
     free(t); free(ti);
+}
+
+/* ------------------------------------------------------------------ CCMM primitives */
+/* Plaintext-ciphertext product in NTT form (both polys), PAPER.md:124 ring arithmetic:
+ * out_p[r][k] = ct_p[r][k] * pt[r][k] mod q_r.  ct/out [2][l][N'], pt [l][N']. */
+void or_mul_plain(const or_ctx* cx, uint32_t level, const uint64_t* ct, const uint64_t* pt, uint64_t* out) {
+    uint32_t n = cx->n;
+    for (uint32_t p = 0; p < 2; p++)
+        for (uint32_t i = 0; i < level; i++)
+            for (uint32_t k = 0; k < n; k++) {
+                size_t o = ((size_t)p * level + i) * n + k;
+                out[o] = mulmod(ct[o], pt[(size_t)i * n + k], cx->mod[i]);
+            }
+}
+
+/* Ciphertext-ciphertext tensor product (the Mult of PAPER.md:124-126 before relinearisation):
+ * (a0, a1) x (b0, b1) -> (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1), so that
+ * d0 + d1 s + d2 s^2 = (a0 + a1 s)(b0 + b1 s).  a, b [2][l][N'] -> out [3][l][N']. */
+void or_mul_ct(const or_ctx* cx, uint32_t level, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+    uint32_t n = cx->n;
+    size_t P = (size_t)level * n;
+    for (uint32_t i = 0; i < level; i++) {
+        uint64_t q = cx->mod[i];
+        for (uint32_t k = 0; k < n; k++) {
+            size_t o = (size_t)i * n + k;
+            out[o] = mulmod(a[o], b[o], q);
+            out[P + o] = addmod(mulmod(a[o], b[P + o], q), mulmod(a[P + o], b[o], q), q);
+            out[2 * P + o] = mulmod(a[P + o], b[P + o], q);
+        }
+    }
+}
+
+/* Relinearisation: key switching of d2 from s^2 to s (O10 with the relinearisation key, no automorphism):
+ * ks = ModDown(KIP(ModUp(d2), rlk)); out = (d0 + ks0, d1 + ks1).  d [3][l][N'] -> out [2][l][N']. */
+void or_relin(const or_ctx* cx, uint32_t level, const uint64_t* d, const uint64_t* key, uint64_t* out) {
+    uint32_t n = cx->n, A = cx->alpha, E = level + A, beta = n_digits(cx, level);
+    size_t P = (size_t)level * n;
+    uint64_t* dig = (uint64_t*)malloc((size_t)beta * E * n * 8);
+    uint64_t* ks = (uint64_t*)malloc(2 * P * 8);
+    or_modup(cx, level, d + 2 * P, dig);
+    kip_moddown(cx, level, dig, key, ks);
+    for (uint32_t i = 0; i < level; i++) {
+        uint64_t q = cx->mod[i];
+        for (uint32_t k = 0; k < n; k++) {
+            size_t o = (size_t)i * n + k;
+            out[o] = addmod(d[o], ks[o], q);
+            out[P + o] = addmod(d[P + o], ks[P + o], q);
+        }
+    }
+    free(dig); free(ks);
 }

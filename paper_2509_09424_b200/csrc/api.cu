@@ -351,6 +351,8 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     cudaFree(ctx->d_tw3);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
+    if (ctx->relin_owned) cudaFree(ctx->d_relin);
+    cudaFree(ctx->cc_buf);
     for (auto& c : ctx->conv) {
         cudaFree(c.d_modup);
         cudaFree(c.d_moddown);
@@ -735,6 +737,108 @@ int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* st
     DeviceGuard g(ctx->device);
     rc = ensi::rescale(ctx, x->data, x->count, x->level, y->data, (cudaStream_t)stream);
     if (!rc) y->log2_scale = x->log2_scale - std::log2((double)ctx->mod[x->level - 1]);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------------------------- CCMM (R18)
+
+int ensi_load_relin_key(ensi_ctx* ctx, const uint64_t* relin_key, uint32_t mem) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!relin_key) return set_err(ctx, ENSI_EINVAL, "NULL relinearisation key");
+    if (ctx->A == 0) return set_err(ctx, ENSI_EINVAL, "relinearisation needs num_p > 0");
+    if (mem != ENSI_MEM_HOST && mem != ENSI_MEM_DEVICE) return set_err(ctx, ENSI_EINVAL, "mem must be HOST or DEVICE");
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->relin_owned) cudaFree(ctx->d_relin);
+    ctx->d_relin = nullptr;
+    ctx->relin_owned = false;
+    if (mem == ENSI_MEM_DEVICE) {
+        ctx->d_relin = const_cast<uint64_t*>(relin_key);
+        return ENSI_OK;
+    }
+    const size_t bytes = (size_t)ctx->dnum * 2 * ctx->T * ctx->n * 8;
+    cudaError_t e = cudaMalloc(&ctx->d_relin, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->d_relin = nullptr;
+        return set_err(ctx, ENSI_ENOMEM, "relinearisation key allocation failed");
+    }
+    ctx->relin_owned = true;
+    e = cudaMemcpy(ctx->d_relin, relin_key, bytes, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "relinearisation key copy");
+}
+
+int ensi_mul_plain(ensi_ctx* ctx, const ensi_ct_view* x, const uint64_t* pt, double pt_log2_scale, ensi_ct_view* y,
+                   void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (!pt) return set_err(ctx, ENSI_EINVAL, "NULL plaintext");
+    if (y->count != x->count) return set_err(ctx, ENSI_EDIM, "y.count != x.count");
+    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level != x.level");
+    if (y->data != x->data && overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y partially aliases x");
+    DeviceGuard g(ctx->device);
+    rc = ensi::mul_plain(ctx, x->data, x->count, x->level, pt, y->data, (cudaStream_t)stream);
+    if (!rc) y->log2_scale = x->log2_scale + pt_log2_scale;
+    return rc;
+}
+
+int ensi_mul_relin(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* b, ensi_ct_view* y, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, a, "a");
+    if (!rc) rc = check_view(ctx, b, "b");
+    if (!rc) rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (a->count != b->count || y->count != a->count) return set_err(ctx, ENSI_EDIM, "a, b, y counts differ");
+    if (a->level != b->level || y->level != a->level) return set_err(ctx, ENSI_ELEVEL, "a, b, y levels differ");
+    if (overlaps(a, y, ctx->n) || overlaps(b, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases a or b");
+    if (!ctx->d_relin) return set_err(ctx, ENSI_ENOKEY, "no relinearisation key loaded");
+    if (a->count == 0) return ENSI_OK;
+    DeviceGuard g(ctx->device);
+    const uint32_t lv = a->level, n = ctx->n;
+    const uint64_t ctw = (uint64_t)2 * lv * n, P = (uint64_t)lv * n;
+    const cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t chunk = std::min<uint32_t>(a->count, 32);
+    rc = ensi::cc_scratch(ctx, (size_t)chunk * 3 * P);
+    for (uint32_t c0 = 0; c0 < a->count && !rc; c0 += chunk) {
+        const uint32_t nc = std::min<uint32_t>(chunk, a->count - c0);
+        for (uint32_t c = 0; c < nc && !rc; c++)
+            rc = ensi::tensor_acc(ctx, a->data + (size_t)(c0 + c) * ctw, ctw, lv, b->data + (size_t)(c0 + c) * ctw, 1,
+                                  ctx->cc_buf + (size_t)c * 3 * P, lv, true, st);
+        if (!rc) rc = ensi::relinearize(ctx, ctx->cc_buf, nc, lv, y->data + (size_t)c0 * ctw, st);
+    }
+    if (!rc) y->log2_scale = a->log2_scale + b->log2_scale;
+    return rc;
+}
+
+int ensi_ccmm(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* src, const uint64_t* mask_pt, ensi_ct_view* y,
+              const ensi_ccmm_opts* opts, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!opts || !mask_pt) return set_err(ctx, ENSI_EINVAL, "NULL opts or mask");
+    int rc = check_view(ctx, a, "a");
+    if (!rc) rc = check_view(ctx, src, "src");
+    if (!rc) rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    const uint32_t form = opts->form, s = opts->block_s, d = opts->d, m = opts->m;
+    if (form != 1 && form != 2) return set_err(ctx, ENSI_EINVAL, "form must be 1 (A.K^T) or 2 (A.B)");
+    if (s < 2 || (s & (s - 1)) || s > ctx->n / 2) return set_err(ctx, ENSI_EDIM, "block_s must be a power of two in [2, N'/2]");
+    if (d == 0 || m == 0) return set_err(ctx, ENSI_EDIM, "d and m must be positive");
+    if (form == 2 && d > s) return set_err(ctx, ENSI_EDIM, "form 2 needs d <= block_s");
+    if (form == 1 && m > s) return set_err(ctx, ENSI_EDIM, "form 1 needs m <= block_s");
+    if (a->count != d) return set_err(ctx, ENSI_EDIM, "a.count != d");
+    if (src->count != (form == 2 ? m : d)) return set_err(ctx, ENSI_EDIM, "src.count != (form 2 ? m : d)");
+    if (y->count != m) return set_err(ctx, ENSI_EDIM, "y.count != m");
+    if (src->level != a->level) return set_err(ctx, ENSI_ELEVEL, "a and src levels differ");
+    if (a->level < 3) return set_err(ctx, ENSI_ELEVEL, "CCMM consumes two levels: a.level >= 3 required");
+    if (y->level != a->level - 2) return set_err(ctx, ENSI_ELEVEL, "y.level must be a.level - 2");
+    if (overlaps(a, y, ctx->n) || overlaps(src, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases an input");
+    if (ctx->A == 0) return set_err(ctx, ENSI_ENOKEY, "context has no special primes: no key switching");
+    if (!ctx->d_relin) return set_err(ctx, ENSI_ENOKEY, "no relinearisation key loaded");
+    DeviceGuard g(ctx->device);
+    rc = ensi::ccmm(ctx, a->data, src->data, form, s, d, m, a->level, mask_pt, y->data, 0, m, (cudaStream_t)stream);
+    if (!rc) y->log2_scale = a->log2_scale + src->log2_scale - std::log2((double)ctx->mod[a->level - 2]);
     return rc;
 }
 

@@ -89,6 +89,10 @@ struct ensi_ctx {
     std::vector<uint64_t> galois;
     uint64_t* d_keys = nullptr;
     bool keys_owned = false;
+    uint64_t* d_relin = nullptr;          // relinearisation key [dnum][2][T][n] (CCMM)
+    bool relin_owned = false;
+    uint64_t* cc_buf = nullptr;           // CCMM scratch
+    size_t cc_words = 0;
     // conversion tables per level (1..L)
     std::vector<ensi::ConvTables> conv;
     // scratch (grown on demand)
@@ -149,9 +153,28 @@ bool tc_supported(const ensi_ctx* ctx, uint32_t level);
 int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out);
 int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
                    uint64_t* out, cudaStream_t st);
+// Key-switching core options beyond plain rotation (CCMM, R18).
+struct KsOpts {
+    const uint64_t* key_base = nullptr;  // switching keys [.][dnum][2][T][N'] used instead of ctx->d_keys
+    bool switch_identity = false;        // g == 1 is key-switched with key_base[0] (relinearisation), not copied
+    uint64_t c1_off = 0;                 // words from a ciphertext to the polynomial that is key-switched (0: level N')
+    uint32_t add_mask = 0;               // bit j: output poly j += an unpermuted polynomial of the input ciphertext
+    uint64_t add1_off = 0;               // words from a ciphertext to the polynomial added to output poly 1 (0: level N')
+};
 int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
-                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st);
+                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st,
+                         const KsOpts* opts = nullptr);
 const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g);
+
+// CCMM (ccmm.cu, R18)
+int mul_plain(ensi_ctx* ctx, const uint64_t* x, uint32_t count, uint32_t level, const uint64_t* pt, uint64_t* out,
+              cudaStream_t st);
+int tensor_acc(ensi_ctx* ctx, const uint64_t* a, uint64_t a_stride, uint32_t la, const uint64_t* e, uint32_t cnt,
+               uint64_t* D, uint32_t lv, bool init, cudaStream_t st);
+int relinearize(ensi_ctx* ctx, const uint64_t* d, uint32_t cnt, uint32_t lv, uint64_t* out, cudaStream_t st);
+int cc_scratch(ensi_ctx* ctx, size_t words);
+int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, uint32_t s, uint32_t d, uint32_t m,
+         uint32_t level, const uint64_t* mask, uint64_t* y, uint32_t i0, uint32_t i1, cudaStream_t st);
 
 // poly (poly.cu)
 int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st);

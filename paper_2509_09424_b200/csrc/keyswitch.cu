@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(kT) k_moddown_convert_fpc(const uint64_t* __re
 __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
                                                       const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
                                                       GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
-                                                      ModTab tab, const uint64_t* __restrict__ cm) {
+                                                      ModTab tab, const uint64_t* __restrict__ cm,
+                                                      uint32_t add_mask, uint64_t add1_off) {
     const uint32_t n = 1u << log_n, E = level + A;
     const uint32_t i = blockIdx.y, gj = blockIdx.z, j = gj & 1;
     const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)gj * level + i) * n + k], q);
     v = mul_shoup(v, pinv[0], pinv[1], q);
     if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
+    if ((add_mask >> j) & 1) v = add_mod(v, c0[c * gb.in_stride + (j ? add1_off : 0) + (size_t)i * n + k], q);
     out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
 }
 
@@ -650,8 +652,13 @@ static int ks_streams() {
 // rotation (c, r) -> out + (c * out_c_stride + r) ciphertexts.  One ModUp per input; per batch of up to 32 Galois
 // elements one key-stationary KIP (each key word read once for all n_ct inputs) and one ModDown over n_ct * cnt.
 int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
-                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st) {
+                         uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st,
+                         const KsOpts* opts) {
     const uint32_t n = ctx->n, A = ctx->A, E = level + A;
+    const KsOpts ko = opts ? *opts : KsOpts{};
+    const uint64_t c1o = ko.c1_off ? ko.c1_off : (uint64_t)level * n;
+    const uint64_t add1o = ko.add1_off ? ko.add1_off : (uint64_t)level * n;
+    const uint64_t* keys_base = ko.key_base ? ko.key_base : ctx->d_keys;
     const uint64_t two_n_mask = 2ull * n - 1;
     const size_t ctw = (size_t)2 * level * n;
     if (A == 0) return set_err(ctx, ENSI_ENOKEY, "context has no special primes (num_p == 0): no key switching");
@@ -660,13 +667,14 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     std::vector<uint64_t> gs;
     for (uint32_t r = 0; r < n_g; r++) {
         uint64_t g = galois[r] & two_n_mask;
-        if (g == 1) {
+        if (g == 1 && !ko.switch_identity) {
+            if (ko.add_mask) return set_err(ctx, ENSI_EINVAL, "identity rotation with an added input");
             for (uint32_t c = 0; c < n_ct; c++)
                 cudaMemcpyAsync(out + ((size_t)c * out_c_stride + r) * ctw, ct + c * in_stride, ctw * 8,
                                 cudaMemcpyDeviceToDevice, st);
             continue;
         }
-        int ki = key_index(ctx, g);
+        int ki = ko.switch_identity ? (g == 1 ? 0 : -1) : key_index(ctx, g);
         if (ki < 0) return set_err(ctx, ENSI_ENOKEY, "no rotation key loaded for Galois element " + std::to_string(g));
         idx.push_back(r);
         gs.push_back(g);
@@ -705,10 +713,9 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     {
         const size_t row_b = (size_t)level * n * 8;
         if (n_ct == 1)
-            cudaMemcpyAsync(coef, ct + (size_t)level * n, row_b, cudaMemcpyDeviceToDevice, st);
+            cudaMemcpyAsync(coef, ct + c1o, row_b, cudaMemcpyDeviceToDevice, st);
         else
-            cudaMemcpy2DAsync(coef, row_b, ct + (size_t)level * n, in_stride * 8, row_b, n_ct,
-                              cudaMemcpyDeviceToDevice, st);
+            cudaMemcpy2DAsync(coef, row_b, ct + c1o, in_stride * 8, row_b, n_ct, cudaMemcpyDeviceToDevice, st);
         ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
         if (ctx->ntt_fp_ok && A <= 4 && beta <= 4 && E <= 16 && moddown_fp() && moddown_fpc()) {
             MUConstFp mc{};
@@ -744,7 +751,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             const size_t own_b = (size_t)A * n * 8;
             for (uint32_t t = 0; t < beta; t++) {
                 uint64_t* dst = ext + ((size_t)t * E + (E - A)) * n;
-                const uint64_t* src = ct + ((size_t)level + t * A) * n;
+                const uint64_t* src = ct + c1o + (size_t)t * A * n;
                 if (n_ct == 1)
                     cudaMemcpyAsync(dst, src, own_b, cudaMemcpyDeviceToDevice, st);
                 else
@@ -780,7 +787,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         GBatch gb{};
         for (uint32_t i = 0; i < cnt; i++) {
             gb.g[i] = gs[b0 + i];
-            gb.key[i] = (uint32_t)key_index(ctx, gs[b0 + i]);
+            gb.key[i] = ko.switch_identity ? 0u : (uint32_t)key_index(ctx, gs[b0 + i]);
             gb.oidx[i] = idx[b0 + i];
         }
         gb.cnt = cnt;
@@ -791,10 +798,10 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         {
             dim3 g(n / kT, E, cnt);
             if (ctx->ntt_fp_ok && beta <= 8 && kip_fp())
-                k_kip_fp<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                k_kip_fp<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
                                            ctx->tab, w_ext1, perm);
             else
-                k_kip2<<<g, kT, 0, st>>>(ext, ctx->d_keys, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                k_kip2<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
                                          ctx->tab, w_ext1, perm);
             ENSI_LAUNCH_CHECK(ctx);
         }
@@ -804,7 +811,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         pm.grp_stride = E;
         pm.grp_off = level;
         ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
-        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0) {
+        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0 && ko.add_mask == 0) {
             const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
             const double2* ninv = tw + (size_t)ctx->T * 2 * n;
             LimbMap zm = identity_map(level);
@@ -863,7 +870,8 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         ntt_forward(ctx, z, nr * 2 * level, identity_map(level), st);
         {
             dim3 g(n / kT, level, nr * 2);
-            k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown);
+            k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
+                                              ko.add_mask, add1o);
             ENSI_LAUNCH_CHECK(ctx);
         }
     }

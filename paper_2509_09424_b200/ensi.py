@@ -28,7 +28,8 @@ KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA, KERNEL_TC
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
-           "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel"]
+           "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel", "ensi_load_relin_key",
+           "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm"]
 
 
 class EnsiError(RuntimeError):
@@ -57,6 +58,10 @@ class PcmmOpts(C.Structure):
 
 
 _LIB = None
+
+
+class CcmmOpts(C.Structure):
+    _fields_ = [("form", C.c_uint32), ("block_s", C.c_uint32), ("d", C.c_uint32), ("m", C.c_uint32)]
 
 
 def lib():
@@ -88,6 +93,11 @@ def lib():
         L.ensi_rescale.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp]
         L.ensi_decrypt_debug.argtypes = [vp, C.POINTER(CtView), u32, vp, vp]
         L.ensi_launch_count.argtypes = [vp]
+        L.ensi_load_relin_key.argtypes = [vp, vp, u32]
+        L.ensi_mul_plain.argtypes = [vp, C.POINTER(CtView), vp, C.c_double, C.POINTER(CtView), vp]
+        L.ensi_mul_relin.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), C.POINTER(CtView), vp]
+        L.ensi_ccmm.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp, C.POINTER(CtView),
+                                C.POINTER(CcmmOpts), vp]
         L.ensi_launch_count.restype = u64
         L.ensi_pcmm_kernel.argtypes = [vp, u32, u32]
         L.ensi_pcmm_kernel.restype = u32
@@ -267,6 +277,47 @@ class Context:
     def rescale(self, x, y, level: int, log2_scale: float = 80.0, stream=None) -> float:
         xv, yv = self.view(x, level, log2_scale), self.view(y, level - 1)
         self._check(lib().ensi_rescale(self.h, C.byref(xv), C.byref(yv), _stream_ptr(stream)))
+        return yv.log2_scale
+
+    # ---- CCMM (R18)
+    def load_relin_key(self, key):
+        """key [dnum][2][num_q+num_p][N']: numpy (host, copied) or torch CUDA tensor (device, referenced)."""
+        if isinstance(key, np.ndarray):
+            k = np.ascontiguousarray(key, np.uint64)
+            self._check(lib().ensi_load_relin_key(self.h, k.ctypes.data, MEM_HOST))
+        else:
+            if not (key.is_cuda and key.is_contiguous() and key.dtype.itemsize == 8):
+                raise ValueError("device relinearisation key must be a contiguous 64-bit CUDA tensor")
+            self._keep_relin = key
+            self._check(lib().ensi_load_relin_key(self.h, key.data_ptr(), MEM_DEVICE))
+
+    @staticmethod
+    def _dev_words(t, shape, what):
+        if not (t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 8) or tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what} must be a contiguous 64-bit CUDA tensor of shape {tuple(shape)}")
+        return t.data_ptr()
+
+    def mul_plain(self, x, pt, y, level: int, log2_scale: float = 40.0, pt_log2_scale: float = 40.0,
+                  stream=None) -> float:
+        xv, yv = self.view(x, level, log2_scale), self.view(y, level)
+        pp = self._dev_words(pt, (level, self.n), "plaintext")
+        self._check(lib().ensi_mul_plain(self.h, C.byref(xv), pp, pt_log2_scale, C.byref(yv), _stream_ptr(stream)))
+        return yv.log2_scale
+
+    def mul_relin(self, a, b, y, level: int, log2_scale: float = 40.0, stream=None) -> float:
+        av, bv, yv = self.view(a, level, log2_scale), self.view(b, level, log2_scale), self.view(y, level)
+        self._check(lib().ensi_mul_relin(self.h, C.byref(av), C.byref(bv), C.byref(yv), _stream_ptr(stream)))
+        return yv.log2_scale
+
+    def ccmm(self, a, src, mask_pt, y, form: int, block_s: int, d: int, m: int, level: int,
+             log2_scale: float = 40.0, stream=None) -> float:
+        """y = CCMM(a, src) (R18): form 2 C = A.B, form 1 C = A.K^T, per head block of block_s slots."""
+        av, sv = self.view(a, level, log2_scale), self.view(src, level, log2_scale)
+        yv = self.view(y, level - 2)
+        mp = self._dev_words(mask_pt, (level, self.n), "mask plaintext")
+        opts = CcmmOpts(form, block_s, d, m)
+        self._check(lib().ensi_ccmm(self.h, C.byref(av), C.byref(sv), mp, C.byref(yv), C.byref(opts),
+                                    _stream_ptr(stream)))
         return yv.log2_scale
 
     def decrypt_debug(self, ct, index: int, level: int, log2_scale: float = 40.0, want_coeffs: bool = False):

@@ -1,0 +1,169 @@
+"""GPU parity for the CCMM path (R18) through the C ABI: the plaintext product,
+Mult + relinearisation and the whole CCMM (both forms) against the oracle, every RNS word, and decryption against
+the float64 matrix product.  C1 (N'=2^12, L=3) with real encryptions; N'=2^16 at the C2 prime chain on random
+words (the key-switching, rescale and NTT kernels take their N'=2^16 FP64 paths there)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from test_oracle_ccmm import _ccmm_setup
+
+pytestmark = pytest.mark.gpu
+DELTA = 2.0 ** 40
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def c1ctx(torch_cuda):
+    from paper_2509_09424_b200 import Context
+    o = oracle.Oracle(12, 3, 1, 3)
+    skc, sk, pk = o.keygen(0x454E5349 + 1)
+    ctx = Context(12, 3, 1, 3)
+    ctx.load_keys(sk_ntt=sk)
+    return o, sk, pk, ctx
+
+
+def _load(ctx, keys, rlk):
+    gs = list(keys.keys())
+    ctx.load_keys(galois=gs, rot_keys=np.stack([keys[g] for g in gs]))
+    ctx.load_relin_key(rlk)
+
+
+def test_mul_plain_bit_exact(c1ctx, torch_cuda):
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    x = synth.gen_words(501, o.q, 5, 3, o.n)
+    pt = synth.gen_words(502, o.q, 1, 3, o.n)[0, 0]
+    yd = torch.empty_like(dev(torch, x))
+    sc = ctx.mul_plain(dev(torch, x), dev(torch, pt), yd, 3, 40.0, 40.0)
+    torch.cuda.synchronize()
+    got = host(yd)
+    for c in range(5):
+        assert (got[c] == o.mul_plain(x[c], pt)).all()
+    assert sc == 80.0
+    xd = dev(torch, x)                                   # in place (y == x) is allowed
+    ctx.mul_plain(xd, dev(torch, pt), xd, 3)
+    torch.cuda.synchronize()
+    assert (host(xd) == got).all()
+
+
+def test_mul_relin_bit_exact_and_decrypts(c1ctx, torch_cuda):
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    rs = np.random.default_rng(503)
+    xs, ys = rs.uniform(-1, 1, (3, o.n // 2)), rs.uniform(-1, 1, (3, o.n // 2))
+    a = np.stack([o.encrypt(600 + c, pk, 3, o.encode(xs[c], 3, DELTA)) for c in range(3)])
+    b = np.stack([o.encrypt(700 + c, pk, 3, o.encode(ys[c], 3, DELTA)) for c in range(3)])
+    rlk = o.relinkey(504, sk)
+    ctx.load_relin_key(rlk)
+    yd = torch.empty((3, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    sc = ctx.mul_relin(dev(torch, a), dev(torch, b), yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    assert sc == 80.0
+    for c in range(3):
+        want = o.relin(o.mul_ct(a[c], b[c]), rlk)
+        assert (got[c] == want).all()
+        z = o.decrypt(sk, got[c], DELTA * DELTA)
+        assert np.max(np.abs(z - xs[c] * ys[c])) < 1e-6
+
+
+@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 64, 16, 2), (2, 4, 1, 2),
+                                        (1, 16, 4, 3), (1, 8, 2, 8)])
+def test_ccmm_bit_exact_c1(c1ctx, torch_cuda, form, s, d, m):
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 900 + 10 * form + d)
+    _load(ctx, keys, rlk)
+    yd = torch.empty((m, 2, 1, o.n), dtype=torch.int64, device="cuda")
+    sc = ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yd, form, s, d, m, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    want = o.ccmm(a, src, form, s, d, m, mask, keys, rlk)
+    assert (got == want).all()
+    assert abs(sc - (80.0 - np.log2(o.q[1]))) < 1e-9
+    H = (o.n // 2) // s
+    for i in range(m):
+        z = o.decrypt(sk, got[i], 2.0 ** sc).reshape(H, s)
+        assert np.max(np.abs(z - ref[:, :, i])) < 1e-4
+
+
+def test_ccmm_errors(c1ctx, torch_cuda):
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_EDIM, ENSI_ELEVEL, ENSI_ENOKEY, ENSI_EINVAL
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    a = torch.zeros((4, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    src = torch.zeros((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    mask = torch.zeros((3, o.n), dtype=torch.int64, device="cuda")
+    y = torch.zeros((2, 2, 1, o.n), dtype=torch.int64, device="cuda")
+    cases = [
+        (dict(form=3, block_s=16, d=4, m=2), ENSI_EINVAL),
+        (dict(form=2, block_s=12, d=4, m=2), ENSI_EDIM),
+        (dict(form=2, block_s=2, d=4, m=2), ENSI_EDIM),      # d > s
+        (dict(form=2, block_s=16, d=3, m=2), ENSI_EDIM),     # a.count != d
+        (dict(form=1, block_s=16, d=4, m=2), ENSI_EDIM),     # src.count != d
+    ]
+    for kw, code in cases:
+        with pytest.raises(EnsiError) as e:
+            ctx.ccmm(a, src, mask, y, level=3, **kw)
+        assert e.value.code == code, kw
+    a2 = torch.zeros((4, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    with pytest.raises(EnsiError) as e:
+        from paper_2509_09424_b200.ensi import CtView, CcmmOpts, lib
+        import ctypes as C
+        src2 = torch.zeros((2, 2, 2, o.n), dtype=torch.int64, device="cuda")
+        av, sv = ctx.view(a2, 2), ctx.view(src2, 2)
+        yv = CtView(y.data_ptr(), 2, 1, 40.0)
+        ctx._check(lib().ensi_ccmm(ctx.h, C.byref(av), C.byref(sv), mask.data_ptr(), C.byref(yv),
+                                   C.byref(CcmmOpts(2, 16, 4, 2)), None))
+    assert e.value.code == ENSI_ELEVEL
+    # rotation key missing: load keys without the alignment rotations
+    ctx.load_keys(galois=[o.galois(-1)], rot_keys=np.zeros((1, 3, 2, 4, o.n), np.uint64))
+    ctx.load_relin_key(np.zeros((3, 2, 4, o.n), np.uint64))
+    with pytest.raises(EnsiError) as e:
+        ctx.ccmm(a, src, mask, y, form=2, block_s=16, d=4, m=2, level=3)
+    assert e.value.code == ENSI_ENOKEY
+
+
+def test_ccmm_n16_c2_primes_bit_exact(torch_cuda):
+    """N'=2^16 at the C2 prime chain (L=12, alpha=4, dnum=3), both forms, random words: the FP64 NTT, key
+    switching (perm ModUp at level 12, plain at 11) and rescale paths."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(16, 12, 4, 3)
+    ctx = Context(16, 12, 4, 3)
+    level = 12
+    rs_keys = {}
+    for form, s, d, m in [(2, 8, 2, 1), (1, 4, 2, 2)]:
+        pi, amounts, _ = oracle.ccmm_plan(form, s, d, m)
+        for r in amounts:
+            g = o.galois(r)
+            if g not in rs_keys:
+                rs_keys[g] = synth.gen_words(8000 + len(rs_keys), o.moduli, 3, o.L + o.alpha, o.n)
+    rlk = synth.gen_words(8100, o.moduli, 3, o.L + o.alpha, o.n)
+    _load(ctx, rs_keys, rlk)
+    for form, s, d, m in [(2, 8, 2, 1), (1, 4, 2, 2)]:
+        a = synth.gen_words(8200 + form, o.q, d, level, o.n)
+        src = synth.gen_words(8300 + form, o.q, m if form == 2 else d, level, o.n)
+        mask = synth.gen_words(8400 + form, o.q, 1, level, o.n)[0, 0]
+        yd = torch.empty((m, 2, level - 2, o.n), dtype=torch.int64, device="cuda")
+        ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yd, form, s, d, m, level)
+        torch.cuda.synchronize()
+        want = o.ccmm(a, src, form, s, d, m, mask, rs_keys, rlk, outputs=[m - 1])
+        assert (host(yd)[m - 1] == want[0]).all(), form

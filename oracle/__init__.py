@@ -406,7 +406,7 @@ class Oracle:
                     r = -pi * (1 << u)
                     P = self.add(P, self.rotate(P, self.galois(r), key(r)))
                 gs = [self.galois(j) for j in range(d)]
-                R = self.rotate_hoisted(P, gs, np.stack([key(j) if j else key(1) for j in range(d)]))
+                R = self.rotate_hoisted(P, gs, np.stack([key(j) if j else np.zeros_like(relin_key) for j in range(d)]))
             else:
                 R = np.stack([src[j] if i == 0 else self.rotate(src[j], self.galois(i), key(i)) for j in range(d)])
             D = None

@@ -121,7 +121,7 @@ def _ccmm_setup(o, sk, pk, form, s, d, m, seed):
     return a, src, mask, keys, rlk, ref
 
 
-@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (1, 16, 4, 3), (1, 8, 2, 8)])
+@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 4, 1, 2), (1, 16, 4, 3), (1, 8, 2, 8)])
 def test_ccmm_decrypts_to_matrix_product(c1, form, s, d, m):
     o, skc, sk, pk = c1
     a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 900 + 10 * form + d)

@@ -388,15 +388,18 @@ class Oracle:
         q_{l-1}; rot_keys {g: key}.  Returns the output columns ``outputs`` (default all m) at level l - 2.
         Steps per output column i, in this order (PAPER.md:354-359 c_i = sum_j a_j (x) b_i^(j)):
           1. form 2: periodic copy P_i = b_i; for u < log2(s/pi): P_i += Rot(P_i, -pi 2^u)
-          2. align   R_j = Rot(P_i, j) (form 2) or Rot(k_j, i) (form 1)
+          2. align   R_j = Rot(P_i, j) (form 2) or Rot(k_j, i) (form 1), every amount r = gam B + b (B = the
+                     baby count of ccmm_plan) taken as Rot(Rot(., b), gam B) (baby-step giant-step: B + R/B keys
+                     instead of R; Rot(., 0) = identity); form 2's babies Rot(P_i, b) share one ModUp (hoisted)
           3. mask    M_j = Rescale(R_j (.) mask)                       -> level l-1, scale Delta
           4. replicate: for u < log2(pi): M_j += Rot(M_j, -2^u)        -> rep(B_ji) on every slot of the block
           5. D_i = sum_j a_j|_{l-1} (x) M_j  (tensor products)
           6. c_i = Rescale(Relin(D_i))                                   -> level l-2"""
         level = a.shape[2]
-        pi = s if form == 1 else 1 << max(0, (d - 1).bit_length())
+        pi, _, _, Ba = ccmm_plan(form, s, d, m)
         lg = lambda v: v.bit_length() - 1
         key = lambda r: rot_keys[self.galois(r)]
+        rot = lambda x, r: x if r == 0 else self.rotate(x, self.galois(r), key(r))
         outs = list(range(m)) if outputs is None else list(outputs)
         res = []
         for i in outs:
@@ -405,10 +408,13 @@ class Oracle:
                 for u in range(lg(s // pi)):
                     r = -pi * (1 << u)
                     P = self.add(P, self.rotate(P, self.galois(r), key(r)))
-                gs = [self.galois(j) for j in range(d)]
-                R = self.rotate_hoisted(P, gs, np.stack([key(j) if j else np.zeros_like(relin_key) for j in range(d)]))
+                nb = min(Ba, d)
+                gs = [self.galois(b) for b in range(nb)]
+                Rb = self.rotate_hoisted(P, gs, np.stack([key(b) if b else np.zeros_like(relin_key) for b in range(nb)]))
+                R = np.stack([rot(Rb[j % Ba], (j // Ba) * Ba) for j in range(d)])
             else:
-                R = np.stack([src[j] if i == 0 else self.rotate(src[j], self.galois(i), key(i)) for j in range(d)])
+                b, gam = i % Ba, i // Ba
+                R = np.stack([rot(rot(src[j], b), gam * Ba) for j in range(d)])
             D = None
             for j in range(d):
                 M = self.rescale(self.mul_plain(R[j], mask_pt))
@@ -429,17 +435,21 @@ class Oracle:
 
 
 def ccmm_plan(form: int, s: int, d: int, m: int):
-    """R18 rotation schedule: (period pi, rotation amounts that need keys, rotations per output column)."""
+    """R18 schedule: (period pi, rotation amounts that need keys, rotations per output column (form 1: the
+    largest over the columns), baby count B).  Alignment amounts r < R (R = d for form 2, m for form 1) are
+    r = gam B + b with B = 2^ceil(ceil(log2 R) / 2)."""
     pi = s if form == 1 else 1 << max(0, (d - 1).bit_length())
     lg = lambda v: v.bit_length() - 1
+    R = d if form == 2 else m
+    Ba = 1 << (((R - 1).bit_length() + 1) // 2)
     amounts = [-(1 << u) for u in range(lg(pi))]
+    amounts += [b for b in range(1, min(Ba, R))] + [g * Ba for g in range(1, -(-R // Ba))]
     if form == 2:
-        amounts += [-pi * (1 << u) for u in range(lg(s // pi))] + list(range(1, d))
-        per_out = lg(s // pi) + (d - 1) + d * lg(pi)
+        amounts += [-pi * (1 << u) for u in range(lg(s // pi))]
+        per_out = lg(s // pi) + (min(Ba, d) - 1) + (d - min(Ba, d)) + d * lg(pi)
     else:
-        amounts += list(range(1, m))
-        per_out = d * lg(pi)        # + d alignment rotations for every output column except i = 0
-    return pi, sorted(set(amounts)), per_out
+        per_out = d * ((1 if R > 1 else 0) + (1 if R > Ba else 0)) + d * lg(pi)
+    return pi, sorted(set(amounts)), per_out, Ba
 
 
 def layout_b_plan(n: int, s: int, d: int, m: int, B: int = 0):

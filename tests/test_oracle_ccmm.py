@@ -110,7 +110,7 @@ def _ccmm_setup(o, sk, pk, form, s, d, m, seed):
         K = rs.uniform(-1, 1, (H, m, d))
         src = enc(slots(K), seed + 1000)
         ref = np.einsum("hsd,hmd->hsm", A, K)
-    pi, amounts, per_out = oracle.ccmm_plan(form, s, d, m)
+    pi, amounts, per_out, _ = oracle.ccmm_plan(form, s, d, m)
     z = np.zeros(o.n // 2)
     for h in range(H):
         z[h * s:h * s + s:pi] = 1.0
@@ -121,7 +121,8 @@ def _ccmm_setup(o, sk, pk, form, s, d, m, seed):
     return a, src, mask, keys, rlk, ref
 
 
-@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 4, 1, 2), (1, 16, 4, 3), (1, 8, 2, 8)])
+@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 4, 1, 2), (2, 16, 11, 2), (1, 16, 4, 3),
+                                        (1, 8, 2, 8), (1, 16, 3, 11)])
 def test_ccmm_decrypts_to_matrix_product(c1, form, s, d, m):
     o, skc, sk, pk = c1
     a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 900 + 10 * form + d)
@@ -136,8 +137,12 @@ def test_ccmm_decrypts_to_matrix_product(c1, form, s, d, m):
 
 
 def test_ccmm_plan_counts():
-    pi, amounts, per = oracle.ccmm_plan(2, 2048, 96, 2048)
-    assert pi == 128 and per == 4 + 95 + 96 * 7
-    assert set(range(1, 96)) <= set(amounts) and -128 * 8 in amounts and -64 in amounts
-    pi, amounts, per = oracle.ccmm_plan(1, 2048, 96, 2048)
-    assert pi == 2048 and per == 96 * 11 and max(amounts) == 2047
+    """Table III shapes: 105 keys instead of ~2060 with the baby-step giant-step alignment."""
+    pi, amounts, per, Ba = oracle.ccmm_plan(2, 2048, 96, 96)
+    assert pi == 128 and Ba == 16 and per == 4 + 15 + 80 + 96 * 7
+    assert set(amounts) == set(range(1, 16)) | {16 * g for g in range(1, 6)} | {-(1 << u) for u in range(7)} \
+        | {-128 * (1 << u) for u in range(4)}
+    pi, amounts, per, Ba = oracle.ccmm_plan(2, 2048, 2048, 96)         # S (2048 x 2048) . V (2048 x 96)
+    assert pi == 2048 and Ba == 64 and len(amounts) == 63 + 31 + 11 and per == 2047 + 2048 * 11
+    pi, amounts, per, Ba = oracle.ccmm_plan(1, 2048, 96, 2048)         # Q (2048 x 96) . K^T
+    assert pi == 2048 and Ba == 64 and len(amounts) == 63 + 31 + 11 and per == 96 * 2 + 96 * 11

@@ -216,7 +216,7 @@ def _random_keys(ctx, gs, cfg, n):
     return keys
 
 
-def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool = True):
+def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool = True, ccmm: bool = True):
     """The other section-8 rows at the same parameters (timing-only uniform words and random keys; every kernel
     is data-oblivious): NTT/INTT per limb (a5), hoisted key-switched rotations (a6+a7, the BASELINE metric's
     rotations/sec), rescale (a4), and the Layout-B PCMM (a8: 765 hoisted rotations + the accumulate)."""
@@ -347,9 +347,54 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
                                "paper_seconds": {"qkv": 1.78, "gate_up": 3.12, "down": 1.57, "fig8_cpu_1core": 1.41},
                                "note": "paper: A100 80GB, Phantom, per input amortized over a batch of 32; limb count "
                                        "unstated (PAPER.md:575,583,588); fig8: i9-14900K single core (PAPER.md:492)"}
+    if ccmm:
+        out["ccmm"] = bench_ccmm(ctx, cfg, st)
     ctx.close()
     torch.cuda.empty_cache()
     return out
+
+
+def bench_ccmm(ctx, cfg, st):
+    """CCMM (R18) at the paper's Table III attention shapes, 16 heads of s = 2048
+    tokens in SIMD over the 32768 slots: Q.K^T (form 1: d = 96, m = 2048) and S.V (form 2:
+    d = 2048, m = 96).  Timing-only uniform words, random keys and mask; a sample of output columns (every column
+    of a form runs the same kernels; the form-1 sample needs both alignment steps, the most expensive case),
+    extrapolated to the whole product."""
+    import torch
+    n, L, s = 1 << cfg["log_n"], cfg["L"], 2048
+    lg = lambda v: v.bit_length() - 1
+    gal = lambda r: pow(5, r % (n // 2), 2 * n)
+    res = {}
+    for name, form, d, m, col0, cols, paper_s in (("qk_t_2048x96_x16", 1, 96, 2048, 65, 2, 192.99),
+                                                  ("sv_2048x2048_x16", 2, 2048, 96, 1, 1, 638.12)):
+        pi = s if form == 1 else 1 << (d - 1).bit_length()
+        R = d if form == 2 else m
+        Ba = 1 << (((R - 1).bit_length() + 1) // 2)
+        am = [-(1 << u) for u in range(lg(pi))] + list(range(1, min(Ba, R))) + [g * Ba for g in range(1, -(-R // Ba))]
+        if form == 2:
+            am += [-pi * (1 << u) for u in range(lg(s // pi))]
+            rot = lg(s // pi) + (d - 1) + d * lg(pi)
+        else:
+            rot = 2 * d + d * lg(pi)
+        gs = [gal(r) for r in sorted(set(am))]
+        keys = _random_keys(ctx, gs, cfg, n)
+        ctx.load_keys(galois=gs, rot_keys=keys)
+        rlk = _random_keys(ctx, [0], cfg, n)[0].contiguous()
+        ctx.load_relin_key(rlk)
+        a = synth.gen_words_torch(21, ctx.q, d, L, n)
+        src = synth.gen_words_torch(22, ctx.q, m if form == 2 else d, L, n)
+        mask = synth.gen_words_torch(23, ctx.q, 1, L, n)[0, 0].contiguous()
+        y = torch.empty((cols, 2, L - 2, n), dtype=torch.int64, device="cuda")
+        ctx.ccmm(a, src, mask, y[:1], form, s, d, m, L, col0=col0, cols=1)         # warm-up: scratch, tables
+        ms = time_loop(lambda: ctx.ccmm(a, src, mask, y, form, s, d, m, L, col0=col0, cols=cols), 1, st) / cols
+        res[name] = {"form": form, "d": d, "m": m, "heads": (n // 2) // s, "ms_per_output_column": ms,
+                     "rotations_per_column": rot, "rotations_per_sec": rot / (ms * 1e-3), "keys": len(gs),
+                     "s_whole_product": ms * m / 1e3, "paper_s": paper_s, "sampled_columns": cols}
+        del keys, rlk, a, src, mask, y
+        torch.cuda.empty_cache()
+    res["note"] = ("paper: A100, Phantom, amortised per input over a batch of 32 (PAPER.md:559,577,580); ours: one "
+                   "B200, N'=2^16, l=12, the R18 construction (mask + rotation extraction, BSGS alignment)")
+    return res
 
 
 def main():
@@ -364,6 +409,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rot", action="store_true", help="skip the secondary rows (NTT, rotations, rescale, Layout B)")
     ap.add_argument("--no-layout-b", action="store_true")
+    ap.add_argument("--no-ccmm", action="store_true", help="skip the CCMM row (SURVEY 8(f) NEXT #3)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)
@@ -506,7 +552,8 @@ def main():
     if not args.no_rot and rank == 0:
         del y
         torch.cuda.empty_cache()
-        sec = bench_secondary(Context, cfg, max(3, args.steps), 2, peaks, layout_b=not args.no_layout_b)
+        sec = bench_secondary(Context, cfg, max(3, args.steps), 2, peaks, layout_b=not args.no_layout_b,
+                              ccmm=not args.no_ccmm)
         out["rotations_per_sec"] = sec.pop("rotations")
         out["secondary"] = sec
     # ---- CPU oracle baseline (rank 0 at N=1 only)

@@ -829,7 +829,10 @@ int ensi_ccmm(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* src, con
     if (form == 1 && m > s) return set_err(ctx, ENSI_EDIM, "form 1 needs m <= block_s");
     if (a->count != d) return set_err(ctx, ENSI_EDIM, "a.count != d");
     if (src->count != (form == 2 ? m : d)) return set_err(ctx, ENSI_EDIM, "src.count != (form 2 ? m : d)");
-    if (y->count != m) return set_err(ctx, ENSI_EDIM, "y.count != m");
+    if (opts->col0 >= m) return set_err(ctx, ENSI_EDIM, "col0 >= m");
+    const uint32_t cols = opts->cols ? opts->cols : m - opts->col0;
+    if (opts->col0 + (uint64_t)cols > m) return set_err(ctx, ENSI_EDIM, "col0 + cols > m");
+    if (y->count != cols) return set_err(ctx, ENSI_EDIM, "y.count != cols");
     if (src->level != a->level) return set_err(ctx, ENSI_ELEVEL, "a and src levels differ");
     if (a->level < 3) return set_err(ctx, ENSI_ELEVEL, "CCMM consumes two levels: a.level >= 3 required");
     if (y->level != a->level - 2) return set_err(ctx, ENSI_ELEVEL, "y.level must be a.level - 2");
@@ -837,7 +840,8 @@ int ensi_ccmm(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* src, con
     if (ctx->A == 0) return set_err(ctx, ENSI_ENOKEY, "context has no special primes: no key switching");
     if (!ctx->d_relin) return set_err(ctx, ENSI_ENOKEY, "no relinearisation key loaded");
     DeviceGuard g(ctx->device);
-    rc = ensi::ccmm(ctx, a->data, src->data, form, s, d, m, a->level, mask_pt, y->data, 0, m, (cudaStream_t)stream);
+    rc = ensi::ccmm(ctx, a->data, src->data, form, s, d, m, a->level, mask_pt, y->data, opts->col0, opts->col0 + cols,
+                    (cudaStream_t)stream);
     if (!rc) y->log2_scale = a->log2_scale + src->log2_scale - std::log2((double)ctx->mod[a->level - 2]);
     return rc;
 }

@@ -3,7 +3,9 @@
 // with rep(B_ji) = a ciphertext holding the element B_ji on every slot of its head block, extracted by a mask
 // product and rotations.  Per output column i (form 2: C = A.B, B column-encoded; form 1: C = A.K^T):
 //   1. form 2: periodic copy P_i = b_i + Rot(., -pi 2^u) ...   (log2(s/pi) rotations; pi = 2^ceil(log2 d))
-//   2. align   R_j = Rot(P_i, j)  (one ModUp, hoisted over j)  |  form 1: R_j = Rot(k_j, i) (key-stationary batch)
+//   2. align   R_j = Rot(P_i, j) | form 1: R_j = Rot(k_j, i), amount r = gam B + b as Rot(Rot(., b), gam B)
+//              (baby-step giant-step: B + R/B keys; form 2's babies share one ModUp, giant steps and form 1 run as
+//              key-stationary batches)
 //   3. mask    M_j = Rescale(R_j (.) mask)                    -> level l-1, scale Delta
 //   4. replicate M_j += Rot(M_j, -2^u), u < log2(pi)          (key-stationary batches over j, add fused in ModDown)
 //   5. D_i = sum_j a_j|_{l-1} (x) M_j                          (one pass: three 64-bit products per word and j)
@@ -128,43 +130,82 @@ static int add_rotated(ensi_ctx* ctx, const uint64_t* x, uint32_t cnt, uint32_t 
     return ENSI_OK;
 }
 
+// alignment baby count: B = 2^ceil(ceil(log2 R) / 2) for alignment amounts r < R (oracle.ccmm_plan)
+static uint32_t baby_count(uint32_t R) {
+    uint32_t c = 0;
+    while ((1u << c) < R) c++;   // ceil(log2 R)
+    return 1u << ((c + 1) / 2);
+}
+
+// out[c] = Rot(x[c], r) for cnt ciphertexts (key-stationary), or a copy when r == 0
+static int rotate_all(ensi_ctx* ctx, const uint64_t* x, uint32_t cnt, uint32_t level, int64_t r, uint64_t* out,
+                      cudaStream_t st) {
+    const uint64_t ctw = (uint64_t)2 * level * ctx->n;
+    if (r == 0) {
+        cudaError_t e = cudaMemcpyAsync(out, x, cnt * ctw * 8, cudaMemcpyDeviceToDevice, st);
+        return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "ccmm copy");
+    }
+    const uint64_t g = galois_of_rotation(ctx->log_n, r);
+    for (uint32_t c0 = 0; c0 < cnt; c0 += 96) {
+        const uint32_t nc = std::min<uint32_t>(96, cnt - c0);
+        int rc = rotate_hoisted_multi(ctx, x + c0 * ctw, nc, ctw, level, 1, &g, out + c0 * ctw, 1, st);
+        if (rc) return rc;
+    }
+    return ENSI_OK;
+}
+
 int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, uint32_t s, uint32_t d, uint32_t m,
          uint32_t level, const uint64_t* mask, uint64_t* y, uint32_t i0, uint32_t i1, cudaStream_t st) {
     const uint32_t n = ctx->n, l1 = level - 1, l2 = level - 2;
     const uint32_t pi = form == 1 ? s : (1u << ilog2(2 * d - 1));     // 2^ceil(log2 d)
+    const uint32_t Ba = baby_count(form == 2 ? d : m), nb = std::min(Ba, d);
     const uint64_t ctw = (uint64_t)2 * level * n, ctw1 = (uint64_t)2 * l1 * n, ctw2 = (uint64_t)2 * l2 * n;
-    const uint32_t jc_max = std::min<uint32_t>(d, 96);
-    // buffers: P, P' [2][ctw] | R [jc][ctw] | M, M' [2][jc][ctw1] | D [3 l1 n] | Cr [ctw1]
-    const size_t need = 2 * ctw + (size_t)jc_max * ctw + 2 * (size_t)jc_max * ctw1 + 3 * (size_t)l1 * n + ctw1;
+    // j chunks: whole giant-step groups of Ba (form 2), at most ~96 ciphertexts
+    const uint32_t chunk = std::min<uint32_t>(d, Ba <= 96 ? (96 / Ba) * Ba : Ba);
+    // buffers: P, P' [2][ctw] | Rb [nb][ctw] | T [chunk][ctw] | R [chunk][ctw] | M, M' [2][chunk][ctw1] | D | Cr
+    const size_t need = (2 + (size_t)nb + 2 * (size_t)chunk) * ctw + 2 * (size_t)chunk * ctw1 + 3 * (size_t)l1 * n + ctw1;
     int rc = cc_scratch(ctx, need);
     if (rc) return rc;
     uint64_t* Pb[2] = {ctx->cc_buf, ctx->cc_buf + ctw};
-    uint64_t* R = Pb[1] + ctw;
-    uint64_t* Mb[2] = {R + (size_t)jc_max * ctw, R + (size_t)jc_max * ctw + (size_t)jc_max * ctw1};
-    uint64_t* D = Mb[1] + (size_t)jc_max * ctw1;
+    uint64_t* Rb = Pb[1] + ctw;
+    uint64_t* T = Rb + (size_t)nb * ctw;
+    uint64_t* R = T + (size_t)chunk * ctw;
+    uint64_t* Mb[2] = {R + (size_t)chunk * ctw, R + (size_t)chunk * ctw + (size_t)chunk * ctw1};
+    uint64_t* D = Mb[1] + (size_t)chunk * ctw1;
     uint64_t* Cr = D + 3 * (size_t)l1 * n;
     std::vector<uint64_t> gs;
     for (uint32_t i = i0; i < i1 && !rc; i++) {
-        const uint64_t* Pi = nullptr;
-        if (form == 2) {   // 1. periodic copy of column i across the block, period pi
+        if (form == 2) {
+            // 1. periodic copy of column i across the block, period pi
             const uint64_t* cur = src + (size_t)i * ctw;
             for (uint32_t u = 0; (pi << u) < s && !rc; u++) {
                 uint64_t* nxt = Pb[u & 1];
                 rc = add_rotated(ctx, cur, 1, level, -(int64_t)pi * (1ll << u), nxt, st);
                 cur = nxt;
             }
-            Pi = cur;
+            // 2a. baby steps Rot(P_i, b), b < min(B, d): one ModUp (hoisted)
+            gs.resize(nb);
+            for (uint32_t b = 0; b < nb; b++) gs[b] = galois_of_rotation(ctx->log_n, (int64_t)b);
+            if (!rc) rc = rotate_hoisted_multi(ctx, cur, 1, 0, level, nb, gs.data(), Rb, nb, st);
         }
-        for (uint32_t j0 = 0; j0 < d && !rc; j0 += jc_max) {
-            const uint32_t jc = std::min<uint32_t>(jc_max, d - j0);
-            // 2. align: element (j, i) to slot 0 of every block (slots h s + u, u = 0 mod pi)
+        for (uint32_t j0 = 0; j0 < d && !rc; j0 += chunk) {
+            const uint32_t jc = std::min<uint32_t>(chunk, d - j0);
+            // 2. align element (j, i) to slot 0 of every period: amount r = gam B + b as Rot(Rot(., b), gam B)
             if (form == 2) {
-                gs.resize(jc);
-                for (uint32_t j = 0; j < jc; j++) gs[j] = galois_of_rotation(ctx->log_n, (int64_t)(j0 + j));
-                rc = rotate_hoisted_multi(ctx, Pi, 1, 0, level, jc, gs.data(), R, jc, st);
+                for (uint32_t j = j0; j < j0 + jc && !rc;) {          // 2b. giant steps, one key per group
+                    const uint32_t gam = j / Ba, b0 = j % Ba, cnt = std::min(Ba - b0, j0 + jc - j);
+                    rc = rotate_all(ctx, Rb + (size_t)b0 * ctw, cnt, level, (int64_t)gam * Ba, R + (size_t)(j - j0) * ctw, st);
+                    j += cnt;
+                }
             } else {
-                const uint64_t g = galois_of_rotation(ctx->log_n, (int64_t)i);
-                rc = rotate_hoisted_multi(ctx, src + (size_t)j0 * ctw, jc, ctw, level, 1, &g, R, 1, st);
+                const uint32_t b = i % Ba, gam = i / Ba;
+                const uint64_t* x = src + (size_t)j0 * ctw;
+                if (b && gam) {
+                    rc = rotate_all(ctx, x, jc, level, b, T, st);
+                    if (!rc) rc = rotate_all(ctx, T, jc, level, (int64_t)gam * Ba, R, st);
+                } else {
+                    rc = rotate_all(ctx, x, jc, level, b ? (int64_t)b : (int64_t)gam * Ba, R, st);
+                }
             }
             if (rc) break;
             // 3. mask (scale q_{l-1}) and rescale: exactly scale Delta at level l-1

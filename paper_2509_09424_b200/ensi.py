@@ -61,7 +61,8 @@ _LIB = None
 
 
 class CcmmOpts(C.Structure):
-    _fields_ = [("form", C.c_uint32), ("block_s", C.c_uint32), ("d", C.c_uint32), ("m", C.c_uint32)]
+    _fields_ = [("form", C.c_uint32), ("block_s", C.c_uint32), ("d", C.c_uint32), ("m", C.c_uint32),
+                ("col0", C.c_uint32), ("cols", C.c_uint32)]
 
 
 def lib():
@@ -310,12 +311,13 @@ class Context:
         return yv.log2_scale
 
     def ccmm(self, a, src, mask_pt, y, form: int, block_s: int, d: int, m: int, level: int,
-             log2_scale: float = 40.0, stream=None) -> float:
-        """y = CCMM(a, src) (R18): form 2 C = A.B, form 1 C = A.K^T, per head block of block_s slots."""
+             log2_scale: float = 40.0, col0: int = 0, cols: int = 0, stream=None) -> float:
+        """y = CCMM(a, src) (R18): form 2 C = A.B, form 1 C = A.K^T, per head block of block_s slots;
+        output columns [col0, col0 + cols) (cols = 0: to m)."""
         av, sv = self.view(a, level, log2_scale), self.view(src, level, log2_scale)
         yv = self.view(y, level - 2)
         mp = self._dev_words(mask_pt, (level, self.n), "mask plaintext")
-        opts = CcmmOpts(form, block_s, d, m)
+        opts = CcmmOpts(form, block_s, d, m, col0, cols)
         self._check(lib().ensi_ccmm(self.h, C.byref(av), C.byref(sv), mp, C.byref(yv), C.byref(opts),
                                     _stream_ptr(stream)))
         return yv.log2_scale

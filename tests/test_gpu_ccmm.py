@@ -84,8 +84,8 @@ def test_mul_relin_bit_exact_and_decrypts(c1ctx, torch_cuda):
         assert np.max(np.abs(z - xs[c] * ys[c])) < 1e-6
 
 
-@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 64, 16, 2), (2, 4, 1, 2),
-                                        (1, 16, 4, 3), (1, 8, 2, 8)])
+@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 64, 16, 2), (2, 4, 1, 2), (2, 16, 11, 2),
+                                        (1, 16, 4, 3), (1, 8, 2, 8), (1, 16, 3, 11)])
 def test_ccmm_bit_exact_c1(c1ctx, torch_cuda, form, s, d, m):
     o, sk, pk, ctx = c1ctx
     torch = torch_cuda
@@ -104,6 +104,20 @@ def test_ccmm_bit_exact_c1(c1ctx, torch_cuda, form, s, d, m):
         assert np.max(np.abs(z - ref[:, :, i])) < 1e-4
 
 
+def test_ccmm_column_range(c1ctx, torch_cuda):
+    """A column shard [col0, col0 + cols) (one rank's share) equals those columns of the full product."""
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    form, s, d, m = 1, 16, 3, 11
+    a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 931)
+    _load(ctx, keys, rlk)
+    yd = torch.empty((4, 2, 1, o.n), dtype=torch.int64, device="cuda")
+    ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yd, form, s, d, m, 3, col0=5, cols=4)
+    torch.cuda.synchronize()
+    want = o.ccmm(a, src, form, s, d, m, mask, keys, rlk, outputs=[5, 6, 7, 8])
+    assert (host(yd) == want).all()
+
+
 def test_ccmm_errors(c1ctx, torch_cuda):
     from paper_2509_09424_b200.ensi import EnsiError, ENSI_EDIM, ENSI_ELEVEL, ENSI_ENOKEY, ENSI_EINVAL
     o, sk, pk, ctx = c1ctx
@@ -118,6 +132,9 @@ def test_ccmm_errors(c1ctx, torch_cuda):
         (dict(form=2, block_s=2, d=4, m=2), ENSI_EDIM),      # d > s
         (dict(form=2, block_s=16, d=3, m=2), ENSI_EDIM),     # a.count != d
         (dict(form=1, block_s=16, d=4, m=2), ENSI_EDIM),     # src.count != d
+        (dict(form=2, block_s=16, d=4, m=2, col0=2), ENSI_EDIM),
+        (dict(form=2, block_s=16, d=4, m=2, col0=1, cols=2), ENSI_EDIM),
+        (dict(form=2, block_s=16, d=4, m=2, col0=1, cols=1), ENSI_EDIM),   # y.count (2) != cols
     ]
     for kw, code in cases:
         with pytest.raises(EnsiError) as e:
@@ -131,7 +148,7 @@ def test_ccmm_errors(c1ctx, torch_cuda):
         av, sv = ctx.view(a2, 2), ctx.view(src2, 2)
         yv = CtView(y.data_ptr(), 2, 1, 40.0)
         ctx._check(lib().ensi_ccmm(ctx.h, C.byref(av), C.byref(sv), mask.data_ptr(), C.byref(yv),
-                                   C.byref(CcmmOpts(2, 16, 4, 2)), None))
+                                   C.byref(CcmmOpts(2, 16, 4, 2, 0, 0)), None))
     assert e.value.code == ENSI_ELEVEL
     # rotation key missing: load keys without the alignment rotations
     ctx.load_keys(galois=[o.galois(-1)], rot_keys=np.zeros((1, 3, 2, 4, o.n), np.uint64))
@@ -151,7 +168,7 @@ def test_ccmm_n16_c2_primes_bit_exact(torch_cuda):
     level = 12
     rs_keys = {}
     for form, s, d, m in [(2, 8, 2, 1), (1, 4, 2, 2)]:
-        pi, amounts, _ = oracle.ccmm_plan(form, s, d, m)
+        pi, amounts, _, _ = oracle.ccmm_plan(form, s, d, m)
         for r in amounts:
             g = o.galois(r)
             if g not in rs_keys:

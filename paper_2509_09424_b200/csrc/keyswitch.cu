@@ -198,13 +198,15 @@ __global__ void __launch_bounds__(kT) k_modup_convert(const uint64_t* __restrict
     ext[(size_t)row * n + k] = out;
 }
 
-// Extended-digit row order.  perm == 0: row = e (limbs in Q_l u P order).  perm != 0 (every digit has A limbs):
-// the E - A converted limbs first, then the digit's own A limbs, which are copied in NTT form from the input
-// instead of being INTT'ed, converted and NTT'ed again -- the ModUp NTT then runs on E - A rows per digit.
-__device__ __forceinline__ uint32_t ext_row(uint32_t perm, uint32_t t, uint32_t e, uint32_t A, uint32_t E) {
+// Extended-digit row order.  perm == 0: row = e (limbs in Q_l u P order).  perm != 0: the E - c_t converted limbs
+// first, then the digit's own c_t limbs (c_t = A, fewer in a partial last digit when A does not divide the level),
+// which are copied in NTT form from the input instead of being INTT'ed, converted and NTT'ed again -- the ModUp
+// NTT then runs on E - c_t rows per digit.
+__device__ __forceinline__ uint32_t ext_row(uint32_t perm, uint32_t t, uint32_t e, uint32_t A, uint32_t E,
+                                            uint32_t level) {
     if (!perm) return e;
-    const uint32_t lo = t * A, hi = lo + A;
-    return e < lo ? e : (e >= hi ? e - A : (E - A) + (e - lo));
+    const uint32_t lo = t * A, hi = min(lo + A, level), c = hi - lo;   // the last digit may hold fewer limbs
+    return e < lo ? e : (e >= hi ? e - c : (E - c) + (e - lo));
 }
 
 // FP64 ModUp conversion, one thread per (input, digit t, position k) producing all E extended limbs: the digit's
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fp(const uint64_t* __restr
                 if (a < cnt) sum += nttfp::mulmod(y[a], __ldg(c + 2 * a), __ldg(c + 2 * a + 1), rd);
             out = nttfp::canon(nttfp::red(sum, rd, 1.0 / rd), r);
         }
-        ext[(size_t)ext_row(perm, t, e, A, E) * n + k] = out;
+        ext[(size_t)ext_row(perm, t, e, A, E, level) * n + k] = out;
     }
 }
 
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __rest
 #pragma unroll
                 for (uint32_t a = 0; a < 4; a++)
                     if (a < cnt) sum += nttfp::mulmod(y[a], mc.c[t][e][a], mc.cq[t][e][a], mc.r[e]);
-                ext[(size_t)ext_row(perm, t, e, A, E) * n + k] =
+                ext[(size_t)ext_row(perm, t, e, A, E, level) * n + k] =
                     nttfp::canon(nttfp::red(sum, mc.r[e], mc.rinv[e]), (uint64_t)mc.r[e]);
             }
         }
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ e
         const uint64_t* ex = ext + (size_t)c * ext_stride + src;
         double s0 = 0.0, s1 = 0.0;
         for (uint32_t t = 0; t < beta; t++) {
-            const double dv = nttfp::i2d((long long)ex[((size_t)t * E + ext_row(perm, t, e, A, E)) * n]);
+            const double dv = nttfp::i2d((long long)ex[((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n]);
             const uint64_t* kp = key + (size_t)t * 2 * T * n;
             s0 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp)), qd, qinv);
             s1 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp + (size_t)T * n)), qd, qinv);
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, c
         const uint64_t* ex = ext + (size_t)c * ext_stride;
         U128 s0{0, 0}, s1{0, 0};
         for (uint32_t t = 0; t < beta; t++) {
-            uint64_t dv = ex[((size_t)t * E + ext_row(perm, t, e, A, E)) * n + src];
+            uint64_t dv = ex[((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n + src];
             mac128(s0, dv, __ldg(key + ((size_t)t * 2 + 0) * T * n));
             mac128(s1, dv, __ldg(key + ((size_t)t * 2 + 1) * T * n));
             if ((t & 3) == 3 && t + 1 < beta) {
@@ -709,7 +711,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     }
 
     // ---- ModUp (once per input; all inputs in one launch per step so small batches still fill the GPU)
-    const uint32_t perm = (ctx->ntt_fp_ok && A <= 8 && moddown_fp() && level % A == 0 && modup_perm()) ? 1u : 0u;
+    const uint32_t perm = (ctx->ntt_fp_ok && A <= 8 && moddown_fp() && modup_perm()) ? 1u : 0u;
     {
         const size_t row_b = (size_t)level * n * 8;
         if (n_ct == 1)
@@ -747,25 +749,41 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         }
         ENSI_LAUNCH_CHECK(ctx);
         if (perm) {
-            // own limbs: the input's c1 limbs [tA, tA + A) in NTT form, to rows [E - A, E) of every digit block
-            const size_t own_b = (size_t)A * n * 8;
+            // own limbs: the input's c1 limbs [tA, tA + c_t) in NTT form (c_t = A, or fewer in a partial last
+            // digit), to rows [E - c_t, E) of every digit block
             for (uint32_t t = 0; t < beta; t++) {
-                uint64_t* dst = ext + ((size_t)t * E + (E - A)) * n;
+                const uint32_t c_t = std::min(A, level - t * A);
+                const size_t own_b = (size_t)c_t * n * 8;
+                uint64_t* dst = ext + ((size_t)t * E + (E - c_t)) * n;
                 const uint64_t* src = ct + c1o + (size_t)t * A * n;
                 if (n_ct == 1)
                     cudaMemcpyAsync(dst, src, own_b, cudaMemcpyDeviceToDevice, st);
                 else
                     cudaMemcpy2DAsync(dst, w_ext1 * 8, src, in_stride * 8, own_b, n_ct, cudaMemcpyDeviceToDevice, st);
             }
-            LimbMap em = identity_map(1);
-            em.period = beta * (E - A);
-            em.grp_rows = E - A;
-            em.grp_stride = E;
-            em.grp_off = 0;
-            for (uint32_t t = 0, r = 0; t < beta; t++)
-                for (uint32_t e = 0; e < E; e++)
-                    if (e < t * A || e >= (t + 1) * A) em.limb[r++] = (uint8_t)ext_limb(ctx, level, e);
-            ntt_forward(ctx, ext, n_ct * beta * (E - A), em, st);
+            if (level % A == 0) {          // every digit has E - A converted rows: one launch over all digits
+                LimbMap em = identity_map(1);
+                em.period = beta * (E - A);
+                em.grp_rows = E - A;
+                em.grp_stride = E;
+                em.grp_off = 0;
+                for (uint32_t t = 0, r = 0; t < beta; t++)
+                    for (uint32_t e = 0; e < E; e++)
+                        if (e < t * A || e >= (t + 1) * A) em.limb[r++] = (uint8_t)ext_limb(ctx, level, e);
+                ntt_forward(ctx, ext, n_ct * beta * (E - A), em, st);
+            } else {                       // partial last digit: one launch per digit (rows per block differ)
+                for (uint32_t t = 0; t < beta; t++) {
+                    const uint32_t lo = t * A, hi = std::min(lo + A, level), rows_t = E - (hi - lo);
+                    LimbMap em = identity_map(1);
+                    em.period = rows_t;
+                    em.grp_rows = rows_t;
+                    em.grp_stride = beta * E;
+                    em.grp_off = t * E;
+                    for (uint32_t e = 0, r = 0; e < E; e++)
+                        if (e < lo || e >= hi) em.limb[r++] = (uint8_t)ext_limb(ctx, level, e);
+                    ntt_forward(ctx, ext, n_ct * rows_t, em, st);
+                }
+            }
         } else {
             ntt_forward(ctx, ext, n_ct * beta * E, ext_map(ctx, level), st);
         }

@@ -184,3 +184,24 @@ def test_ccmm_n16_c2_primes_bit_exact(torch_cuda):
         torch.cuda.synchronize()
         want = o.ccmm(a, src, form, s, d, m, mask, rs_keys, rlk, outputs=[m - 1])
         assert (host(yd)[m - 1] == want[0]).all(), form
+
+
+@pytest.mark.parametrize("level", [11, 9])
+def test_rotation_partial_last_digit_n16(torch_cuda, level):
+    """Key switching at a level alpha does not divide (C2 primes, alpha = 4: last digit of 3 / 1 limbs) -- the
+    CCMM replicate steps run at level l - 1 = 11: hoisted and key-stationary batches vs the oracle, every word."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(16, 12, 4, 3)
+    ctx = Context(16, 12, 4, 3)
+    gs = [o.galois(3), o.galois(-5)]
+    keys = np.stack([synth.gen_words(8500 + i, o.moduli, 3, 16, o.n) for i in range(2)])
+    ctx.load_keys(galois=gs, rot_keys=keys)
+    x = synth.gen_words(8600 + level, o.q, 2, level, o.n)
+    yh = torch.empty((2, 2, level, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(dev(torch, x[:1]), gs, yh, level)
+    yb = torch.empty((2, 2, level, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_batch(dev(torch, x), gs[1:], yb, level)
+    torch.cuda.synchronize()
+    assert (host(yh)[1] == o.rotate(x[0], gs[1], keys[1])).all()
+    assert (host(yb)[1] == o.rotate(x[1], gs[1], keys[1])).all()

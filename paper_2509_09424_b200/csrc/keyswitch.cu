@@ -322,9 +322,11 @@ __device__ __forceinline__ double kip_mul(double a, double b, double q, double q
 __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
                                                   uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
                                                   uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab,
-                                                  uint64_t ext_stride, uint32_t perm) {
+                                                  uint64_t ext_stride, uint32_t perm, uint32_t limb_major) {
     const uint32_t n = 1u << log_n, E = level + A, T = L + A;
-    const uint32_t e = blockIdx.y, gi = blockIdx.z;
+    // limb_major: grid (k blocks, rotations, limbs) -- all rotations of one extended limb run back to back, so the
+    // gathered digit rows of that limb (beta x N' words per input) stay in L2 across the batch's rotations
+    const uint32_t e = limb_major ? blockIdx.z : blockIdx.y, gi = limb_major ? blockIdx.y : blockIdx.z;
     const uint32_t li = e < level ? e : L + (e - level);
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
     const uint32_t src = galois_src_index(k, gb.g[gi], log_n);
@@ -621,6 +623,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_KIP_ORDER=rot: the key inner product's grid walks rotation-major (A/B timing); default limb-major
+static bool kip_limb_major() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KIP_ORDER");
+        v = (e && std::string(e) == "rot") ? 0 : 1;
+    }
+    return v != 0;
+}
+
 static bool moddown_fpc() {
     static int v = -1;
     if (v < 0) {
@@ -815,9 +827,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         const uint32_t nr = n_ct * cnt;   // rotations in this batch
         {
             dim3 g(n / kT, E, cnt);
-            if (ctx->ntt_fp_ok && beta <= 8 && kip_fp())
-                k_kip_fp<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                           ctx->tab, w_ext1, perm);
+            if (ctx->ntt_fp_ok && beta <= 8 && kip_fp()) {
+                const uint32_t lm = kip_limb_major() ? 1u : 0u;
+                dim3 gk = lm ? dim3(n / kT, cnt, E) : g;
+                k_kip_fp<<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
+                                            ctx->tab, w_ext1, perm, lm);
+            }
             else
                 k_kip2<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
                                          ctx->tab, w_ext1, perm);

@@ -1,5 +1,6 @@
 // ensi_internal.h -- context and launch helpers shared by the CUDA translation units of libensi.so.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -135,6 +136,8 @@ int ensure_scratch(ensi_ctx* ctx, size_t bytes);
 
 // NTT (ntt.cu): in-place on rows [rows][n], row r modulus = map.limb[r % map.period]
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);
+// tensor map of a row buffer for the FP64 NTT's TMA block passes (false: TMA unavailable or disabled)
+bool ntt_row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, CUtensorMap* tm);
 void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);
 
 // accumulate (accum.cu)

@@ -556,6 +556,7 @@ struct ModDownInFp {
     }
 };
 struct ModDownOut {
+    static constexpr bool kFused = true;
     const uint64_t* acc;
     const uint64_t* c0;
     uint64_t* out;
@@ -563,14 +564,17 @@ struct ModDownOut {
     ModTab tab;
     GBatch gb;
     uint32_t level, A, E;
+    uint32_t add_mask;
+    uint64_t add1_off;
     __device__ __forceinline__ void store(uint64_t*, uint32_t row, uint32_t i, uint32_t k, uint64_t zt) const {
         const uint32_t n = 65536, gj = row / level, j = gj & 1;
         const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
         const uint64_t q = tab.q[i];
         const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
-        uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], zt, q);
-        v = mul_shoup(v, pinv[0], pinv[1], q);
+        uint64_t v = sub_mod(__ldcs(acc + ((size_t)gj * E + i) * n + k), zt, q);
+        v = mul_shoup(v, __ldg(pinv), __ldg(pinv + 1), q);
         if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], 16)], q);
+        if ((add_mask >> j) & 1) v = add_mod(v, c0[c * gb.in_stride + (j ? add1_off : 0) + (size_t)i * n + k], q);
         out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
     }
 };
@@ -590,9 +594,11 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
 }
 
 // ModDown fusion level at N' = 2^16 (ENSI_KS for A/B timing): 0 = separate convert / NTT / final kernels
-// (default, fastest measured: 17.9k rot/s with the FP64 NTT and conversion), 1 = final combine fused into the last
-// NTT pass (17.3k), 2 = conversion also fused into the first pass (15.6k: the alpha P-limb loads and products per
-// point and per target limb lengthen the pass).  Integer-NTT era: 11.0k / 10.8k / 9.8k.
+// (default, fastest measured), 1 = final combine fused into the last NTT pass (its TMA tile staging read back
+// lane-consecutively: 23.5k vs 24.3k rot/s hoisted, 12.4k vs 12.8k independent inputs, CCMM 104 vs 100 ms per
+// Q.K^T column -- the heavier pass loses more than the z round trip it saves), 2 = conversion also fused into the
+// first pass (15.6k vs 17.9k in an earlier round: the alpha P-limb loads and products per point and target limb
+// lengthen the pass).
 static int fused_moddown() {
     static int v = -1;
     if (v < 0) {
@@ -844,11 +850,11 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         pm.grp_stride = E;
         pm.grp_off = level;
         ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
-        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0 && ko.add_mask == 0) {
+        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0) {
             const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
             const double2* ninv = tw + (size_t)ctx->T * 2 * n;
             LimbMap zm = identity_map(level);
-            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E};
+            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E, ko.add_mask, add1o};
             dim3 g(16, nr * 2 * level);
             if (fused_moddown() == 2) {
                 ModDownInFp in{acc, cvt->d_moddown_fp, ctx->tab, level, ctx->L, A, E};
@@ -860,8 +866,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv);
                 ctx->launches += 1;
             }
-            nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv,
-                                                                                       nttfp::PlainIn(), outf);
+            CUtensorMap tm;
+            if (ntt_row_tmap(ctx, z, nr * 2 * level, zm, &tm))
+                nttfp::k_ntt256_tma<nttfp::FWD_B, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv, tm, outf);
+            else
+                nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv,
+                                                                                           nttfp::PlainIn(), outf);
             ctx->launches += 2;
             continue;
         }

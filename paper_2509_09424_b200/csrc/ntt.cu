@@ -216,6 +216,10 @@ static bool row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const L
            CUDA_SUCCESS;
 }
 
+bool ntt_row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, CUtensorMap* tm) {
+    return row_tmap(ctx, data, rows, map, tm);
+}
+
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st) {
     if (rows == 0) return;
     const uint32_t log_n = ctx->log_n, n = ctx->n;

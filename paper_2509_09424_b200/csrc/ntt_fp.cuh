@@ -63,6 +63,7 @@ struct PlainIn {
     __device__ __forceinline__ uint64_t load(const uint64_t* a, uint32_t, uint32_t, uint32_t k) const { return a[k]; }
 };
 struct PlainOut {
+    static constexpr bool kFused = false;   // true: the TMA block pass hands every word to store() (lane-consecutive)
     __device__ __forceinline__ void store(uint64_t* a, uint32_t, uint32_t, uint32_t k, uint64_t v) const { a[k] = v; }
 };
 
@@ -200,9 +201,21 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             for (uint32_t j = 0; j < 8; j++)
                 *reinterpret_cast<ulonglong2*>(tile + tile_off(r, j)) =
                     make_ulonglong2(canon(red(v[2 * j], qd, qinv), q), canon(red(v[2 * j + 1], qd, qinv), q));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (threadIdx.x == 0) tile_store(tmap, tile, (int32_t)(256 * blockIdx.x), (int32_t)prow);
+            if constexpr (OUT::kFused) {
+                // fused epilogue: lane-consecutive words of the tile (coalesced global traffic in out.store)
+                __syncthreads();
+#pragma unroll 4
+                for (uint32_t k = 0; k < 16; k++) {
+                    const uint32_t w = threadIdx.x + 256 * k, r2 = w >> 4;
+                    const uint64_t zt =
+                        *reinterpret_cast<const uint64_t*>(tile + tile_off(r2, (w >> 1) & 7) + 8 * (w & 1));
+                    out.store(a, row, limb, 4096 * blockIdx.x + w, zt);
+                }
+            } else {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) tile_store(tmap, tile, (int32_t)(256 * blockIdx.x), (int32_t)prow);
+            }
         } else {
             __syncthreads();
 #pragma unroll
@@ -298,10 +311,10 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256(uint64_t* __res
 // Block passes with TMA tile I/O (PlainIn / PlainOut only): INV_B loads its 16 blocks with one bulk-tensor load,
 // FWD_B stores them with one bulk-tensor store, instead of a shared-memory transpose around coalesced
 // per-thread accesses.  tmap: the data buffer as a 3D tensor {16 words, N'/16 chunks, physical rows}.
-template <int PASS>
+template <int PASS, class OUT = PlainOut>
 __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
                                                     const double2* __restrict__ tw, const double2* __restrict__ ninv,
-                                                    const __grid_constant__ CUtensorMap tmap) {
+                                                    const __grid_constant__ CUtensorMap tmap, OUT out = OUT()) {
     __shared__ __align__(1024) double sm[16 * kRow];
     __shared__ __align__(8) uint64_t bar;
     const uint32_t n = 65536;
@@ -319,9 +332,8 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* _
         __syncthreads();
     }
     const PlainIn in;
-    const PlainOut out;
-    if (q >= (1ull << 41)) ntt256_body<PASS, true, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
-    else ntt256_body<PASS, false, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
+    if (q >= (1ull << 41)) ntt256_body<PASS, true, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
+    else ntt256_body<PASS, false, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
 }
 
 }  // namespace nttfp

@@ -65,6 +65,7 @@ struct RescaleInFp {
     }
 };
 struct RescaleOutFp {
+    static constexpr bool kFused = true;
     const uint64_t* in;                 // [count*2][level][n]
     uint64_t* out;                      // [count*2][level-1][n]
     uint32_t level, lm1;

@@ -9,6 +9,8 @@ One process per GPU, `torch.distributed` over NCCL.  Two shardings:
   [r*S, (r+1)*S) with S = ceil(m / world) (the last shard zero-padded), computes them with its slice of W,
   and one `all_gather_into_tensor` over NCCL assembles the m output ciphertexts on every rank.
 
+CCMM (R18) shards the same way by output columns: `ccmm_shard` gives a rank's (col0, cols).
+
 The compute step is a callable `pcmm(x, W_slice, y_local)`; the product passes the CUDA path
 (`Context.pcmm_ternary`), the CPU tests pass a reference to exercise the shard/gather logic with `gloo`.
 """
@@ -32,6 +34,14 @@ def column_shard(m: int, world: int, rank: int):
     lo = min(m, rank * S)
     hi = min(m, lo + S)
     return lo, hi, S
+
+
+def ccmm_shard(m: int, world: int, rank: int):
+    """(col0, cols) for `Context.ccmm(..., col0=, cols=)`: CCMM output columns are independent (R18), so a
+    rank computes its contiguous column range from the replicated inputs with no data-path collective (weak
+    scaling); gathering the columns, if a consumer needs all of them, is the same all-gather as the PCMM's."""
+    lo, hi, _ = column_shard(m, world, rank)
+    return lo, hi - lo
 
 
 class ColumnShardedPCMM:

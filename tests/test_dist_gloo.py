@@ -80,3 +80,49 @@ def test_column_sharded_allgather_equals_single_process(d, m):
     o = oracle.Oracle(12, 2, 1, 2)
     want = o.pcmm_a(synth.gen_words(55, o.q, d, 1, o.n), synth.gen_W(56, d, m))
     assert (got == want).all()
+
+
+def _ccmm_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    import torch.distributed as dist
+    import oracle
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_oracle_ccmm import _ccmm_setup
+    from paper_2509_09424_b200.dist import ccmm_shard, column_shard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = oracle.Oracle(12, 3, 1, 3)
+    skc, sk, pk = o.keygen(0x454E5349 + 1)
+    form, s, d, m = 1, 8, 2, 5
+    a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 77)   # same seeds: replicated inputs
+    col0, cols = ccmm_shard(m, world, rank)
+    S = column_shard(m, world, rank)[2]
+    loc = np.zeros((S, 2, 1, o.n), np.uint64)
+    if cols:
+        loc[:cols] = o.ccmm(a, src, form, s, d, m, mask, keys, rlk, outputs=range(col0, col0 + cols))  # the "kernel"
+    parts = [torch.zeros((S, 2, 1, o.n), dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, torch.from_numpy(loc.view(np.int64)))
+    if rank == 0:
+        out_q.put(torch.cat(parts)[:m].numpy().view(np.uint64).copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_ccmm_column_shards_gather_to_single_process():
+    """CCMM output columns sharded over two gloo ranks (ccmm_shard) gather to the single-process product."""
+    import oracle
+    from test_oracle_ccmm import _ccmm_setup
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ccmm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    o = oracle.Oracle(12, 3, 1, 3)
+    skc, sk, pk = o.keygen(0x454E5349 + 1)
+    a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, 1, 8, 2, 5, 77)
+    assert (got == o.ccmm(a, src, 1, 8, 2, 5, mask, keys, rlk)).all()

@@ -48,6 +48,60 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock and clock-event reasons polled through NVML every ~1 ms on a background thread while the timed
+    region runs (the timed region of a 5-step C2 run is ~27 ms, far shorter than nvidia-smi's sampling period)."""
+
+    def __init__(self, device_index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+        self.rows = []
+        self.run = False
+        self.th = None
+
+    def _poll(self):
+        nv = self.nv
+        while self.run:
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def start(self):
+        import threading
+        self.run = True
+        self.th = threading.Thread(target=self._poll, daemon=True)
+        self.th.start()
+
+    def stop(self):
+        self.run = False
+        if self.th is not None:
+            self.th.join(timeout=2)
+        nv = self.nv
+        smmax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        if not self.rows:
+            return None
+        names = ((nv.nvmlClocksEventReasonHwSlowdown, "hw_slowdown"),
+                 (nv.nvmlClocksEventReasonHwThermalSlowdown, "hw_thermal_slowdown"),
+                 (nv.nvmlClocksEventReasonSwThermalSlowdown, "sw_thermal_slowdown"),
+                 (nv.nvmlClocksEventReasonSwPowerCap, "sw_power_cap"),
+                 (nv.nvmlClocksEventReasonHwPowerBrakeSlowdown, "hw_power_brake"))
+        reasons = sorted({name for _, r in self.rows for bit, name in names if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.rows), "sm_max_mhz": smmax, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, ~1 ms polling during the timed region"}
+
+
+def clock_sampler(device_index: int):
+    try:
+        return NvmlClockSampler(device_index)
+    except Exception:
+        return ClockSampler(device_index)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms while the timed region runs."""
 
@@ -434,7 +488,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = clock_sampler(local)
     clocks.start()
     l0 = ctx.launch_count()
     barrier(world)

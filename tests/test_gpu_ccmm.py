@@ -84,7 +84,7 @@ def test_mul_relin_bit_exact_and_decrypts(c1ctx, torch_cuda):
         assert np.max(np.abs(z - xs[c] * ys[c])) < 1e-6
 
 
-@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 64, 16, 2), (2, 4, 1, 2), (2, 16, 11, 2),
+@pytest.mark.parametrize("form,s,d,m", [(2, 16, 4, 3), (2, 16, 3, 2), (2, 64, 16, 2), (2, 4, 1, 2), (2, 16, 11, 2), (2, 8, 8, 1),
                                         (1, 16, 4, 3), (1, 8, 2, 8), (1, 16, 3, 11)])
 def test_ccmm_bit_exact_c1(c1ctx, torch_cuda, form, s, d, m):
     o, sk, pk, ctx = c1ctx

@@ -517,14 +517,15 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
                                                       const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
                                                       GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
                                                       ModTab tab, const uint64_t* __restrict__ cm,
-                                                      uint32_t add_mask, uint64_t add1_off) {
+                                                      uint32_t add_mask, uint64_t add1_off, uint32_t gj0) {
     const uint32_t n = 1u << log_n, E = level + A;
-    const uint32_t i = blockIdx.y, gj = blockIdx.z, j = gj & 1;
+    // gj: rotation-polynomial index in the batch; z holds the rows of this launch's sub-batch [gj0, gj0 + gridDim.z)
+    const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1;
     const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
     const uint64_t q = tab.q[i];
     const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
-    uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)gj * level + i) * n + k], q);
+    uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)blockIdx.z * level + i) * n + k], q);
     v = mul_shoup(v, pinv[0], pinv[1], q);
     if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
     if ((add_mask >> j) & 1) v = add_mod(v, c0[c * gb.in_stride + (j ? add1_off : 0) + (size_t)i * n + k], q);
@@ -629,6 +630,17 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_MD_SUB=<k>: ModDown sub-batch of k rotation-polynomials (0 = the whole batch in one pass per step)
+static uint32_t moddown_sub() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_MD_SUB");
+        v = e ? atoi(e) : 0;
+        if (v < 0) v = 0;
+    }
+    return (uint32_t)v;
+}
+
 // ENSI_KIP_ORDER=rot: the key inner product's grid walks rotation-major (A/B timing); default limb-major
 static bool kip_limb_major() {
     static int v = -1;
@@ -849,8 +861,8 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         pm.grp_rows = A;
         pm.grp_stride = E;
         pm.grp_off = level;
-        ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
         if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0) {
+            ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
             const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
             const double2* ninv = tw + (size_t)ctx->T * 2 * n;
             LimbMap zm = identity_map(level);
@@ -875,8 +887,16 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             ctx->launches += 2;
             continue;
         }
+        // ModDown in sub-batches of `sub` rotation-polynomials: INTT of the P rows, conversion, NTT and final
+        // combine of one sub-batch run back to back on one z sub-buffer, so z and the P rows stay in L2 between
+        // the four steps instead of making four DRAM round trips per batch
+        const uint32_t GJ = nr * 2, sub = moddown_sub() ? std::min(GJ, moddown_sub()) : GJ;
+        for (uint32_t g0 = 0; g0 < GJ; g0 += sub) {
+        const uint32_t gcnt = std::min(sub, GJ - g0);
+        uint64_t* accs = acc + (size_t)g0 * E * n;
+        ntt_inverse(ctx, accs, gcnt * A, pm, st);
         if (A <= 8 && ctx->ntt_fp_ok && moddown_fp()) {
-            dim3 g(n / kT, nr * 2);
+            dim3 g(n / kT, gcnt);
             if (level <= 16 && moddown_fpc()) {
                 MDConstFp mc{};
                 const std::vector<double>& mf = cvt->h_moddown_fp;
@@ -895,27 +915,28 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                         mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
                     }
                 }
-                k_moddown_convert_fpc<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, A, mc);
+                k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
             } else
-            k_moddown_convert_fp<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
+            k_moddown_convert_fp<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                    cvt->d_moddown_fp);
             ENSI_LAUNCH_CHECK(ctx);
         } else if (A <= 8) {
-            dim3 g(n / kT, nr * 2);
-            k_moddown_convert2<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
+            dim3 g(n / kT, gcnt);
+            k_moddown_convert2<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
                                                  cvt->d_moddown2);
             ENSI_LAUNCH_CHECK(ctx);
         } else {
-            dim3 g(n / kT, level, nr * 2);
-            k_moddown_convert<<<g, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
+            dim3 g(n / kT, level, gcnt);
+            k_moddown_convert<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
             ENSI_LAUNCH_CHECK(ctx);
         }
-        ntt_forward(ctx, z, nr * 2 * level, identity_map(level), st);
+        ntt_forward(ctx, z, gcnt * level, identity_map(level), st);
         {
-            dim3 g(n / kT, level, nr * 2);
+            dim3 g(n / kT, level, gcnt);
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
-                                              ko.add_mask, add1o);
+                                              ko.add_mask, add1o, g0);
             ENSI_LAUNCH_CHECK(ctx);
+        }
         }
     }
     if (nsets == 2) {

@@ -425,11 +425,15 @@ def bench_ccmm(ctx, cfg, st):
         R = d if form == 2 else m
         Ba = 1 << (((R - 1).bit_length() + 1) // 2)
         am = [-(1 << u) for u in range(lg(pi))] + list(range(1, min(Ba, R))) + [g * Ba for g in range(1, -(-R // Ba))]
+        G = -(-R // Ba)
         if form == 2:
             am += [-pi * (1 << u) for u in range(lg(s // pi))]
-            rot = lg(s // pi) + (d - 1) + d * lg(pi)
-        else:
-            rot = 2 * d + d * lg(pi)
+            rot = cols * (lg(s // pi) + (d - 1) + d * lg(pi))                 # in the timed sample
+            rot_all = m * (lg(s // pi) + (d - 1) + d * lg(pi))                # in the whole product
+        else:   # giant step Rot(k_j, gam B) once per giant step in the range, babies for b != 0, replicate
+            cs = range(col0, col0 + cols)
+            rot = d * len({c // Ba for c in cs if c // Ba}) + d * sum(1 for c in cs if c % Ba) + cols * d * lg(pi)
+            rot_all = d * (G - 1) + d * (m - G) + m * d * lg(pi)
         gs = [gal(r) for r in sorted(set(am))]
         keys = _random_keys(ctx, gs, cfg, n)
         ctx.load_keys(galois=gs, rot_keys=keys)
@@ -440,10 +444,14 @@ def bench_ccmm(ctx, cfg, st):
         mask = synth.gen_words_torch(23, ctx.q, 1, L, n)[0, 0].contiguous()
         y = torch.empty((cols, 2, L - 2, n), dtype=torch.int64, device="cuda")
         ctx.ccmm(a, src, mask, y[:1], form, s, d, m, L, col0=col0, cols=1)         # warm-up: scratch, tables
-        ms = time_loop(lambda: ctx.ccmm(a, src, mask, y, form, s, d, m, L, col0=col0, cols=cols), 1, st) / cols
-        res[name] = {"form": form, "d": d, "m": m, "heads": (n // 2) // s, "ms_per_output_column": ms,
-                     "rotations_per_column": rot, "rotations_per_sec": rot / (ms * 1e-3), "keys": len(gs),
-                     "s_whole_product": ms * m / 1e3, "paper_s": paper_s, "sampled_columns": cols}
+        ms_all = time_loop(lambda: ctx.ccmm(a, src, mask, y, form, s, d, m, L, col0=col0, cols=cols), 1, st)
+        rps = rot / (ms_all * 1e-3)
+        res[name] = {"form": form, "d": d, "m": m, "heads": (n // 2) // s, "ms_per_output_column": ms_all / cols,
+                     "rotations_in_sample": rot, "rotations_per_sec": rps, "keys": len(gs),
+                     "rotations_whole_product": rot_all, "s_whole_product": rot_all / rps,
+                     "extrapolation": "whole product = its rotation count / the sample's rotation rate (rotations "
+                                      "are > 97 % of the launches' time)",
+                     "paper_s": paper_s, "sampled_columns": [col0, col0 + cols]}
         del keys, rlk, a, src, mask, y
         torch.cuda.empty_cache()
     res["note"] = ("paper: A100, Phantom, amortised per input over a batch of 32 (PAPER.md:559,577,580); ours: one "

@@ -389,8 +389,10 @@ class Oracle:
         Steps per output column i, in this order (PAPER.md:354-359 c_i = sum_j a_j (x) b_i^(j)):
           1. form 2: periodic copy P_i = b_i; for u < log2(s/pi): P_i += Rot(P_i, -pi 2^u)
           2. align   R_j = Rot(P_i, j) (form 2) or Rot(k_j, i) (form 1), every amount r = gam B + b (B = the
-                     baby count of ccmm_plan) taken as Rot(Rot(., b), gam B) (baby-step giant-step: B + R/B keys
-                     instead of R; Rot(., 0) = identity); form 2's babies Rot(P_i, b) share one ModUp (hoisted)
+                     baby count of ccmm_plan) taken as Rot(Rot(., gam B), b) -- giant step first (baby-step
+                     giant-step: B + R/B keys instead of R; Rot(., 0) = identity).  Form 2: the giant steps of P_i
+                     share one ModUp and the babies of each giant step share one (hoisted); form 1: contiguous
+                     output columns of one giant step share Rot(k_j, gam B)
           3. mask    M_j = Rescale(R_j (.) mask)                       -> level l-1, scale Delta
           4. replicate: for u < log2(pi): M_j += Rot(M_j, -2^u)        -> rep(B_ji) on every slot of the block
           5. D_i = sum_j a_j|_{l-1} (x) M_j  (tensor products)
@@ -408,13 +410,19 @@ class Oracle:
                 for u in range(lg(s // pi)):
                     r = -pi * (1 << u)
                     P = self.add(P, self.rotate(P, self.galois(r), key(r)))
-                nb = min(Ba, d)
-                gs = [self.galois(b) for b in range(nb)]
-                Rb = self.rotate_hoisted(P, gs, np.stack([key(b) if b else np.zeros_like(relin_key) for b in range(nb)]))
-                R = np.stack([rot(Rb[j % Ba], (j // Ba) * Ba) for j in range(d)])
+                zero = np.zeros_like(relin_key)
+                G = -(-d // Ba)
+                Gs = self.rotate_hoisted(P, [self.galois(g * Ba) for g in range(G)],
+                                         np.stack([key(g * Ba) if g else zero for g in range(G)]))
+                R = []
+                for g in range(G):
+                    nb = min(Ba, d - g * Ba)
+                    R += list(self.rotate_hoisted(Gs[g], [self.galois(b) for b in range(nb)],
+                                                  np.stack([key(b) if b else zero for b in range(nb)])))
+                R = np.stack(R)
             else:
                 b, gam = i % Ba, i // Ba
-                R = np.stack([rot(rot(src[j], b), gam * Ba) for j in range(d)])
+                R = np.stack([rot(rot(src[j], gam * Ba), b) for j in range(d)])
             D = None
             for j in range(d):
                 M = self.rescale(self.mul_plain(R[j], mask_pt))

@@ -3,9 +3,9 @@
 // with rep(B_ji) = a ciphertext holding the element B_ji on every slot of its head block, extracted by a mask
 // product and rotations.  Per output column i (form 2: C = A.B, B column-encoded; form 1: C = A.K^T):
 //   1. form 2: periodic copy P_i = b_i + Rot(., -pi 2^u) ...   (log2(s/pi) rotations; pi = 2^ceil(log2 d))
-//   2. align   R_j = Rot(P_i, j) | form 1: R_j = Rot(k_j, i), amount r = gam B + b as Rot(Rot(., b), gam B)
-//              (baby-step giant-step: B + R/B keys; form 2's babies share one ModUp, giant steps and form 1 run as
-//              key-stationary batches)
+//   2. align   R_j = Rot(P_i, j) | form 1: R_j = Rot(k_j, i), amount r = gam B + b as Rot(Rot(., gam B), b)
+//              (baby-step giant-step: B + R/B keys; form 2: the giant steps share one ModUp, the babies of each
+//              giant step share one; form 1: Rot(k_j, gam B) is shared by B contiguous output columns)
 //   3. mask    M_j = Rescale(R_j (.) mask)                    -> level l-1, scale Delta
 //   4. replicate M_j += Rot(M_j, -2^u), u < log2(pi)          (key-stationary batches over j, add fused in ModDown)
 //   5. D_i = sum_j a_j|_{l-1} (x) M_j                          (one pass: three 64-bit products per word and j)
@@ -158,23 +158,28 @@ int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, u
          uint32_t level, const uint64_t* mask, uint64_t* y, uint32_t i0, uint32_t i1, cudaStream_t st) {
     const uint32_t n = ctx->n, l1 = level - 1, l2 = level - 2;
     const uint32_t pi = form == 1 ? s : (1u << ilog2(2 * d - 1));     // 2^ceil(log2 d)
-    const uint32_t Ba = baby_count(form == 2 ? d : m), nb = std::min(Ba, d);
+    const uint32_t Ba = baby_count(form == 2 ? d : m);
+    const uint32_t G2 = form == 2 ? (d + Ba - 1) / Ba : 0;           // form 2: giant steps per column
     const uint64_t ctw = (uint64_t)2 * level * n, ctw1 = (uint64_t)2 * l1 * n, ctw2 = (uint64_t)2 * l2 * n;
-    // j chunks: whole giant-step groups of Ba (form 2), at most ~96 ciphertexts
+    // j chunks: whole baby groups of Ba (form 2), at most ~96 ciphertexts
     const uint32_t chunk = std::min<uint32_t>(d, Ba <= 96 ? (96 / Ba) * Ba : Ba);
-    // buffers: P, P' [2][ctw] | Rb [nb][ctw] | T [chunk][ctw] | R [chunk][ctw] | M, M' [2][chunk][ctw1] | D | Cr
-    const size_t need = (2 + (size_t)nb + 2 * (size_t)chunk) * ctw + 2 * (size_t)chunk * ctw1 + 3 * (size_t)l1 * n + ctw1;
+    // form 1: Rot(k_j, gam B) for all j is kept across the contiguous output columns of one giant step (d <= 256)
+    const bool cache1 = form == 1 && d <= 256;
+    const size_t g_cts = form == 2 ? G2 : (cache1 ? d : chunk);
+    // buffers: P, P' [2][ctw] | Gs [g_cts][ctw] | R [chunk][ctw] | M, M' [2][chunk][ctw1] | D | Cr
+    const size_t need = (2 + g_cts + (size_t)chunk) * ctw + 2 * (size_t)chunk * ctw1 + 3 * (size_t)l1 * n + ctw1;
     int rc = cc_scratch(ctx, need);
     if (rc) return rc;
     uint64_t* Pb[2] = {ctx->cc_buf, ctx->cc_buf + ctw};
-    uint64_t* Rb = Pb[1] + ctw;
-    uint64_t* T = Rb + (size_t)nb * ctw;
-    uint64_t* R = T + (size_t)chunk * ctw;
+    uint64_t* Gs = Pb[1] + ctw;
+    uint64_t* R = Gs + g_cts * ctw;
     uint64_t* Mb[2] = {R + (size_t)chunk * ctw, R + (size_t)chunk * ctw + (size_t)chunk * ctw1};
     uint64_t* D = Mb[1] + (size_t)chunk * ctw1;
     uint64_t* Cr = D + 3 * (size_t)l1 * n;
     std::vector<uint64_t> gs;
+    uint32_t cached_gam = 0xFFFFFFFFu;
     for (uint32_t i = i0; i < i1 && !rc; i++) {
+        const uint64_t* G1 = src;                  // form 1: Rot(k_., gam B) for this column's giant step
         if (form == 2) {
             // 1. periodic copy of column i across the block, period pi
             const uint64_t* cur = src + (size_t)i * ctw;
@@ -183,29 +188,37 @@ int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, u
                 rc = add_rotated(ctx, cur, 1, level, -(int64_t)pi * (1ll << u), nxt, st);
                 cur = nxt;
             }
-            // 2a. baby steps Rot(P_i, b), b < min(B, d): one ModUp (hoisted)
-            gs.resize(nb);
-            for (uint32_t b = 0; b < nb; b++) gs[b] = galois_of_rotation(ctx->log_n, (int64_t)b);
-            if (!rc) rc = rotate_hoisted_multi(ctx, cur, 1, 0, level, nb, gs.data(), Rb, nb, st);
+            // 2a. giant steps Rot(P_i, gam B), gam < G: one ModUp (hoisted)
+            gs.resize(G2);
+            for (uint32_t g = 0; g < G2; g++) gs[g] = galois_of_rotation(ctx->log_n, (int64_t)g * Ba);
+            if (!rc) rc = rotate_hoisted_multi(ctx, cur, 1, 0, level, G2, gs.data(), Gs, G2, st);
+        } else if (i / Ba != 0 && cache1) {
+            // 2a. giant step Rot(k_j, gam B) for every j, shared by the columns gam B .. gam B + B - 1
+            if (i / Ba != cached_gam) {
+                rc = rotate_all(ctx, src, d, level, (int64_t)(i / Ba) * Ba, Gs, st);
+                cached_gam = i / Ba;
+            }
+            G1 = Gs;
         }
         for (uint32_t j0 = 0; j0 < d && !rc; j0 += chunk) {
             const uint32_t jc = std::min<uint32_t>(chunk, d - j0);
-            // 2. align element (j, i) to slot 0 of every period: amount r = gam B + b as Rot(Rot(., b), gam B)
+            // 2. align element (j, i) to slot 0 of every period: amount r = gam B + b as Rot(Rot(., gam B), b)
             if (form == 2) {
-                for (uint32_t j = j0; j < j0 + jc && !rc;) {          // 2b. giant steps, one key per group
-                    const uint32_t gam = j / Ba, b0 = j % Ba, cnt = std::min(Ba - b0, j0 + jc - j);
-                    rc = rotate_all(ctx, Rb + (size_t)b0 * ctw, cnt, level, (int64_t)gam * Ba, R + (size_t)(j - j0) * ctw, st);
-                    j += cnt;
+                for (uint32_t g = j0 / Ba; g * Ba < j0 + jc && !rc; g++) {    // 2b. babies of giant step g, hoisted
+                    const uint32_t nb = std::min(Ba, d - g * Ba);
+                    gs.resize(nb);
+                    for (uint32_t b = 0; b < nb; b++) gs[b] = galois_of_rotation(ctx->log_n, (int64_t)b);
+                    rc = rotate_hoisted_multi(ctx, Gs + (size_t)g * ctw, 1, 0, level, nb, gs.data(),
+                                              R + (size_t)(g * Ba - j0) * ctw, nb, st);
                 }
             } else {
                 const uint32_t b = i % Ba, gam = i / Ba;
-                const uint64_t* x = src + (size_t)j0 * ctw;
-                if (b && gam) {
-                    rc = rotate_all(ctx, x, jc, level, b, T, st);
-                    if (!rc) rc = rotate_all(ctx, T, jc, level, (int64_t)gam * Ba, R, st);
-                } else {
-                    rc = rotate_all(ctx, x, jc, level, b ? (int64_t)b : (int64_t)gam * Ba, R, st);
+                const uint64_t* x = G1 + (size_t)j0 * ctw;
+                if (gam && !cache1) {                  // large d: giant step per chunk into R, then babies in place
+                    rc = rotate_all(ctx, src + (size_t)j0 * ctw, jc, level, (int64_t)gam * Ba, Gs, st);
+                    x = Gs;
                 }
+                if (!rc) rc = rotate_all(ctx, x, jc, level, (int64_t)b, R, st);
             }
             if (rc) break;
             // 3. mask (scale q_{l-1}) and rescale: exactly scale Delta at level l-1

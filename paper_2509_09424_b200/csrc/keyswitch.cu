@@ -322,7 +322,8 @@ __device__ __forceinline__ double kip_mul(double a, double b, double q, double q
 __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
                                                   uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n, uint32_t level,
                                                   uint32_t L, uint32_t A, uint32_t dnum, uint32_t beta, ModTab tab,
-                                                  uint64_t ext_stride, uint32_t perm, uint32_t limb_major) {
+                                                  uint64_t ext_stride, uint32_t perm, uint32_t limb_major,
+                                                  const uint64_t* __restrict__ c1p, uint64_t in_stride) {
     const uint32_t n = 1u << log_n, E = level + A, T = L + A;
     // limb_major: grid (k blocks, rotations, limbs) -- all rotations of one extended limb run back to back, so the
     // gathered digit rows of that limb (beta x N' words per input) stay in L2 across the batch's rotations
@@ -337,7 +338,11 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ e
         const uint64_t* ex = ext + (size_t)c * ext_stride + src;
         double s0 = 0.0, s1 = 0.0;
         for (uint32_t t = 0; t < beta; t++) {
-            const double dv = nttfp::i2d((long long)ex[((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n]);
+            // perm == 2: a digit's own limbs are read straight from the input's c1 (NTT form), never copied
+            const bool own = perm == 2 && e >= t * A && e < t * A + A && e < level;
+            const uint64_t* dp = own ? c1p + (size_t)c * in_stride + (size_t)e * n + src
+                                     : ex + ((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n;
+            const double dv = nttfp::i2d((long long)*dp);
             const uint64_t* kp = key + (size_t)t * 2 * T * n;
             s0 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp)), qd, qinv);
             s1 += kip_mul(dv, nttfp::i2d((long long)__ldg(kp + (size_t)T * n)), qd, qinv);
@@ -630,6 +635,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_OWN_COPY=1: copy the digits' own limbs into the extended digits (A/B timing); default: read in place
+static bool own_direct_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_OWN_COPY");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v != 0;
+}
+
 // ENSI_MD_SUB=<k>: ModDown sub-batch of k rotation-polynomials (0 = the whole batch in one pass per step)
 static uint32_t moddown_sub() {
     static int v = -1;
@@ -742,6 +757,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
 
     // ---- ModUp (once per input; all inputs in one launch per step so small batches still fill the GPU)
     const uint32_t perm = (ctx->ntt_fp_ok && A <= 8 && moddown_fp() && modup_perm()) ? 1u : 0u;
+    const bool own_direct = perm && ctx->ntt_fp_ok && beta <= 8 && kip_fp() && own_direct_env();
     {
         const size_t row_b = (size_t)level * n * 8;
         if (n_ct == 1)
@@ -780,8 +796,9 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         ENSI_LAUNCH_CHECK(ctx);
         if (perm) {
             // own limbs: the input's c1 limbs [tA, tA + c_t) in NTT form (c_t = A, or fewer in a partial last
-            // digit), to rows [E - c_t, E) of every digit block
-            for (uint32_t t = 0; t < beta; t++) {
+            // digit), to rows [E - c_t, E) of every digit block -- unless the key inner product reads them straight
+            // from the input (own_direct)
+            for (uint32_t t = 0; t < beta && !own_direct; t++) {
                 const uint32_t c_t = std::min(A, level - t * A);
                 const size_t own_b = (size_t)c_t * n * 8;
                 uint64_t* dst = ext + ((size_t)t * E + (E - c_t)) * n;
@@ -849,7 +866,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 const uint32_t lm = kip_limb_major() ? 1u : 0u;
                 dim3 gk = lm ? dim3(n / kT, cnt, E) : g;
                 k_kip_fp<<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                            ctx->tab, w_ext1, perm, lm);
+                                            ctx->tab, w_ext1, own_direct ? 2u : perm, lm, ct + c1o, in_stride);
             }
             else
                 k_kip2<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,

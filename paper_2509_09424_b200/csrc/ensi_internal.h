@@ -136,6 +136,9 @@ int ensure_scratch(ensi_ctx* ctx, size_t bytes);
 
 // NTT (ntt.cu): in-place on rows [rows][n], row r modulus = map.limb[r % map.period]
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);
+// out-of-place INTT: rows of src (smap.phys) -> dst (dmap); false when the FP64/TMA path is unavailable (nothing done)
+bool ntt_inverse_from(ensi_ctx* ctx, const uint64_t* src, const LimbMap& smap, uint64_t* dst, uint32_t rows,
+                      const LimbMap& dmap, cudaStream_t st);
 // tensor map of a row buffer for the FP64 NTT's TMA block passes (false: TMA unavailable or disabled)
 bool ntt_row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, CUtensorMap* tm);
 void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st);

@@ -635,6 +635,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_OOP_INTT=0: copy the inputs' c1 before an in-place INTT (A/B timing); default: out-of-place first pass
+static bool oop_intt_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_OOP_INTT");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
+
 // ENSI_OWN_COPY=1: copy the digits' own limbs into the extended digits (A/B timing); default: read in place
 static bool own_direct_env() {
     static int v = -1;
@@ -760,11 +770,20 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     const bool own_direct = perm && ctx->ntt_fp_ok && beta <= 8 && kip_fp() && own_direct_env();
     {
         const size_t row_b = (size_t)level * n * 8;
-        if (n_ct == 1)
-            cudaMemcpyAsync(coef, ct + c1o, row_b, cudaMemcpyDeviceToDevice, st);
-        else
-            cudaMemcpy2DAsync(coef, row_b, ct + c1o, in_stride * 8, row_b, n_ct, cudaMemcpyDeviceToDevice, st);
-        ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
+        // INTT of every input's c1 into coef: out of place (the first pass reads the input rows through a TMA
+        // tensor map) when the strides allow, else copy + in place
+        LimbMap sm = identity_map(level);
+        sm.grp_rows = level;
+        sm.grp_stride = (uint32_t)((n_ct > 1 ? in_stride : 2ull * level * n) / n);
+        sm.grp_off = (uint32_t)(c1o / n);
+        const bool strided_ok = in_stride % n == 0 && c1o % n == 0 && oop_intt_env();
+        if (!(strided_ok && ntt_inverse_from(ctx, ct, sm, coef, n_ct * level, identity_map(level), st))) {
+            if (n_ct == 1)
+                cudaMemcpyAsync(coef, ct + c1o, row_b, cudaMemcpyDeviceToDevice, st);
+            else
+                cudaMemcpy2DAsync(coef, row_b, ct + c1o, in_stride * 8, row_b, n_ct, cudaMemcpyDeviceToDevice, st);
+            ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
+        }
         if (ctx->ntt_fp_ok && A <= 4 && beta <= 4 && E <= 16 && moddown_fp() && moddown_fpc()) {
             MUConstFp mc{};
             const std::vector<double>& uf = cvt->h_modup_fp;

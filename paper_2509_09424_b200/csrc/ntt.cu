@@ -256,6 +256,22 @@ void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
     ENSI_LAUNCH_CHECK(ctx);
 }
 
+bool ntt_inverse_from(ensi_ctx* ctx, const uint64_t* src, const LimbMap& smap, uint64_t* dst, uint32_t rows,
+                      const LimbMap& dmap, cudaStream_t st) {
+    if (rows == 0) return true;
+    if (!use_fp(ctx)) return false;
+    CUtensorMap tm;
+    if (!row_tmap(ctx, const_cast<uint64_t*>(src), rows, smap, &tm)) return false;
+    const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
+    const uint32_t n = ctx->n;
+    dim3 g(16, rows);
+    nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
+                                                         nttfp::PlainOut(), smap, 1u);
+    nttfp::k_ntt256<nttfp::INV_A><<<g, 256, 0, st>>>(dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
+    ctx->launches += 2;
+    return true;
+}
+
 void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st) {
     if (rows == 0) return;
     const uint32_t log_n = ctx->log_n, n = ctx->n;

@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256(uint64_t* __res
 template <int PASS, class OUT = PlainOut>
 __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
                                                     const double2* __restrict__ tw, const double2* __restrict__ ninv,
-                                                    const __grid_constant__ CUtensorMap tmap, OUT out = OUT()) {
+                                                    const __grid_constant__ CUtensorMap tmap, OUT out = OUT(),
+                                                    LimbMap smap = LimbMap(), uint32_t oop = 0) {
     __shared__ __align__(1024) double sm[16 * kRow];
     __shared__ __align__(8) uint64_t bar;
     const uint32_t n = 65536;
@@ -322,8 +323,9 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* _
     const uint64_t q = tab.q[limb];
     const bool fwd = PASS == FWD_A || PASS == FWD_B;
     const double2* W2 = tw + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n;
-    const uint32_t prow = (uint32_t)map.phys(row);
-    uint64_t* a = data + (uint64_t)prow * n;
+    // oop (INV_B only): tile loaded from row smap.phys(row) of tmap's buffer, results written to data (map)
+    const uint32_t prow = oop ? (uint32_t)smap.phys(row) : (uint32_t)map.phys(row);
+    uint64_t* a = data + map.phys(row) * n;
     if (PASS == INV_B) {
         if (threadIdx.x == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));

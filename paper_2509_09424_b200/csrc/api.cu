@@ -594,9 +594,28 @@ int ensi_pcmm_ternary(ensi_ctx* ctx, const ensi_ct_view* x, const int8_t* W, uin
     return rc;
 }
 
-int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level, double log2_scale,
-                           const ensi_weights* wc, uint64_t* y_host, uint32_t kernel, void* stream) {
-    (void)log2_scale;
+// Wire format: limb r of a polynomial is N' words of w_r = ceil(bitlen(q_r) / 8) bytes,
+// little-endian; a ciphertext is [poly 0: limb 0 .. level-1][poly 1: ...].
+static uint32_t wire_width(const ensi_ctx* ctx, uint32_t limb) {
+    uint32_t b = 0;
+    while (b < 64 && (ctx->mod[limb] >> b)) b++;
+    return (b + 7) / 8;
+}
+static size_t wire_poly_bytes(const ensi_ctx* ctx, uint32_t level) {
+    size_t s = 0;
+    for (uint32_t r = 0; r < level; r++) s += (size_t)ctx->n * wire_width(ctx, r);
+    return s;
+}
+
+uint64_t ensi_wire_bytes(const ensi_ctx* ctx, uint32_t level) {
+    if (!ctx || level < 1 || level > ctx->L) return 0;
+    return 2 * wire_poly_bytes(ctx, level);
+}
+
+// one (poly, limb) slice of every input (and output) ciphertext moves per pipeline step: host -> device (wire
+// bytes unpacked on the device when wire), accumulate, device -> host (packed on the device when wire)
+static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, const ensi_weights* wc, void* y_host,
+                          uint32_t kernel, void* stream, bool wire) {
     if (!ctx) return ENSI_EINVAL;
     if (!x_host || !y_host || !wc) return set_err(ctx, ENSI_EINVAL, "NULL argument");
     ensi_weights* w = const_cast<ensi_weights*>(wc);
@@ -604,21 +623,23 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
     if (level < 1 || level > ctx->L) return set_err(ctx, ENSI_ELEVEL, "level out of range");
     DeviceGuard g(ctx->device);
     const uint32_t d = w->d, m = w->m, n = ctx->n, slices = 2 * level;
-    const size_t ctb = (size_t)2 * level * n * 8, rowb = (size_t)n * 8;
+    const size_t ctb = wire ? 2 * wire_poly_bytes(ctx, level) : (size_t)2 * level * n * 8;
     const size_t stage_words = (size_t)(d + m) * n;          // one slice of every input and output
-    if (!ctx->host_stage || ctx->host_stage_words < 2 * stage_words) {
+    // per buffer: the u64 slice stage, plus (wire) the same slice in wire bytes (<= 8 bytes per word)
+    const size_t buf_words = wire ? 2 * stage_words : stage_words;
+    if (!ctx->host_stage || ctx->host_stage_words < 2 * buf_words) {
         if (ctx->host_stage) {
             cudaDeviceSynchronize();
             cudaFree(ctx->host_stage);
         }
         ctx->host_stage = nullptr;
-        cudaError_t e = cudaMalloc(&ctx->host_stage, 2 * stage_words * 8);
+        cudaError_t e = cudaMalloc(&ctx->host_stage, 2 * buf_words * 8);
         if (e != cudaSuccess) {
             cudaGetLastError();
             ctx->host_stage_words = 0;
             return set_err(ctx, ENSI_ENOMEM, "staging allocation failed");
         }
-        ctx->host_stage_words = 2 * stage_words;
+        ctx->host_stage_words = 2 * buf_words;
     }
     if (!ctx->st_h2d) {
         cudaStreamCreateWithFlags(&ctx->st_h2d, cudaStreamNonBlocking);
@@ -632,6 +653,8 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
     }
     cudaStream_t st = (cudaStream_t)stream;
     const bool tc = (kernel >= 2) || (kernel == 0 && tc_supported(ctx, level));
+    const uint8_t* xh = (const uint8_t*)x_host;
+    uint8_t* yh = (uint8_t*)y_host;
     // start: the copy streams wait for everything already queued on the caller's stream
     cudaEventRecord(ctx->ev_start, st);
     cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_start, 0);
@@ -639,20 +662,36 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
     int rc = ENSI_OK;
     for (uint32_t s = 0; s < slices && !rc; s++) {
         const int b = s & 1;
-        uint64_t* xs = ctx->host_stage + (size_t)b * stage_words;
+        uint64_t* xs = ctx->host_stage + (size_t)b * buf_words;
         uint64_t* ys = xs + (size_t)d * n;
+        uint8_t* xw = (uint8_t*)(xs + stage_words);                        // wire stage (wire only)
+        uint8_t* yw = xw + (size_t)d * n * 8;
         const uint32_t poly = s / level, limb = s % level;
-        const size_t off = ((size_t)poly * level + limb) * n;   // word offset of this slice inside a ct
+        const uint32_t wb = wire ? wire_width(ctx, limb) : 8;
+        const size_t rowb = (size_t)n * wb;
+        // byte offset of this slice inside a ciphertext
+        size_t off = 0;
+        if (wire) {
+            off = (size_t)poly * wire_poly_bytes(ctx, level);
+            for (uint32_t r = 0; r < limb; r++) off += (size_t)n * wire_width(ctx, r);
+        } else {
+            off = ((size_t)poly * level + limb) * n * 8;
+        }
         if (s >= 2) cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_comp[b], 0);   // x stage b free again
-        cudaMemcpy2DAsync(xs, rowb, x_host + off, ctb, rowb, d, cudaMemcpyHostToDevice, ctx->st_h2d);
+        cudaMemcpy2DAsync(wire ? (void*)xw : (void*)xs, rowb, xh + off, ctb, rowb, d, cudaMemcpyHostToDevice,
+                          ctx->st_h2d);
         cudaEventRecord(ctx->ev_h2d[b], ctx->st_h2d);
         cudaStreamWaitEvent(st, ctx->ev_h2d[b], 0);
         if (s >= 2) cudaStreamWaitEvent(st, ctx->ev_d2h[b], 0);             // y stage b drained
-        rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, tc_variant(kernel))
-                : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
+        if (wire) rc = wire_unpack(ctx, xw, xs, (size_t)d * n, wb, st);
+        if (!rc)
+            rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, tc_variant(kernel))
+                    : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
+        if (!rc && wire) rc = wire_pack(ctx, ys, yw, (size_t)m * n, wb, st);
         cudaEventRecord(ctx->ev_comp[b], st);
         cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[b], 0);
-        cudaMemcpy2DAsync(y_host + off, ctb, ys, rowb, rowb, m, cudaMemcpyDeviceToHost, ctx->st_d2h);
+        cudaMemcpy2DAsync(yh + off, ctb, wire ? (const void*)yw : (const void*)ys, rowb, rowb, m,
+                          cudaMemcpyDeviceToHost, ctx->st_d2h);
         cudaEventRecord(ctx->ev_d2h[b], ctx->st_d2h);
     }
     // the caller's stream completes only after the last device->host copy
@@ -662,6 +701,58 @@ int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = cuda_err(ctx, e, "pcmm_host");
     }
+    return rc;
+}
+
+int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level, double log2_scale,
+                           const ensi_weights* wc, uint64_t* y_host, uint32_t kernel, void* stream) {
+    (void)log2_scale;
+    return pcmm_host_impl(ctx, x_host, level, wc, y_host, kernel, stream, false);
+}
+
+int ensi_pcmm_ternary_host_wire(ensi_ctx* ctx, const uint8_t* x_wire, uint32_t level, double log2_scale,
+                                const ensi_weights* wc, uint8_t* y_wire, uint32_t kernel, void* stream) {
+    (void)log2_scale;
+    return pcmm_host_impl(ctx, x_wire, level, wc, y_wire, kernel, stream, true);
+}
+
+int ensi_wire_pack(ensi_ctx* ctx, const ensi_ct_view* x, uint8_t* out, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, x, "x");
+    if (rc) return rc;
+    if (!out) return set_err(ctx, ENSI_EINVAL, "NULL output");
+    DeviceGuard g(ctx->device);
+    const uint32_t lv = x->level, n = ctx->n;
+    const size_t pb = wire_poly_bytes(ctx, lv);
+    for (uint32_t c = 0; c < x->count && !rc; c++)
+        for (uint32_t p = 0; p < 2 && !rc; p++) {
+            size_t off = (size_t)c * 2 * pb + p * pb;
+            for (uint32_t r = 0; r < lv && !rc; r++) {
+                const uint32_t wb = wire_width(ctx, r);
+                rc = wire_pack(ctx, x->data + (((size_t)c * 2 + p) * lv + r) * n, out + off, n, wb, (cudaStream_t)stream);
+                off += (size_t)n * wb;
+            }
+        }
+    return rc;
+}
+
+int ensi_wire_unpack(ensi_ctx* ctx, const uint8_t* in, ensi_ct_view* y, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_view(ctx, y, "y");
+    if (rc) return rc;
+    if (!in) return set_err(ctx, ENSI_EINVAL, "NULL input");
+    DeviceGuard g(ctx->device);
+    const uint32_t lv = y->level, n = ctx->n;
+    const size_t pb = wire_poly_bytes(ctx, lv);
+    for (uint32_t c = 0; c < y->count && !rc; c++)
+        for (uint32_t p = 0; p < 2 && !rc; p++) {
+            size_t off = (size_t)c * 2 * pb + p * pb;
+            for (uint32_t r = 0; r < lv && !rc; r++) {
+                const uint32_t wb = wire_width(ctx, r);
+                rc = wire_unpack(ctx, in + off, y->data + (((size_t)c * 2 + p) * lv + r) * n, n, wb, (cudaStream_t)stream);
+                off += (size_t)n * wb;
+            }
+        }
     return rc;
 }
 

@@ -182,6 +182,10 @@ int cc_scratch(ensi_ctx* ctx, size_t words);
 int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, uint32_t s, uint32_t d, uint32_t m,
          uint32_t level, const uint64_t* mask, uint64_t* y, uint32_t i0, uint32_t i1, cudaStream_t st);
 
+// wire format (poly.cu): words <-> wb-byte little-endian packing, words a multiple of 4
+int wire_unpack(ensi_ctx* ctx, const uint8_t* in, uint64_t* out, size_t words, uint32_t wb, cudaStream_t st);
+int wire_pack(ensi_ctx* ctx, const uint64_t* in, uint8_t* out, size_t words, uint32_t wb, cudaStream_t st);
+
 // poly (poly.cu)
 int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st);
 int decrypt_mu(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint64_t* mu, cudaStream_t st);

@@ -193,4 +193,86 @@ void add_into(ensi_ctx* ctx, uint64_t* y, const uint64_t* x, uint32_t count, uin
     ENSI_LAUNCH_CHECK(ctx);
 }
 
+// ---------------------------------------------------------------- wire format (compact host transfers)
+// Each thread moves 4 consecutive words = wb 32-bit words of wire bytes (4 wb bytes, 4-byte aligned).
+template <uint32_t WB>
+__global__ void __launch_bounds__(kT) k_wire_unpack(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                    size_t groups) {
+    const size_t gi = (size_t)blockIdx.x * kT + threadIdx.x;
+    if (gi >= groups) return;
+    uint32_t u[WB + 1];
+#pragma unroll
+    for (uint32_t i = 0; i < WB; i++) u[i] = __ldcs(in + gi * WB + i);
+    u[WB] = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 4; k++) {
+        const uint32_t bit = k * WB * 8, wi = bit / 32, sh = bit % 32;   // compile-time after unrolling
+        const uint64_t lo = (uint64_t)__funnelshift_r(u[wi], u[wi + 1], sh);
+        const uint64_t hi = (uint64_t)__funnelshift_r(u[wi + 1], WB > wi + 2 ? u[wi + 2] : 0u, sh);
+        uint64_t v = lo | (hi << 32);
+        if (WB < 8) v &= (1ull << (8 * WB)) - 1;
+        out[gi * 4 + k] = v;
+    }
+}
+template <uint32_t WB>
+__global__ void __launch_bounds__(kT) k_wire_pack(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                  size_t groups) {
+    const size_t gi = (size_t)blockIdx.x * kT + threadIdx.x;
+    if (gi >= groups) return;
+    uint32_t u[WB + 2];
+#pragma unroll
+    for (uint32_t i = 0; i < WB + 2; i++) u[i] = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < 4; k++) {
+        const uint64_t v = __ldcs(in + gi * 4 + k);
+        const uint32_t bit = k * WB * 8, wi = bit / 32, sh = bit % 32;
+        // place the low 8 WB bytes of v at bit offset `bit`
+        const uint64_t vlo = (uint64_t)(uint32_t)v << sh;             // bits of word wi / wi+1
+        const uint64_t vhi = (v >> 32) << sh;
+        u[wi] |= (uint32_t)vlo;
+        u[wi + 1] |= (uint32_t)(vlo >> 32) | (uint32_t)vhi;
+        u[wi + 2] |= (uint32_t)(vhi >> 32);
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < WB; i++) out[gi * WB + i] = u[i];
+}
+
+template <uint32_t WB>
+static void wire_launch(bool unpack, const void* in, void* out, size_t groups, cudaStream_t st) {
+    const uint32_t g = (uint32_t)((groups + kT - 1) / kT);
+    if (unpack) k_wire_unpack<WB><<<g, kT, 0, st>>>((const uint32_t*)in, (uint64_t*)out, groups);
+    else k_wire_pack<WB><<<g, kT, 0, st>>>((const uint64_t*)in, (uint32_t*)out, groups);
+}
+
+static int wire_dispatch(ensi_ctx* ctx, bool unpack, const void* in, void* out, size_t words, uint32_t wb,
+                         cudaStream_t st) {
+    if (words % 4) return set_err(ctx, ENSI_EINVAL, "wire transfers move multiples of 4 words");
+    const size_t groups = words / 4;
+    switch (wb) {
+        case 1: wire_launch<1>(unpack, in, out, groups, st); break;
+        case 2: wire_launch<2>(unpack, in, out, groups, st); break;
+        case 3: wire_launch<3>(unpack, in, out, groups, st); break;
+        case 4: wire_launch<4>(unpack, in, out, groups, st); break;
+        case 5: wire_launch<5>(unpack, in, out, groups, st); break;
+        case 6: wire_launch<6>(unpack, in, out, groups, st); break;
+        case 7: wire_launch<7>(unpack, in, out, groups, st); break;
+        case 8: {
+            cudaError_t e = cudaMemcpyAsync(out, in, words * 8, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_err(ctx, e, "wire copy");
+            return ENSI_OK;
+        }
+        default: return set_err(ctx, ENSI_EINVAL, "wire width must be 1..8 bytes");
+    }
+    ctx->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "wire");
+}
+
+int wire_unpack(ensi_ctx* ctx, const uint8_t* in, uint64_t* out, size_t words, uint32_t wb, cudaStream_t st) {
+    return wire_dispatch(ctx, true, in, out, words, wb, st);
+}
+int wire_pack(ensi_ctx* ctx, const uint64_t* in, uint8_t* out, size_t words, uint32_t wb, cudaStream_t st) {
+    return wire_dispatch(ctx, false, in, out, words, wb, st);
+}
+
 }  // namespace ensi

@@ -29,7 +29,8 @@ EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
            "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel", "ensi_load_relin_key",
-           "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm"]
+           "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm", "ensi_wire_bytes", "ensi_pcmm_ternary_host_wire",
+           "ensi_wire_pack", "ensi_wire_unpack"]
 
 
 class EnsiError(RuntimeError):
@@ -95,6 +96,11 @@ def lib():
         L.ensi_decrypt_debug.argtypes = [vp, C.POINTER(CtView), u32, vp, vp]
         L.ensi_launch_count.argtypes = [vp]
         L.ensi_load_relin_key.argtypes = [vp, vp, u32]
+        L.ensi_wire_bytes.restype = C.c_uint64
+        L.ensi_wire_bytes.argtypes = [vp, u32]
+        L.ensi_pcmm_ternary_host_wire.argtypes = [vp, vp, u32, C.c_double, vp, vp, u32, vp]
+        L.ensi_wire_pack.argtypes = [vp, C.POINTER(CtView), vp, vp]
+        L.ensi_wire_unpack.argtypes = [vp, vp, C.POINTER(CtView), vp]
         L.ensi_mul_plain.argtypes = [vp, C.POINTER(CtView), vp, C.c_double, C.POINTER(CtView), vp]
         L.ensi_mul_relin.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), C.POINTER(CtView), vp]
         L.ensi_ccmm.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp, C.POINTER(CtView),
@@ -255,6 +261,33 @@ class Context:
         self._check(lib().ensi_pcmm_ternary_host(self.h, _np_ptr(x_host), level, log2_scale, w.h, _np_ptr(y_host),
                                                  kernel, _stream_ptr(stream)))
 
+    # ---- compact wire format (host transfers)
+    def wire_widths(self, level: int):
+        return [(int(q).bit_length() + 7) // 8 for q in self.moduli[:level]]
+
+    def wire_bytes(self, level: int) -> int:
+        return int(lib().ensi_wire_bytes(self.h, level))
+
+    def pcmm_ternary_host_wire(self, x_wire: np.ndarray, w: Weights, y_wire: np.ndarray, level: int,
+                               kernel: int = 0, stream=None, log2_scale: float = 40.0):
+        """End-to-end Layout A on host buffers in the wire format (uint8, pinned recommended)."""
+        wb = self.wire_bytes(level)
+        if not (x_wire.dtype == np.uint8 and y_wire.dtype == np.uint8 and x_wire.flags.c_contiguous
+                and y_wire.flags.c_contiguous):
+            raise ValueError("wire buffers must be C-contiguous uint8 arrays")
+        if x_wire.size != w.d * wb or y_wire.size != w.m * wb:
+            raise ValueError(f"wire buffers must hold d / m ciphertexts of {wb} bytes")
+        self._check(lib().ensi_pcmm_ternary_host_wire(self.h, _np_ptr(x_wire), level, log2_scale, w.h,
+                                                      _np_ptr(y_wire), kernel, _stream_ptr(stream)))
+
+    def wire_pack(self, x, out, level: int, stream=None):
+        xv = self.view(x, level)
+        self._check(lib().ensi_wire_pack(self.h, C.byref(xv), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+
+    def wire_unpack(self, inp, y, level: int, stream=None):
+        yv = self.view(y, level)
+        self._check(lib().ensi_wire_unpack(self.h, C.c_void_p(inp.data_ptr()), C.byref(yv), _stream_ptr(stream)))
+
     # ---- primitives (rows a5-a7, a4, a10)
     def ntt(self, data, limb_of_row, inverse: bool = False, stream=None):
         lm = np.ascontiguousarray(limb_of_row, np.uint32)
@@ -329,6 +362,28 @@ class Context:
         self._check(lib().ensi_decrypt_debug(self.h, C.byref(cv), index,
                                              _np_ptr(coeffs) if want_coeffs else None, _np_ptr(slots)))
         return (slots, coeffs) if want_coeffs else slots
+
+
+def wire_pack_host(x: np.ndarray, widths) -> np.ndarray:
+    """Host-side wire packing of [count][2][level][N'] uint64 words (the client's serialisation; numpy only):
+    limb r keeps the low widths[r] bytes of each little-endian word."""
+    x = np.ascontiguousarray(x, np.uint64)
+    cnt, _, level, n = x.shape
+    b = x.view(np.uint8).reshape(cnt, 2, level, n, 8)
+    parts = [b[:, :, r, :, :widths[r]].reshape(cnt, 2, -1) for r in range(level)]
+    return np.ascontiguousarray(np.concatenate(parts, axis=2).reshape(cnt, -1))
+
+
+def wire_unpack_host(wb: np.ndarray, widths, level: int, n: int) -> np.ndarray:
+    """Inverse of wire_pack_host: [count][wire bytes] -> [count][2][level][N'] uint64."""
+    cnt = wb.shape[0]
+    w2 = wb.reshape(cnt, 2, -1)
+    out = np.zeros((cnt, 2, level, n, 8), np.uint8)
+    off = 0
+    for r in range(level):
+        out[:, :, r, :, :widths[r]] = w2[:, :, off:off + n * widths[r]].reshape(cnt, 2, n, widths[r])
+        off += n * widths[r]
+    return out.reshape(cnt, 2, level, n * 8).view(np.uint64).reshape(cnt, 2, level, n)
 
 
 def galois_elt(log_n: int, r: int) -> int:

@@ -551,3 +551,58 @@ def test_custom_moduli_all_size_classes_n16(torch_cuda):
     ctx.rescale(dev(torch, x), yr, 4)
     torch.cuda.synchronize()
     assert (host(yr) == np.stack([o.rescale(x[c]) for c in range(2)])).all()
+
+
+# ---------------------------------------------------------------- compact wire format (host transfers)
+
+@pytest.mark.parametrize("log_n,L,alpha", [(12, 3, 1), (16, 12, 4)])
+def test_wire_pack_unpack_device(torch_cuda, log_n, L, alpha):
+    """Device pack / unpack == the numpy host serialisation (low ceil(bits/8) bytes of each word), both ways."""
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import wire_pack_host
+    torch = torch_cuda
+    ctx = Context(log_n, L, alpha, 3)
+    x = synth.gen_words(9100 + log_n, ctx.q, 3, L, ctx.n)
+    widths = ctx.wire_widths(L)
+    want = wire_pack_host(x, widths)
+    assert want.shape[1] == ctx.wire_bytes(L)
+    out = torch.empty(want.size, dtype=torch.uint8, device="cuda")
+    ctx.wire_pack(dev(torch, x), out, L)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == want.reshape(-1)).all()
+    back = torch.empty((3, 2, L, ctx.n), dtype=torch.int64, device="cuda")
+    ctx.wire_unpack(torch.from_numpy(want.reshape(-1)).cuda(), back, L)
+    torch.cuda.synchronize()
+    assert (host(back) == x).all()
+
+
+def test_pcmm_host_wire_bit_exact(setup_c1, torch_cuda):
+    """End-to-end PCMM on wire-format host buffers == the oracle (C1, real encryptions), and == the uint64 host
+    path at C2 parameters on a 96 x 40 layer."""
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import wire_pack_host, wire_unpack_host
+    o, sk, pk, ctx = setup_c1
+    d, m = 24, 19
+    X = synth.gen_X(9200, 16, d)
+    W = synth.gen_W(9201, d, m)
+    m_res = np.stack([o.encode(X[:, j], 3, DELTA) for j in range(d)])
+    x = o.encrypt_batch(np.arange(d, dtype=np.uint64) + np.uint64(9300), pk, 3, m_res)
+    widths = ctx.wire_widths(3)
+    xw = wire_pack_host(x, widths)
+    yw = np.zeros((m, ctx.wire_bytes(3)), np.uint8)
+    w = ctx.weights(W)
+    ctx.pcmm_ternary_host_wire(xw, w, yw, level=3)
+    torch_cuda.cuda.synchronize()
+    assert (wire_unpack_host(yw, widths, 3, o.n) == o.pcmm_a(x, W)).all()
+    c2 = Context(16, 12, 4, 3)
+    d, m = 96, 40
+    x2 = synth.gen_words(9400, c2.q, d, 12, c2.n)
+    W2 = synth.gen_W(9401, d, m)
+    w2 = c2.weights(W2)
+    y64 = np.zeros((m, 2, 12, c2.n), np.uint64)
+    c2.pcmm_ternary_host(x2, w2, y64, level=12)
+    w12 = c2.wire_widths(12)
+    yw2 = np.zeros((m, c2.wire_bytes(12)), np.uint8)
+    c2.pcmm_ternary_host_wire(wire_pack_host(x2, w12), w2, yw2, level=12)
+    torch_cuda.cuda.synchronize()
+    assert (wire_unpack_host(yw2, w12, 12, c2.n) == y64).all()

@@ -57,3 +57,19 @@ def test_product_never_imports_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, flags=re.M), f
                 assert "liboracle" not in txt, f
                 assert "ensi_oracle" not in txt, f
+
+
+def test_wire_host_serialisation_round_trip():
+    """The wire format keeps the low ceil(bits/8) bytes of each canonical word, limb blocks in order (numpy, CPU)."""
+    import numpy as np
+    from paper_2509_09424_b200.ensi import wire_pack_host, wire_unpack_host
+    rs = np.random.default_rng(3)
+    widths = [7, 5, 5, 6]
+    n, level = 32, 4
+    x = np.stack([rs.integers(0, 1 << (8 * w - 1), (2, 2, n), dtype=np.uint64) for w in widths], axis=2)
+    p = wire_pack_host(x, widths)
+    assert p.shape == (2, 2 * n * sum(widths))
+    # limb 1 of poly 0 of ciphertext 0 starts after limb 0's n * 7 bytes; word 3 is little-endian
+    off = n * widths[0] + 3 * widths[1]
+    assert int.from_bytes(p[0, off:off + widths[1]].tobytes(), "little") == int(x[0, 0, 1, 3])
+    assert (wire_unpack_host(p, widths, level, n) == x).all()

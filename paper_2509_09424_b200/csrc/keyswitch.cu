@@ -353,6 +353,50 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ e
     }
 }
 
+// Same key inner product specialised on the digit count (BETA <= 4): the digit row offsets are resolved once per
+// thread, both key words of every digit are loaded once and reused for every input of the batch, and the digit loops
+// are unrolled.  ncu had the generic kernel issue-bound (85 % issue active, 519 warp instructions per 32 words and
+// limb, 45 % of them uniform-datapath index arithmetic re-evaluated inside the input and digit loops).
+template <uint32_t BETA>
+__global__ void __launch_bounds__(kT, 8) k_kip_fpt(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
+                                                   uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n,
+                                                   uint32_t level, uint32_t L, uint32_t A, uint32_t dnum, ModTab tab,
+                                                   uint64_t ext_stride, uint32_t perm, uint32_t limb_major,
+                                                   const uint64_t* __restrict__ c1p, uint64_t in_stride) {
+    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
+    const uint32_t e = limb_major ? blockIdx.z : blockIdx.y, gi = limb_major ? blockIdx.y : blockIdx.z;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint32_t src = galois_src_index(k, gb.g[gi], log_n);
+    const size_t TN = (size_t)T * n;
+    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * TN + (size_t)li * n + k;
+    const uint64_t q = tab.q[li];
+    const double qd = (double)q, qinv = 1.0 / qd;
+    const uint64_t* base[BETA];
+    double kb0[BETA], kb1[BETA];
+#pragma unroll
+    for (uint32_t t = 0; t < BETA; t++) {
+        const bool own = perm == 2 && e >= t * A && e < t * A + A && e < level;
+        base[t] = own ? c1p + (size_t)e * n + src : ext + ((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n + src;
+        kb0[t] = nttfp::i2d((long long)__ldg(key + (size_t)t * 2 * TN));
+        kb1[t] = nttfp::i2d((long long)__ldg(key + (size_t)t * 2 * TN + TN));
+    }
+    const bool own_any = perm == 2;
+    for (uint32_t c = 0; c < gb.n_ct; c++) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (uint32_t t = 0; t < BETA; t++) {
+            const bool own = own_any && e >= t * A && e < t * A + A && e < level;
+            const double dv = nttfp::i2d((long long)base[t][(size_t)c * (own ? in_stride : ext_stride)]);
+            s0 += kip_mul(dv, kb0[t], qd, qinv);
+            s1 += kip_mul(dv, kb1[t], qd, qinv);
+        }
+        const size_t r = (size_t)c * gb.cnt + gi;
+        acc[((r * 2 + 0) * E + e) * n + k] = nttfp::canon(nttfp::red(s0, qd, qinv), q);
+        acc[((r * 2 + 1) * E + e) * n + k] = nttfp::canon(nttfp::red(s1, qd, qinv), q);
+    }
+}
+
 // Key inner product with the automorphism fused on load, both key polynomials per thread (the digit gathers are
 // shared): acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r), j = 0, 1.
 __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
@@ -635,6 +679,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_KIP_GENERIC=1: the generic (loop) FP64 key inner product instead of the digit-count specialisations
+static bool kip_generic() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KIP_GENERIC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v != 0;
+}
+
 // ENSI_OOP_INTT=0: copy the inputs' c1 before an in-place INTT (A/B timing); default: out-of-place first pass
 static bool oop_intt_env() {
     static int v = -1;
@@ -884,8 +938,23 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             if (ctx->ntt_fp_ok && beta <= 8 && kip_fp()) {
                 const uint32_t lm = kip_limb_major() ? 1u : 0u;
                 dim3 gk = lm ? dim3(n / kT, cnt, E) : g;
-                k_kip_fp<<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,
-                                            ctx->tab, w_ext1, own_direct ? 2u : perm, lm, ct + c1o, in_stride);
+                const uint32_t pm = own_direct ? 2u : perm;
+                const uint64_t* c1p = ct + c1o;
+                switch (kip_generic() ? 0u : beta) {
+#define ENSI_KIPT(B)                                                                                                   \
+    case B:                                                                                                            \
+        k_kip_fpt<B><<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, ctx->tab,   \
+                                        w_ext1, pm, lm, c1p, in_stride);                                               \
+        break;
+                    ENSI_KIPT(1)
+                    ENSI_KIPT(2)
+                    ENSI_KIPT(3)
+                    ENSI_KIPT(4)
+#undef ENSI_KIPT
+                    default:
+                        k_kip_fp<<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,
+                                                    beta, ctx->tab, w_ext1, pm, lm, c1p, in_stride);
+                }
             }
             else
                 k_kip2<<<g, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, beta,

@@ -266,15 +266,15 @@ struct MUConstFp {
     double c[4][16][4], cq[4][16][4];     // [t][e][a]: [Q_t/q_i]_{r_e} centred, RN(./r_e)
     double qs[16], r[16], rinv[16];       // q of the source limbs (Q order), r_e, RN(1/r_e)
 };
-__global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
-                                                          uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
-                                                          const __grid_constant__ MUConstFp mc, uint32_t perm) {
-    const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
-    const uint32_t t = blockIdx.y;
-    const uint32_t k = blockIdx.x * kT + threadIdx.x;
-    coef += (size_t)blockIdx.z * level * n;
-    ext += ((size_t)blockIdx.z * beta + t) * E * n;
-    const uint32_t lo = t * A, hi = min((t + 1) * A, level), cnt = hi - lo;
+// The digit index is a template parameter so every constant (Q_t/q_i)^-1, [Q_t/q_i]_{r_e} is a compile-time offset
+// into the parameter bank (ncu: the runtime-indexed version spent 150 of 1331 warp instructions per position on
+// LDC constant loads plus their address arithmetic).
+template <uint32_t TT>
+__device__ __forceinline__ void modup_fpc_body(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                               uint32_t n, uint32_t level, uint32_t L, uint32_t A,
+                                               const MUConstFp& mc, uint32_t perm, uint32_t k) {
+    const uint32_t E = level + A;
+    const uint32_t lo = TT * A, hi = min(lo + A, level), cnt = hi - lo;
     uint64_t own[4];
     double y[4];
 #pragma unroll
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __rest
         if (a < cnt) {
             const double qa = mc.qs[lo + a];
             own[a] = coef[(size_t)(lo + a) * n + k];
-            const double rr = nttfp::mulmod(nttfp::i2d((long long)own[a]), mc.cinv[t][a], mc.cinvq[t][a], qa);
+            const double rr = nttfp::mulmod(nttfp::i2d((long long)own[a]), mc.cinv[TT][a], mc.cinvq[TT][a], qa);
             y[a] = rr < 0.0 ? rr + qa : rr;                           // canonical [0, q_a)
         }
     }
@@ -301,11 +301,26 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __rest
                 double sum = 0.0;
 #pragma unroll
                 for (uint32_t a = 0; a < 4; a++)
-                    if (a < cnt) sum += nttfp::mulmod(y[a], mc.c[t][e][a], mc.cq[t][e][a], mc.r[e]);
-                ext[(size_t)ext_row(perm, t, e, A, E, level) * n + k] =
+                    if (a < cnt) sum += nttfp::mulmod(y[a], mc.c[TT][e][a], mc.cq[TT][e][a], mc.r[e]);
+                ext[(size_t)ext_row(perm, TT, e, A, E, level) * n + k] =
                     nttfp::canon(nttfp::red(sum, mc.r[e], mc.rinv[e]), (uint64_t)mc.r[e]);
             }
         }
+    }
+}
+__global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                          uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                          const __grid_constant__ MUConstFp mc, uint32_t perm) {
+    const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
+    const uint32_t t = blockIdx.y;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    coef += (size_t)blockIdx.z * level * n;
+    ext += ((size_t)blockIdx.z * beta + t) * E * n;
+    switch (t) {
+        case 0: modup_fpc_body<0>(coef, ext, n, level, L, A, mc, perm, k); break;
+        case 1: modup_fpc_body<1>(coef, ext, n, level, L, A, mc, perm, k); break;
+        case 2: modup_fpc_body<2>(coef, ext, n, level, L, A, mc, perm, k); break;
+        default: modup_fpc_body<3>(coef, ext, n, level, L, A, mc, perm, k); break;
     }
 }
 

@@ -53,6 +53,7 @@ struct ConvTables {
     // modup for the FP64 conversion: same indexing as d_modup, (centred constant, RN(constant / modulus)) pairs
     double* d_modup_fp = nullptr;
     std::vector<double> h_modup_fp;       // host copy (kernel-parameter constants)
+    std::vector<uint64_t> h_pinv;         // [level]: P^{-1} mod q_i (canonical), for the FP64 final combine
 };
 
 }  // namespace ensi

@@ -90,6 +90,7 @@ int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out) {
         }
         uint64_t pinv = invmod_h(P, q);
         size_t idx = (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
+        ct.h_pinv.push_back(pinv);
         md[idx] = pinv;
         md[idx + 1] = shoup_h(pinv, q);
         for (uint32_t k = 0; k < A; k++)
@@ -596,6 +597,31 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
 }
 
+// FP64 final combine: out = (acc_{q_i} - z) P^{-1} (+ sigma_g(c0)) (+ added input) with one exact FP64 product
+// (ncu had the integer kernel issue-bound at 74 %, 35 % IMAD from the 64-bit Shoup product and a runtime
+// division for (input, element)); the FP64 pipe is otherwise idle here.
+struct MDFinConst {
+    double pinv[16], pinvq[16], q[16], qinv[16];   // [P^-1]_{q_i} centred, RN(./q_i), q_i, RN(1/q_i)
+};
+__global__ void __launch_bounds__(kT) k_moddown_final_fp(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
+                                                         const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
+                                                         GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
+                                                         const __grid_constant__ MDFinConst fc, uint32_t add_mask,
+                                                         uint64_t add1_off, uint32_t gj0) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1, r = gj >> 1;
+    const uint32_t c = gb.n_ct == 1 ? 0u : r / gb.cnt, gi = r - c * gb.cnt;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const double qd = fc.q[i], qinv = fc.qinv[i];
+    const long long dv = (long long)acc[((size_t)gj * E + i) * n + k] - (long long)z[((size_t)blockIdx.z * level + i) * n + k];
+    double v = nttfp::mulmod(nttfp::i2d(dv), fc.pinv[i], fc.pinvq[i], qd);          // |v| <= 0.625 q
+    const uint64_t* cb = c0 + c * gb.in_stride + (size_t)i * n;
+    if (j == 0) v += nttfp::i2d((long long)cb[galois_src_index(k, gb.g[gi], log_n)]);
+    if ((add_mask >> j) & 1) v += nttfp::i2d((long long)cb[(j ? add1_off : 0) + k]);
+    out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] =
+        nttfp::canon(nttfp::red(v, qd, qinv), (uint64_t)qd);
+}
+
 // ---------------------------------------------------------------- fused ModDown (N' = 2^16, FP64 NTT passes; opt-in)
 // Row r of the z NTT = (gj = r / level, limb i = r % level).  The first NTT pass computes the centred fast
 // conversion of the INTT'ed P limbs on load (no z round trip through HBM); the last pass forms
@@ -694,6 +720,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_MDFINAL=int: the integer (Shoup) final combine (A/B timing); default FP64
+static bool mdfinal_fp() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_MDFINAL");
+        v = (e && std::string(e) == "int") ? 0 : 1;
+    }
+    return v != 0;
+}
+
 // ENSI_KIP_GENERIC=1: the generic (loop) FP64 key inner product instead of the digit-count specialisations
 static bool kip_generic() {
     static int v = -1;
@@ -1053,6 +1089,18 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         ntt_forward(ctx, z, gcnt * level, identity_map(level), st);
         {
             dim3 g(n / kT, level, gcnt);
+            if (ctx->ntt_fp_ok && level <= 16 && mdfinal_fp()) {
+                MDFinConst fc{};
+                for (uint32_t i = 0; i < level; i++) {
+                    const uint64_t q = ctx->mod[i], w = cvt->h_pinv[i];
+                    fc.q[i] = (double)q;
+                    fc.qinv[i] = 1.0 / fc.q[i];
+                    fc.pinv[i] = w > q / 2 ? -(double)(q - w) : (double)w;
+                    fc.pinvq[i] = fc.pinv[i] / fc.q[i];
+                }
+                k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask, add1o,
+                                                     g0);
+            } else
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
                                               ko.add_mask, add1o, g0);
             ENSI_LAUNCH_CHECK(ctx);

@@ -74,10 +74,11 @@ __device__ __forceinline__ uint64_t reduce_signed(int64_t v, const Barrett& b) {
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, uint32_t bits) { return __brev(x) >> (32 - bits); }
 
 // NTT-domain Galois automorphism: out[k] = in[perm(k)] with 2 brv(perm)+1 == (2 brv(k)+1) g mod 2N'
+// (only the product mod 2N' <= 2^18 is needed, so 32-bit arithmetic -- the low bits of a product -- is exact)
 __device__ __forceinline__ uint32_t galois_src_index(uint32_t k, uint64_t g, uint32_t log_n) {
-    const uint64_t mask = (2ull << log_n) - 1;          // mod 2N'
-    uint64_t e = ((2ull * bitrev(k, log_n) + 1) * g) & mask;
-    return bitrev((uint32_t)((e - 1) >> 1), log_n);
+    const uint32_t mask = (2u << log_n) - 1;            // mod 2N'
+    const uint32_t e = ((2u * bitrev(k, log_n) + 1u) * (uint32_t)g) & mask;
+    return bitrev((e - 1) >> 1, log_n);
 }
 
 }  // namespace ensi

@@ -369,12 +369,16 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ e
     }
 }
 
+#ifndef ENSI_KIPT_MINB
+#define ENSI_KIPT_MINB 6
+#endif
 // Same key inner product specialised on the digit count (BETA <= 4): the digit row offsets are resolved once per
 // thread, both key words of every digit are loaded once and reused for every input of the batch, and the digit loops
 // are unrolled.  ncu had the generic kernel issue-bound (85 % issue active, 519 warp instructions per 32 words and
 // limb, 45 % of them uniform-datapath index arithmetic re-evaluated inside the input and digit loops).
 template <uint32_t BETA>
-__global__ void __launch_bounds__(kT, 8) k_kip_fpt(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(kT, ENSI_KIPT_MINB) k_kip_fpt(const uint64_t* __restrict__ ext,
+                                                   const uint64_t* __restrict__ keys,
                                                    uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n,
                                                    uint32_t level, uint32_t L, uint32_t A, uint32_t dnum, ModTab tab,
                                                    uint64_t ext_stride, uint32_t perm, uint32_t limb_major,
@@ -388,28 +392,32 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fpt(const uint64_t* __restrict__ 
     const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * TN + (size_t)li * n + k;
     const uint64_t q = tab.q[li];
     const double qd = (double)q, qinv = 1.0 / qd;
-    const uint64_t* base[BETA];
+    // per digit: a pointer walking the inputs (own limbs read in place from c1, the rest from the extended digits)
+    const uint64_t* p[BETA];
+    size_t str[BETA];
     double kb0[BETA], kb1[BETA];
 #pragma unroll
     for (uint32_t t = 0; t < BETA; t++) {
         const bool own = perm == 2 && e >= t * A && e < t * A + A && e < level;
-        base[t] = own ? c1p + (size_t)e * n + src : ext + ((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n + src;
+        p[t] = own ? c1p + (size_t)e * n + src : ext + ((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n + src;
+        str[t] = own ? in_stride : ext_stride;
         kb0[t] = nttfp::i2d((long long)__ldg(key + (size_t)t * 2 * TN));
         kb1[t] = nttfp::i2d((long long)__ldg(key + (size_t)t * 2 * TN + TN));
     }
-    const bool own_any = perm == 2;
+    uint64_t* o = acc + ((size_t)gi * 2 * E + e) * n + k;
+    const size_t ostep = (size_t)gb.cnt * 2 * E * n, en = (size_t)E * n;
     for (uint32_t c = 0; c < gb.n_ct; c++) {
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
         for (uint32_t t = 0; t < BETA; t++) {
-            const bool own = own_any && e >= t * A && e < t * A + A && e < level;
-            const double dv = nttfp::i2d((long long)base[t][(size_t)c * (own ? in_stride : ext_stride)]);
+            const double dv = nttfp::i2d((long long)*p[t]);
+            p[t] += str[t];
             s0 += kip_mul(dv, kb0[t], qd, qinv);
             s1 += kip_mul(dv, kb1[t], qd, qinv);
         }
-        const size_t r = (size_t)c * gb.cnt + gi;
-        acc[((r * 2 + 0) * E + e) * n + k] = nttfp::canon(nttfp::red(s0, qd, qinv), q);
-        acc[((r * 2 + 1) * E + e) * n + k] = nttfp::canon(nttfp::red(s1, qd, qinv), q);
+        o[0] = nttfp::canon(nttfp::red(s0, qd, qinv), q);
+        o[en] = nttfp::canon(nttfp::red(s1, qd, qinv), q);
+        o += ostep;
     }
 }
 

@@ -49,51 +49,79 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+_NVML_POLL = r"""
+import sys, time, pynvml
+pynvml.nvmlInitWithFlags(0) if hasattr(pynvml, "nvmlInitWithFlags") else pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+out = open(sys.argv[2], "w", buffering=1)
+out.write("ready %d\n" % pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+while True:
+    out.write("%.6f %d %d\n" % (time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                 pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    time.sleep(0.0005)
+"""
+
+
 class NvmlClockSampler:
-    """SM clock and clock-event reasons polled through NVML every ~1 ms on a background thread while the timed
-    region runs (the timed region of a 5-step C2 run is ~27 ms, far shorter than nvidia-smi's sampling period)."""
+    """SM clock and clock-event reasons polled through NVML every ~0.5 ms by a separate process (no GIL
+    contention with the timed loop); only the samples whose host timestamps fall inside the timed region count.
+    Start it before the warm-up (the poller needs ~0.2 s to come up), mark the region with begin()/end()."""
 
     def __init__(self, device_index: int):
-        import pynvml
-        self.nv = pynvml
-        pynvml.nvmlInit()
-        self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
-        self.rows = []
-        self.run = False
-        self.th = None
-
-    def _poll(self):
-        nv = self.nv
-        while self.run:
-            try:
-                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
-                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
-            except Exception:
-                pass
-            time.sleep(0.001)
+        import pynvml  # noqa: F401  (fail here, not in the child, when NVML is missing)
+        self.dev = device_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".clk", delete=False)
+        self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
-        import threading
-        self.run = True
-        self.th = threading.Thread(target=self._poll, daemon=True)
-        self.th.start()
+        self.proc = subprocess.Popen([sys.executable, "-c", _NVML_POLL, str(self.dev), self.f.name],
+                                     stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        for _ in range(200):                       # wait until the poller is sampling (<= 2 s)
+            time.sleep(0.01)
+            try:
+                if open(self.f.name).read().count("\n") >= 2:
+                    break
+            except OSError:
+                pass
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
 
     def stop(self):
-        self.run = False
-        if self.th is not None:
-            self.th.join(timeout=2)
-        nv = self.nv
-        smmax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
-        if not self.rows:
+        time.sleep(0.005)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        lines = open(self.f.name).read().split("\n")
+        os.unlink(self.f.name)
+        smmax, rows = None, []
+        for ln in lines:
+            p = ln.split()
+            if len(p) == 2 and p[0] == "ready":
+                smmax = int(p[1])
+            elif len(p) == 3:
+                t, c, r = float(p[0]), int(p[1]), int(p[2])
+                if self.t0 is not None and self.t0 <= t <= (self.t1 or t):
+                    rows.append((c, r))
+        if not rows:
             return None
+        import pynvml as nv
         names = ((nv.nvmlClocksEventReasonHwSlowdown, "hw_slowdown"),
                  (nv.nvmlClocksEventReasonHwThermalSlowdown, "hw_thermal_slowdown"),
                  (nv.nvmlClocksEventReasonSwThermalSlowdown, "sw_thermal_slowdown"),
                  (nv.nvmlClocksEventReasonSwPowerCap, "sw_power_cap"),
                  (nv.nvmlClocksEventReasonHwPowerBrakeSlowdown, "hw_power_brake"))
-        reasons = sorted({name for _, r in self.rows for bit, name in names if r & bit})
-        return {"sm_mhz": statistics.median(c for c, _ in self.rows), "sm_max_mhz": smmax, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml, ~1 ms polling during the timed region"}
+        reasons = sorted({name for _, r in rows for bit, name in names if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in rows), "sm_max_mhz": smmax, "reasons": reasons,
+                "samples": len(rows), "min_mhz": min(c for c, _ in rows),
+                "source": "nvml polled every ~0.5 ms by a separate process, samples inside the timed region"}
 
 
 def clock_sampler(device_index: int):
@@ -494,20 +522,24 @@ def main():
     st = torch.cuda.current_stream()
     step = lambda: ctx.pcmm_ternary(x, w, y, level=L, kernel=args.kernel)  # noqa: E731
 
+    clocks = clock_sampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clocks = clock_sampler(local)
-    clocks.start()
     l0 = ctx.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     ev_s, ev_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if hasattr(clocks, "begin"):
+        clocks.begin()
     ev_s.record(st)
     for _ in range(args.steps):
         step()
     ev_e.record(st)
     torch.cuda.synchronize()
+    if hasattr(clocks, "end"):
+        clocks.end()
     barrier(world)
     ms_rank = ev_s.elapsed_time(ev_e) / args.steps
     launches = (ctx.launch_count() - l0)

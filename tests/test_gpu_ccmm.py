@@ -205,3 +205,63 @@ def test_rotation_partial_last_digit_n16(torch_cuda, level):
     torch.cuda.synchronize()
     assert (host(yh)[1] == o.rotate(x[0], gs[1], keys[1])).all()
     assert (host(yb)[1] == o.rotate(x[1], gs[1], keys[1])).all()
+
+
+def test_integer_paths_large_moduli(torch_cuda):
+    """Moduli >= 2^50 (up to just under 2^60) take the integer NTT, ModUp/KIP/ModDown and accumulate paths (no FP64
+    shortcuts): PCMM, hoisted and batched rotations, Mult + relinearisation, rescale and a CCMM, word for word."""
+    import sympy
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    m2n = 1 << 13
+
+    def primes(below, cnt, skip=0):
+        out, v = [], (below - 1) // m2n * m2n + 1
+        while len(out) < cnt + skip:
+            if sympy.isprime(v):
+                out.append(v)
+            v -= m2n
+        return out[skip:]
+    q = primes(1 << 60, 1) + primes(1 << 55, 2)
+    p = primes(1 << 60, 1, skip=1)
+    o = oracle.Oracle(12, 3, 1, 3, q=q, p=p)
+    ctx = Context(12, 3, 1, 3, q=q, p=p)
+    assert ctx.moduli == o.moduli
+    skc, sk, pk = o.keygen(777)
+    ctx.load_keys(sk_ntt=sk)
+    # PCMM (Layout A)
+    x = synth.gen_words(9500, o.q, 20, 3, o.n)
+    W = synth.gen_W(9501, 20, 9)
+    yd = torch.empty((9, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(dev(torch, x), W, yd, level=3)
+    torch.cuda.synchronize()
+    assert (host(yd) == o.pcmm_a(x, W)).all()
+    # rotations (hoisted and independent-input batches) and rescale
+    gs = [o.galois(5), o.galois(-3)]
+    keys = np.stack([o.rotkey(9600 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(galois=gs, rot_keys=keys)
+    ct = synth.gen_words(9602, o.q, 2, 3, o.n)
+    yh = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(dev(torch, ct[:1]), gs, yh, 3)
+    yb = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_batch(dev(torch, ct), gs[1:], yb, 3)
+    yr = torch.empty((2, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(dev(torch, ct), yr, 3)
+    torch.cuda.synchronize()
+    assert (host(yh) == o.rotate_hoisted(ct[0], gs, keys)).all()
+    assert (host(yb)[1] == o.rotate(ct[1], gs[1], keys[1])).all()
+    assert (host(yr)[0] == o.rescale(ct[0])).all()
+    # Mult + relinearisation, then a CCMM (form 2) on real encryptions
+    rlk = o.relinkey(9700, sk)
+    ctx.load_relin_key(rlk)
+    ym = torch.empty((1, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.mul_relin(dev(torch, ct[:1]), dev(torch, ct[1:]), ym, 3)
+    torch.cuda.synchronize()
+    assert (host(ym)[0] == o.relin(o.mul_ct(ct[0], ct[1]), rlk)).all()
+    form, s, d, m = 2, 16, 3, 2
+    a, src, mask, ckeys, crlk, ref = _ccmm_setup(o, sk, pk, form, s, d, m, 9800)
+    _load(ctx, ckeys, crlk)
+    yc = torch.empty((m, 2, 1, o.n), dtype=torch.int64, device="cuda")
+    ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yc, form, s, d, m, 3)
+    torch.cuda.synchronize()
+    assert (host(yc) == o.ccmm(a, src, form, s, d, m, mask, ckeys, crlk)).all()

@@ -421,6 +421,60 @@ __global__ void __launch_bounds__(kT, ENSI_KIPT_MINB) k_kip_fpt(const uint64_t* 
     }
 }
 
+// Two consecutive positions per thread: the key words of both come with one 16-byte load per digit and key
+// polynomial, the outputs go out as 16-byte stores, and the per-thread setup is shared (ENSI_KIP_PAIR=0: one
+// position per thread).
+template <uint32_t BETA>
+__global__ void __launch_bounds__(kT, 4) k_kip_fpt2(const uint64_t* __restrict__ ext,
+                                                    const uint64_t* __restrict__ keys,
+                                                    uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n,
+                                                    uint32_t level, uint32_t L, uint32_t A, uint32_t dnum, ModTab tab,
+                                                    uint64_t ext_stride, uint32_t perm, uint32_t limb_major,
+                                                    const uint64_t* __restrict__ c1p, uint64_t in_stride) {
+    const uint32_t n = 1u << log_n, E = level + A, T = L + A;
+    const uint32_t e = limb_major ? blockIdx.z : blockIdx.y, gi = limb_major ? blockIdx.y : blockIdx.z;
+    const uint32_t li = e < level ? e : L + (e - level);
+    const uint32_t k = 2 * (blockIdx.x * kT + threadIdx.x);
+    const uint64_t g = gb.g[gi];
+    const uint32_t srcA = galois_src_index(k, g, log_n), srcB = galois_src_index(k + 1, g, log_n);
+    const size_t TN = (size_t)T * n;
+    const uint64_t* key = keys + (size_t)gb.key[gi] * dnum * 2 * TN + (size_t)li * n + k;
+    const uint64_t q = tab.q[li];
+    const double qd = (double)q, qinv = 1.0 / qd;
+    const uint64_t* p[BETA];
+    size_t str[BETA];
+    double k0a[BETA], k0b[BETA], k1a[BETA], k1b[BETA];
+#pragma unroll
+    for (uint32_t t = 0; t < BETA; t++) {
+        const bool own = perm == 2 && e >= t * A && e < t * A + A && e < level;
+        p[t] = own ? c1p + (size_t)e * n : ext + ((size_t)t * E + ext_row(perm, t, e, A, E, level)) * n;
+        str[t] = own ? in_stride : ext_stride;
+        const ulonglong2 w0 = __ldg(reinterpret_cast<const ulonglong2*>(key + (size_t)t * 2 * TN));
+        const ulonglong2 w1 = __ldg(reinterpret_cast<const ulonglong2*>(key + (size_t)t * 2 * TN + TN));
+        k0a[t] = nttfp::i2d((long long)w0.x), k0b[t] = nttfp::i2d((long long)w0.y);
+        k1a[t] = nttfp::i2d((long long)w1.x), k1b[t] = nttfp::i2d((long long)w1.y);
+    }
+    uint64_t* o = acc + ((size_t)gi * 2 * E + e) * n + k;
+    const size_t ostep = (size_t)gb.cnt * 2 * E * n, en = (size_t)E * n;
+    for (uint32_t c = 0; c < gb.n_ct; c++) {
+        double s0a = 0.0, s1a = 0.0, s0b = 0.0, s1b = 0.0;
+#pragma unroll
+        for (uint32_t t = 0; t < BETA; t++) {
+            const double da = nttfp::i2d((long long)p[t][srcA]), db = nttfp::i2d((long long)p[t][srcB]);
+            p[t] += str[t];
+            s0a += kip_mul(da, k0a[t], qd, qinv);
+            s1a += kip_mul(da, k1a[t], qd, qinv);
+            s0b += kip_mul(db, k0b[t], qd, qinv);
+            s1b += kip_mul(db, k1b[t], qd, qinv);
+        }
+        *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(nttfp::canon(nttfp::red(s0a, qd, qinv), q),
+                                                             nttfp::canon(nttfp::red(s0b, qd, qinv), q));
+        *reinterpret_cast<ulonglong2*>(o + en) = make_ulonglong2(nttfp::canon(nttfp::red(s1a, qd, qinv), q),
+                                                                  nttfp::canon(nttfp::red(s1b, qd, qinv), q));
+        o += ostep;
+    }
+}
+
 // Key inner product with the automorphism fused on load, both key polynomials per thread (the digit gathers are
 // shared): acc[gi][j][e][k] = sum_t ext[t][e][src_g(k)] * key[gi][t][j][limb(e)][k]  (mod r), j = 0, 1.
 __global__ void __launch_bounds__(kT) k_kip2(const uint64_t* __restrict__ ext, const uint64_t* __restrict__ keys,
@@ -728,6 +782,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_KIP_PAIR=0: one position per thread in the specialised key inner product (A/B timing)
+static bool kip_pair() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KIP_PAIR");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
+
 // ENSI_MDFINAL=int: the integer (Shoup) final combine (A/B timing); default FP64
 static bool mdfinal_fp() {
     static int v = -1;
@@ -1002,8 +1066,14 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 switch (kip_generic() ? 0u : beta) {
 #define ENSI_KIPT(B)                                                                                                   \
     case B:                                                                                                            \
-        k_kip_fpt<B><<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum, ctx->tab,   \
-                                        w_ext1, pm, lm, c1p, in_stride);                                               \
+        if (kip_pair() && n >= 2 * kT) {                                                                               \
+            dim3 g2(gk.x / 2, gk.y, gk.z);                                                                             \
+            k_kip_fpt2<B><<<g2, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,         \
+                                             ctx->tab, w_ext1, pm, lm, c1p, in_stride);                                \
+        } else {                                                                                                       \
+            k_kip_fpt<B><<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,          \
+                                            ctx->tab, w_ext1, pm, lm, c1p, in_stride);                                 \
+        }                                                                                                              \
         break;
                     ENSI_KIPT(1)
                     ENSI_KIPT(2)

@@ -684,6 +684,38 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp(const uint64_t* __restr
         nttfp::canon(nttfp::red(v, qd, qinv), (uint64_t)qd);
 }
 
+// Same combine for two consecutive positions per thread (16-byte loads of acc / z / the added input and 16-byte
+// stores; the per-thread setup is shared).
+__global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __restrict__ acc, const uint64_t* __restrict__ z,
+                                                          const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
+                                                          GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
+                                                          const __grid_constant__ MDFinConst fc, uint32_t add_mask,
+                                                          uint64_t add1_off, uint32_t gj0) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1, r = gj >> 1;
+    const uint32_t c = gb.n_ct == 1 ? 0u : r / gb.cnt, gi = r - c * gb.cnt;
+    const uint32_t k = 2 * (blockIdx.x * kT + threadIdx.x);
+    const double qd = fc.q[i], qinv = fc.qinv[i], pw = fc.pinv[i], pq = fc.pinvq[i];
+    const ulonglong2 av = *reinterpret_cast<const ulonglong2*>(acc + ((size_t)gj * E + i) * n + k);
+    const ulonglong2 zv = *reinterpret_cast<const ulonglong2*>(z + ((size_t)blockIdx.z * level + i) * n + k);
+    double va = nttfp::mulmod(nttfp::i2d((long long)av.x - (long long)zv.x), pw, pq, qd);
+    double vb = nttfp::mulmod(nttfp::i2d((long long)av.y - (long long)zv.y), pw, pq, qd);
+    const uint64_t* cb = c0 + c * gb.in_stride + (size_t)i * n;
+    if (j == 0) {
+        const uint64_t g = gb.g[gi];
+        va += nttfp::i2d((long long)cb[galois_src_index(k, g, log_n)]);
+        vb += nttfp::i2d((long long)cb[galois_src_index(k + 1, g, log_n)]);
+    }
+    if ((add_mask >> j) & 1) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(cb + (j ? add1_off : 0) + k);
+        va += nttfp::i2d((long long)w.x);
+        vb += nttfp::i2d((long long)w.y);
+    }
+    const uint64_t q = (uint64_t)qd;
+    *reinterpret_cast<ulonglong2*>(out + ((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k) =
+        make_ulonglong2(nttfp::canon(nttfp::red(va, qd, qinv), q), nttfp::canon(nttfp::red(vb, qd, qinv), q));
+}
+
 // ---------------------------------------------------------------- fused ModDown (N' = 2^16, FP64 NTT passes; opt-in)
 // Row r of the z NTT = (gj = r / level, limb i = r % level).  The first NTT pass computes the centred fast
 // conversion of the INTT'ed P limbs on load (no z round trip through HBM); the last pass forms
@@ -1176,8 +1208,13 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                     fc.pinv[i] = w > q / 2 ? -(double)(q - w) : (double)w;
                     fc.pinvq[i] = fc.pinv[i] / fc.q[i];
                 }
-                k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask, add1o,
-                                                     g0);
+                if (kip_pair() && n >= 2 * kT) {
+                    dim3 g2(g.x / 2, g.y, g.z);
+                    k_moddown_final_fp2<<<g2, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
+                                                           add1o, g0);
+                } else
+                    k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
+                                                         add1o, g0);
             } else
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
                                               ko.add_mask, add1o, g0);

@@ -325,6 +325,69 @@ __global__ void __launch_bounds__(kT) k_modup_convert_fpc(const uint64_t* __rest
     }
 }
 
+// two consecutive positions per thread (16-byte loads and stores)
+template <uint32_t TT>
+__device__ __forceinline__ void modup_fpc_body2(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                uint32_t n, uint32_t level, uint32_t L, uint32_t A,
+                                                const MUConstFp& mc, uint32_t perm, uint32_t k) {
+    const uint32_t E = level + A;
+    const uint32_t lo = TT * A, hi = min(lo + A, level), cnt = hi - lo;
+    ulonglong2 own[4];
+    double ya[4], yb[4];
+#pragma unroll
+    for (uint32_t a = 0; a < 4; a++) {
+        if (a < cnt) {
+            const double qa = mc.qs[lo + a];
+            own[a] = *reinterpret_cast<const ulonglong2*>(coef + (size_t)(lo + a) * n + k);
+            const double ra = nttfp::mulmod(nttfp::i2d((long long)own[a].x), mc.cinv[TT][a], mc.cinvq[TT][a], qa);
+            const double rb = nttfp::mulmod(nttfp::i2d((long long)own[a].y), mc.cinv[TT][a], mc.cinvq[TT][a], qa);
+            ya[a] = ra < 0.0 ? ra + qa : ra;                          // canonical [0, q_a)
+            yb[a] = rb < 0.0 ? rb + qa : rb;
+        }
+    }
+#pragma unroll
+    for (uint32_t e = 0; e < 16; e++) {
+        if (e < E) {
+            const uint32_t li = e < level ? e : L + (e - level);
+            if (li >= lo && li < hi) {
+                if (perm) continue;
+                ulonglong2 out = make_ulonglong2(0, 0);
+#pragma unroll
+                for (uint32_t a = 0; a < 4; a++)
+                    if (a < cnt && lo + a == li) out = own[a];
+                *reinterpret_cast<ulonglong2*>(ext + (size_t)e * n + k) = out;
+            } else {
+                double sa = 0.0, sb = 0.0;
+#pragma unroll
+                for (uint32_t a = 0; a < 4; a++)
+                    if (a < cnt) {
+                        sa += nttfp::mulmod(ya[a], mc.c[TT][e][a], mc.cq[TT][e][a], mc.r[e]);
+                        sb += nttfp::mulmod(yb[a], mc.c[TT][e][a], mc.cq[TT][e][a], mc.r[e]);
+                    }
+                const uint64_t r = (uint64_t)mc.r[e];
+                *reinterpret_cast<ulonglong2*>(ext + (size_t)ext_row(perm, TT, e, A, E, level) * n + k) =
+                    make_ulonglong2(nttfp::canon(nttfp::red(sa, mc.r[e], mc.rinv[e]), r),
+                                    nttfp::canon(nttfp::red(sb, mc.r[e], mc.rinv[e]), r));
+            }
+        }
+    }
+}
+__global__ void __launch_bounds__(kT) k_modup_convert_fpc2(const uint64_t* __restrict__ coef, uint64_t* __restrict__ ext,
+                                                           uint32_t log_n, uint32_t level, uint32_t L, uint32_t A,
+                                                           const __grid_constant__ MUConstFp mc, uint32_t perm) {
+    const uint32_t n = 1u << log_n, E = level + A, beta = (level + A - 1) / A;
+    const uint32_t t = blockIdx.y;
+    const uint32_t k = 2 * (blockIdx.x * kT + threadIdx.x);
+    coef += (size_t)blockIdx.z * level * n;
+    ext += ((size_t)blockIdx.z * beta + t) * E * n;
+    switch (t) {
+        case 0: modup_fpc_body2<0>(coef, ext, n, level, L, A, mc, perm, k); break;
+        case 1: modup_fpc_body2<1>(coef, ext, n, level, L, A, mc, perm, k); break;
+        case 2: modup_fpc_body2<2>(coef, ext, n, level, L, A, mc, perm, k); break;
+        default: modup_fpc_body2<3>(coef, ext, n, level, L, A, mc, perm, k); break;
+    }
+}
+
 // FP64 key inner product, lean (<= 32 registers, 8 CTAs/SM: the kernel is memory-latency sensitive): per digit one
 // exact FP64 product per key polynomial (a, b < q < 2^50: h = ab, l = fma(a, b, -h), t = rint(h / q),
 // r = fma(-t, q, h) + l, |r| <= 0.75 q), beta partial products summed (|s| < 6 q), one centred reduction, canonical
@@ -635,6 +698,40 @@ __global__ void __launch_bounds__(kT) k_moddown_convert_fpc(const uint64_t* __re
             for (uint32_t a = 0; a < 8; a++)
                 if (a < A) s += nttfp::mulmod(y[a], mc.c[i][a], mc.cq[i][a], mc.q[i]);
             z[((size_t)gj * level + i) * n + k] = nttfp::canon(nttfp::red(s, mc.q[i], mc.qinv[i]), (uint64_t)mc.q[i]);
+        }
+    }
+}
+
+// two consecutive positions per thread (16-byte loads and stores)
+__global__ void __launch_bounds__(kT) k_moddown_convert_fpc2(const uint64_t* __restrict__ acc, uint64_t* __restrict__ z,
+                                                             uint32_t log_n, uint32_t level, uint32_t A,
+                                                             const __grid_constant__ MDConstFp mc) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t gj = blockIdx.y;
+    const uint32_t k = 2 * (blockIdx.x * kT + threadIdx.x);
+    const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
+    double ya[4], yb[4];
+#pragma unroll
+    for (uint32_t a = 0; a < 4; a++)
+        if (a < A) {
+            const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(pc + (size_t)a * n);
+            ya[a] = y_centred(nttfp::i2d((long long)w.x), mc.p[a], mc.hp[a], mc.yw[a], mc.ywq[a]);
+            yb[a] = y_centred(nttfp::i2d((long long)w.y), mc.p[a], mc.hp[a], mc.yw[a], mc.ywq[a]);
+        }
+#pragma unroll
+    for (uint32_t i = 0; i < 16; i++) {
+        if (i < level) {
+            double sa = 0.0, sb = 0.0;
+#pragma unroll
+            for (uint32_t a = 0; a < 4; a++)
+                if (a < A) {
+                    sa += nttfp::mulmod(ya[a], mc.c[i][a], mc.cq[i][a], mc.q[i]);
+                    sb += nttfp::mulmod(yb[a], mc.c[i][a], mc.cq[i][a], mc.q[i]);
+                }
+            const uint64_t q = (uint64_t)mc.q[i];
+            *reinterpret_cast<ulonglong2*>(z + ((size_t)gj * level + i) * n + k) =
+                make_ulonglong2(nttfp::canon(nttfp::red(sa, mc.q[i], mc.qinv[i]), q),
+                                nttfp::canon(nttfp::red(sb, mc.q[i], mc.qinv[i]), q));
         }
     }
 }
@@ -1012,7 +1109,11 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 mc.rinv[e] = 1.0 / mc.r[e];
             }
             dim3 g(n / kT, beta, n_ct);
-            k_modup_convert_fpc<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, mc, perm);
+            if (kip_pair() && n >= 2 * kT)
+                k_modup_convert_fpc2<<<dim3(g.x / 2, g.y, g.z), kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A,
+                                                                           mc, perm);
+            else
+                k_modup_convert_fpc<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, mc, perm);
         } else if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
             dim3 g(n / kT, beta, n_ct);
             k_modup_convert_fp<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab,
@@ -1181,7 +1282,10 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                         mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
                     }
                 }
-                k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
+                if (kip_pair() && A <= 4 && n >= 2 * kT)
+                    k_moddown_convert_fpc2<<<dim3(g.x / 2, g.y), kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
+                else
+                    k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
             } else
             k_moddown_convert_fp<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                    cvt->d_moddown_fp);

@@ -265,3 +265,57 @@ def test_integer_paths_large_moduli(torch_cuda):
     ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yc, form, s, d, m, 3)
     torch.cuda.synchronize()
     assert (host(yc) == o.ccmm(a, src, form, s, d, m, mask, ckeys, crlk)).all()
+
+
+@pytest.mark.parametrize("form", [2, 1])
+def test_ccmm_full_ring_decrypts(torch_cuda, form):
+    """The full C2 ring (N'=2^16, L=12, 16 heads of s = 2048 tokens, real encryptions): CCMM output columns decrypt
+    on the device (ensi_decrypt_debug) to the float64 products -- form 2 (A.B, d = 8) and form 1 (A.K^T with the
+    Table III inner dimension 96 and m = 2048 keys' worth of alignment, sampled at columns 65 and 66: giant and baby
+    steps)."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(16, 12, 4, 3)
+    skc, sk, pk = o.keygen(0x454E5349 + 2)
+    ctx = Context(16, 12, 4, 3)
+    ctx.load_keys(sk_ntt=sk)
+    s, level = 2048, 12
+    H = (o.n // 2) // s
+    rs = np.random.default_rng(4400 + form)
+    d, m, col0, cols = (8, 2, 0, 2) if form == 2 else (96, 2048, 65, 2)
+    A = rs.uniform(-1, 1, (H, s, d))
+
+    def enc(mat, sd):                      # mat [H][rows][ncols] -> one ciphertext per column
+        Hh, rows, nc = mat.shape
+        z = np.zeros((nc, o.n // 2))
+        for h in range(Hh):
+            z[:, h * s:h * s + rows] = mat[h].T
+        m_res = np.stack([o.encode(v, level, DELTA) for v in z])
+        return o.encrypt_batch(np.arange(nc, dtype=np.uint64) + np.uint64(sd), pk, level, m_res)
+    a = enc(A, 100)
+    if form == 2:
+        Bm = rs.uniform(-1, 1, (H, d, m))
+        src = enc(Bm, 200)
+        ref = np.einsum("hsd,hdm->hsm", A, Bm)
+    else:
+        K = rs.uniform(-1, 1, (H, m, d))
+        src = enc(K, 200)
+        ref = np.einsum("hsd,hmd->hsm", A, K)
+    pi, amounts, _, Ba = oracle.ccmm_plan(form, s, d, m)
+    if form == 1:                          # only the keys the sampled columns use
+        amounts = [r for r in amounts if r < 0] + [1, 2, Ba]
+    z = np.zeros(o.n // 2)
+    for h in range(H):
+        z[h * s:h * s + s:pi] = 1.0
+    coeffs = o.encode(z, level, float(o.q[level - 1]))
+    mask = np.stack([o.ntt(i, coeffs[i]) for i in range(level)])
+    gs = [o.galois(r) for r in amounts]
+    ctx.load_keys(galois=gs, rot_keys=np.stack([o.rotkey(4500 + i, g, sk) for i, g in enumerate(gs)]))
+    ctx.load_relin_key(o.relinkey(4600, sk))
+    yd = torch.empty((cols, 2, level - 2, o.n), dtype=torch.int64, device="cuda")
+    sc = ctx.ccmm(dev(torch, a), dev(torch, src), dev(torch, mask), yd, form, s, d, m, level, col0=col0, cols=cols)
+    torch.cuda.synchronize()
+    for c in range(cols):
+        got = ctx.decrypt_debug(yd, c, level - 2, log2_scale=sc).reshape(H, s)
+        err = np.max(np.abs(got - ref[:, :, col0 + c]))
+        assert err < 1e-4, (form, c, err)

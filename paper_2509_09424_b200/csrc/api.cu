@@ -333,6 +333,11 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
         }
         e = cudaMalloc(&ctx->d_tw3, tw3.size() * 8);
         if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw3, tw3.data(), tw3.size() * 8, cudaMemcpyHostToDevice);
+        // compact copy (w only) for the narrow-limb block passes: [T][fwd, inv][n] doubles, same positions
+        std::vector<double> tw1((size_t)ctx->T * 2 * n);
+        for (size_t i = 0; i < tw1.size(); i++) tw1[i] = tw3[2 * i];
+        if (e == cudaSuccess) e = cudaMalloc(&ctx->d_tw1, tw1.size() * 8);
+        if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw1, tw1.data(), tw1.size() * 8, cudaMemcpyHostToDevice);
     }
     if (e != cudaSuccess) {
         ensi_ctx_destroy(ctx);
@@ -349,6 +354,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     cudaFree(ctx->d_tw);
     cudaFree(ctx->d_tw2);
     cudaFree(ctx->d_tw3);
+    cudaFree(ctx->d_tw1);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
     if (ctx->relin_owned) cudaFree(ctx->d_relin);

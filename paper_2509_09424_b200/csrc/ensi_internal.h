@@ -84,6 +84,7 @@ struct ensi_ctx {
     // FP64 NTT (ntt_fp.cuh, all moduli < 2^50): [T][fwd, inv][n] of (w centred, RN(w/q)), then [T] of
     // (n^-1 centred, RN(n^-1/q)), as double2
     double* d_tw3 = nullptr;
+    double* d_tw1 = nullptr;              // compact [T][fwd, inv][n] w-only copy (narrow-limb block passes)
     bool ntt_fp_ok = false;
     uint64_t ninv[ENSI_MAXT] = {}, ninv_sh[ENSI_MAXT] = {};
     // keys

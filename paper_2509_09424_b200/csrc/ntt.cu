@@ -188,6 +188,15 @@ static int ntt_env() {
 }
 static bool use_v2(uint32_t log_n) { return log_n == 16 && ntt_env() >= 2; }
 static bool use_fp(const ensi_ctx* ctx) { return ctx->log_n == 16 && ctx->ntt_fp_ok && ntt_env() == 3; }
+// compact twiddles for the narrow-limb block passes (ENSI_NTT_TW1=0: the double2 table everywhere, A/B timing)
+static const double* tw1_of(const ensi_ctx* ctx) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_NTT_TW1");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v ? ctx->d_tw1 : nullptr;
+}
 
 // Tensor map of a row buffer for the TMA block passes: {16 words, N'/16 chunks, physical rows}, box {16, 256, 1},
 // SWIZZLE_128B.  ENSI_NTT_TMA=0 keeps the shared-memory transpose (A/B timing).
@@ -229,7 +238,8 @@ void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         CUtensorMap tm;
         nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         if (row_tmap(ctx, data, rows, map, &tm))
-            nttfp::k_ntt256_tma<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm);
+            nttfp::k_ntt256_tma<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
+                                                                 nttfp::PlainOut(), LimbMap(), 0u, tw1_of(ctx));
         else
             nttfp::k_ntt256<nttfp::FWD_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         ctx->launches += 2;
@@ -266,7 +276,7 @@ bool ntt_inverse_from(ensi_ctx* ctx, const uint64_t* src, const LimbMap& smap, u
     const uint32_t n = ctx->n;
     dim3 g(16, rows);
     nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
-                                                         nttfp::PlainOut(), smap, 1u);
+                                                         nttfp::PlainOut(), smap, 1u, tw1_of(ctx));
     nttfp::k_ntt256<nttfp::INV_A><<<g, 256, 0, st>>>(dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
     ctx->launches += 2;
     return true;
@@ -283,7 +293,8 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         dim3 g(16, rows);
         CUtensorMap tm;
         if (row_tmap(ctx, data, rows, map, &tm))
-            nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm);
+            nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
+                                                                 nttfp::PlainOut(), LimbMap(), 0u, tw1_of(ctx));
         else
             nttfp::k_ntt256<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);
         nttfp::k_ntt256<nttfp::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n);

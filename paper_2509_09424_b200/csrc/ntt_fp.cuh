@@ -105,10 +105,22 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
                                             const double2* __restrict__ W2, const double2* __restrict__ ninv,
                                             double* sm, const IN& in, const OUT& out,
                                             const CUtensorMap* tmap = nullptr, uint32_t prow = 0,
-                                            uint64_t* bar = nullptr) {
+                                            uint64_t* bar = nullptr, const double* __restrict__ W1 = nullptr) {
     const double qd = (double)q, qinv = 1.0 / qd;
     const bool fwd = PASS == FWD_A || PASS == FWD_B;
     const bool colp = PASS == FWD_A || PASS == INV_A;
+    // block-pass twiddles of the narrow limbs come from the compact table (w only, 8 bytes) with the quotient
+    // companion formed here: RN(w RN(1/q)) is within 2^-52 relative of w/q, and for |V| < 2^44 (narrow limbs)
+    // the quotient estimate moves by < 2^-9, so the |r| <= 0.625 q bound of mulmod holds -- this halves the
+    // per-block twiddle bytes the block passes pull from L2 (twice their data bytes with the double2 table)
+    const bool compact = !colp && !WIDE && W1 != nullptr;
+    auto twf = [&](uint32_t idx) -> double2 {
+        if (compact) {
+            const double w = __ldg(W1 + idx);
+            return make_double2(w, w * qinv);
+        }
+        return W2[idx];
+    };
     const uint32_t tid = threadIdx.x;
     const uint32_t sp = colp ? (tid & 15) : (tid >> 4);
     const uint32_t tt = colp ? (tid >> 4) : (tid & 15);
@@ -152,7 +164,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             for (int lt = 7; lt >= 4; lt--) {
                 const uint32_t sh = lt - 3, base = pre(lt);
 #pragma unroll
-                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (7 - lt)) - 1) + j] = W2[base + j];
+                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (7 - lt)) - 1) + j] = twf(base + j);
             }
 #pragma unroll
             for (int lt = 7; lt >= 4; lt--) {
@@ -178,7 +190,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
                 const uint32_t sh = lt + 1, base = colp ? pre(lt) + (tt << (3 - lt)) : pre(lt) + tt;
                 const uint32_t step = colp ? 1u : 16u;
 #pragma unroll
-                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (3 - lt)) - 1) + j] = W2[base + step * j];
+                for (uint32_t j = 0; j < (16u >> sh); j++) tw[((1u << (3 - lt)) - 1) + j] = twf(base + step * j);
             }
 #pragma unroll
             for (int lt = 3; lt >= 0; lt--) {
@@ -261,7 +273,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             double2 w;
 #pragma unroll
             for (uint32_t k = 0; k < 16; k++) {
-                if (!(k & ((1u << sh) - 1))) w = W2[base + step * (k >> sh)];
+                if (!(k & ((1u << sh) - 1))) w = twf(base + step * (k >> sh));
                 if (!(k & ks)) gs(v[k], v[k + ks], w, rd);
             }
         }
@@ -278,7 +290,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             double2 w;
 #pragma unroll
             for (uint32_t k = 0; k < 16; k++) {
-                if (!(k & ((1u << sh) - 1))) w = W2[base + (k >> sh)];
+                if (!(k & ((1u << sh) - 1))) w = twf(base + (k >> sh));
                 if (!(k & ks)) gs(v[k], v[k + ks], w, rd);
             }
         }
@@ -315,7 +327,8 @@ template <int PASS, class OUT = PlainOut>
 __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
                                                     const double2* __restrict__ tw, const double2* __restrict__ ninv,
                                                     const __grid_constant__ CUtensorMap tmap, OUT out = OUT(),
-                                                    LimbMap smap = LimbMap(), uint32_t oop = 0) {
+                                                    LimbMap smap = LimbMap(), uint32_t oop = 0,
+                                                    const double* __restrict__ tw1 = nullptr) {
     __shared__ __align__(1024) double sm[16 * kRow];
     __shared__ __align__(8) uint64_t bar;
     const uint32_t n = 65536;
@@ -334,8 +347,9 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* _
         __syncthreads();
     }
     const PlainIn in;
+    const double* W1 = tw1 ? tw1 + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n : nullptr;
     if (q >= (1ull << 41)) ntt256_body<PASS, true, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
-    else ntt256_body<PASS, false, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
+    else ntt256_body<PASS, false, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar, W1);
 }
 
 }  // namespace nttfp

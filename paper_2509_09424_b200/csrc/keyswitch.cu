@@ -16,7 +16,7 @@
 namespace ensi {
 
 static constexpr uint32_t kT = 256;
-static constexpr uint32_t kMaxBatch = 32;
+static constexpr uint32_t kMaxBatch = 64;
 
 // A batch of cnt Galois elements applied to n_ct input ciphertexts (key-stationary: each key word is read once
 // for all n_ct inputs).  Rotation (c, gi) reads input c at c0 + c * in_stride and writes output ciphertext
@@ -911,6 +911,24 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_KS_BATCH=<g> Galois elements per key-switch batch (<= 64), ENSI_KS_ROTCAP=<r> rotations per batch (A/B)
+static uint32_t ks_batch() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KS_BATCH");
+        v = e ? std::max(1, std::min(64, atoi(e))) : 32;
+    }
+    return (uint32_t)v;
+}
+static uint32_t ks_rot_cap() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KS_ROTCAP");
+        v = e ? std::max(1, atoi(e)) : 96;
+    }
+    return (uint32_t)v;
+}
+
 // ENSI_KIP_PAIR=0: one position per thread in the specialised key inner product (A/B timing)
 static bool kip_pair() {
     static int v = -1;
@@ -1050,7 +1068,8 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     if (beta > 8) return set_err(ctx, ENSI_EINVAL, "more than 8 key-switch digits");
     // rotations per key-switch batch: up to 32 Galois elements, and at most ~96 rotations (n_ct * cnt) so the
     // (acc, z) scratch stays bounded (~2.8 GB per set at C2)
-    const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(), std::max<uint32_t>(1, std::min<uint32_t>(kMaxBatch, 96 / n_ct)));
+    const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(),
+                                           std::max<uint32_t>(1, std::min<uint32_t>(ks_batch(), ks_rot_cap() / n_ct)));
     const uint32_t nbatches = (uint32_t)((idx.size() + nb - 1) / nb);
     // Batches alternate between two internal streams, each with its own (acc, z) buffers: the key inner product of
     // batch b+1 (HBM-bound) runs alongside the ModDown transforms of batch b (FP64/LSU-bound).

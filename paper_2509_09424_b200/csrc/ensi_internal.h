@@ -168,6 +168,7 @@ struct KsOpts {
     uint64_t c1_off = 0;                 // words from a ciphertext to the polynomial that is key-switched (0: level N')
     uint32_t add_mask = 0;               // bit j: output poly j += an unpermuted polynomial of the input ciphertext
     uint64_t add1_off = 0;               // words from a ciphertext to the polynomial added to output poly 1 (0: level N')
+    uint64_t* scratch = nullptr;         // internal: caller-provided scratch region (no ensure_scratch, no splitting)
 };
 int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
                          uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st,

@@ -911,6 +911,16 @@ static bool kip_fp() {
 }
 
 // ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
+// ENSI_KS_SPLIT=0: no two-stream split of single-element batches over many inputs (A/B timing)
+static bool ks_split() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ENSI_KS_SPLIT");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
+
 // ENSI_KS_BATCH=<g> Galois elements per key-switch batch (<= 64), ENSI_KS_ROTCAP=<r> rotations per batch (A/B)
 static uint32_t ks_batch() {
     static int v = -1;
@@ -1066,6 +1076,38 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     if (rc) return rc;
     const uint32_t beta = cvt->beta;
     if (beta > 8) return set_err(ctx, ENSI_EINVAL, "more than 8 key-switch digits");
+    // One Galois element over many inputs (independent-input rotations, CCMM's replicate steps): the inputs are
+    // split in two halves that run ModUp -> KIP -> ModDown on the two internal streams with disjoint scratch, so
+    // one half's HBM-bound key inner product overlaps the other half's FP64-bound transforms.
+    if (!ko.scratch && idx.size() == 1 && n_ct >= 8 && ks_streams() > 1 && ks_split()) {
+        const uint32_t h0 = n_ct / 2, h1 = n_ct - h0;
+        auto words = [&](uint32_t h) -> size_t {
+            return (size_t)h * level * n + (size_t)h * beta * E * n + (size_t)h * 2 * E * n + (size_t)h * 2 * level * n;
+        };
+        rc = ensure_scratch(ctx, (words(h0) + words(h1)) * 8);
+        if (rc) return rc;
+        if (!ctx->st_ks[0]) {
+            for (int i = 0; i < 2; i++) {
+                cudaStreamCreateWithFlags(&ctx->st_ks[i], cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&ctx->ev_ks_done[i], cudaEventDisableTiming);
+            }
+            cudaEventCreateWithFlags(&ctx->ev_ks_fork, cudaEventDisableTiming);
+        }
+        cudaEventRecord(ctx->ev_ks_fork, st);
+        for (int i = 0; i < 2; i++) cudaStreamWaitEvent(ctx->st_ks[i], ctx->ev_ks_fork, 0);
+        KsOpts k0 = ko, k1 = ko;
+        k0.scratch = (uint64_t*)ctx->scratch;
+        k1.scratch = (uint64_t*)ctx->scratch + words(h0);
+        rc = rotate_hoisted_multi(ctx, ct, h0, in_stride, level, n_g, galois, out, out_c_stride, ctx->st_ks[0], &k0);
+        if (!rc)
+            rc = rotate_hoisted_multi(ctx, ct + (size_t)h0 * in_stride, h1, in_stride, level, n_g, galois,
+                                      out + (size_t)h0 * out_c_stride * ctw, out_c_stride, ctx->st_ks[1], &k1);
+        for (int i = 0; i < 2; i++) {
+            cudaEventRecord(ctx->ev_ks_done[i], ctx->st_ks[i]);
+            cudaStreamWaitEvent(st, ctx->ev_ks_done[i], 0);
+        }
+        return rc;
+    }
     // rotations per key-switch batch: up to 32 Galois elements, and at most ~96 rotations (n_ct * cnt) so the
     // (acc, z) scratch stays bounded (~2.8 GB per set at C2)
     const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(),
@@ -1077,9 +1119,11 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     // scratch: coef [n_ct][level][n] | ext [n_ct][beta][E][n] | nsets x (acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n])
     const size_t w_coef = (size_t)n_ct * level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
                  w_z = (size_t)n_ct * nb * 2 * level * n;
-    rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + nsets * (w_acc + w_z)) * 8);
-    if (rc) return rc;
-    uint64_t* coef = (uint64_t*)ctx->scratch;
+    if (!ko.scratch) {
+        rc = ensure_scratch(ctx, (w_coef + n_ct * w_ext1 + nsets * (w_acc + w_z)) * 8);
+        if (rc) return rc;
+    }
+    uint64_t* coef = ko.scratch ? ko.scratch : (uint64_t*)ctx->scratch;
     uint64_t* ext = coef + w_coef;
     uint64_t* set0 = ext + n_ct * w_ext1;
     if (nsets == 2 && !ctx->st_ks[0]) {

@@ -319,3 +319,20 @@ def test_ccmm_full_ring_decrypts(torch_cuda, form):
         got = ctx.decrypt_debug(yd, c, level - 2, log2_scale=sc).reshape(H, s)
         err = np.max(np.abs(got - ref[:, :, col0 + c]))
         assert err < 1e-4, (form, c, err)
+
+
+def test_mul_relin_many_pairs_split(c1ctx, torch_cuda):
+    """Nine Mult + relinearisation pairs: the key switch of one element over >= 8 inputs runs split over the two
+    internal streams -- still the oracle's words."""
+    o, sk, pk, ctx = c1ctx
+    torch = torch_cuda
+    a = synth.gen_words(9900, o.q, 9, 3, o.n)
+    b = synth.gen_words(9901, o.q, 9, 3, o.n)
+    rlk = o.relinkey(9902, sk)
+    ctx.load_relin_key(rlk)
+    yd = torch.empty((9, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.mul_relin(dev(torch, a), dev(torch, b), yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd)
+    for c in (0, 4, 8):
+        assert (got[c] == o.relin(o.mul_ct(a[c], b[c]), rlk)).all()

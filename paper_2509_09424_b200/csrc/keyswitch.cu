@@ -875,169 +875,75 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
     return -1;
 }
 
-// ModDown fusion level at N' = 2^16 (ENSI_KS for A/B timing): 0 = separate convert / NTT / final kernels
-// (default, fastest measured), 1 = final combine fused into the last NTT pass (its TMA tile staging read back
-// lane-consecutively: 23.5k vs 24.3k rot/s hoisted, 12.4k vs 12.8k independent inputs, CCMM 104 vs 100 ms per
-// Q.K^T column -- the heavier pass loses more than the z round trip it saves), 2 = conversion also fused into the
-// first pass (15.6k vs 17.9k in an earlier round: the alpha P-limb loads and products per point and target limb
-// lengthen the pass).
-static int fused_moddown() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KS");
-        v = !e ? 0 : std::string(e) == "final" ? 1 : std::string(e) == "full" ? 2 : 0;
-    }
-    return v;
+// A/B switches of the key-switching core, read once from the environment.  Every default is the measured-best
+// path; the alternatives stay selectable for A/B timing (tools/README.md, DESIGN.md section 4 has the numbers):
+//   ENSI_KS=final|full     final combine (and conversion) fused into the z NTT passes (slower: 23.5k vs 24.3k rot/s)
+//   ENSI_MODDOWN=int       integer ModDown conversion (default FP64 when every modulus < 2^50)
+//   ENSI_MODDOWN_FPC=0     FP64 ModDown conversion with its constants in global memory
+//   ENSI_KIP=int           integer key inner product;  ENSI_KIP_GENERIC=1: the unspecialised FP64 one
+//   ENSI_KIP_PAIR=0        one position per thread in the specialised key-switching kernels
+//   ENSI_KIP_ORDER=rot     rotation-major key-inner-product grid (default limb-major)
+//   ENSI_MDFINAL=int       integer (Shoup) final combine
+//   ENSI_MODUP_PERM=0      INTT -> convert -> NTT round trip for the digits' own limbs
+//   ENSI_OWN_COPY=1        own limbs copied into the extended digits instead of read in place
+//   ENSI_OOP_INTT=0        copy of the inputs' c1 before an in-place INTT
+//   ENSI_KS_STREAMS=1      every batch on the caller's stream;  ENSI_KS_SPLIT=0: no two-stream input split
+//   ENSI_KS_BATCH=<g>, ENSI_KS_ROTCAP=<r>, ENSI_MD_SUB=<k>  batch sizes (32, 96, whole batch)
+struct KsEnv {
+    int fused = 0;
+    bool moddown_fp = true, moddown_fpc = true, kip_fp = true, kip_generic = false, kip_pair = true;
+    bool kip_limb_major = true, mdfinal_fp = true, modup_perm = true, own_direct = true, oop_intt = true;
+    bool split = true;
+    int streams = 2;
+    uint32_t batch = 32, rotcap = 96, md_sub = 0;
+};
+static const KsEnv& ks_env() {
+    static const KsEnv env = [] {
+        KsEnv v;
+        auto is = [](const char* k, const char* val) {
+            const char* e = getenv(k);
+            return e && std::string(e) == val;
+        };
+        auto num = [](const char* k, int dflt) {
+            const char* e = getenv(k);
+            return e ? atoi(e) : dflt;
+        };
+        v.fused = is("ENSI_KS", "final") ? 1 : is("ENSI_KS", "full") ? 2 : 0;
+        v.moddown_fp = !is("ENSI_MODDOWN", "int");
+        v.moddown_fpc = !is("ENSI_MODDOWN_FPC", "0");
+        v.kip_fp = !is("ENSI_KIP", "int");
+        v.kip_generic = is("ENSI_KIP_GENERIC", "1");
+        v.kip_pair = !is("ENSI_KIP_PAIR", "0");
+        v.kip_limb_major = !is("ENSI_KIP_ORDER", "rot");
+        v.mdfinal_fp = !is("ENSI_MDFINAL", "int");
+        v.modup_perm = !is("ENSI_MODUP_PERM", "0");
+        v.own_direct = !is("ENSI_OWN_COPY", "1");
+        v.oop_intt = !is("ENSI_OOP_INTT", "0");
+        v.split = !is("ENSI_KS_SPLIT", "0");
+        v.streams = is("ENSI_KS_STREAMS", "1") ? 1 : 2;
+        v.batch = (uint32_t)std::max(1, std::min(64, num("ENSI_KS_BATCH", 32)));
+        v.rotcap = (uint32_t)std::max(1, num("ENSI_KS_ROTCAP", 96));
+        v.md_sub = (uint32_t)std::max(0, num("ENSI_MD_SUB", 0));
+        return v;
+    }();
+    return env;
 }
-
-// ENSI_MODDOWN=int forces the integer conversion kernel (A/B timing); default FP64 when every modulus < 2^50
-static bool moddown_fp() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_MODDOWN");
-        v = (e && std::string(e) == "int") ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// ENSI_KIP=int selects the integer key inner product (A/B timing)
-static bool kip_fp() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KIP");
-        v = (e && e[0] == 'i') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// ENSI_MODDOWN_FPC=0 keeps the global-memory constant version of the FP64 ModDown conversion (A/B timing)
-// ENSI_KS_SPLIT=0: no two-stream split of single-element batches over many inputs (A/B timing)
-static bool ks_split() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KS_SPLIT");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v != 0;
-}
-
-// ENSI_KS_BATCH=<g> Galois elements per key-switch batch (<= 64), ENSI_KS_ROTCAP=<r> rotations per batch (A/B)
-static uint32_t ks_batch() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KS_BATCH");
-        v = e ? std::max(1, std::min(64, atoi(e))) : 32;
-    }
-    return (uint32_t)v;
-}
-static uint32_t ks_rot_cap() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KS_ROTCAP");
-        v = e ? std::max(1, atoi(e)) : 96;
-    }
-    return (uint32_t)v;
-}
-
-// ENSI_KIP_PAIR=0: one position per thread in the specialised key inner product (A/B timing)
-static bool kip_pair() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KIP_PAIR");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v != 0;
-}
-
-// ENSI_MDFINAL=int: the integer (Shoup) final combine (A/B timing); default FP64
-static bool mdfinal_fp() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_MDFINAL");
-        v = (e && std::string(e) == "int") ? 0 : 1;
-    }
-    return v != 0;
-}
-
-// ENSI_KIP_GENERIC=1: the generic (loop) FP64 key inner product instead of the digit-count specialisations
-static bool kip_generic() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KIP_GENERIC");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v != 0;
-}
-
-// ENSI_OOP_INTT=0: copy the inputs' c1 before an in-place INTT (A/B timing); default: out-of-place first pass
-static bool oop_intt_env() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_OOP_INTT");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v != 0;
-}
-
-// ENSI_OWN_COPY=1: copy the digits' own limbs into the extended digits (A/B timing); default: read in place
-static bool own_direct_env() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_OWN_COPY");
-        v = (e && e[0] == '1') ? 0 : 1;
-    }
-    return v != 0;
-}
-
-// ENSI_MD_SUB=<k>: ModDown sub-batch of k rotation-polynomials (0 = the whole batch in one pass per step)
-static uint32_t moddown_sub() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_MD_SUB");
-        v = e ? atoi(e) : 0;
-        if (v < 0) v = 0;
-    }
-    return (uint32_t)v;
-}
-
-// ENSI_KIP_ORDER=rot: the key inner product's grid walks rotation-major (A/B timing); default limb-major
-static bool kip_limb_major() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KIP_ORDER");
-        v = (e && std::string(e) == "rot") ? 0 : 1;
-    }
-    return v != 0;
-}
-
-static bool moddown_fpc() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_MODDOWN_FPC");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// ENSI_MODUP_PERM=0 keeps the INTT -> copy -> NTT round trip of the digits' own limbs (A/B timing)
-static bool modup_perm() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_MODUP_PERM");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-
-// ENSI_KS_STREAMS=1 runs every batch on the caller's stream (A/B timing); default 2 internal streams
-static int ks_streams() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_KS_STREAMS");
-        v = e ? atoi(e) : 2;
-    }
-    return v;
-}
+static int fused_moddown() { return ks_env().fused; }
+static bool moddown_fp() { return ks_env().moddown_fp; }
+static bool moddown_fpc() { return ks_env().moddown_fpc; }
+static bool kip_fp() { return ks_env().kip_fp; }
+static bool kip_generic() { return ks_env().kip_generic; }
+static bool kip_pair() { return ks_env().kip_pair; }
+static bool kip_limb_major() { return ks_env().kip_limb_major; }
+static bool mdfinal_fp() { return ks_env().mdfinal_fp; }
+static bool modup_perm() { return ks_env().modup_perm; }
+static bool own_direct_env() { return ks_env().own_direct; }
+static bool oop_intt_env() { return ks_env().oop_intt; }
+static bool ks_split() { return ks_env().split; }
+static int ks_streams() { return ks_env().streams; }
+static uint32_t ks_batch() { return ks_env().batch; }
+static uint32_t ks_rot_cap() { return ks_env().rotcap; }
+static uint32_t moddown_sub() { return ks_env().md_sub; }
 
 // Hoisted rotations of n_ct ciphertexts (input c at ct + c * in_stride words, [2][level][N']) by n_g Galois elements:
 // rotation (c, r) -> out + (c * out_c_stride + r) ciphertexts.  One ModUp per input; per batch of up to 32 Galois

@@ -17,7 +17,12 @@ Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` pri
   cpu_baseline= the CPU oracle (oracle/ensi_oracle.c, as it stands) on a bounded sample of output columns,
                 extrapolated by nnz (the oracle's cost is exactly linear in nnz).
   rotations   = hoisted key-switched rotations/s at the same parameters (alpha=4, dnum=3), BASELINE metric's
-                second clause.
+                second clause (also 32 per ModUp and independent inputs).
+  clocks      = SM clock / clock-event reasons polled through NVML by a separate process inside the timed region.
+  secondary   = the other SURVEY 8 rows at C2 parameters: NTT/INTT, rescale, Layout B, Layout-A shapes of C3-C5,
+                one C5 transformer block, the paper's Table III PCMM shapes at N'=2^14, and CCMM (R18) at the
+                Table III attention shapes (a sample of output columns, extrapolated by rotation count).
+  --no-rot / --no-layout-b / --no-ccmm / --no-e2e / --no-cpu skip parts (tests and quick runs).
 """
 from __future__ import annotations
 

@@ -604,29 +604,36 @@ def main():
            "gpu_launches": launches, "clocks": clk, "roofline": roofline}
 
     # ---- e2e through the host-buffer entry point (pinned host in, pinned host out)
+    xh_t = None
     if not args.no_e2e:
-        xh_t = torch.empty((d, 2, L, n), dtype=torch.int64, pin_memory=True)
-        yh_t = torch.empty((m, 2, L, n), dtype=torch.int64, pin_memory=True)
-        xh_t.copy_(x)
-        xh, yh = xh_t.numpy(), yh_t.numpy()
-        e2e_step = lambda: ctx.pcmm_ternary_host(xh, w, yh, level=L, kernel=args.kernel)  # noqa: E731
-        e2e_step()
-        torch.cuda.synchronize()
-        barrier(world)
-        e2e_ms = max_over_ranks(world, time_loop(e2e_step, max(1, min(args.steps, 3)), st))
-        ok = bool((yh_t[5, 1, 3, :4096] == y[5, 1, 3, :4096].cpu()).all())
-        e2e_u64 = {"value": e2e_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": world * d * ct_bytes,
-                   "d2h_bytes_per_step": world * m * ct_bytes, "matches_device_path": ok,
-                   "api": "ensi_pcmm_ternary_host (uint64 words)", "per_rank_ms": e2e_ms,
-                   "pcie_GBps_per_rank": (d + m) * ct_bytes / (e2e_ms * 1e-3) / 1e9}
-        del yh_t
+        e2e_u64 = None
+        if world == 1:
+            # the uint64-word host API beside the wire one (N = 1 only: at N > 1 every rank would pin another
+            # 19 GB of host memory)
+            xh_t = torch.empty((d, 2, L, n), dtype=torch.int64, pin_memory=True)
+            yh_t = torch.empty((m, 2, L, n), dtype=torch.int64, pin_memory=True)
+            xh_t.copy_(x)
+            xh, yh = xh_t.numpy(), yh_t.numpy()
+            e2e_step = lambda: ctx.pcmm_ternary_host(xh, w, yh, level=L, kernel=args.kernel)  # noqa: E731
+            e2e_step()
+            torch.cuda.synchronize()
+            e2e_ms = time_loop(e2e_step, max(1, min(args.steps, 3)), st)
+            ok = bool((yh_t[5, 1, 3, :4096] == y[5, 1, 3, :4096].cpu()).all())
+            e2e_u64 = {"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": d * ct_bytes,
+                       "d2h_bytes_per_step": m * ct_bytes, "matches_device_path": ok,
+                       "api": "ensi_pcmm_ternary_host (uint64 words)", "per_rank_ms": e2e_ms,
+                       "pcie_GBps_per_rank": (d + m) * ct_bytes / (e2e_ms * 1e-3) / 1e9}
+            del yh_t
         # the same layer through the compact wire format (each limb's words in ceil(bits/8) bytes; 62 of every 96
         # bytes at C2): the client's ciphertexts arrive serialised, cross PCIe packed, unpacked on the device
         from paper_2509_09424_b200.ensi import wire_pack_host
         wbytes = ctx.wire_bytes(L)
         xw_t = torch.empty((d, wbytes), dtype=torch.uint8, pin_memory=True)
         yw_t = torch.empty((m, wbytes), dtype=torch.uint8, pin_memory=True)
-        xw_t.numpy()[:] = wire_pack_host(x.cpu().numpy().view(np.uint64), ctx.wire_widths(L))
+        xw_dev = torch.empty((d, wbytes), dtype=torch.uint8, device="cuda")
+        ctx.wire_pack(x, xw_dev, L)                 # the client's serialisation, made here on the device (untimed)
+        xw_t.copy_(xw_dev)
+        del xw_dev
         xw, yw = xw_t.numpy(), yw_t.numpy()
         wire_step = lambda: ctx.pcmm_ternary_host_wire(xw, w, yw, level=L, kernel=args.kernel)  # noqa: E731
         wire_step()
@@ -680,7 +687,7 @@ def main():
         out["secondary"] = sec
     # ---- CPU oracle baseline (rank 0 at N=1 only)
     if not args.no_cpu and rank == 0 and world == 1:
-        x_host = (xh_t.numpy().view(np.uint64) if not args.no_e2e else x.cpu().numpy().view(np.uint64))
+        x_host = (xh_t.numpy().view(np.uint64) if xh_t is not None else x.cpu().numpy().view(np.uint64))
         nth = max(1, min(64, os.cpu_count() or 1))
         ncols = max(1, min(m, nth))
         ms_cpu, dt, cols = oracle_sample_ms(cfg, W, x_host, ncols, nth)

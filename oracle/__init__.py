@@ -67,7 +67,8 @@ def lib():
         L.or_galois_elt.restype = C.c_uint64
         L.or_galois_elt.argtypes = [C.c_uint32, C.c_int64]
         L.or_pcmm_b.restype = C.c_int
-        L.or_pcmm_b.argtypes = [C.c_void_p] + [C.c_uint32] * 8 + [u64p, i8p, C.c_uint32, u64p, u64p, u64p]
+        L.or_pcmm_b.argtypes = [C.c_void_p] + [C.c_uint32] * 8 + [u64p, i8p, C.c_uint32, u64p, u64p, C.c_void_p,
+                                                                 C.c_void_p, C.c_uint32, C.c_uint32]
         L.or_rescale.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
         L.or_relinkey.argtypes = [C.c_void_p, C.c_uint64, u64p, u64p, C.c_void_p]
         L.or_mul_plain.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
@@ -330,14 +331,19 @@ class Oracle:
         return out
 
     # -- PCMM Layout B (O11)
-    def pcmm_b(self, x: np.ndarray, W: np.ndarray, s: int, k: int, B: int, gkeys, keys: np.ndarray) -> np.ndarray:
+    def pcmm_b(self, x: np.ndarray, W: np.ndarray, s: int, k: int, B: int, gkeys, keys: np.ndarray, cols=None,
+               nthreads: int = 1) -> np.ndarray:
+        """O11.  cols: compute only these output columns (returns one ciphertext per listed column)."""
         W = np.ascontiguousarray(W, np.int8)
         d, m = W.shape
         n_in, _, level, _ = x.shape
-        y = np.zeros((m, 2, level, self.n), np.uint64)
+        ca = None if cols is None else np.ascontiguousarray(cols, np.uint32)
+        ncols = m if ca is None else ca.shape[0]
+        y = np.zeros((ncols, 2, level, self.n), np.uint64)
         ga = np.ascontiguousarray(gkeys, np.uint64)
         rc = lib().or_pcmm_b(self.h, level, s, k, B, d, m, m, n_in, np.ascontiguousarray(x, np.uint64), W,
-                             ga.shape[0], ga, np.ascontiguousarray(keys), y)
+                             ga.shape[0], ga, np.ascontiguousarray(keys), y.ctypes.data,
+                             ca.ctypes.data if ca is not None else None, ncols, nthreads)
         if rc != 0:
             raise KeyError("missing rotation key")
         return y

@@ -614,37 +614,46 @@ static const uint64_t* find_key(const or_ctx* cx, uint32_t n_keys, const uint64_
     for (uint32_t i = 0; i < n_keys; i++) if (gkeys[i] == g) return keys + i * keyw;
     return NULL;
 }
-int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t B, uint32_t d, uint32_t m, uint32_t ldw,
-              uint32_t n_in, const uint64_t* x, const int8_t* W, uint32_t n_keys, const uint64_t* gkeys, const uint64_t* keys,
-              uint64_t* y) {
-    uint32_t n = cx->n, G = k / B;
-    size_t ctw = (size_t)2 * level * n;
-    uint64_t* R = (uint64_t*)malloc((size_t)n_in * B * ctw * 8);     /* R[c][b] */
-    uint64_t* gb = (uint64_t*)malloc((size_t)B * 8);
-    size_t keyw = (size_t)cx->dnum * 2 * (cx->L + cx->alpha) * n;
-    uint64_t* kb = (uint64_t*)malloc((size_t)B * keyw * 8);
-    for (uint32_t b = 0; b < B; b++) {
-        gb[b] = or_galois_elt(cx->log_n, (int64_t)s * b);
-        if (b == 0) continue;
-        const uint64_t* kk = find_key(cx, n_keys, gkeys, keys, gb[b]);
-        if (!kk) { free(R); free(gb); free(kb); return 5; }
-        memcpy(kb + b * keyw, kk, keyw * 8);
+/* Baby-step rotations R[c][b] = Rot(ct_c; s*b) for b in [b0, b1) of one input c: one worker job (the hoisted
+ * rotations of one input are split into chunks so every host thread has work; bits are identical by O10). */
+typedef struct { const or_ctx* cx; uint32_t level, B, n_in, nchunk; const uint64_t* gb; const uint64_t* kb; const uint64_t* x;
+                 uint64_t* R; uint32_t tid, nth; } baby_job;
+static void* baby_worker(void* p) {
+    baby_job* j = (baby_job*)p;
+    size_t ctw = (size_t)2 * j->level * j->cx->n, keyw = (size_t)j->cx->dnum * 2 * (j->cx->L + j->cx->alpha) * j->cx->n;
+    uint32_t per = (j->B + j->nchunk - 1) / j->nchunk;
+    for (uint32_t t = j->tid; t < j->n_in * j->nchunk; t += j->nth) {
+        uint32_t c = t / j->nchunk, b0 = (t % j->nchunk) * per, b1 = b0 + per < j->B ? b0 + per : j->B;
+        if (b0 >= b1) continue;
+        or_rotate_hoisted(j->cx, j->level, b1 - b0, j->gb + b0, j->kb + (size_t)b0 * keyw, j->x + c * ctw,
+                          j->R + ((size_t)c * j->B + b0) * ctw);
     }
-    for (uint32_t c = 0; c < n_in; c++) or_rotate_hoisted(cx, level, B, gb, kb, x + c * ctw, R + (size_t)c * B * ctw);
+    return NULL;
+}
+/* Output columns cols[0..ncols) (all m when cols == NULL); y holds one ciphertext per computed column. */
+typedef struct { const or_ctx* cx; uint32_t level, s, k, B, d, ldw, n_in, n_keys; const int8_t* W; const uint64_t* gkeys;
+                 const uint64_t* keys; const uint64_t* R; uint64_t* y; const uint32_t* cols; uint32_t ncols, tid, nth;
+                 int rc; } bcol_job;
+static void* bcol_worker(void* p) {
+    bcol_job* j = (bcol_job*)p;
+    const or_ctx* cx = j->cx;
+    uint32_t n = cx->n, level = j->level, G = j->k / j->B;
+    size_t ctw = (size_t)2 * level * n;
     uint64_t* Tt = (uint64_t*)malloc(ctw * 8);
     uint64_t* rot = (uint64_t*)malloc(ctw * 8);
-    for (uint32_t i = 0; i < m; i++) {
-        uint64_t* yi = y + (size_t)i * ctw;
+    for (uint32_t ci = j->tid; ci < j->ncols; ci += j->nth) {
+        uint32_t i = j->cols ? j->cols[ci] : ci;
+        uint64_t* yi = j->y + (size_t)ci * ctw;
         memset(yi, 0, ctw * 8);
         for (uint32_t gam = 0; gam < G; gam++) {
             memset(Tt, 0, ctw * 8);
-            for (uint32_t c = 0; c < n_in; c++)
-                for (uint32_t b = 0; b < B; b++) {
-                    uint32_t col = c * k + gam * B + b;
-                    if (col >= d) continue;
-                    int8_t w = W[(size_t)col * ldw + i];
+            for (uint32_t c = 0; c < j->n_in; c++)
+                for (uint32_t b = 0; b < j->B; b++) {
+                    uint32_t col = c * j->k + gam * j->B + b;
+                    if (col >= j->d) continue;
+                    int8_t w = j->W[(size_t)col * j->ldw + i];
                     if (w == 0) continue;
-                    const uint64_t* rc = R + ((size_t)c * B + b) * ctw;
+                    const uint64_t* rc = j->R + ((size_t)c * j->B + b) * ctw;
                     for (uint32_t poly = 0; poly < 2; poly++)
                         for (uint32_t rr = 0; rr < level; rr++) {
                             uint64_t q = cx->mod[rr]; size_t off = ((size_t)poly * level + rr) * n;
@@ -654,9 +663,9 @@ int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t
                 }
             const uint64_t* src = Tt;
             if (gam > 0) {
-                uint64_t g = or_galois_elt(cx->log_n, (int64_t)s * B * gam);
-                const uint64_t* kk = find_key(cx, n_keys, gkeys, keys, g);
-                if (!kk) { free(R); free(gb); free(kb); free(Tt); free(rot); return 5; }
+                uint64_t g = or_galois_elt(cx->log_n, (int64_t)j->s * j->B * gam);
+                const uint64_t* kk = find_key(cx, j->n_keys, j->gkeys, j->keys, g);
+                if (!kk) { j->rc = 5; break; }
                 or_rotate(cx, level, g, kk, Tt, rot);
                 src = rot;
             }
@@ -666,9 +675,53 @@ int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t
                     for (uint32_t kk = 0; kk < n; kk++) yi[off + kk] = addmod(yi[off + kk], src[off + kk], q);
                 }
         }
+        if (j->rc) break;
     }
-    free(R); free(gb); free(kb); free(Tt); free(rot);
-    return 0;
+    free(Tt); free(rot);
+    return NULL;
+}
+/* Threads (nthreads >= 1) split the baby rotations and then the output columns; the arithmetic of every word is the
+ * sequence written above (threading changes no result). */
+int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t B, uint32_t d, uint32_t m, uint32_t ldw,
+              uint32_t n_in, const uint64_t* x, const int8_t* W, uint32_t n_keys, const uint64_t* gkeys, const uint64_t* keys,
+              uint64_t* y, const uint32_t* cols, uint32_t ncols, uint32_t nthreads) {
+    uint32_t n = cx->n;
+    size_t ctw = (size_t)2 * level * n;
+    if (!cols) ncols = m;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    uint64_t* R = (uint64_t*)malloc((size_t)n_in * B * ctw * 8);     /* R[c][b] */
+    uint64_t* gb = (uint64_t*)malloc((size_t)B * 8);
+    size_t keyw = (size_t)cx->dnum * 2 * (cx->L + cx->alpha) * n;
+    uint64_t* kb = (uint64_t*)calloc((size_t)B * keyw, 8);
+    for (uint32_t b = 0; b < B; b++) {
+        gb[b] = or_galois_elt(cx->log_n, (int64_t)s * b);
+        if (b == 0) continue;
+        const uint64_t* kk = find_key(cx, n_keys, gkeys, keys, gb[b]);
+        if (!kk) { free(R); free(gb); free(kb); return 5; }
+        memcpy(kb + b * keyw, kk, keyw * 8);
+    }
+    pthread_t th[256];
+    uint32_t nchunk = (nthreads + n_in - 1) / n_in;
+    if (nchunk > B) nchunk = B;
+    baby_job bj[256];
+    for (uint32_t t = 0; t < nthreads; t++) {
+        bj[t] = (baby_job){cx, level, B, n_in, nchunk, gb, kb, x, R, t, nthreads};
+        pthread_create(&th[t], NULL, baby_worker, &bj[t]);
+    }
+    for (uint32_t t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    bcol_job cj[256];
+    int rc = 0;
+    for (uint32_t t = 0; t < nthreads; t++) {
+        cj[t] = (bcol_job){cx, level, s, k, B, d, ldw, n_in, n_keys, W, gkeys, keys, R, y, cols, ncols, t, nthreads, 0};
+        pthread_create(&th[t], NULL, bcol_worker, &cj[t]);
+    }
+    for (uint32_t t = 0; t < nthreads; t++) {
+        pthread_join(th[t], NULL);
+        if (cj[t].rc) rc = cj[t].rc;
+    }
+    free(R); free(gb); free(kb);
+    return rc;
 }
 
 /* ------------------------------------------------------------------ rescale (O12) */

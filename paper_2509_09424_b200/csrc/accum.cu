@@ -8,9 +8,13 @@
 //   all 8 warps (each x word is fetched from L2/HBM once per 64 outputs).
 //   The weight sign is warp-uniform: one branch per (j, output) covers 8 words per lane, and zeros are
 //   skipped exactly as Alg. 1 lines 4-8 skip W = 0.
-// Accumulation is signed, lazy 64-bit: |acc| <= d 2^50 < 2^63 for d <= 8184 terms; longer sums are reduced
-// every 8184 rows.  The epilogue maps acc to the canonical word in [0, q) (Barrett), so the output is the
-// unique canonical value and equals the oracle bit for bit.
+// Accumulation is signed, lazy 64-bit: the host derives `ared`, the number of rows between intermediate
+// reductions, from the widest active modulus (accum_rows_between_reductions) so that |acc| never leaves the
+// int64 range nor the Barrett input range: 8191 rows for the O1 primes (< 2^50), 7 for a modulus near 2^60.
+// The epilogue maps acc to the canonical word in [0, q) (Barrett), so the output is the unique canonical value
+// and equals the oracle bit for bit.
+#include <algorithm>
+
 #include "ensi_internal.h"
 
 #ifndef ENSI_ACC_AP
@@ -25,7 +29,6 @@ static constexpr int AW = 8;          // warps per CTA
 static constexpr int ATI = AO * AW;   // 64 outputs per CTA
 static constexpr int ATW = 32 * AP;   // 256 positions per CTA
 static constexpr int AKC = 8;         // x rows per pipeline stage
-static constexpr int ARED = 8184;     // rows between intermediate reductions (multiple of AKC)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -43,7 +46,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 __global__ void __launch_bounds__(256, 8 / AP)
     k_accum_ternary(const uint64_t* __restrict__ x, uint32_t d, uint64_t ctw, const uint32_t* __restrict__ planes,
                     uint32_t mw, uint32_t m, uint64_t* __restrict__ y, uint32_t log_n, uint32_t level, uint32_t limb0,
-                    ModTab tab) {
+                    ModTab tab, uint32_t ared) {
     __shared__ __align__(16) uint64_t sx[2][AKC][ATW];
     __shared__ uint32_t ssg[2][AKC][4];   // pos lo, pos hi, neg lo, neg hi (64 outputs)
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -61,6 +64,7 @@ __global__ void __launch_bounds__(256, 8 / AP)
         for (int p = 0; p < AP; p++) acc[o][p] = 0;
 
     const uint32_t nstages = (d + AKC - 1) / AKC;
+    uint32_t since = 0;   // rows accumulated since the last reduction (every acc is then canonical, in [0, q))
     auto load_stage = [&](uint32_t s, int buf) {
         const uint32_t j0 = s * AKC;
         // x: AKC rows x ATW words in 16-byte chunks, AKC * ATW / 512 per thread
@@ -92,6 +96,14 @@ __global__ void __launch_bounds__(256, 8 / AP)
         __syncthreads();
 #pragma unroll 1
         for (int r = 0; r < AKC; r++) {
+            if (since == ared) {   // CTA-uniform: |acc| <= (ared + 1)(q - 1) stays inside int64 and Barrett's range
+#pragma unroll
+                for (int o = 0; o < AO; o++)
+#pragma unroll
+                    for (int p = 0; p < AP; p++) acc[o][p] = (int64_t)reduce_signed(acc[o][p], br);
+                since = 0;
+            }
+            since++;
             const uint32_t pb = (ssg[buf][r][wsel] >> wsh) & 0xFFu;
             const uint32_t nb = (ssg[buf][r][2 + wsel] >> wsh) & 0xFFu;
             if ((pb | nb) == 0) continue;
@@ -109,12 +121,6 @@ __global__ void __launch_bounds__(256, 8 / AP)
                 }
             }
         }
-        if ((((s + 1) * AKC) % ARED) == 0 && s + 1 < nstages) {
-#pragma unroll
-            for (int o = 0; o < AO; o++)
-#pragma unroll
-                for (int p = 0; p < AP; p++) acc[o][p] = (int64_t)reduce_signed(acc[o][p], br);
-        }
         __syncthreads();
     }
     // epilogue: canonical words, coalesced stores (32 consecutive positions per warp store)
@@ -129,12 +135,28 @@ __global__ void __launch_bounds__(256, 8 / AP)
     }
 }
 
+// Rows between intermediate reductions: after a reduction every accumulator is canonical, and n further signed
+// terms of magnitude <= q - 1 keep it in [-n (q-1), (n+1)(q-1)].  That must stay below 2^63 (int64) and below
+// 2^(2w+2) (the Barrett input bound of reduce64, w = bitlen(q)), for every active limb.
+uint32_t accum_rows_between_reductions(const ensi_ctx* ctx, uint32_t level) {
+    uint64_t best = UINT32_MAX;
+    for (uint32_t r = 0; r < level; r++) {
+        const uint64_t q = ctx->mod[r];
+        const uint32_t w = ctx->tab.w[r];
+        const uint64_t bound = (2 * w + 2 >= 64) ? (uint64_t)INT64_MAX : ((1ull << (2 * w + 2)) - 1);
+        const uint64_t n = bound / (q - 1) - 1;
+        best = std::min<uint64_t>(best, n);
+    }
+    return (uint32_t)std::max<uint64_t>(1, best);
+}
+
 int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
                   uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw, uint32_t limb0) {
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
     if (ctw % ATW) return set_err(ctx, ENSI_EINVAL, "ring too small for the accumulate tile");
     dim3 grid((m + ATI - 1) / ATI, (uint32_t)(ctw / ATW));
-    k_accum_ternary<<<grid, 256, 0, st>>>(x, d, ctw, planes, mw, m, y, ctx->log_n, level, limb0, ctx->tab);
+    k_accum_ternary<<<grid, 256, 0, st>>>(x, d, ctw, planes, mw, m, y, ctx->log_n, level, limb0, ctx->tab,
+                                          accum_rows_between_reductions(ctx, level));
     ENSI_LAUNCH_CHECK(ctx);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_ternary");

@@ -646,8 +646,10 @@ bool tc_supported(const ensi_ctx* ctx, uint32_t level) {
     if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return false;
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     if (major != 10 || minor != 0) return false;   // built for sm_100a only
+    // epilogue ranges: the 64-bit narrow combine needs 2^32 < q (mu32 = floor(2^64/q) < 2^32), the 128-bit combine
+    // needs V + off < 2^(2w+2) with off ~ 2^80 (w >= 40, i.e. every limb that is not narrow), and q < 2^60
     for (uint32_t i = 0; i < ctx->L; i++)
-        if (ctx->mod[i] >= (1ull << 60)) return false;
+        if (ctx->mod[i] >= (1ull << 60) || ctx->mod[i] <= (1ull << 32)) return false;
     return get_encode() != nullptr;
 }
 

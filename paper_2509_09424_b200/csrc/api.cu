@@ -103,6 +103,19 @@ int pack_planes(ensi_ctx* ctx, const int8_t* W, uint32_t d, uint32_t m, uint32_t
 // opts.kernel -> tensor-core variant: 0/2 best, 3 single CTA, 4 pairs without multicast
 int tc_variant(uint32_t kernel) { return kernel == 3 ? TC_ONE_CTA : kernel == 4 ? TC_PAIR : TC_AUTO; }
 
+// opts.kernel -> accumulate path (*tc: tensor cores).  0 picks the tensor-core path when the device and moduli
+// allow it (sm_100a, 2^32 < q < 2^60, d < 2^22 for the epilogue's 64-bit narrow combine), else the CUDA cores;
+// 2..4 request a tensor-core variant and fail with EINVAL where it is unavailable.
+int select_kernel(ensi_ctx* ctx, uint32_t kernel, uint32_t level, uint32_t d, bool* tc) {
+    if (kernel > 4) return set_err(ctx, ENSI_EINVAL, "opts.kernel must be 0..4");
+    const bool ok = tc_supported(ctx, level) && d < (1u << 22);
+    if (kernel >= 2 && !ok)
+        return set_err(ctx, ENSI_EINVAL,
+                       "tensor-core accumulate not available for these parameters (sm_100a, 2^32 < q < 2^60, d < 2^22)");
+    *tc = kernel >= 2 || (kernel == 0 && ok);
+    return ENSI_OK;
+}
+
 struct LayoutBPlan {
     uint32_t k, n_in, B, G, rotations;
 };
@@ -166,6 +179,60 @@ int weights_b(ensi_ctx* ctx, ensi_weights* w, uint32_t k, uint32_t B, uint32_t n
     slot = std::move(subs);
     *out = &slot;
     return ENSI_OK;
+}
+
+// Layout B (R11) after validation: hoisted baby steps of all inputs, the Algorithm-1 accumulate per giant step,
+// and the giant-step rotations of the m partial sums.  The giant steps are key-stationary: one
+// rotate_hoisted_multi call per chunk of outputs reads the giant key once for the whole chunk, and its final
+// combine adds the running sum in place (out = acc_out, add_src = acc_out), so no per-output rotation launch, no
+// rotated copy and no separate add pass.  Output words are those of O11 (modular additions are exact).
+int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const std::vector<ensi_weights*>& subs,
+                 const LayoutBPlan& p, const ensi_pcmm_opts& o, bool tc, uint64_t* acc_out, cudaStream_t st) {
+    const uint32_t m = w->m, level = x->level;
+    const size_t ctw = (size_t)2 * level * ctx->n;
+    const uint32_t rows = p.n_in * p.B;
+    // rotated inputs R [rows] and (G > 1) the giant-step partials T [m]: ctx-owned, grown on demand (cudaMallocAsync
+    // would return the 9+ GB to the OS at every synchronisation under the default pool release threshold)
+    const size_t need = ((size_t)rows + (p.G > 1 ? (size_t)m : 0)) * ctw;
+    if (ctx->lb_words < need) {
+        cudaStreamSynchronize(st);
+        cudaFree(ctx->lb_buf);
+        ctx->lb_buf = nullptr;
+        ctx->lb_words = 0;
+        cudaError_t ea = cudaMalloc(&ctx->lb_buf, need * 8);
+        if (ea != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(ctx, ENSI_ENOMEM, "layout B scratch allocation failed");
+        }
+        ctx->lb_words = need;
+    }
+    uint64_t* R = ctx->lb_buf;
+    uint64_t* Tg = p.G > 1 ? R + (size_t)rows * ctw : nullptr;
+    auto accum_b = [&](uint32_t gm, uint64_t* dst) -> int {
+        ensi_weights* sw = subs[gm];
+        return tc ? accum_ternary_tc(ctx, R, sw->d, sw, dst, level, st, 0, 0, tc_variant(o.kernel))
+                  : accum_ternary(ctx, R, sw->d, sw->d_planes, sw->mw, m, dst, level, st);
+    };
+    std::vector<uint64_t> gb(p.B);
+    for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
+    // baby steps for all inputs at once: key-stationary (each rotation key read once for the n_in inputs)
+    int rc = rotate_hoisted_multi(ctx, x->data, p.n_in, ctw, level, p.B, gb.data(), R, p.B, st);
+    if (!rc) rc = accum_b(0, acc_out);
+    for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
+        rc = accum_b(gm, Tg);
+        const uint64_t gg = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm);
+        // chunks of at most 96 outputs bound the key-switching scratch (as ensi_rotate_batch)
+        for (uint32_t c0 = 0; c0 < m && !rc; c0 += 96) {
+            const uint32_t nc = std::min<uint32_t>(96, m - c0);
+            KsOpts ko;
+            ko.add_mask = 3;
+            ko.add_src = acc_out + (size_t)c0 * ctw;
+            ko.add_stride = ctw;
+            rc = rotate_hoisted_multi(ctx, Tg + (size_t)c0 * ctw, nc, ctw, level, 1, &gg, acc_out + (size_t)c0 * ctw, 1,
+                                      st, &ko);
+        }
+    }
+    return rc;
 }
 
 // iterative radix-2 complex FFT (host, debug decode only): a[k] = sum_j a_j e^{sign 2 pi i jk / n}
@@ -495,82 +562,63 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
     if (opts) o = *opts;
     const uint32_t d = w->d, m = w->m, level = x->level, n = ctx->n;
     const uint32_t out_level = o.rescale_out ? level - 1 : level;
+    // ---- every check happens before any allocation or enqueue
     if (o.rescale_out && level < 2) return set_err(ctx, ENSI_ELEVEL, "rescale_out needs level >= 2");
     if (y->level != out_level) return set_err(ctx, ENSI_ELEVEL, "y.level must be x.level (-1 with rescale_out)");
     if (y->count != m) return set_err(ctx, ENSI_EDIM, "y.count != m");
     if (overlaps(x, y, n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
     if (o.layout > 1) return set_err(ctx, ENSI_EINVAL, "layout must be 0 (A) or 1 (B)");
-    cudaStream_t st = (cudaStream_t)stream;
-    DeviceGuard g(ctx->device);
-    const size_t ctw = (size_t)2 * level * n;
-    // output of the accumulate goes to y directly unless a rescale epilogue follows
-    uint64_t* acc_out = y->data;
-    uint64_t* owned = nullptr;
-    if (o.rescale_out) {
-        cudaError_t e = cudaMallocAsync((void**)&owned, (size_t)m * ctw * 8, st);
-        if (e != cudaSuccess) return cuda_err(ctx, e, "pcmm temp");
-        acc_out = owned;
-    }
+    bool tc = false;
+    rc = select_kernel(ctx, o.kernel, level, d, &tc);
+    if (rc) return rc;
+    LayoutBPlan p{};
+    const std::vector<ensi_weights*>* subs = nullptr;
     if (o.layout == 0) {
         if (x->count != d) return set_err(ctx, ENSI_EDIM, "Layout A: x.count must equal d");
-        bool tc = (o.kernel >= 2) || (o.kernel == 0 && tc_supported(ctx, level));
-        if (o.kernel > 4) return set_err(ctx, ENSI_EINVAL, "opts.kernel must be 0..4");
-        if (o.kernel >= 2 && !tc_supported(ctx, level))
-            return set_err(ctx, ENSI_EINVAL, "tensor-core accumulate not available for these parameters");
-        rc = tc ? accum_ternary_tc(ctx, x->data, d, w, acc_out, level, st, 0, 0, tc_variant(o.kernel))
-                : accum_ternary(ctx, x->data, d, w->d_planes, w->mw, m, acc_out, level, st);
     } else {
-        LayoutBPlan p;
         rc = plan_b(ctx, d, m, o.block_s, o.baby, &p);
         if (rc) return rc;
         if (x->count != p.n_in) return set_err(ctx, ENSI_EDIM, "Layout B: x.count must be ceil(d/k)");
+        if (ctx->A == 0 && p.rotations > 0)
+            return set_err(ctx, ENSI_ENOKEY, "context has no special primes (num_p == 0): no key switching");
         for (uint32_t b = 1; b < p.B; b++)
             if (!find_key(ctx, galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b)))
                 return set_err(ctx, ENSI_ENOKEY, "missing baby-step key for rotation " + std::to_string(o.block_s * b));
         for (uint32_t gm = 1; gm < p.G; gm++)
             if (!find_key(ctx, galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm)))
-                return set_err(ctx, ENSI_ENOKEY, "missing giant-step key");
-        const std::vector<ensi_weights*>* subs = nullptr;
+                return set_err(ctx, ENSI_ENOKEY, "missing giant-step key for rotation " +
+                                                     std::to_string(o.block_s * p.B * gm));
         rc = weights_b(ctx, w, p.k, p.B, p.n_in, &subs);
         if (rc) return rc;
-        const bool tcb = (o.kernel >= 2) || (o.kernel == 0 && tc_supported(ctx, level));
-        const uint32_t rows = p.n_in * p.B;
-        // rotated inputs R [rows] and giant-step partials: ctx-owned, grown on demand (cudaMallocAsync would return
-        // the 9+ GB to the OS at every synchronisation under the default pool release threshold)
-        const size_t need = ((size_t)rows + (p.G > 1 ? (size_t)m + 1 : 0)) * ctw;
-        if (ctx->lb_words < need) {
-            cudaStreamSynchronize(st);
-            cudaFree(ctx->lb_buf);
-            ctx->lb_buf = nullptr;
-            ctx->lb_words = 0;
-            cudaError_t ea = cudaMalloc(&ctx->lb_buf, need * 8);
-            if (ea != cudaSuccess) {
-                cudaGetLastError();
-                return set_err(ctx, ENSI_ENOMEM, "layout B scratch allocation failed");
-            }
-            ctx->lb_words = need;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceGuard g(ctx->device);
+    const size_t ctw = (size_t)2 * level * n;
+    // output of the accumulate goes to y directly unless a rescale epilogue follows (then into a stream-ordered
+    // temporary that every exit path below returns)
+    uint64_t* acc_out = y->data;
+    struct StreamBuf {
+        uint64_t* p = nullptr;
+        cudaStream_t st = nullptr;
+        ~StreamBuf() {
+            if (p) cudaFreeAsync(p, st);
         }
-        uint64_t* R = ctx->lb_buf;
-        uint64_t* Tg = p.G > 1 ? R + (size_t)rows * ctw : nullptr;
-        uint64_t* Tr = p.G > 1 ? Tg + (size_t)m * ctw : nullptr;
-        auto accum_b = [&](uint32_t gm, uint64_t* dst) -> int {
-            ensi_weights* sw = (*subs)[gm];
-            return tcb ? accum_ternary_tc(ctx, R, sw->d, sw, dst, level, st, 0, 0, tc_variant(o.kernel))
-                       : accum_ternary(ctx, R, sw->d, sw->d_planes, sw->mw, m, dst, level, st);
-        };
-        std::vector<uint64_t> gb(p.B);
-        for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
-        // baby steps for all inputs at once: key-stationary (each rotation key read once for the n_in inputs)
-        rc = rotate_hoisted_multi(ctx, x->data, p.n_in, ctw, level, p.B, gb.data(), R, p.B, st);
-        if (!rc) rc = accum_b(0, acc_out);
-        for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
-            rc = accum_b(gm, Tg);
-            uint64_t gg = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm);
-            for (uint32_t i = 0; i < m && !rc; i++) {
-                rc = rotate_hoisted(ctx, Tg + (size_t)i * ctw, level, 1, &gg, Tr, st);
-                if (!rc) add_into(ctx, acc_out + (size_t)i * ctw, Tr, 1, level, st);
-            }
+    } owned;
+    if (o.rescale_out) {
+        owned.st = st;
+        cudaError_t e = cudaMallocAsync((void**)&owned.p, (size_t)m * ctw * 8, st);
+        if (e != cudaSuccess) {
+            owned.p = nullptr;
+            cudaGetLastError();
+            return set_err(ctx, ENSI_ENOMEM, "pcmm rescale temporary");
         }
+        acc_out = owned.p;
+    }
+    if (o.layout == 0) {
+        rc = tc ? accum_ternary_tc(ctx, x->data, d, w, acc_out, level, st, 0, 0, tc_variant(o.kernel))
+                : accum_ternary(ctx, x->data, d, w->d_planes, w->mw, m, acc_out, level, st);
+    } else {
+        rc = layout_b_run(ctx, x, w, *subs, p, o, tc, acc_out, st);
     }
     if (!rc && o.rescale_out) {
         rc = ensi::rescale(ctx, acc_out, m, level, y->data, st);
@@ -578,7 +626,6 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
     } else if (!rc) {
         y->log2_scale = x->log2_scale;
     }
-    if (owned) cudaFreeAsync(owned, st);
     if (!rc) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = cuda_err(ctx, e, "pcmm");
@@ -629,6 +676,9 @@ static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, con
     if (level < 1 || level > ctx->L) return set_err(ctx, ENSI_ELEVEL, "level out of range");
     DeviceGuard g(ctx->device);
     const uint32_t d = w->d, m = w->m, n = ctx->n, slices = 2 * level;
+    bool tc = false;
+    int rc = select_kernel(ctx, kernel, level, d, &tc);
+    if (rc) return rc;
     const size_t ctb = wire ? 2 * wire_poly_bytes(ctx, level) : (size_t)2 * level * n * 8;
     const size_t stage_words = (size_t)(d + m) * n;          // one slice of every input and output
     // per buffer: the u64 slice stage, plus (wire) the same slice in wire bytes (<= 8 bytes per word)
@@ -658,14 +708,12 @@ static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, con
         cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming);
     }
     cudaStream_t st = (cudaStream_t)stream;
-    const bool tc = (kernel >= 2) || (kernel == 0 && tc_supported(ctx, level));
     const uint8_t* xh = (const uint8_t*)x_host;
     uint8_t* yh = (uint8_t*)y_host;
     // start: the copy streams wait for everything already queued on the caller's stream
     cudaEventRecord(ctx->ev_start, st);
     cudaStreamWaitEvent(ctx->st_h2d, ctx->ev_start, 0);
     cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_start, 0);
-    int rc = ENSI_OK;
     for (uint32_t s = 0; s < slices && !rc; s++) {
         const int b = s & 1;
         uint64_t* xs = ctx->host_stage + (size_t)b * buf_words;

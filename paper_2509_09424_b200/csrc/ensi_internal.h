@@ -150,6 +150,7 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
 // (limb0 + w / N') % level.  A staged chunk holding one limb r of every ct passes ctw = N', limb0 = r.
 int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* planes, uint32_t mw, uint32_t m,
                   uint64_t* y, uint32_t level, cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0);
+uint32_t accum_rows_between_reductions(const ensi_ctx* ctx, uint32_t level);
 // tensor-core variants: pairs with cluster multicast (default when 2*ceil(m/256) <= 8), pairs without
 // multicast, single CTA (cta_group::1)
 enum { TC_AUTO = 0, TC_PAIR_MC = 1, TC_PAIR = 2, TC_ONE_CTA = 3 };
@@ -168,6 +169,8 @@ struct KsOpts {
     uint64_t c1_off = 0;                 // words from a ciphertext to the polynomial that is key-switched (0: level N')
     uint32_t add_mask = 0;               // bit j: output poly j += an unpermuted polynomial of the input ciphertext
     uint64_t add1_off = 0;               // words from a ciphertext to the polynomial added to output poly 1 (0: level N')
+    const uint64_t* add_src = nullptr;   // non-NULL: the added polynomials come from add_src + c * add_stride (input c)
+    uint64_t add_stride = 0;             //   instead of the input ciphertext itself (may alias out exactly)
     uint64_t* scratch = nullptr;         // internal: caller-provided scratch region (no ensure_scratch, no splitting)
 };
 int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,

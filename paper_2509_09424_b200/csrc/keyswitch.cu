@@ -432,15 +432,12 @@ __global__ void __launch_bounds__(kT, 8) k_kip_fp(const uint64_t* __restrict__ e
     }
 }
 
-#ifndef ENSI_KIPT_MINB
-#define ENSI_KIPT_MINB 6
-#endif
 // Same key inner product specialised on the digit count (BETA <= 4): the digit row offsets are resolved once per
 // thread, both key words of every digit are loaded once and reused for every input of the batch, and the digit loops
 // are unrolled.  ncu had the generic kernel issue-bound (85 % issue active, 519 warp instructions per 32 words and
 // limb, 45 % of them uniform-datapath index arithmetic re-evaluated inside the input and digit loops).
 template <uint32_t BETA>
-__global__ void __launch_bounds__(kT, ENSI_KIPT_MINB) k_kip_fpt(const uint64_t* __restrict__ ext,
+__global__ void __launch_bounds__(kT, 6) k_kip_fpt(const uint64_t* __restrict__ ext,
                                                    const uint64_t* __restrict__ keys,
                                                    uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n,
                                                    uint32_t level, uint32_t L, uint32_t A, uint32_t dnum, ModTab tab,
@@ -741,7 +738,8 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
                                                       const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
                                                       GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
                                                       ModTab tab, const uint64_t* __restrict__ cm,
-                                                      uint32_t add_mask, uint64_t add1_off, uint32_t gj0) {
+                                                      uint32_t add_mask, uint64_t add1_off, uint32_t gj0,
+                                                      const uint64_t* __restrict__ add_src, uint64_t add_stride) {
     const uint32_t n = 1u << log_n, E = level + A;
     // gj: rotation-polynomial index in the batch; z holds the rows of this launch's sub-batch [gj0, gj0 + gridDim.z)
     const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1;
@@ -752,7 +750,10 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)blockIdx.z * level + i) * n + k], q);
     v = mul_shoup(v, pinv[0], pinv[1], q);
     if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
-    if ((add_mask >> j) & 1) v = add_mod(v, c0[c * gb.in_stride + (j ? add1_off : 0) + (size_t)i * n + k], q);
+    if ((add_mask >> j) & 1) {
+        const uint64_t* ab = add_src ? add_src + c * add_stride : c0 + c * gb.in_stride;
+        v = add_mod(v, ab[(j ? add1_off : 0) + (size_t)i * n + k], q);
+    }
     out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
 }
 
@@ -766,7 +767,8 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp(const uint64_t* __restr
                                                          const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
                                                          GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
                                                          const __grid_constant__ MDFinConst fc, uint32_t add_mask,
-                                                         uint64_t add1_off, uint32_t gj0) {
+                                                         uint64_t add1_off, uint32_t gj0,
+                                                         const uint64_t* __restrict__ add_src, uint64_t add_stride) {
     const uint32_t n = 1u << log_n, E = level + A;
     const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1, r = gj >> 1;
     const uint32_t c = gb.n_ct == 1 ? 0u : r / gb.cnt, gi = r - c * gb.cnt;
@@ -776,7 +778,10 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp(const uint64_t* __restr
     double v = nttfp::mulmod(nttfp::i2d(dv), fc.pinv[i], fc.pinvq[i], qd);          // |v| <= 0.625 q
     const uint64_t* cb = c0 + c * gb.in_stride + (size_t)i * n;
     if (j == 0) v += nttfp::i2d((long long)cb[galois_src_index(k, gb.g[gi], log_n)]);
-    if ((add_mask >> j) & 1) v += nttfp::i2d((long long)cb[(j ? add1_off : 0) + k]);
+    if ((add_mask >> j) & 1) {
+        const uint64_t* ab = (add_src ? add_src + c * add_stride : c0 + c * gb.in_stride) + (size_t)i * n;
+        v += nttfp::i2d((long long)ab[(j ? add1_off : 0) + k]);
+    }
     out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] =
         nttfp::canon(nttfp::red(v, qd, qinv), (uint64_t)qd);
 }
@@ -787,7 +792,8 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __rest
                                                           const uint64_t* __restrict__ c0, uint64_t* __restrict__ out,
                                                           GBatch gb, uint32_t log_n, uint32_t level, uint32_t A,
                                                           const __grid_constant__ MDFinConst fc, uint32_t add_mask,
-                                                          uint64_t add1_off, uint32_t gj0) {
+                                                          uint64_t add1_off, uint32_t gj0,
+                                                          const uint64_t* __restrict__ add_src, uint64_t add_stride) {
     const uint32_t n = 1u << log_n, E = level + A;
     const uint32_t i = blockIdx.y, gj = gj0 + blockIdx.z, j = gj & 1, r = gj >> 1;
     const uint32_t c = gb.n_ct == 1 ? 0u : r / gb.cnt, gi = r - c * gb.cnt;
@@ -804,7 +810,8 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __rest
         vb += nttfp::i2d((long long)cb[galois_src_index(k + 1, g, log_n)]);
     }
     if ((add_mask >> j) & 1) {
-        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(cb + (j ? add1_off : 0) + k);
+        const uint64_t* ab = (add_src ? add_src + c * add_stride : c0 + c * gb.in_stride) + (size_t)i * n;
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(ab + (j ? add1_off : 0) + k);
         va += nttfp::i2d((long long)w.x);
         vb += nttfp::i2d((long long)w.y);
     }
@@ -812,54 +819,6 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __rest
     *reinterpret_cast<ulonglong2*>(out + ((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k) =
         make_ulonglong2(nttfp::canon(nttfp::red(va, qd, qinv), q), nttfp::canon(nttfp::red(vb, qd, qinv), q));
 }
-
-// ---------------------------------------------------------------- fused ModDown (N' = 2^16, FP64 NTT passes; opt-in)
-// Row r of the z NTT = (gj = r / level, limb i = r % level).  The first NTT pass computes the centred fast
-// conversion of the INTT'ed P limbs on load (no z round trip through HBM); the last pass forms
-// (acc_{q_i} - NTT(z)) P^{-1} (+ sigma_g(c0)) on store and writes the rotated ciphertext directly.
-struct ModDownInFp {
-    const uint64_t* acc;
-    const double* mf;
-    ModTab tab;
-    uint32_t level, L, A, E;
-    __device__ __forceinline__ uint64_t load(const uint64_t*, uint32_t row, uint32_t i, uint32_t k) const {
-        const uint32_t n = 65536, gj = row / level;
-        const uint64_t* pc = acc + ((size_t)gj * E + level) * n + k;
-        const double qd = (double)tab.q[i];
-        const double* c = mf + (size_t)A * 2 + (size_t)i * A * 2;
-        double s = 0.0;
-        for (uint32_t a = 0; a < A; a++) {
-            const uint64_t p = tab.q[L + a];
-            const double y = y_centred(nttfp::i2d((long long)pc[(size_t)a * n]), (double)p, (double)(p >> 1),
-                                       __ldg(mf + 2 * a), __ldg(mf + 2 * a + 1));
-            s += nttfp::mulmod(y, __ldg(c + 2 * a), __ldg(c + 2 * a + 1), qd);
-        }
-        return nttfp::canon(nttfp::red(s, qd, 1.0 / qd), tab.q[i]);
-    }
-};
-struct ModDownOut {
-    static constexpr bool kFused = true;
-    const uint64_t* acc;
-    const uint64_t* c0;
-    uint64_t* out;
-    const uint64_t* cm;
-    ModTab tab;
-    GBatch gb;
-    uint32_t level, A, E;
-    uint32_t add_mask;
-    uint64_t add1_off;
-    __device__ __forceinline__ void store(uint64_t*, uint32_t row, uint32_t i, uint32_t k, uint64_t zt) const {
-        const uint32_t n = 65536, gj = row / level, j = gj & 1;
-        const uint32_t c = gb.c_of(gj >> 1), gi = gb.gi_of(gj >> 1);
-        const uint64_t q = tab.q[i];
-        const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
-        uint64_t v = sub_mod(__ldcs(acc + ((size_t)gj * E + i) * n + k), zt, q);
-        v = mul_shoup(v, __ldg(pinv), __ldg(pinv + 1), q);
-        if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], 16)], q);
-        if ((add_mask >> j) & 1) v = add_mod(v, c0[c * gb.in_stride + (j ? add1_off : 0) + (size_t)i * n + k], q);
-        out[((((size_t)c * gb.out_c_stride + gb.oidx[gi]) * 2 + j) * level + i) * n + k] = v;
-    }
-};
 
 // ---------------------------------------------------------------- host driver
 
@@ -875,75 +834,10 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
     return -1;
 }
 
-// A/B switches of the key-switching core, read once from the environment.  Every default is the measured-best
-// path; the alternatives stay selectable for A/B timing (tools/README.md, DESIGN.md section 4 has the numbers):
-//   ENSI_KS=final|full     final combine (and conversion) fused into the z NTT passes (slower: 23.5k vs 24.3k rot/s)
-//   ENSI_MODDOWN=int       integer ModDown conversion (default FP64 when every modulus < 2^50)
-//   ENSI_MODDOWN_FPC=0     FP64 ModDown conversion with its constants in global memory
-//   ENSI_KIP=int           integer key inner product;  ENSI_KIP_GENERIC=1: the unspecialised FP64 one
-//   ENSI_KIP_PAIR=0        one position per thread in the specialised key-switching kernels
-//   ENSI_KIP_ORDER=rot     rotation-major key-inner-product grid (default limb-major)
-//   ENSI_MDFINAL=int       integer (Shoup) final combine
-//   ENSI_MODUP_PERM=0      INTT -> convert -> NTT round trip for the digits' own limbs
-//   ENSI_OWN_COPY=1        own limbs copied into the extended digits instead of read in place
-//   ENSI_OOP_INTT=0        copy of the inputs' c1 before an in-place INTT
-//   ENSI_KS_STREAMS=1      every batch on the caller's stream;  ENSI_KS_SPLIT=0: no two-stream input split
-//   ENSI_KS_BATCH=<g>, ENSI_KS_ROTCAP=<r>, ENSI_MD_SUB=<k>  batch sizes (32, 96, whole batch)
-struct KsEnv {
-    int fused = 0;
-    bool moddown_fp = true, moddown_fpc = true, kip_fp = true, kip_generic = false, kip_pair = true;
-    bool kip_limb_major = true, mdfinal_fp = true, modup_perm = true, own_direct = true, oop_intt = true;
-    bool split = true;
-    int streams = 2;
-    uint32_t batch = 32, rotcap = 96, md_sub = 0;
-};
-static const KsEnv& ks_env() {
-    static const KsEnv env = [] {
-        KsEnv v;
-        auto is = [](const char* k, const char* val) {
-            const char* e = getenv(k);
-            return e && std::string(e) == val;
-        };
-        auto num = [](const char* k, int dflt) {
-            const char* e = getenv(k);
-            return e ? atoi(e) : dflt;
-        };
-        v.fused = is("ENSI_KS", "final") ? 1 : is("ENSI_KS", "full") ? 2 : 0;
-        v.moddown_fp = !is("ENSI_MODDOWN", "int");
-        v.moddown_fpc = !is("ENSI_MODDOWN_FPC", "0");
-        v.kip_fp = !is("ENSI_KIP", "int");
-        v.kip_generic = is("ENSI_KIP_GENERIC", "1");
-        v.kip_pair = !is("ENSI_KIP_PAIR", "0");
-        v.kip_limb_major = !is("ENSI_KIP_ORDER", "rot");
-        v.mdfinal_fp = !is("ENSI_MDFINAL", "int");
-        v.modup_perm = !is("ENSI_MODUP_PERM", "0");
-        v.own_direct = !is("ENSI_OWN_COPY", "1");
-        v.oop_intt = !is("ENSI_OOP_INTT", "0");
-        v.split = !is("ENSI_KS_SPLIT", "0");
-        v.streams = is("ENSI_KS_STREAMS", "1") ? 1 : 2;
-        v.batch = (uint32_t)std::max(1, std::min(64, num("ENSI_KS_BATCH", 32)));
-        v.rotcap = (uint32_t)std::max(1, num("ENSI_KS_ROTCAP", 96));
-        v.md_sub = (uint32_t)std::max(0, num("ENSI_MD_SUB", 0));
-        return v;
-    }();
-    return env;
-}
-static int fused_moddown() { return ks_env().fused; }
-static bool moddown_fp() { return ks_env().moddown_fp; }
-static bool moddown_fpc() { return ks_env().moddown_fpc; }
-static bool kip_fp() { return ks_env().kip_fp; }
-static bool kip_generic() { return ks_env().kip_generic; }
-static bool kip_pair() { return ks_env().kip_pair; }
-static bool kip_limb_major() { return ks_env().kip_limb_major; }
-static bool mdfinal_fp() { return ks_env().mdfinal_fp; }
-static bool modup_perm() { return ks_env().modup_perm; }
-static bool own_direct_env() { return ks_env().own_direct; }
-static bool oop_intt_env() { return ks_env().oop_intt; }
-static bool ks_split() { return ks_env().split; }
-static int ks_streams() { return ks_env().streams; }
-static uint32_t ks_batch() { return ks_env().batch; }
-static uint32_t ks_rot_cap() { return ks_env().rotcap; }
-static uint32_t moddown_sub() { return ks_env().md_sub; }
+// Batch sizes of the key-switching core (measured): up to 32 Galois elements and ~96
+// rotations per key inner product, and at least 8 inputs before a single-element call is split over the two
+// internal streams.
+static constexpr uint32_t kKsBatch = 32, kKsRotCap = 96, kKsSplitMin = 8;
 
 // Hoisted rotations of n_ct ciphertexts (input c at ct + c * in_stride words, [2][level][N']) by n_g Galois elements:
 // rotation (c, r) -> out + (c * out_c_stride + r) ciphertexts.  One ModUp per input; per batch of up to 32 Galois
@@ -985,7 +879,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     // One Galois element over many inputs (independent-input rotations, CCMM's replicate steps): the inputs are
     // split in two halves that run ModUp -> KIP -> ModDown on the two internal streams with disjoint scratch, so
     // one half's HBM-bound key inner product overlaps the other half's FP64-bound transforms.
-    if (!ko.scratch && idx.size() == 1 && n_ct >= 8 && ks_streams() > 1 && ks_split()) {
+    if (!ko.scratch && idx.size() == 1 && n_ct >= kKsSplitMin) {
         const uint32_t h0 = n_ct / 2, h1 = n_ct - h0;
         auto words = [&](uint32_t h) -> size_t {
             return (size_t)h * level * n + (size_t)h * beta * E * n + (size_t)h * 2 * E * n + (size_t)h * 2 * level * n;
@@ -1004,6 +898,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         KsOpts k0 = ko, k1 = ko;
         k0.scratch = (uint64_t*)ctx->scratch;
         k1.scratch = (uint64_t*)ctx->scratch + words(h0);
+        if (ko.add_src) k1.add_src = ko.add_src + (size_t)h0 * ko.add_stride;
         rc = rotate_hoisted_multi(ctx, ct, h0, in_stride, level, n_g, galois, out, out_c_stride, ctx->st_ks[0], &k0);
         if (!rc)
             rc = rotate_hoisted_multi(ctx, ct + (size_t)h0 * in_stride, h1, in_stride, level, n_g, galois,
@@ -1017,11 +912,11 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     // rotations per key-switch batch: up to 32 Galois elements, and at most ~96 rotations (n_ct * cnt) so the
     // (acc, z) scratch stays bounded (~2.8 GB per set at C2)
     const uint32_t nb = std::min<uint32_t>((uint32_t)idx.size(),
-                                           std::max<uint32_t>(1, std::min<uint32_t>(ks_batch(), ks_rot_cap() / n_ct)));
+                                           std::max<uint32_t>(1, std::min<uint32_t>(kKsBatch, kKsRotCap / n_ct)));
     const uint32_t nbatches = (uint32_t)((idx.size() + nb - 1) / nb);
     // Batches alternate between two internal streams, each with its own (acc, z) buffers: the key inner product of
     // batch b+1 (HBM-bound) runs alongside the ModDown transforms of batch b (FP64/LSU-bound).
-    const uint32_t nsets = (nbatches > 1 && ks_streams() > 1) ? 2 : 1;
+    const uint32_t nsets = nbatches > 1 ? 2 : 1;
     // scratch: coef [n_ct][level][n] | ext [n_ct][beta][E][n] | nsets x (acc [n_ct][nb][2][E][n] | z [n_ct][nb][2][level][n])
     const size_t w_coef = (size_t)n_ct * level * n, w_ext1 = (size_t)beta * E * n, w_acc = (size_t)n_ct * nb * 2 * E * n,
                  w_z = (size_t)n_ct * nb * 2 * level * n;
@@ -1041,8 +936,8 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     }
 
     // ---- ModUp (once per input; all inputs in one launch per step so small batches still fill the GPU)
-    const uint32_t perm = (ctx->ntt_fp_ok && A <= 8 && moddown_fp() && modup_perm()) ? 1u : 0u;
-    const bool own_direct = perm && ctx->ntt_fp_ok && beta <= 8 && kip_fp() && own_direct_env();
+    const uint32_t perm = (ctx->ntt_fp_ok && A <= 8) ? 1u : 0u;
+    const bool own_direct = perm && beta <= 8;
     {
         const size_t row_b = (size_t)level * n * 8;
         // INTT of every input's c1 into coef: out of place (the first pass reads the input rows through a TMA
@@ -1051,7 +946,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         sm.grp_rows = level;
         sm.grp_stride = (uint32_t)((n_ct > 1 ? in_stride : 2ull * level * n) / n);
         sm.grp_off = (uint32_t)(c1o / n);
-        const bool strided_ok = in_stride % n == 0 && c1o % n == 0 && oop_intt_env();
+        const bool strided_ok = in_stride % n == 0 && c1o % n == 0;
         if (!(strided_ok && ntt_inverse_from(ctx, ct, sm, coef, n_ct * level, identity_map(level), st))) {
             if (n_ct == 1)
                 cudaMemcpyAsync(coef, ct + c1o, row_b, cudaMemcpyDeviceToDevice, st);
@@ -1059,7 +954,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 cudaMemcpy2DAsync(coef, row_b, ct + c1o, in_stride * 8, row_b, n_ct, cudaMemcpyDeviceToDevice, st);
             ntt_inverse(ctx, coef, n_ct * level, identity_map(level), st);
         }
-        if (ctx->ntt_fp_ok && A <= 4 && beta <= 4 && E <= 16 && moddown_fp() && moddown_fpc()) {
+        if (ctx->ntt_fp_ok && A <= 4 && beta <= 4 && E <= 16) {
             MUConstFp mc{};
             const std::vector<double>& uf = cvt->h_modup_fp;
             const size_t off1 = (size_t)beta * A * 2;
@@ -1078,12 +973,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                 mc.rinv[e] = 1.0 / mc.r[e];
             }
             dim3 g(n / kT, beta, n_ct);
-            if (kip_pair() && n >= 2 * kT)
+            if (n >= 2 * kT)
                 k_modup_convert_fpc2<<<dim3(g.x / 2, g.y, g.z), kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A,
                                                                            mc, perm);
             else
                 k_modup_convert_fpc<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, mc, perm);
-        } else if (ctx->ntt_fp_ok && A <= 8 && moddown_fp()) {
+        } else if (ctx->ntt_fp_ok && A <= 8) {
             dim3 g(n / kT, beta, n_ct);
             k_modup_convert_fp<<<g, kT, 0, st>>>(coef, ext, ctx->log_n, level, ctx->L, A, ctx->tab,
                                                  cvt->d_modup_fp, perm);
@@ -1160,15 +1055,15 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         const uint32_t nr = n_ct * cnt;   // rotations in this batch
         {
             dim3 g(n / kT, E, cnt);
-            if (ctx->ntt_fp_ok && beta <= 8 && kip_fp()) {
-                const uint32_t lm = kip_limb_major() ? 1u : 0u;
+            if (ctx->ntt_fp_ok && beta <= 8) {
+                const uint32_t lm = 1u;   // limb-major grid: a limb's gathered digit rows stay in L2 across the batch
                 dim3 gk = lm ? dim3(n / kT, cnt, E) : g;
                 const uint32_t pm = own_direct ? 2u : perm;
                 const uint64_t* c1p = ct + c1o;
-                switch (kip_generic() ? 0u : beta) {
+                switch (beta) {
 #define ENSI_KIPT(B)                                                                                                   \
     case B:                                                                                                            \
-        if (kip_pair() && n >= 2 * kT) {                                                                               \
+        if (n >= 2 * kT) {                                                                                             \
             dim3 g2(gk.x / 2, gk.y, gk.z);                                                                             \
             k_kip_fpt2<B><<<g2, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,         \
                                              ctx->tab, w_ext1, pm, lm, c1p, in_stride);                                \
@@ -1197,43 +1092,14 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         pm.grp_rows = A;
         pm.grp_stride = E;
         pm.grp_off = level;
-        if (ctx->log_n == 16 && ctx->ntt_fp_ok && fused_moddown() != 0) {
-            ntt_inverse(ctx, acc, nr * 2 * A, pm, st);
-            const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
-            const double2* ninv = tw + (size_t)ctx->T * 2 * n;
-            LimbMap zm = identity_map(level);
-            ModDownOut outf{acc, ct, out, cvt->d_moddown, ctx->tab, gb, level, A, E, ko.add_mask, add1o};
-            dim3 g(16, nr * 2 * level);
-            if (fused_moddown() == 2) {
-                ModDownInFp in{acc, cvt->d_moddown_fp, ctx->tab, level, ctx->L, A, E};
-                nttfp::k_ntt256<nttfp::FWD_A, ModDownInFp><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv, in);
-            } else {
-                dim3 gc(n / kT, nr * 2);
-                k_moddown_convert_fp<<<gc, kT, 0, st>>>(acc, z, ctx->log_n, level, ctx->L, A, ctx->tab,
-                                                        cvt->d_moddown_fp);
-                nttfp::k_ntt256<nttfp::FWD_A><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv);
-                ctx->launches += 1;
-            }
-            CUtensorMap tm;
-            if (ntt_row_tmap(ctx, z, nr * 2 * level, zm, &tm))
-                nttfp::k_ntt256_tma<nttfp::FWD_B, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv, tm, outf);
-            else
-                nttfp::k_ntt256<nttfp::FWD_B, nttfp::PlainIn, ModDownOut><<<g, 256, 0, st>>>(z, zm, ctx->tab, tw, ninv,
-                                                                                           nttfp::PlainIn(), outf);
-            ctx->launches += 2;
-            continue;
-        }
-        // ModDown in sub-batches of `sub` rotation-polynomials: INTT of the P rows, conversion, NTT and final
-        // combine of one sub-batch run back to back on one z sub-buffer, so z and the P rows stay in L2 between
-        // the four steps instead of making four DRAM round trips per batch
-        const uint32_t GJ = nr * 2, sub = moddown_sub() ? std::min(GJ, moddown_sub()) : GJ;
-        for (uint32_t g0 = 0; g0 < GJ; g0 += sub) {
-        const uint32_t gcnt = std::min(sub, GJ - g0);
-        uint64_t* accs = acc + (size_t)g0 * E * n;
+        // ModDown of the batch's 2 nr polynomials: INTT of the P rows, conversion, NTT, final combine
+        const uint32_t g0 = 0, gcnt = nr * 2;
+        uint64_t* accs = acc;
+        {
         ntt_inverse(ctx, accs, gcnt * A, pm, st);
-        if (A <= 8 && ctx->ntt_fp_ok && moddown_fp()) {
+        if (A <= 8 && ctx->ntt_fp_ok) {
             dim3 g(n / kT, gcnt);
-            if (level <= 16 && moddown_fpc()) {
+            if (level <= 16) {
                 MDConstFp mc{};
                 const std::vector<double>& mf = cvt->h_moddown_fp;
                 for (uint32_t a = 0; a < A; a++) {
@@ -1251,7 +1117,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                         mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
                     }
                 }
-                if (kip_pair() && A <= 4 && n >= 2 * kT)
+                if (A <= 4 && n >= 2 * kT)
                     k_moddown_convert_fpc2<<<dim3(g.x / 2, g.y), kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
                 else
                     k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
@@ -1272,7 +1138,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         ntt_forward(ctx, z, gcnt * level, identity_map(level), st);
         {
             dim3 g(n / kT, level, gcnt);
-            if (ctx->ntt_fp_ok && level <= 16 && mdfinal_fp()) {
+            if (ctx->ntt_fp_ok && level <= 16) {
                 MDFinConst fc{};
                 for (uint32_t i = 0; i < level; i++) {
                     const uint64_t q = ctx->mod[i], w = cvt->h_pinv[i];
@@ -1281,16 +1147,16 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                     fc.pinv[i] = w > q / 2 ? -(double)(q - w) : (double)w;
                     fc.pinvq[i] = fc.pinv[i] / fc.q[i];
                 }
-                if (kip_pair() && n >= 2 * kT) {
+                if (n >= 2 * kT) {
                     dim3 g2(g.x / 2, g.y, g.z);
                     k_moddown_final_fp2<<<g2, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
-                                                           add1o, g0);
+                                                           add1o, g0, ko.add_src, ko.add_stride);
                 } else
                     k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
-                                                         add1o, g0);
+                                                         add1o, g0, ko.add_src, ko.add_stride);
             } else
             k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
-                                              ko.add_mask, add1o, g0);
+                                              ko.add_mask, add1o, g0, ko.add_src, ko.add_stride);
             ENSI_LAUNCH_CHECK(ctx);
         }
         }

@@ -177,45 +177,29 @@ __global__ void __launch_bounds__(kThreads) k_intt_strided(uint64_t* __restrict_
 static uint32_t split_log_n2(uint32_t log_n) { return log_n <= 12 ? log_n : log_n - log_n / 2; }
 
 // Kernel choice at N' = 2^16: the FP64 passes (ntt_fp.cuh) when every modulus is below 2^50, else the integer v2
-// passes.  ENSI_NTT=v1 / v2 force the generic / integer kernels (A/B timing).
-static int ntt_env() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = getenv("ENSI_NTT");
-        env = (e && e[0] == 'v' && e[1] == '1') ? 1 : (e && e[0] == 'v' && e[1] == '2') ? 2 : 3;
-    }
-    return env;
-}
-static bool use_v2(uint32_t log_n) { return log_n == 16 && ntt_env() >= 2; }
-static bool use_fp(const ensi_ctx* ctx) { return ctx->log_n == 16 && ctx->ntt_fp_ok && ntt_env() == 3; }
-// compact twiddles for the narrow-limb block passes (ENSI_NTT_TW1=0: the double2 table everywhere, A/B timing)
-static const double* tw1_of(const ensi_ctx* ctx) {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_NTT_TW1");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v ? ctx->d_tw1 : nullptr;
-}
+// passes; other sizes use the generic shared-memory kernels above.  The narrow-limb FP64 block passes read the
+// compact w-only twiddle table (ctx->d_tw1).
+static bool use_fp(const ensi_ctx* ctx) { return ctx->log_n == 16 && ctx->ntt_fp_ok; }
+static bool use_v2(const ensi_ctx* ctx) { return ctx->log_n == 16 && !ctx->ntt_fp_ok; }
+static const double* tw1_of(const ensi_ctx* ctx) { return ctx->d_tw1; }
 
 // Tensor map of a row buffer for the TMA block passes: {16 words, N'/16 chunks, physical rows}, box {16, 256, 1},
-// SWIZZLE_128B.  ENSI_NTT_TMA=0 keeps the shared-memory transpose (A/B timing).
+// SWIZZLE_128B (false if the driver entry point is unavailable; the callers then use the shared-memory transpose).
 typedef CUresult (*PFN_tmapEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static bool row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, CUtensorMap* tm) {
-    static int env = -1;
+    static int init = 0;
     static PFN_tmapEncode enc = nullptr;
-    if (env < 0) {
-        const char* e = getenv("ENSI_NTT_TMA");
-        env = (e && e[0] == '0') ? 0 : 1;
+    if (!init) {
+        init = 1;
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             enc = (PFN_tmapEncode)p;
     }
-    if (!env || !enc || rows == 0) return false;
+    if (!enc || rows == 0) return false;
     const uint64_t n = ctx->n;
     cuuint64_t dims[3] = {16, n / 16, map.phys(rows - 1) + 1};
     cuuint64_t strides[2] = {128, n * 8};
@@ -245,7 +229,7 @@ void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         ctx->launches += 2;
         return;
     }
-    if (use_v2(log_n)) {
+    if (use_v2(ctx)) {
         const uint64_t* ninv = ctx->d_tw + (size_t)ctx->T * 4 * n;
         dim3 g(16, rows);
         v2::k_ntt256<v2::FWD_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
@@ -301,7 +285,7 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         ctx->launches += 2;
         return;
     }
-    if (use_v2(log_n)) {
+    if (use_v2(ctx)) {
         dim3 g(16, rows);
         v2::k_ntt256<v2::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);
         v2::k_ntt256<v2::INV_A><<<g, 256, 0, st>>>(data, map, ctx->tab, ctx->d_tw2, ninv);

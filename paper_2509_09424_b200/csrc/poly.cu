@@ -79,16 +79,6 @@ struct RescaleOutFp {
     }
 };
 
-// ENSI_RESCALE=unfused forces the separate convert / NTT / final kernels (A/B timing)
-static bool rescale_fused() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("ENSI_RESCALE");
-        v = (e && e[0] == 'u') ? 0 : 1;
-    }
-    return v == 1;
-}
-
 static int rescale_chunk(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out,
                          cudaStream_t st) {
     const uint32_t n = ctx->n, lm1 = level - 1;
@@ -111,7 +101,9 @@ static int rescale_chunk(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint
     LimbMap lm = identity_map(1);
     lm.limb[0] = (uint8_t)lm1;
     ntt_inverse(ctx, tl, count * 2, lm, st);
-    if (ctx->log_n == 16 && ctx->ntt_fp_ok && rescale_fused()) {
+    if (ctx->log_n == 16 && ctx->ntt_fp_ok) {
+        // conversion fused into the first NTT pass, the final combine into the last (other rings / moduli >= 2^50:
+        // the separate convert / NTT / final kernels below)
         RescaleInFp fin{};
         RescaleOutFp fout{};
         fin.tl = tl;

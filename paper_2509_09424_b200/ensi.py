@@ -280,13 +280,25 @@ class Context:
         self._check(lib().ensi_pcmm_ternary_host_wire(self.h, _np_ptr(x_wire), level, log2_scale, w.h,
                                                       _np_ptr(y_wire), kernel, _stream_ptr(stream)))
 
+    def _wire_buf(self, t, count: int, level: int, what: str):
+        need = count * self.wire_bytes(level)
+        if not (t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 1):
+            raise ValueError(f"{what} must be a contiguous 8-bit CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{what} on cuda:{t.device.index}, context on cuda:{self.device}")
+        if t.numel() != need:
+            raise ValueError(f"{what} must hold {count} x {self.wire_bytes(level)} bytes, got {t.numel()}")
+        return C.c_void_p(t.data_ptr())
+
     def wire_pack(self, x, out, level: int, stream=None):
         xv = self.view(x, level)
-        self._check(lib().ensi_wire_pack(self.h, C.byref(xv), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        op = self._wire_buf(out, xv.count, level, "wire output")
+        self._check(lib().ensi_wire_pack(self.h, C.byref(xv), op, _stream_ptr(stream)))
 
     def wire_unpack(self, inp, y, level: int, stream=None):
         yv = self.view(y, level)
-        self._check(lib().ensi_wire_unpack(self.h, C.c_void_p(inp.data_ptr()), C.byref(yv), _stream_ptr(stream)))
+        ip = self._wire_buf(inp, yv.count, level, "wire input")
+        self._check(lib().ensi_wire_unpack(self.h, ip, C.byref(yv), _stream_ptr(stream)))
 
     # ---- primitives (rows a5-a7, a4, a10)
     def ntt(self, data, limb_of_row, inverse: bool = False, stream=None):

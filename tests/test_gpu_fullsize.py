@@ -172,3 +172,124 @@ def test_layout_b_full_ring_bit_exact(c2, torch_cuda, B):
     for i in range(m):
         z = bctx.decrypt_debug(yd, i, 12)
         assert np.max(np.abs(z[:s] - ref[:, i])) < 1e-4
+
+
+def _rotkeys_parallel(o, sk, gs, seed0):
+    """Real rotation keys for many Galois elements, generated on all host cores (the oracle's C keygen releases the
+    GIL under ctypes)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(NTH) as ex:
+        return np.stack(list(ex.map(lambda ig: o.rotkey(seed0 + ig[0], ig[1], sk), enumerate(gs))))
+
+
+def test_c2_rotate_hoisted_128_elements(c2, torch_cuda):
+    """The hoisted-rotations/s bench shape at C2 parameters: one ciphertext rotated by 128 Galois elements in one
+    call (four key-switch batches of 32 on the two internal streams with their own scratch sets).  Keys are seeded
+    uniform words (the key switch is data-oblivious); outputs 0, 31, 32, 63, 64, 127 (every batch edge, both
+    streams) == the oracle's hoisted rotations word for word."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    gs = [o.galois(r) for r in range(1, 129)]
+    keys = synth.gen_words_torch(synth.SEED_BASE + 40, o.moduli, 128 * 3, 16, o.n).view(128, 3, 2, 16, o.n)
+    rctx = Context(16, 12, 4, 3)
+    rctx.load_keys(galois=gs, rot_keys=keys)
+    ct = synth.gen_words(synth.SEED_BASE + 41, o.q, 1, 12, o.n)
+    yd = torch.empty((128, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    rctx.rotate_hoisted(_dev(torch, ct), gs, yd, 12)
+    torch.cuda.synchronize()
+    sel = [0, 31, 32, 63, 64, 127]
+    got = yd[sel].cpu().numpy().view(np.uint64)
+    del yd
+    ksel = keys[sel].cpu().numpy().view(np.uint64)
+    want = o.rotate_hoisted(ct[0], [gs[i] for i in sel], ksel)
+    assert (got == want).all()
+
+
+def test_layout_b_c2_bench_schedule(c2, torch_cuda):
+    """Layout B exactly as bench.py times it (C2: s = 128 tokens, 768 -> 768, k = 256 columns per ciphertext,
+    n_in = 3 inputs, B = 256 baby steps, G = 1: 765 hoisted rotations with 255 keys in 8 key-switch batches on the
+    two internal streams) on real pk-encryptions: output columns 0, 383, 767 == the oracle's O11 schedule word for
+    word, and block 0 decrypts to X.W within 1e-4."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    s, d, m = 128, 768, 768
+    k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, 0)
+    assert (k, n_in, B, G, rots) == (256, 3, 256, 1, 765)
+    X = synth.gen_X(synth.SEED_BASE + 42, s, d) * 0.25
+    W = synth.gen_W(synth.SEED_BASE + 142, d, m)
+    slots = o.n // 2
+    zs = np.zeros((n_in, slots))
+    for c in range(n_in):
+        for b in range(k):
+            if c * k + b < d:
+                zs[c, b * s:(b + 1) * s] = X[:, c * k + b]
+    m_res = np.stack([o.encode(zs[c], 12, DELTA) for c in range(n_in)])
+    x = o.encrypt_batch(np.arange(n_in, dtype=np.uint64) + np.uint64(4200), pk, 12, m_res)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
+    keys = _rotkeys_parallel(o, sk, gk, 4300)
+    bctx = Context(16, 12, 4, 3)
+    bctx.load_keys(sk_ntt=sk, galois=gk, rot_keys=keys)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    bctx.pcmm_ternary(_dev(torch, x), bctx.weights(W), yd, level=12, layout=1, block_s=s)
+    torch.cuda.synchronize()
+    cols = [0, 383, 767]
+    got = yd[cols].cpu().numpy().view(np.uint64)
+    ref = X @ W.astype(np.float64)
+    for i in cols:
+        z = bctx.decrypt_debug(yd, i, 12)
+        assert np.max(np.abs(z[:s] - ref[:, i])) < 1e-4, i
+    del yd
+    want = o.pcmm_b(x, W, s, k, B, gk, keys, cols=cols, nthreads=NTH)
+    assert (got == want).all()
+
+
+def test_c2_integer_ntt_and_keyswitch_wide_moduli(torch_cuda):
+    """N' = 2^16 with moduli >= 2^50: the integer v2 NTT passes (not the FP64 ones) in both directions on extreme and
+    random rows, then hoisted rotations and rescale through the integer key-switching kernels -- word for word."""
+    import sympy
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    m2n = 1 << 17
+
+    def primes(below, cnt, skip=0):
+        out, v = [], (below - 1) // m2n * m2n + 1
+        while len(out) < cnt + skip:
+            if v < below and sympy.isprime(v):
+                out.append(v)
+            v -= m2n
+        return out[skip:]
+    q = primes(1 << 56, 1) + primes(1 << 51, 2)
+    p = primes(1 << 59, 1)
+    o = oracle.Oracle(16, 3, 1, 3, q=q, p=p)
+    ctx = Context(16, 3, 1, 3, q=q, p=p)
+    assert ctx.moduli == o.moduli
+    rows, limbs = [], []
+    for li in range(4):
+        qq = o.moduli[li]
+        for pat in (np.full(o.n, qq - 1, np.uint64), np.tile(np.array([0, qq - 1], np.uint64), o.n // 2),
+                    synth.gen_words(500 + li, [qq], 1, 1, o.n)[0, 0, 0]):
+            rows.append(pat)
+            limbs.append(li)
+    rows = np.stack(rows)
+    t = _dev(torch, rows)
+    ctx.ntt(t, limbs)
+    torch.cuda.synchronize()
+    assert (t.cpu().numpy().view(np.uint64) == np.stack([o.ntt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+    t = _dev(torch, rows)
+    ctx.ntt(t, limbs, inverse=True)
+    torch.cuda.synchronize()
+    assert (t.cpu().numpy().view(np.uint64) == np.stack([o.intt(limbs[i], rows[i]) for i in range(len(rows))])).all()
+    skc, sk, pk = o.keygen(4600)
+    gs = [o.galois(5), o.galois(-1024)]
+    keys = np.stack([o.rotkey(4700 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    ct = synth.gen_words(4800, o.q, 1, 3, o.n)
+    yd = torch.empty((2, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_hoisted(_dev(torch, ct), gs, yd, 3)
+    yr = torch.empty((1, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(_dev(torch, ct), yr, 3)
+    torch.cuda.synchronize()
+    assert (yd.cpu().numpy().view(np.uint64) == o.rotate_hoisted(ct[0], gs, keys)).all()
+    assert (yr.cpu().numpy().view(np.uint64)[0] == o.rescale(ct[0])).all()

@@ -256,6 +256,95 @@ def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda, kernel):
         assert (got[i] == np.uint64((coef * (q - 1)) % q)).all()
 
 
+@pytest.mark.parametrize("kernel", [1, 2, 3, 0])
+def test_pcmm_a_wide_moduli_long_sum(torch_cuda, kernel):
+    """Moduli just under 2^60 (the ctx maximum) with d = 8300 terms of q - 1: the CUDA-core path must reduce its
+    int64 accumulators every 7 rows there (accum_rows_between_reductions), the tcgen05 path takes the 128-bit
+    combine -- closed-form expected words (sum_j W_ji) (q - 1) mod q, and == the oracle on one column."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    m2n = 1 << 13
+    q = [_primes_1mod(m2n, 1 << 60, 1)[0], _primes_1mod(m2n, 1 << 59, 1)[0]]
+    p = [_primes_1mod(m2n, 1 << 60, 1, skip=1)[0]]
+    ctx = Context(12, 2, 1, 2, q=q, p=p)
+    d, m, level = 8300, 3, 2
+    x = np.empty((d, 2, level, ctx.n), np.uint64)
+    for r in range(level):
+        x[:, :, r, :] = np.uint64(q[r] - 1)
+    W = np.ones((d, m), np.int8)
+    W[:, 1] = -1
+    W[::3, 2] = -1
+    yd = torch.empty((m, 2, level, ctx.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(dev(torch, x), W, yd, level=level, kernel=kernel)
+    torch.cuda.synchronize()
+    got = host(yd)
+    for i in range(m):
+        coef = int(np.sum(W[:, i].astype(np.int64)))
+        for r in range(level):
+            assert (got[i, :, r] == np.uint64((coef * (q[r] - 1)) % q[r])).all(), (i, r)
+    o = oracle.Oracle(12, 2, 1, 2, q=q, p=p)
+    xs = x[:40].copy()
+    xs[::2, 0, 0, ::5] = np.uint64(0)
+    Ws = synth.gen_W(14000, 40, 3)
+    yd = torch.empty((3, 2, level, ctx.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(dev(torch, xs), Ws, yd, level=level, kernel=kernel)
+    torch.cuda.synchronize()
+    assert (host(yd) == o.pcmm_a(xs, Ws)).all()
+
+
+def test_pcmm_a_small_modulus_takes_cuda_cores(torch_cuda):
+    """A modulus below 2^32 is outside the tcgen05 epilogue's range: the default kernel falls back to the CUDA
+    cores (still the oracle's words), and requesting tcgen05 explicitly is ENSI_EINVAL."""
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_EINVAL
+    torch = torch_cuda
+    m2n = 1 << 13
+    q = [_primes_1mod(m2n, 1 << 31, 1)[0], _primes_1mod(m2n, 1 << 45, 1)[0]]
+    p = [_primes_1mod(m2n, 1 << 50, 1)[0]]
+    ctx = Context(12, 2, 1, 2, q=q, p=p)
+    o = oracle.Oracle(12, 2, 1, 2, q=q, p=p)
+    assert ctx.kernel_name(0, 2) == "cuda-core"
+    x = synth.gen_words(14100, o.q, 300, 2, o.n)
+    W = synth.gen_W(14101, 300, 70)
+    yd = torch.empty((70, 2, 2, o.n), dtype=torch.int64, device="cuda")
+    ctx.pcmm_ternary(dev(torch, x), W, yd, level=2)
+    torch.cuda.synchronize()
+    assert (host(yd) == o.pcmm_a(x, W, nthreads=4)).all()
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary(dev(torch, x), W, yd, level=2, kernel=2)
+    assert e.value.code == ENSI_EINVAL
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary(dev(torch, x), W, yd, level=2, kernel=5)
+    assert e.value.code == ENSI_EINVAL
+
+
+@pytest.mark.parametrize("L,alpha,dnum", [(18, 6, 3), (10, 2, 5)])
+def test_rotation_generic_keyswitch_kernels(torch_cuda, L, alpha, dnum):
+    """Parameter sets outside the specialised key-switching kernels' bounds: E = L + alpha = 24 > 16 extended limbs
+    (generic FP64 ModUp / ModDown conversions, per-limb final combine) and beta = 5 > 4 digits (generic key inner
+    product) -- hoisted rotations and a rescale, word for word against the oracle."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(12, L, alpha, dnum)
+    ctx = Context(12, L, alpha, dnum)
+    assert ctx.moduli == o.moduli
+    skc, sk, pk = o.keygen(14200 + L)
+    gs = [o.galois(3), o.galois(-77)]
+    keys = np.stack([o.rotkey(14300 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    for level in (L, L - 1):
+        ct = synth.gen_words(14400 + level, o.q, 1, level, o.n)[0]
+        yd = torch.empty((2, 2, level, o.n), dtype=torch.int64, device="cuda")
+        ctx.rotate_hoisted(dev(torch, ct[None]), gs, yd, level)
+        torch.cuda.synchronize()
+        assert (host(yd) == o.rotate_hoisted(ct, gs, keys)).all(), level
+    x = synth.gen_words(14500, o.q, 2, L, o.n)
+    yr = torch.empty((2, 2, L - 1, o.n), dtype=torch.int64, device="cuda")
+    ctx.rescale(dev(torch, x), yr, L)
+    torch.cuda.synchronize()
+    assert (host(yr) == np.stack([o.rescale(x[c]) for c in range(2)])).all()
+
+
 def test_pcmm_errors(setup_c1, torch_cuda):
     from paper_2509_09424_b200.ensi import EnsiError, ENSI_ENOTTERNARY, ENSI_EDIM, ENSI_EINVAL
     o, sk, pk, ctx = setup_c1
@@ -321,6 +410,49 @@ def test_rotate_batch_bit_exact(rot_setup, torch_cuda, n_ct, sel):
                 assert (got[c * len(sel) + r] == o.rotate(x[c], gs[i], keys[i])).all()
 
 
+def test_rotate_hoisted_128_elements_two_streams(setup_c1, torch_cuda):
+    """128 Galois elements in one ensi_rotate_hoisted call (the hoisted rotations/s bench shape): four key-switch
+    batches of 32 that alternate between the two internal streams, each with its own (acc, z) scratch set -- every
+    output word == the oracle's hoisted rotation (O10), and the last one decrypts to the cyclic shift."""
+    from paper_2509_09424_b200 import Context
+    o, sk, pk, _ = setup_c1
+    torch = torch_cuda
+    ctx = Context(12, 3, 1, 3)
+    gs = [o.galois(r) for r in range(1, 129)]
+    keys = np.stack([o.rotkey(12000 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    z = np.random.default_rng(128).uniform(-1, 1, o.n // 2)
+    ct = o.encrypt(12500, pk, 3, o.encode(z, 3, DELTA))
+    want = o.rotate_hoisted(ct, gs, keys)
+    yd = torch.empty((128, 2, 3, o.n), dtype=torch.int64, device="cuda")
+    for _ in range(2):                      # twice: the second call reuses both scratch sets
+        yd.zero_()
+        ctx.rotate_hoisted(dev(torch, ct[None]), gs, yd, 3)
+        torch.cuda.synchronize()
+        assert (host(yd) == want).all()
+    got = ctx.decrypt_debug(yd, 127, 3)
+    assert np.max(np.abs(got - np.roll(z, -128))) < 1e-5
+
+
+def test_rotate_batch_multi_batch_two_streams(setup_c1, torch_cuda):
+    """ensi_rotate_batch with 5 inputs x 40 Galois elements = 200 rotations > 96: key-switch batches of 19 elements
+    (<= 96 rotations each) on the two internal streams -- all 200 outputs == the oracle."""
+    from paper_2509_09424_b200 import Context
+    o, sk, pk, _ = setup_c1
+    torch = torch_cuda
+    ctx = Context(12, 3, 1, 3)
+    gs = [o.galois(r) for r in range(-20, 21) if r != 0]
+    keys = np.stack([o.rotkey(13000 + i, g, sk) for i, g in enumerate(gs)])
+    ctx.load_keys(sk_ntt=sk, galois=gs, rot_keys=keys)
+    x = synth.gen_words(13500, o.q, 5, 3, o.n)
+    yd = torch.empty((5 * len(gs), 2, 3, o.n), dtype=torch.int64, device="cuda")
+    ctx.rotate_batch(dev(torch, x), gs, yd, 3)
+    torch.cuda.synchronize()
+    got = host(yd).reshape(5, len(gs), 2, 3, o.n)
+    for c in range(5):
+        assert (got[c] == o.rotate_hoisted(x[c], gs, keys)).all()
+
+
 def test_rotate_identity_element_copies(rot_setup, torch_cuda):
     o, sk, pk, ctx, gs, keys = rot_setup
     torch = torch_cuda
@@ -347,13 +479,15 @@ def test_rotate_missing_key(rot_setup, torch_cuda):
 
 # ---------------------------------------------------------------- Layout B
 
-@pytest.mark.parametrize("d,m,B", [(16, 16, 0), (16, 16, 4), (20, 6, 4)])
-def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B):
+@pytest.mark.parametrize("d,m,B,s", [(16, 16, 0, 16), (16, 16, 4, 16), (20, 6, 4, 16), (100, 130, 4, 64)])
+def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B, s):
+    """Layout B (O11) on real encryptions, every output word == the oracle; (100, 130, 4, 64): 7 giant steps over 130
+    outputs = two key-stationary chunks (96 + 34) each split over the two internal streams, with the running sum
+    added in place by the final combine."""
     from paper_2509_09424_b200 import Context
     o, sk, pk, _ = setup_c1
     torch = torch_cuda
     ctx = Context(12, 3, 1, 3)
-    s = 16
     k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, B)
     X = synth.gen_X(61 + d, s, d)
     W = synth.gen_W(62 + d, d, m)

@@ -1,0 +1,242 @@
+"""Independent big-integer mini-oracle for N' <= 256 ("an independent Python big-integer
+mini-oracle for N' <= 256 cross-checks the C oracle word for word").
+
+TEST INFRASTRUCTURE ONLY (like the rest of oracle/): only tests/ import it.  It shares no code with
+``ensi_oracle.c`` nor with the CUDA path: every step is written from its definition with Python integers,
+by a different route wherever one exists, so that a slip in the C oracle's index algebra, digit handling or
+rounding convention shows up as a word mismatch:
+
+* NTT      -- the defining sum NTT(a)[k] = sum_i a_i psi^{(2 brv(k)+1) i} (O2), O(N'^2); INTT solves it back
+              with the explicit inverse sum (N'^{-1} sum_k A_k psi^{-(2 brv(k)+1) i}).
+* sigma_g  -- in the COEFFICIENT domain, a(X) -> a(X^g) with X^{N'} = -1 (O9), then the NTT (the C oracle
+              permutes NTT slots by index algebra instead).
+* ModUp    -- per digit the exact integer sum_i y_i (Q_t/q_i) reduced mod every target r (O10: "no overflow
+              correction", so ext = x + u Q_t with 0 <= u < |D_t|), instead of per-target modular sums.
+* ModDown  -- the exact signed integer v = sum_k y_k (P/p_k) with y_k centred in (-p_k/2, p_k/2] (R10),
+              reduced mod q_i, then (acc - NTT(v)) P^{-1}.
+* Rot      -- ModUp first, then sigma_g on every extended digit (O10), KIP, ModDown, + sigma_g(c0).
+* Layout B -- O11 step by step (baby rotations, Algorithm-1 partial sums, giant rotations, sum).
+* rescale  -- O12 in the coefficient domain: (c_i - t) q_{l-1}^{-1} with t the centred last limb, then NTT.
+
+Ciphertexts are lists of polynomials: ct[poly][limb] = list of N' Python ints (NTT form, canonical).
+"""
+from __future__ import annotations
+
+
+def _brv(x: int, bits: int) -> int:
+    r = 0
+    for _ in range(bits):
+        r = (r << 1) | (x & 1)
+        x >>= 1
+    return r
+
+
+def min_root(q: int, n: int) -> int:
+    """O2: the smallest x in [1, q) with x^{N'} = -1 mod q (a primitive 2N'-th root); every primitive 2N'-th root is
+    an odd power of any one of them."""
+    assert (q - 1) % (2 * n) == 0
+    for base in range(2, 1000):
+        r = pow(base, (q - 1) // (2 * n), q)
+        if pow(r, n, q) == q - 1:
+            break
+    else:
+        raise ValueError("no 2N'-th root found")
+    return min(pow(r, 2 * j + 1, q) for j in range(n))
+
+
+class Mini:
+    """One parameter set: moduli q_0..q_{L-1}, p_0..p_{alpha-1} (given, e.g. the O1 rule's), dnum digits."""
+
+    def __init__(self, log_n: int, q: list, p: list, dnum: int):
+        self.log_n, self.n = log_n, 1 << log_n
+        self.q, self.p = [int(v) for v in q], [int(v) for v in p]
+        self.L, self.alpha, self.dnum = len(self.q), len(self.p), dnum
+        self.moduli = self.q + self.p
+        self._pw = {}
+        for m in self.moduli:
+            psi = min_root(m, self.n)
+            pw = [1] * (2 * self.n)
+            for e in range(1, 2 * self.n):
+                pw[e] = pw[e - 1] * psi % m
+            self._pw[m] = pw
+
+    # ---------------------------------------------------------------- O2
+    def ntt(self, m: int, a: list) -> list:
+        n, lg, pw = self.n, self.log_n, self._pw[m]
+        out = []
+        for k in range(n):
+            e = 2 * _brv(k, lg) + 1
+            out.append(sum(a[i] * pw[(e * i) % (2 * n)] for i in range(n)) % m)
+        return out
+
+    def intt(self, m: int, A: list) -> list:
+        n, lg, pw = self.n, self.log_n, self._pw[m]
+        ninv = pow(n, -1, m)
+        out = []
+        for i in range(n):
+            s = 0
+            for k in range(n):
+                e = (2 * _brv(k, lg) + 1) * i % (2 * n)
+                s += A[k] * pw[(2 * n - e) % (2 * n)]
+            out.append(s * ninv % m)
+        return out
+
+    # ---------------------------------------------------------------- O9
+    def automorph_coeff(self, m: int, a: list, g: int) -> list:
+        """a(X) -> a(X^g) in Z_m[X]/(X^{N'}+1)."""
+        n = self.n
+        out = [0] * n
+        for i, c in enumerate(a):
+            e = i * g % (2 * n)
+            if e < n:
+                out[e] = (out[e] + c) % m
+            else:
+                out[e - n] = (out[e - n] - c) % m
+        return out
+
+    def automorph_ntt(self, m: int, A: list, g: int) -> list:
+        return self.ntt(m, self.automorph_coeff(m, self.intt(m, A), g))
+
+    def galois(self, r: int) -> int:
+        return pow(5, r % (self.n // 2), 2 * self.n)
+
+    # ---------------------------------------------------------------- O10
+    def _ext_moduli(self, level: int) -> list:
+        return self.q[:level] + self.p
+
+    def _digits(self, level: int) -> list:
+        a = self.alpha
+        return [list(range(t * a, min((t + 1) * a, level))) for t in range(-(-level // a))]
+
+    def modup(self, level: int, c: list) -> list:
+        """c [level][N'] NTT form -> [beta][level + alpha][N'] NTT form over Q_l u P."""
+        ext_mod = self._ext_moduli(level)
+        out = []
+        for D in self._digits(level):
+            Qt = 1
+            for i in D:
+                Qt *= self.q[i]
+            coef = {i: self.intt(self.q[i], c[i]) for i in D}
+            # y_i = [c_i (Q_t/q_i)^{-1}]_{q_i}; the exact integer X = sum_i y_i (Q_t/q_i) (no correction: X = x + u Q_t)
+            ys = {i: [v * pow(Qt // self.q[i], -1, self.q[i]) % self.q[i] for v in coef[i]] for i in D}
+            X = [sum(ys[i][k] * (Qt // self.q[i]) for i in D) for k in range(self.n)]
+            rows = []
+            for e, r in enumerate(ext_mod):
+                if e < level and e in D:
+                    rows.append(list(c[e]))                       # the digit's own limbs: the input's NTT words
+                else:
+                    rows.append(self.ntt(r, [v % r for v in X]))
+            out.append(rows)
+        return out
+
+    def moddown(self, level: int, acc: list, variant: str = "centred") -> list:
+        """acc [level + alpha][N'] NTT form over Q_l u P -> [level][N'] NTT form over Q_l.  variant "centred" is
+        R10 (the definition); "uncentred" (y_k in [0, p_k)) and "exact" (v = the centred residue of acc mod P,
+        an exact CRT) exist only so tests can show the cross-check tells the conventions apart."""
+        P = 1
+        for pk in self.p:
+            P *= pk
+        pc = [self.intt(pk, acc[level + k]) for k, pk in enumerate(self.p)]
+        v = [0] * self.n
+        for k, pk in enumerate(self.p):
+            w = pow(P // pk, -1, pk)
+            for j in range(self.n):
+                y = pc[k][j] * w % pk
+                if y > pk // 2 and variant == "centred":
+                    y -= pk                                        # centred in (-p_k/2, p_k/2]
+                v[j] += y * (P // pk)
+        if variant == "exact":
+            v = [x % P - (P if x % P > P // 2 else 0) for x in v]
+        out = []
+        for i in range(level):
+            qi = self.q[i]
+            z = self.ntt(qi, [x % qi for x in v])
+            pinv = pow(P, -1, qi)
+            out.append([(acc[i][j] - z[j]) * pinv % qi for j in range(self.n)])
+        return out
+
+    def rotate(self, ct: list, g: int, key: list) -> list:
+        """Rot(ct; g) (O9 + O10).  key [dnum][2][L + alpha][N'] (key[t][0] = b_t, key[t][1] = a_t)."""
+        level = len(ct[0])
+        if g % (2 * self.n) == 1:
+            return [[list(r) for r in ct[0]], [list(r) for r in ct[1]]]
+        ext_mod = self._ext_moduli(level)
+        ext_idx = list(range(level)) + [self.L + k for k in range(self.alpha)]
+        dig = self.modup(level, ct[1])                              # ModUp first ...
+        dig = [[self.automorph_ntt(ext_mod[e], row, g) for e, row in enumerate(d)] for d in dig]   # ... then sigma_g
+        ks = []
+        for j in range(2):
+            acc = []
+            for e, r in enumerate(ext_mod):
+                acc.append([sum(dig[t][e][k] * key[t][j][ext_idx[e]][k] for t in range(len(dig))) % r
+                            for k in range(self.n)])
+            ks.append(self.moddown(level, acc))
+        c0g = [self.automorph_ntt(self.q[i], ct[0][i], g) for i in range(level)]
+        out0 = [[(c0g[i][k] + ks[0][i][k]) % self.q[i] for k in range(self.n)] for i in range(level)]
+        return [out0, ks[1]]
+
+    # ---------------------------------------------------------------- O8 / O11
+    def add(self, a: list, b: list, sign: int = 1) -> list:
+        return [[[(x + sign * y) % self.q[i] for x, y in zip(a[p][i], b[p][i])] for i in range(len(a[p]))]
+                for p in range(2)]
+
+    def zero(self, level: int) -> list:
+        return [[[0] * self.n for _ in range(level)] for _ in range(2)]
+
+    def pcmm_a(self, x: list, W) -> list:
+        """Algorithm 1: y_i = sum_j W[j][i] x_j from the trivial ciphertext (0, 0)."""
+        d, m = len(W), len(W[0])
+        level = len(x[0][0])
+        ys = []
+        for i in range(m):
+            y = self.zero(level)
+            for j in range(d):
+                if W[j][i]:
+                    y = self.add(y, x[j], int(W[j][i]))
+            ys.append(y)
+        return ys
+
+    def pcmm_b(self, x: list, W, s: int, k: int, B: int, keys: dict) -> list:
+        """O11: R_{c,b} = Rot(ct_c; s b), T_{i,gam} = sum_{c,b} W[c k + gam B + b][i] R_{c,b},
+        y_i = T_{i,0} + sum_{gam >= 1} Rot(T_{i,gam}; s B gam).  keys: {galois element: key}."""
+        d, m = len(W), len(W[0])
+        level = len(x[0][0])
+        G = k // B
+        R = {}
+        for c in range(len(x)):
+            for b in range(B):
+                g = self.galois(s * b)
+                R[c, b] = x[c] if b == 0 else self.rotate(x[c], g, keys[g])
+        ys = []
+        for i in range(m):
+            y = self.zero(level)
+            for gam in range(G):
+                T = self.zero(level)
+                for c in range(len(x)):
+                    for b in range(B):
+                        col = c * k + gam * B + b
+                        if col < d and W[col][i]:
+                            T = self.add(T, R[c, b], int(W[col][i]))
+                if gam:
+                    g = self.galois(s * B * gam)
+                    T = self.rotate(T, g, keys[g])
+                y = self.add(y, T)
+            ys.append(y)
+        return ys
+
+    # ---------------------------------------------------------------- O12
+    def rescale(self, ct: list) -> list:
+        level = len(ct[0])
+        ql = self.q[level - 1]
+        out = []
+        for p in range(2):
+            t = self.intt(ql, ct[p][level - 1])
+            t = [v - ql if v > ql // 2 else v for v in t]            # centred last limb
+            rows = []
+            for i in range(level - 1):
+                qi = self.q[i]
+                ci = self.intt(qi, ct[p][i])
+                inv = pow(ql, -1, qi)
+                rows.append(self.ntt(qi, [(a - b) * inv % qi for a, b in zip(ci, t)]))
+            out.append(rows)
+        return out

@@ -273,8 +273,10 @@ def test_modup_crt_identity():
 
 
 def test_moddown_exact_identity():
-    """ModDown(acc) * P + v == acc over Q_l, where v = [acc]_P + u P is the fast-converted (centred, R10)
-    P-residue with a small integer overflow u, |u| <= alpha."""
+    """ModDown(acc) * P + v == acc over Q_l (exact big-integer identity) with v the fast-converted P-residue of R10:
+    v = sum_k y_k (P/p_k), y_k = [acc_{p_k} (P/p_k)^{-1}]_{p_k} CENTRED in (-p_k/2, p_k/2], no overflow correction.
+    Pinned to that v exactly, so an exact-CRT ModDown (v = the centred residue of acc mod P) or an uncentred
+    conversion (y_k in [0, p_k)) fails; the overflow u = (v - [acc]_P) / P must also take more than one value."""
     o = _tiny_ks_ctx()
     level = 3
     rs = np.random.default_rng(10)
@@ -284,14 +286,19 @@ def test_moddown_exact_identity():
     P = o.p[0] * o.p[1]
     acc_c = np.stack([o.intt(li, acc[e]) for e, li in enumerate(ext_limbs)])
     out_c = np.stack([o.intt(i, out[i]) for i in range(level)])
-    xp = [v % P for v in oracle.crt_centered(acc_c[level:], o.p)]
-    for i in range(level):
-        q = o.q[i]
-        for k in range(o.n):
-            # v = xp + u P for some u in [0, alpha): out*P + v == acc (mod q)
-            ok = any((int(out_c[i, k]) * P + xp[k] + u * P - int(acc_c[i, k])) % q == 0
-                     for u in range(-o.alpha, o.alpha + 1))
-            assert ok
+    xp = [v % P for v in oracle.crt_centered(acc_c[level:], o.p)]      # [acc]_P in [0, P)
+    us = set()
+    for k in range(o.n):
+        v = 0
+        for kk, pk in enumerate(o.p):
+            y = int(acc_c[level + kk, k]) * pow(P // pk, -1, pk) % pk
+            v += (y - pk if y > pk // 2 else y) * (P // pk)
+        assert (v - xp[k]) % P == 0
+        us.add((v - xp[k]) // P)
+        for i in range(level):
+            q = o.q[i]
+            assert (int(out_c[i, k]) * P + v - int(acc_c[i, k])) % q == 0, (i, k)
+    assert len(us) > 1 and max(abs(u) for u in us) <= o.alpha
 
 
 def test_rotation_decrypts_to_cyclic_shift(c1):

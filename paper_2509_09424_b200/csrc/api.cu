@@ -679,6 +679,8 @@ static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, con
     bool tc = false;
     int rc = select_kernel(ctx, kernel, level, d, &tc);
     if (rc) return rc;
+    // wire slices go straight through the compact kernel where it applies (default or tcgen05 pairs requested)
+    const bool compact = wire && tc && (kernel == 0 || kernel == 2) && tcc_supported(ctx, level);
     const size_t ctb = wire ? 2 * wire_poly_bytes(ctx, level) : (size_t)2 * level * n * 8;
     const size_t stage_words = (size_t)(d + m) * n;          // one slice of every input and output
     // per buffer: the u64 slice stage, plus (wire) the same slice in wire bytes (<= 8 bytes per word)
@@ -737,11 +739,16 @@ static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, con
         cudaEventRecord(ctx->ev_h2d[b], ctx->st_h2d);
         cudaStreamWaitEvent(st, ctx->ev_h2d[b], 0);
         if (s >= 2) cudaStreamWaitEvent(st, ctx->ev_d2h[b], 0);             // y stage b drained
-        if (wire) rc = wire_unpack(ctx, xw, xs, (size_t)d * n, wb, st);
-        if (!rc)
-            rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, tc_variant(kernel))
-                    : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
-        if (!rc && wire) rc = wire_pack(ctx, ys, yw, (size_t)m * n, wb, st);
+        if (compact) {
+            // the wire slice is a compact slice: the compact tensor-core kernel reads and writes it directly
+            rc = accum_ternary_tcc(ctx, xw, d, w, yw, level, st, (int)limb);
+        } else {
+            if (wire) rc = wire_unpack(ctx, xw, xs, (size_t)d * n, wb, st);
+            if (!rc)
+                rc = tc ? accum_ternary_tc(ctx, xs, d, w, ys, level, st, n, limb, tc_variant(kernel))
+                        : accum_ternary(ctx, xs, d, w->d_planes, w->mw, m, ys, level, st, n, limb);
+            if (!rc && wire) rc = wire_pack(ctx, ys, yw, (size_t)m * n, wb, st);
+        }
         cudaEventRecord(ctx->ev_comp[b], st);
         cudaStreamWaitEvent(ctx->st_d2h, ctx->ev_comp[b], 0);
         cudaMemcpy2DAsync(yh + off, ctb, wire ? (const void*)yw : (const void*)ys, rowb, rowb, m,
@@ -768,6 +775,33 @@ int ensi_pcmm_ternary_host_wire(ensi_ctx* ctx, const uint8_t* x_wire, uint32_t l
                                 const ensi_weights* wc, uint8_t* y_wire, uint32_t kernel, void* stream) {
     (void)log2_scale;
     return pcmm_host_impl(ctx, x_wire, level, wc, y_wire, kernel, stream, true);
+}
+
+int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc, ensi_compact_view* y,
+                              const ensi_pcmm_opts* opts, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!wc) return set_err(ctx, ENSI_EINVAL, "NULL weights");
+    ensi_weights* w = const_cast<ensi_weights*>(wc);
+    if (w->ctx != ctx) return set_err(ctx, ENSI_EINVAL, "weights belong to another context");
+    if (!x || !x->data || !y || !y->data) return set_err(ctx, ENSI_EINVAL, "NULL view or data");
+    if (x->level < 1 || x->level > ctx->L) return set_err(ctx, ENSI_ELEVEL, "x.level outside [1, num_q]");
+    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level must equal x.level");
+    ensi_pcmm_opts o{};
+    if (opts) o = *opts;
+    if (o.layout != 0) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: Layout A only");
+    if (o.rescale_out) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: no rescale epilogue");
+    if (o.kernel != 0 && o.kernel != 2) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: kernel must be 0 or 2");
+    if (x->count != w->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
+    if (y->count != w->m) return set_err(ctx, ENSI_EDIM, "y.count != m");
+    const uint64_t cb = 2 * wire_poly_bytes(ctx, x->level);
+    const uint8_t *x0 = x->data, *x1 = x0 + (size_t)x->count * cb, *y0 = y->data, *y1 = y0 + (size_t)y->count * cb;
+    if (x0 < y1 && y0 < x1) return set_err(ctx, ENSI_EINVAL, "y aliases x");
+    if (!tcc_supported(ctx, x->level) || w->d >= (1u << 22))
+        return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable (sm_100a, 5..8-byte words, N' >= 256)");
+    DeviceGuard g(ctx->device);
+    int rc = accum_ternary_tcc(ctx, x->data, w->d, w, y->data, x->level, (cudaStream_t)stream);
+    if (!rc) y->log2_scale = x->log2_scale;
+    return rc;
 }
 
 int ensi_wire_pack(ensi_ctx* ctx, const ensi_ct_view* x, uint8_t* out, void* stream) {

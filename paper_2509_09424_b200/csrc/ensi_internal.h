@@ -157,6 +157,12 @@ enum { TC_AUTO = 0, TC_PAIR_MC = 1, TC_PAIR = 2, TC_ONE_CTA = 3 };
 int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights* w, uint64_t* y, uint32_t level,
                      cudaStream_t st, uint64_t ctw = 0, uint32_t limb0 = 0, int variant = TC_AUTO);
 bool tc_supported(const ensi_ctx* ctx, uint32_t level);
+// compact word layout (accum_tcc.cu): w_r = ceil(bitlen(q_r)/8) bytes per word of limb r
+uint32_t compact_word_bytes(const ensi_ctx* ctx, uint32_t limb);
+bool tcc_supported(const ensi_ctx* ctx, uint32_t level);
+// x: d compact ciphertexts (slice_limb < 0) or d copies of one staged (poly, limb) slice of limb slice_limb
+int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
+                      cudaStream_t st, int slice_limb = -1);
 
 // key switching (keyswitch.cu)
 int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out);

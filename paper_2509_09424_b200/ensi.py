@@ -30,7 +30,7 @@ EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
            "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel", "ensi_load_relin_key",
            "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm", "ensi_wire_bytes", "ensi_pcmm_ternary_host_wire",
-           "ensi_wire_pack", "ensi_wire_unpack"]
+           "ensi_wire_pack", "ensi_wire_unpack", "ensi_pcmm_ternary_compact"]
 
 
 class EnsiError(RuntimeError):
@@ -45,6 +45,10 @@ class Params(C.Structure):
 
 
 class CtView(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("count", C.c_uint32), ("level", C.c_uint32), ("log2_scale", C.c_double)]
+
+
+class CompactView(C.Structure):
     _fields_ = [("data", C.c_void_p), ("count", C.c_uint32), ("level", C.c_uint32), ("log2_scale", C.c_double)]
 
 
@@ -101,6 +105,8 @@ def lib():
         L.ensi_pcmm_ternary_host_wire.argtypes = [vp, vp, u32, C.c_double, vp, vp, u32, vp]
         L.ensi_wire_pack.argtypes = [vp, C.POINTER(CtView), vp, vp]
         L.ensi_wire_unpack.argtypes = [vp, vp, C.POINTER(CtView), vp]
+        L.ensi_pcmm_ternary_compact.argtypes = [vp, C.POINTER(CompactView), vp, C.POINTER(CompactView),
+                                                C.POINTER(PcmmOpts), vp]
         L.ensi_mul_plain.argtypes = [vp, C.POINTER(CtView), vp, C.c_double, C.POINTER(CtView), vp]
         L.ensi_mul_relin.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), C.POINTER(CtView), vp]
         L.ensi_ccmm.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp, C.POINTER(CtView),
@@ -260,6 +266,27 @@ class Context:
             raise ValueError("host buffers must hold [count][2][level][N'] words")
         self._check(lib().ensi_pcmm_ternary_host(self.h, _np_ptr(x_host), level, log2_scale, w.h, _np_ptr(y_host),
                                                  kernel, _stream_ptr(stream)))
+
+    # ---- compact device layout (ensi_compact_view)
+    def compact_view(self, t, level: int, log2_scale: float = 40.0) -> CompactView:
+        """uint8 CUDA tensor [count][ensi_wire_bytes(level)] -> ensi_compact_view."""
+        wb = self.wire_bytes(level)
+        if not (t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 1):
+            raise ValueError("compact ciphertexts must be a contiguous 8-bit CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"tensor on cuda:{t.device.index}, context on cuda:{self.device}")
+        if t.dim() != 2 or t.shape[1] != wb:
+            raise ValueError(f"expected [count][{wb}] bytes, got {tuple(t.shape)}")
+        return CompactView(t.data_ptr(), t.shape[0], level, log2_scale)
+
+    def pcmm_ternary_compact(self, x, w: "Weights", y, level: int, kernel: int = 0, stream=None,
+                             log2_scale: float = 40.0) -> float:
+        """y = x (x) W on compact ciphertexts (Layout A); returns y's log2 scale."""
+        xv, yv = self.compact_view(x, level, log2_scale), self.compact_view(y, level)
+        opts = PcmmOpts(0, 0, 0, 0, kernel)
+        self._check(lib().ensi_pcmm_ternary_compact(self.h, C.byref(xv), w.h, C.byref(yv), C.byref(opts),
+                                                    _stream_ptr(stream)))
+        return yv.log2_scale
 
     # ---- compact wire format (host transfers)
     def wire_widths(self, level: int):

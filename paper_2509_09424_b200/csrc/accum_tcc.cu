@@ -9,7 +9,7 @@
 //
 // Tiles: a word tile of one (poly, limb) slice is 48 words (w = 5, N = 240 bytes), 40 (w = 6, N = 240), 32 (w = 7,
 // N = 224; w = 8, N = 256); the last tile of a slice may be shorter (N' mod 48 or mod 40 words).  CTA pairs
-// (cta_group::2, M = 256 outputs): each CTA holds N/2 bytes of every K row of the tile in a 128-byte SWIZZLE_128B
+// (cta_group::2, M = 256 outputs): each CTA holds its half of every K row of the tile (half_cols) in a 128-byte SWIZZLE_128B
 // atom (a 128-byte TMA box, the few bytes past N/2 belong to the next tile and are ignored), W^T resident; clusters
 // of pairs over consecutive output groups share every X sub-box by TMA multicast, as in k_accum_tc2.  Epilogue:
 // the two warps of a TMEM lane quarter each drain half the tile's words (tcgen05.ld x8 pieces), recombine the
@@ -32,7 +32,7 @@ static constexpr uint32_t kBStage = 128 * 128;          // 16 KB: 128 K rows x o
 static constexpr uint32_t kYQuarter = 32 * 256;         // staging per TMEM lane quarter: 32 outputs x <= 256 bytes
 static constexpr uint32_t kAResMax = 96 * 1024;
 static constexpr uint32_t kMaxSlices = 96;
-static constexpr uint32_t kMaxMaps = 4;
+static constexpr uint32_t kMaxMaps = 8;
 
 // Tile table (kernel-parameter bank): slice s = (poly, limb) of a ciphertext (or the one staged slice).
 struct Tiles {
@@ -63,6 +63,15 @@ __device__ __forceinline__ TileInfo tile_info(const Tiles& tl, uint32_t t, uint3
     ti.map = nw == wpt ? tl.map_full[s] : tl.map_tail[s];
     return ti;
 }
+
+// Tile halves.  A tile of n = 2 hb bytes is split between the pair: CTA 0 loads its 128-byte box from the tile's
+// first byte, CTA 1 from byte (hb & ~15) -- TMA box starts stay 16-byte aligned (hb = 120 or 40 at w = 5, 120 / 72
+// / 24 at w = 6 are not; a misaligned start is an illegal instruction on sm_100a, measured).  The MMA takes P
+// columns from each CTA (N = 2P, P a multiple of 16 as cta_group::2 needs): CTA 0's bytes [0, hb) are columns
+// [0, hb), CTA 1's bytes [hb, n) are columns [P + (hb & 15), P + (hb & 15) + hb).  Columns outside those hold
+// neighbouring bytes (or TMA zero fill) that the epilogue never reads.
+__host__ __device__ constexpr uint32_t half_cols(uint32_t hb) { return (hb + (hb & 15) + 15) & ~15u; }
+__host__ __device__ constexpr uint32_t half1_col(uint32_t hb) { return half_cols(hb) + (hb & 15); }
 
 #define TMEM_LD_X8(taddr, r)                                                                                        \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                         \
@@ -132,7 +141,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tbase_q, uint32_t release_addr
                                          uint32_t byte, uint32_t row0) {
     constexpr uint32_t NB = W * HW;             // bytes of this warp's half row segment
     uint64_t u[NB / 8];
-    epi_words<W, HW>(tbase_q + half * NB, release_addr, lane, ea, u);
+    epi_words<W, HW>(tbase_q + half * half1_col(NB), release_addr, lane, ea, u);
     // staging free: the previous TMA store of this quarter has read it
     if (half == 0 && lane == 0) tma_store_wait_read0();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t s = 0, ph = 0, sl = 0;
             for (uint32_t t = p; t < ntiles; t += per_group) {
                 const TileInfo ti = tile_info(tl, t, sl);
-                const int32_t x0 = (int32_t)(ti.byte + rank * (ti.n >> 1));   // this CTA's N half
+                const int32_t x0 = (int32_t)(ti.byte + rank * ((ti.n >> 1) & ~15u));   // this CTA's half (half_cols)
                 for (uint32_t kb = 0; kb < kblocks; kb++) {
                     mbar_wait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[s], 2 * (kBStage + (A_RES ? 0 : kABox)));
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t s = 0, ph = 0, it = 0, sl = 0;
             for (uint32_t t = p; t < ntiles; t += per_group, it++) {
                 const TileInfo ti = tile_info(tl, t, sl);
-                const uint32_t idesc = idesc_i8(256, ti.n);
+                const uint32_t idesc = idesc_i8(256, 2 * half_cols(ti.n >> 1));   // see half_cols
                 const uint32_t acc = it & 1, use = it >> 1;
                 mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 tc_fence_after();

@@ -304,6 +304,25 @@ def _random_keys(ctx, gs, cfg, n):
     return keys
 
 
+def layout_b_plan(n: int, s: int, d: int, m: int, B: int = 0):
+    """The product's Layout-B schedule (api.cu plan_b, R11): k = min((N'/2)/s, 2^ceil(log2 d)), n_in = ceil(d/k),
+    B = argmin (B-1) n_in + (k/B - 1) m unless given; returns (k, n_in, B, G, rotations)."""
+    k = min((n // 2) // s, 1 << max(0, (d - 1).bit_length()))
+    n_in = -(-d // k)
+    if B == 0:
+        B = min((((b - 1) * n_in + (k // b - 1) * m, b) for b in (1 << i for i in range(k.bit_length()))
+                 if b <= k))[1]
+    G = k // B
+    return k, n_in, B, G, (B - 1) * n_in + (G - 1) * m
+
+
+# SURVEY 8(d) algorithmic bytes per key-switched rotation at C2 parameters (N'=2^16, l=12, alpha=4, dnum=3): the
+# 50.3 MB key plus the extended-basis digits and the ciphertext in/out -- 88 MB hoisted (ModUp shared), 126 MB for a
+# rotation of an independent input
+KS_BYTES_HOISTED = 88e6
+KS_BYTES_INDEPENDENT = 126e6
+
+
 def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool = True, ccmm: bool = True):
     """The other section-8 rows at the same parameters (timing-only uniform words and random keys; every kernel
     is data-oblivious): NTT/INTT per limb (a5), hoisted key-switched rotations (a6+a7, the BASELINE metric's
@@ -345,7 +364,8 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         ms = time_loop(lambda: ctx.rotate_hoisted(x, gs, y, L), steps, st)
         r = {"value": batch / (ms * 1e-3), "unit": "rotations/s", "ms_per_call": ms,
              "mode": f"hoisted, {batch} Galois elements per ModUp, N'=2^16, L=12, alpha=4, dnum=3",
-             "key_GBps": batch * key_bytes / (ms * 1e-3) / 1e9}
+             "key_GBps": batch * key_bytes / (ms * 1e-3) / 1e9,
+             "hbm_frac": batch * KS_BYTES_HOISTED / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
         if batch == 128:
             out["rotations"] = r
         else:
@@ -363,6 +383,7 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
     ms = time_loop(lambda: ctx.rotate_batch(xb, gs1, yb, L), steps, st)
     out["rotations"]["independent_inputs"] = {
         "value": 96 / (ms * 1e-3), "unit": "rotations/s", "ms_per_call": ms,
+        "hbm_frac": 96 * KS_BYTES_INDEPENDENT / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
         "mode": "96 independent ciphertexts x 1 Galois element (ensi_rotate_batch; one ModUp per rotation)"}
     del keys, xb, yb
     # rescale 64 ciphertexts (level 12 -> 11)
@@ -389,20 +410,53 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         out["pcmm_layout_b"] = {"value": ms, "unit": "ms/layer", "rotations": (k - 1) * n_in, "block_s": s,
                                 "k": k, "n_in": n_in, "rotations_per_sec": (k - 1) * n_in / (ms * 1e-3)}
         del keys, xb, yb
-    # Layout-A throughput at the other BASELINE shapes (C3 FFN pair, C4/C5 hidden-2048 projections)
+        # SURVEY 8(f) NEXT #4 (R19, lazy ModDown of the giant steps) before / after: BASELINE configs[2]'s down
+        # projection on its default plan (G = 2: one giant rotation per output, lazy == eager) and the C2 layer with
+        # B = 64 (G = 4: three giant steps per output summed over Q_l u P, one ModDown instead of three)
+        lz = {}
+        for name, (dd, mm, bb) in (("C3_down_3072x768_default", (3072, 768, 0)), ("C2_768x768_B64", (768, 768, 64))):
+            kk, nin, B, G, rots = layout_b_plan(n, s, dd, mm, bb)
+            gkb = sorted({pow(5, s * b, 2 * n) for b in range(1, B)} | {pow(5, s * B * g, 2 * n) for g in range(1, G)})
+            keys = _random_keys(ctx, gkb, cfg, n)
+            ctx.load_keys(galois=gkb, rot_keys=keys)
+            W = synth.gen_W(synth.SEED_BASE + 7 + dd, dd, mm)
+            w = ctx.weights(W)
+            xb = synth.gen_words_torch(14, ctx.q, nin, L, n)
+            yb = torch.empty((mm, 2, L, n), dtype=torch.int64, device="cuda")
+            row = {"k": kk, "n_in": nin, "B": B, "G": G, "rotations": rots}
+            for mode in (False, True):
+                fn = lambda: ctx.pcmm_ternary(xb, w, yb, level=L, layout=1, block_s=s, baby=B, moddown_lazy=mode)  # noqa
+                fn()
+                row["lazy_ms" if mode else "eager_ms"] = time_loop(fn, max(1, steps // 2), st)
+            lz[name] = row
+            del keys, xb, yb, w
+            torch.cuda.empty_cache()
+        out["layout_b_lazy_moddown"] = lz
+    # Layout-A throughput at the other BASELINE shapes (C3 FFN pair, C4/C5 hidden-2048 projections), compact
+    # resident layout (the headline's), and the C2 layer in the uint64 layout (k_accum_tc2) for comparison
     sweep = {}
-    for name, (dd, mm) in (("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)), ("C4_2048x2048", (2048, 2048)),
-                           ("C5_2048x5504", (2048, 5504)), ("C5_5504x2048", (5504, 2048)),
-                           ("C5_qkv_2048x6144", (2048, 6144))):
+    wb = ctx.wire_bytes(L)
+    for name, (dd, mm) in (("C2_768x768_u64", (768, 768)), ("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)),
+                           ("C4_2048x2048", (2048, 2048)), ("C5_2048x5504", (2048, 5504)),
+                           ("C5_5504x2048", (5504, 2048)), ("C5_qkv_2048x6144", (2048, 6144))):
         W = synth.gen_W(synth.SEED_BASE + dd + mm, dd, mm)
         w = ctx.weights(W)
-        xs = synth.gen_words_torch(17, ctx.q, dd, L, n)
-        ys = torch.empty((mm, 2, L, n), dtype=torch.int64, device="cuda")
-        ctx.pcmm_ternary(xs, w, ys, level=L)
-        ms = time_loop(lambda: ctx.pcmm_ternary(xs, w, ys, level=L), max(1, steps // 2), st)
-        ops = 2.0 * (2 * L * n * 8) * (-(-dd // 128) * 128) * (-(-mm // 256) * 256)
+        if name.endswith("_u64"):
+            xs = synth.gen_words_torch(17, ctx.q, dd, L, n)
+            ys = torch.empty((mm, 2, L, n), dtype=torch.int64, device="cuda")
+            fn = lambda: ctx.pcmm_ternary(xs, w, ys, level=L)  # noqa: E731
+            ctb = 2 * L * n * 8
+        else:
+            xs = gen_compact(ctx, 17, dd, L)
+            ys = torch.empty((mm, wb), dtype=torch.uint8, device="cuda")
+            fn = lambda: ctx.pcmm_ternary_compact(xs, w, ys, level=L)  # noqa: E731
+            ctb = wb
+        fn()
+        ms = time_loop(fn, max(1, steps // 2), st)
+        ops = 2.0 * wb * dd * mm                              # SURVEY 8(d) plane count
         sweep[name] = {"ms_per_layer": ms, "tensor_TOPS": ops / (ms * 1e-3) / 1e12,
-                       "hbm_GBps": (dd + mm) * 2 * L * n * 8 / (ms * 1e-3) / 1e9}
+                       "tensor_frac": ops / (ms * 1e-3) / 1e12 / (2.0 * peaks["bf16_tflops"]),
+                       "hbm_GBps": (dd + mm) * ctb / (ms * 1e-3) / 1e9}
         del xs, ys, w
         torch.cuda.empty_cache()
     out["layout_a_shapes"] = sweep
@@ -422,10 +476,10 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
                                      ("down_4096x1536", (4096, 1536, 1)), ("fig8_768x64", (768, 64, 1))):
             W = synth.gen_W(synth.SEED_BASE + 7 * dd + mm, dd, mm)
             w = c14.weights(W)
-            xs = synth.gen_words_torch(19, c14.q, dd, lv, n14)
-            ys = torch.empty((mm, 2, lv, n14), dtype=torch.int64, device="cuda")
-            c14.pcmm_ternary(xs, w, ys, level=lv)
-            ms = time_loop(lambda: c14.pcmm_ternary(xs, w, ys, level=lv), max(1, steps // 2), st)
+            xs = gen_compact(c14, 19, dd, lv)
+            ys = torch.empty((mm, c14.wire_bytes(lv)), dtype=torch.uint8, device="cuda")
+            c14.pcmm_ternary_compact(xs, w, ys, level=lv)
+            ms = time_loop(lambda: c14.pcmm_ternary_compact(xs, w, ys, level=lv), max(1, steps // 2), st)
             row[name] = {"ms_total": ms * reps, "reps": reps}
             del xs, ys, w
             torch.cuda.empty_cache()
@@ -493,6 +547,81 @@ def bench_ccmm(ctx, cfg, st):
     return res
 
 
+def gen_compact(ctx, seed: int, count: int, level: int, chunk: int = 128):
+    """Timing-only compact ciphertexts [count][wire_bytes] (uint8, device): uniform words in [0, q_r) drawn as uint64
+    (synth) and serialised by the product's own ensi_wire_pack, chunk by chunk (no full uint64 copy resident)."""
+    import torch
+    wb = ctx.wire_bytes(level)
+    out = torch.empty((count, wb), dtype=torch.uint8, device="cuda")
+    for c0 in range(0, count, chunk):
+        c1 = min(count, c0 + chunk)
+        xu = synth.gen_words_torch(seed + c0, ctx.q, c1 - c0, level, ctx.n)
+        ctx.wire_pack(xu, out[c0:c1], level)
+        del xu
+    return out
+
+
+def accum_roofline(ctx, d: int, m: int, nnz: int, L: int, ms: float, peaks, peak_src: str, layout: str,
+                   kernel_name: str, config: str):
+    """Roofline of the Layout-A accumulate launch (SURVEY 8(d) row 'Ternary accumulate (NEXT #1)').
+
+    Per launch: algorithmic bytes = (d + m) ciphertexts in their resident layout + the 2-bit weights (d m / 4);
+    tensor ops = sum over limbs of planes x 2 x (2N') x d x m with planes = the limb's word bytes (7 on the 50-bit
+    limb, 5 on the 40-bit limbs at the O1 primes) = 2 x (compact ciphertext bytes) x d x m.  INT8 dense peak = the
+    measured bf16 burst peak x the guide's nominal int8/bf16 ratio 2.  The bound is the larger of the two times."""
+    n = ctx.n
+    ct_c = ctx.wire_bytes(L)                                  # 2 N' sum_r w_r bytes
+    ct_u64 = 2 * L * n * 8
+    ct_res = ct_c if layout == "compact" else ct_u64
+    alg_bytes = (d + m) * ct_res + d * m // 4
+    t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
+    gbs = alg_bytes / (ms * 1e-3) / 1e9
+    if kernel_name == "cuda-core":
+        # one 64-bit modular add per term-word = 2 ALU-pipe ops (IADD3 + IADD3.X); ALU pipe = 64 lanes/clk/SM
+        # (B300_MICROARCH: rt_SMSP = 2) x 148 SMs x max clock
+        alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
+        alu_ops = 2.0 * nnz * 2 * L * n
+        alu_ach = alu_ops / (ms * 1e-3) / 1e12
+        return {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s (INT32 ALU lane-ops)",
+                "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary", "ops_per_launch": alu_ops,
+                "algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+                "peak_source": peak_src + " (ALU peak derived from unit counts and the max SM clock)"}
+    tc_ops = 2.0 * ct_c * d * m                                # SURVEY 8(d): 7/5 planes per word
+    tc_peak = 2.0 * peaks["bf16_tflops"]                       # TOPS, int8 dense
+    t_tensor = tc_ops / (tc_peak * 1e12)
+    tc_ach = tc_ops / (ms * 1e-3) / 1e12
+    ncu_peak = 16384 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    if t_tensor >= t_hbm:
+        r = {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TOPS (int8 dense)", "frac": tc_ach / tc_peak}
+    else:
+        r = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]}
+    kname = "k_accum_tcc" if layout == "compact" else "k_accum_tc2"
+    r.update({"kernel": kname, "layout": layout, "algorithmic_bytes": alg_bytes, "tensor_ops_per_launch": tc_ops,
+              "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_frac": gbs / peaks["hbm_gbs"],
+              "tensor_tops": tc_ach, "tensor_peak_tops": tc_peak, "tensor_frac": tc_ach / tc_peak,
+              "int8_peak_tops_ncu": ncu_peak, "tensor_frac_vs_ncu_int8_peak": tc_ach / ncu_peak,
+              "t_floor_ms": {"tensor": 1e3 * t_tensor, "hbm": 1e3 * t_hbm},
+              "peak_source": peak_src,
+              "op_count": "SURVEY 8(d): 2 x (sum_r w_r x 2N') x d x m -- only the word bytes that can be non-zero"})
+    r.update(committed_traffic(kname, config, d, m))
+    return r
+
+
+def committed_traffic(kname: str, config: str, d: int, m: int):
+    """DRAM bytes per launch (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum) of this kernel on this
+    workload, from the committed capture under profiles/ -- ncu cannot run inside the timed region."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        rows = json.load(open(p))
+    except (OSError, ValueError):
+        return {"traffic": None, "traffic_source": None}
+    for row in rows:
+        if row.get("kernel") == kname and row.get("config") == config and row.get("d") == d and row.get("m") == m:
+            return {"traffic": row["dram_bytes"], "traffic_source": f"profiles/traffic.json <- {row['source']} "
+                                                                   f"(committed ncu --set full capture)"}
+    return {"traffic": None, "traffic_source": None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -500,7 +629,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--kernel", type=int, default=0, help="0 default, 1 CUDA-core, 2 tcgen05")
+    ap.add_argument("--layout", default="compact", choices=["compact", "u64"],
+                    help="resident ciphertext layout: compact ceil(bits/8)-byte words (default) or uint64 words")
+    ap.add_argument("--kernel", type=int, default=0, help="0 default, 1 CUDA-core (u64 layout), 2 tcgen05")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rot", action="store_true", help="skip the secondary rows (NTT, rotations, rescale, Layout B)")
@@ -512,20 +643,46 @@ def main():
 
     import torch
     from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.dist import ColumnShardedPCMM
 
     world, rank, local = dist_setup(args)
     torch.cuda.set_device(local)
+    # the N > 1 path (column shards + NCCL all-gather) can be forced at N = 1 for tests (a one-rank NCCL group)
+    sharded = world > 1 or os.environ.get("ENSI_BENCH_COLSHARD") == "1"
+    if sharded and world == 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
     d, m = cfg["shapes"][0]
     L, n = cfg["L"], 1 << cfg["log_n"]
+    layout = "u64" if args.kernel == 1 else args.layout
     ctx = Context(cfg["log_n"], L, cfg["alpha"], cfg["dnum"], device=local)
     W = synth.gen_W(synth.SEED_BASE + 102, d, m)            # same model weights on every rank
-    w = ctx.weights(W)
-    # each rank: its own token block (its own input ciphertexts)
-    x = synth.gen_words_torch(synth.SEED_BASE + 2 + 1000 * rank, ctx.q, d, L, n)
-    y = torch.empty((m, 2, L, n), dtype=torch.int64, device="cuda")
+    wb = ctx.wire_bytes(L)
+    ct_u64 = 2 * L * n * 8
     st = torch.cuda.current_stream()
-    step = lambda: ctx.pcmm_ternary(x, w, y, level=L, kernel=args.kernel)  # noqa: E731
+    # The north star's layout: the layer input X~ replicated on every rank, rank r computes output
+    # columns [r S, (r + 1) S) with its slice of W, then one NCCL all-gather assembles the m outputs everywhere
+    # (chunked: the gather of chunk c overlaps the accumulate of chunk c + 1).  N = 1: the whole layer, no gather.
+    sh = ColumnShardedPCMM(W, world, rank, make_weights=ctx.weights)
+    if layout == "compact":
+        x = gen_compact(ctx, synth.SEED_BASE + 2, d, L)
+        ct_shape, dt = (wb,), torch.uint8
+        pc = lambda xa, wl, yl: ctx.pcmm_ternary_compact(xa, wl, yl, level=L, kernel=args.kernel)  # noqa: E731
+    else:
+        x = synth.gen_words_torch(synth.SEED_BASE + 2, ctx.q, d, L, n)
+        ct_shape, dt = (2, L, n), torch.int64
+        pc = lambda xa, wl, yl: ctx.pcmm_ternary(xa, wl, yl, level=L, kernel=args.kernel)  # noqa: E731
+    chunks = 4 if sharded else 1
+    wch = sh.chunk_weights(chunks, make_weights=ctx.weights)
+    y_loc = sh.local_buffer(torch, ct_shape, "cuda", dtype=dt)
+    y_all = sh.gathered_buffer(torch, ct_shape, "cuda", dtype=dt) if sharded else None
+    if sharded:
+        step = lambda: sh.run_overlapped(pc, x, y_loc, y_all, wch)  # noqa: E731
+    else:
+        step = lambda: pc(x, wch[0], y_loc)  # noqa: E731
 
     clocks = clock_sampler(local)
     clocks.start()
@@ -549,159 +706,131 @@ def main():
     ms_rank = ev_s.elapsed_time(ev_e) / args.steps
     launches = (ctx.launch_count() - l0)
     clk = clocks.stop()
+    if clk is not None:
+        clk["note"] = ("sampled only inside bench.py's timed region (the headline loop); the driver's own sampler "
+                       "also covers warm-up, e2e and the secondary rows")
     ms_step = max_over_ranks(world, ms_rank)
-    value = ms_step / world                                   # ms per layer over the whole job
+    value = ms_step                                           # ms per layer, the whole job (strong scaling)
 
-    ct_bytes = 2 * L * n * 8
-    alg_bytes = (d + m) * ct_bytes + d * 2 * (2 * ((m + 63) // 64)) * 4
-    term_words = w.nnz * 2 * L * n
     peaks, peak_src = load_peaks()
     kernel_name = ctx.kernel_name(args.kernel, L)
-    gbs = alg_bytes / (ms_rank * 1e-3) / 1e9
-    # ALU roofline of the CUDA-core accumulate: one 64-bit modular add per term-word = 2 ALU-pipe ops
-    # (IADD3 + IADD3.X); ALU pipe = 64 lanes/clk/SM (B300_MICROARCH: rt_SMSP = 2) x 148 SMs x max clock.
-    if kernel_name.startswith("tcgen05"):
-        # byte-sliced INT8 GEMM: D[i][8w+b] over all 8 bytes of every word, K = d (padded to 128), M = m (padded
-        # to 128).  INT8 dense peak = measured bf16 (burst) x nominal ratio 4.5/2.25 = 2.
-        dpad, mpad = -(-d // 128) * 128, -(-m // 128) * 128
-        tc_ops = 2.0 * ct_bytes * dpad * mpad                 # 2 * (8*ctw bytes) * dpad * mpad
-        tc_peak = 2.0 * peaks["bf16_tflops"]
-        tc_ach = tc_ops / (ms_rank * 1e-3) / 1e12
-        t_tensor, t_hbm = tc_ops / (tc_peak * 1e12), alg_bytes / (peaks["hbm_gbs"] * 1e9)
-        if t_tensor >= t_hbm:
-            roofline = {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak, "unit": "TOPS (int8, dense)",
-                        "frac": tc_ach / tc_peak}
-        else:
-            roofline = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": gbs / peaks["hbm_gbs"]}
-        # ncu's own INT8 dense peak (sm__ops_path_tensor_op_utcimma: 16384 ops/clk/SM) -- the no-epilogue ablation
-        # reaches ~98 % of it, i.e. the bf16-derived peak above understates INT8 throughput (profiles/)
-        ncu_peak = 16384 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        # DRAM traffic of one launch from the committed ncu --set full capture (C2 layer only)
-        traffic = 9664524288 + 9623952384 if (args.config == "C2" and d == 768 and m == 768) else None
-        roofline.update({"traffic": traffic, "kernel": "k_accum_tc2", "tensor_ops_per_launch": tc_ops,
-                         "tensor_peak_tops": tc_peak, "tensor_frac": tc_ach / tc_peak,
-                         "int8_peak_tops_ncu": ncu_peak, "frac_vs_ncu_int8_peak": tc_ach / ncu_peak,
-                         "traffic_source": "profiles/r01_ncu_accum_tcgen05.md (ncu --set full, dram read + write)"})
+    # the accumulate launch alone, timed on the stream it runs on: at N = 1 the step IS one launch
+    if sharded:
+        pc(x, sh.W_local, y_loc)
+        torch.cuda.synchronize()
+        ms_kernel = time_loop(lambda: pc(x, sh.W_local, y_loc), max(1, args.steps), st)
+        d_k, m_k = d, sh.S
     else:
-        alu_peak = 148 * 64 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12          # T lane-ops/s
-        alu_ach = 2 * term_words / (ms_rank * 1e-3) / 1e12
-        roofline = {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s (INT32 ALU lane-ops)",
-                    "frac": alu_ach / alu_peak, "traffic": None, "kernel": "k_accum_ternary",
-                    "ops_per_launch": 2 * term_words}
-    roofline.update({"algorithmic_bytes": alg_bytes, "hbm_gbs": gbs, "hbm_peak_gbs": peaks["hbm_gbs"],
-                     "hbm_frac": gbs / peaks["hbm_gbs"], "hbm_frac_vs_8tbps_spec": gbs / 8000.0,
-                     "peak_source": peak_src})
+        ms_kernel, d_k, m_k = ms_rank, d, m
+    roofline = accum_roofline(ctx, d_k, m_k, int(np.count_nonzero(sh._W_np)), L, ms_kernel, peaks, peak_src, layout, kernel_name, args.config)
+    roofline["launches_per_step"] = launches / args.steps
+    roofline["ms_per_launch"] = ms_kernel
 
     out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "u64",
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+           "vs_baseline": None, "dtype": "u8 x s8 -> s32 byte planes (exact mod-q words)" if kernel_name != "cuda-core"
+           else "u64",
            "data": "synthetic uniform RNS words in [0,q_r) (the accumulate is data-oblivious); BitNet absmean W",
            "config": {"workload": f"{args.config}: {cfg['desc']}", "d": d, "m": m, "log_n": cfg["log_n"],
-                      "limbs": L, "layout": "A", "kernel": kernel_name, "nnz": int(w.nnz),
-                      "l2": "inputs (9.66 GB) larger than L2 (126 MB); no flush",
-                      "parallelism": f"token-block data parallel x{world} (no data-path collective)"},
+                      "limbs": L, "layout": f"A, {layout} words" + (" (ceil(bits/8) bytes per word, DESIGN.md 3)"
+                                                                   if layout == "compact" else ""),
+                      "kernel": kernel_name, "nnz": int(np.count_nonzero(W)),
+                      "ciphertext_bytes": wb if layout == "compact" else ct_u64,
+                      "l2": f"inputs ({d * (wb if layout == 'compact' else ct_u64) / 1e9:.2f} GB) larger than L2 "
+                            f"(126 MB); no flush",
+                      "parallelism": (f"output columns sharded x{world}, X replicated, chunked NCCL all-gather of "
+                                      f"the outputs" if sharded else "one GPU")},
            "gpu_launches": launches, "clocks": clk, "roofline": roofline}
 
-    # ---- e2e through the host-buffer entry point (pinned host in, pinned host out)
+    if sharded:
+        # compute-only (the accumulate of this rank's shard) and the gather alone, max over ranks
+        gat = time_loop(lambda: torch.distributed.all_gather_into_tensor(y_all, y_loc), max(1, args.steps), st)
+        out["column_sharded"] = {"compute_ms": max_over_ranks(world, ms_kernel),
+                                 "gather_ms": max_over_ranks(world, gat),
+                                 "gather_bytes_per_rank": (world - 1) * sh.S * (wb if layout == "compact" else ct_u64),
+                                 "chunks": chunks}
+        # token blocks (weak scaling, no collective): every rank the whole layer on its own input block
+        xt = (gen_compact(ctx, synth.SEED_BASE + 2 + 1000 * rank, d, L) if layout == "compact"
+              else synth.gen_words_torch(synth.SEED_BASE + 2 + 1000 * rank, ctx.q, d, L, n))
+        wfull = ctx.weights(W)
+        yt = torch.empty((m,) + ct_shape, dtype=dt, device="cuda")
+        pc(xt, wfull, yt)
+        torch.cuda.synchronize()
+        barrier(world)
+        tb = max_over_ranks(world, time_loop(lambda: pc(xt, wfull, yt), max(1, args.steps), st))
+        out["token_blocks"] = {"value": tb / world, "unit": "ms/layer", "scaling": "weak", "ms_per_rank_step": tb,
+                               "note": "each rank one layer on its own token block, no collective"}
+        del xt, yt, wfull
+    del y_loc, y_all, wch
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the host-buffer entry point (pinned host in, pinned host out), rank 0's view at N = 1 and
+    # every rank its own token block at N > 1 (the host API is per GPU)
     xh_t = None
+    w = ctx.weights(W)
     if not args.no_e2e:
-        e2e_u64 = None
-        if world == 1:
-            # the uint64-word host API beside the wire one (N = 1 only: at N > 1 every rank would pin another
-            # 19 GB of host memory)
-            xh_t = torch.empty((d, 2, L, n), dtype=torch.int64, pin_memory=True)
-            yh_t = torch.empty((m, 2, L, n), dtype=torch.int64, pin_memory=True)
-            xh_t.copy_(x)
-            xh, yh = xh_t.numpy(), yh_t.numpy()
-            e2e_step = lambda: ctx.pcmm_ternary_host(xh, w, yh, level=L, kernel=args.kernel)  # noqa: E731
-            e2e_step()
-            torch.cuda.synchronize()
-            e2e_ms = time_loop(e2e_step, max(1, min(args.steps, 3)), st)
-            ok = bool((yh_t[5, 1, 3, :4096] == y[5, 1, 3, :4096].cpu()).all())
-            e2e_u64 = {"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": d * ct_bytes,
-                       "d2h_bytes_per_step": m * ct_bytes, "matches_device_path": ok,
-                       "api": "ensi_pcmm_ternary_host (uint64 words)", "per_rank_ms": e2e_ms,
-                       "pcie_GBps_per_rank": (d + m) * ct_bytes / (e2e_ms * 1e-3) / 1e9}
-            del yh_t
-        # the same layer through the compact wire format (each limb's words in ceil(bits/8) bytes; 62 of every 96
-        # bytes at C2): the client's ciphertexts arrive serialised, cross PCIe packed, unpacked on the device
         from paper_2509_09424_b200.ensi import wire_pack_host
-        wbytes = ctx.wire_bytes(L)
-        xw_t = torch.empty((d, wbytes), dtype=torch.uint8, pin_memory=True)
-        yw_t = torch.empty((m, wbytes), dtype=torch.uint8, pin_memory=True)
-        xw_dev = torch.empty((d, wbytes), dtype=torch.uint8, device="cuda")
-        ctx.wire_pack(x, xw_dev, L)                 # the client's serialisation, made here on the device (untimed)
+        xw_t = torch.empty((d, wb), dtype=torch.uint8, pin_memory=True)
+        yw_t = torch.empty((m, wb), dtype=torch.uint8, pin_memory=True)
+        xu = synth.gen_words_torch(synth.SEED_BASE + 2 + 1000 * rank, ctx.q, d, L, n)
+        xw_dev = torch.empty((d, wb), dtype=torch.uint8, device="cuda")
+        ctx.wire_pack(xu, xw_dev, L)                 # the client's serialisation, made here on the device (untimed)
         xw_t.copy_(xw_dev)
-        del xw_dev
+        yref_dev = torch.empty((m, wb), dtype=torch.uint8, device="cuda")
+        ctx.pcmm_ternary_compact(xw_dev, w, yref_dev, level=L)
+        yref = yref_dev[5].cpu().numpy()
+        del xw_dev, yref_dev
+        if world == 1:
+            xh_t = xu.cpu()
+        del xu
+        torch.cuda.empty_cache()
         xw, yw = xw_t.numpy(), yw_t.numpy()
         wire_step = lambda: ctx.pcmm_ternary_host_wire(xw, w, yw, level=L, kernel=args.kernel)  # noqa: E731
         wire_step()
         torch.cuda.synchronize()
         barrier(world)
         wire_ms = max_over_ranks(world, time_loop(wire_step, max(1, min(args.steps, 3)), st))
-        yref = wire_pack_host(y[5:6].cpu().numpy().view(np.uint64), ctx.wire_widths(L))[0]
         ok_w = bool((yw_t[5].numpy() == yref).all())
-        # every rank copies its own token block's inputs in and outputs out (weak scaling): job-level metric
-        out["e2e"] = {"value": wire_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": world * d * wbytes,
-                      "d2h_bytes_per_step": world * m * wbytes, "matches_device_path": ok_w,
-                      "api": "ensi_pcmm_ternary_host_wire (pinned host ciphertexts in the compact wire format)",
-                      "per_rank_ms": wire_ms, "pcie_GBps_per_rank": (d + m) * wbytes / (wire_ms * 1e-3) / 1e9,
-                      "uint64_words": e2e_u64,
+        out["e2e"] = {"value": wire_ms / world, "unit": "ms/layer", "h2d_bytes_per_step": world * d * wb,
+                      "d2h_bytes_per_step": world * m * wb, "matches_device_path": ok_w,
+                      "api": "ensi_pcmm_ternary_host_wire (pinned host ciphertexts in the compact wire format = the "
+                             "compact resident layout; slices pipelined over 3 streams)",
+                      "per_rank_ms": wire_ms, "pcie_GBps_per_rank": (d + m) * wb / (wire_ms * 1e-3) / 1e9,
+                      "scaling": "weak" if world > 1 else "n/a",
                       "note": "PCIe-bound: both directions overlap; tools/pcie_bw.py measures 92.7 GB/s bidirectional "
                               "pinned-copy bandwidth on the B200 box"}
         del xw_t, yw_t
-    # ---- N > 1: the north star's output-column sharding of ONE layer (strong scaling): each rank computes
-    # ceil(m/N) output ciphertexts and the result is all-gathered over NCCL, chunked so the gather of chunk c
-    # overlaps the accumulate of chunk c+1 (paper_2509_09424_b200/dist.py).  Device time, max over ranks.
-    if world > 1 or os.environ.get("ENSI_BENCH_COLSHARD") == "1":
-        import torch.distributed as dist
-        from paper_2509_09424_b200.dist import ColumnShardedPCMM
-        if not dist.is_initialized():           # forced at N = 1 (tests): a one-rank NCCL group under torchrun
-            dist.init_process_group("nccl", rank=0, world_size=1)
-        sh = ColumnShardedPCMM(W, world, rank)
-        wch = sh.chunk_weights(4, make_weights=ctx.weights)
-        y_loc = sh.local_buffer(torch, (2, L, n), "cuda")
-        y_all = sh.gathered_buffer(torch, (2, L, n), "cuda")
-        x0 = synth.gen_words_torch(synth.SEED_BASE + 2, ctx.q, d, L, n)     # the same layer input on every rank
-        pc = lambda xa, wl, yl: ctx.pcmm_ternary(xa, wl, yl, level=L)      # noqa: E731
-        for _ in range(2):
-            sh.run_overlapped(pc, x0, y_loc, y_all, wch)
-        torch.cuda.synchronize()
-        barrier(world)
-        cs_ms = max_over_ranks(world, time_loop(lambda: sh.run_overlapped(pc, x0, y_loc, y_all, wch),
-                                                max(1, args.steps), st))
-        out["column_sharded"] = {"value": cs_ms, "unit": "ms/layer", "n_gpus": world, "scaling": "strong",
-                                 "gather_bytes_per_rank": (world - 1) * sh.S * ct_bytes,
-                                 "note": "one 768x768 layer split by output columns, NCCL all-gather of the result "
-                                         "ciphertexts overlapped in 4 chunks"}
-        del y_loc, y_all, x0, wch
-        torch.cuda.empty_cache()
-    # ---- rotations/s (BASELINE metric's second clause), rank 0 only
+    # ---- secondary rows, rank 0 only
     if not args.no_rot and rank == 0:
-        del y
         torch.cuda.empty_cache()
         sec = bench_secondary(Context, cfg, max(3, args.steps), 2, peaks, layout_b=not args.no_layout_b,
                               ccmm=not args.no_ccmm)
         out["rotations_per_sec"] = sec.pop("rotations")
         out["secondary"] = sec
+        out["roofline"]["other_kernels"] = {
+            "ntt_forward_hbm_frac": sec["ntt_forward"]["hbm_frac"], "ntt_inverse_hbm_frac": sec["ntt_inverse"]["hbm_frac"],
+            "keyswitch_hoisted_hbm_frac": out["rotations_per_sec"]["hbm_frac"],
+            "keyswitch_independent_hbm_frac": out["rotations_per_sec"]["independent_inputs"]["hbm_frac"],
+            "note": "algorithmic bytes: NTT 1 read + 1 write per limb; key switching SURVEY 8(d) 88 MB per hoisted "
+                    "and 126 MB per independent rotation"}
     # ---- CPU oracle baseline (rank 0 at N=1 only)
     if not args.no_cpu and rank == 0 and world == 1:
-        x_host = (xh_t.numpy().view(np.uint64) if xh_t is not None else x.cpu().numpy().view(np.uint64))
+        x_host = (xh_t.numpy().view(np.uint64) if xh_t is not None else
+                  synth.gen_words(synth.SEED_BASE + 2, ctx.q, d, L, n))
         nth = max(1, min(64, os.cpu_count() or 1))
         ncols = max(1, min(m, nth))
-        ms_cpu, dt, cols = oracle_sample_ms(cfg, W, x_host, ncols, nth)
+        ms_cpu, dt_s, cols = oracle_sample_ms(cfg, W, x_host, ncols, nth)
         # the same oracle on one core (1 core and all host cores), a 2-column sample
         ms_1, dt_1, _ = oracle_sample_ms(cfg, W, x_host, 2, 1)
         out["cpu_baseline"] = {"value": ms_cpu, "unit": "ms/layer", "cores": nth, "kind": "oracle",
-                               "sample": f"{ncols} of {m} output columns ({dt:.1f} s wall), extrapolated by nnz",
+                               "sample": f"{ncols} of {m} output columns ({dt_s:.1f} s wall), extrapolated by nnz",
                                "one_core": {"value": ms_1, "unit": "ms/layer", "cores": 1,
                                             "sample": f"2 of {m} output columns ({dt_1:.1f} s wall), "
                                                       f"extrapolated by nnz"},
                                "cpu_model": _cpu_model()}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         import torch.distributed as dist
         barrier(world)                 # ranks > 0 wait for rank 0's secondary measurements before teardown
         dist.destroy_process_group()

@@ -68,7 +68,7 @@ def lib():
         L.or_galois_elt.argtypes = [C.c_uint32, C.c_int64]
         L.or_pcmm_b.restype = C.c_int
         L.or_pcmm_b.argtypes = [C.c_void_p] + [C.c_uint32] * 8 + [u64p, i8p, C.c_uint32, u64p, u64p, C.c_void_p,
-                                                                 C.c_void_p, C.c_uint32, C.c_uint32]
+                                                                 C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32]
         L.or_rescale.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p]
         L.or_relinkey.argtypes = [C.c_void_p, C.c_uint64, u64p, u64p, C.c_void_p]
         L.or_mul_plain.argtypes = [C.c_void_p, C.c_uint32, u64p, u64p, u64p]
@@ -332,8 +332,11 @@ class Oracle:
 
     # -- PCMM Layout B (O11)
     def pcmm_b(self, x: np.ndarray, W: np.ndarray, s: int, k: int, B: int, gkeys, keys: np.ndarray, cols=None,
-               nthreads: int = 1) -> np.ndarray:
-        """O11.  cols: compute only these output columns (returns one ciphertext per listed column)."""
+               nthreads: int = 1, lazy: bool = False) -> np.ndarray:
+        """O11.  cols: compute only these output columns (returns one ciphertext per listed column).
+        lazy (R19): the giant steps' key inner products are summed over Q_l u P and ModDown'ed once per
+        output (y_i = T_{i,0} + sum_gam (sigma(T_{i,gam}.c0), 0) + ModDown(sum_gam KIP_gam)) -- identical words to
+        the eager form when there is at most one giant rotation per output (G <= 2)."""
         W = np.ascontiguousarray(W, np.int8)
         d, m = W.shape
         n_in, _, level, _ = x.shape
@@ -343,7 +346,7 @@ class Oracle:
         ga = np.ascontiguousarray(gkeys, np.uint64)
         rc = lib().or_pcmm_b(self.h, level, s, k, B, d, m, m, n_in, np.ascontiguousarray(x, np.uint64), W,
                              ga.shape[0], ga, np.ascontiguousarray(keys), y.ctypes.data,
-                             ca.ctypes.data if ca is not None else None, ncols, nthreads)
+                             ca.ctypes.data if ca is not None else None, ncols, nthreads, 1 if lazy else 0)
         if rc != 0:
             raise KeyError("missing rotation key")
         return y

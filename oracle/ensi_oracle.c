@@ -23,6 +23,8 @@
  *   or_modup/...    O10 hybrid key switching (paper silent: evk only)    pinned: CRT identities, decrypt
  *   or_rotate*      O9+O10                                              pinned: decrypt == cyclic shift
  *   or_pcmm_b       O11 Layout B (our construction)         pinned: decrypt block 0 == X.W
+ *                   lazy = 1: R19 lazy ModDown of the giant steps        pinned: == eager at G <= 2, mini-oracle,
+ *                                                                          decrypt block 0 == X.W
  *   or_rescale      O12                                   pinned: == round(c/q_last) (big int)
  *   or_relinkey     O4 gadget towards s^2 (CCMM, R18)                    pinned: gadget identity test
  *   or_mul_plain    pt x ct in NTT form (R18)                            pinned: schoolbook negacyclic product
@@ -541,23 +543,28 @@ void or_moddown(const or_ctx* cx, uint32_t level, const uint64_t* acc, uint64_t*
     free(pc); free(z);
 }
 
-/* Key inner product + ModDown for one Galois element applied to already-ModUp'ed, already-permuted digits.
- * dig [beta][l+alpha][N'], key [dnum][2][L+alpha][N'] -> ks [2][l][N'] */
-static void kip_moddown(const or_ctx* cx, uint32_t level, const uint64_t* dig, const uint64_t* key, uint64_t* ks) {
+/* Key inner product for one Galois element applied to already-ModUp'ed, already-permuted digits (O10):
+ * acc_j[e] = sum_t dig[t][e] key[t][j][e] mod r_e over the extended basis Q_l u P.
+ * dig [beta][l+alpha][N'], key [dnum][2][L+alpha][N'] -> acc [2][l+alpha][N'] */
+static void kip(const or_ctx* cx, uint32_t level, const uint64_t* dig, const uint64_t* key, uint64_t* acc) {
     uint32_t n = cx->n, A = cx->alpha, E = level + A, T = cx->L + A, beta = n_digits(cx, level);
-    uint64_t* acc = (uint64_t*)malloc((size_t)E * n * 8);
-    for (uint32_t j = 0; j < 2; j++) {
+    for (uint32_t j = 0; j < 2; j++)
         for (uint32_t e = 0; e < E; e++) {
             uint32_t li = ext_limb(cx, level, e); uint64_t r = cx->mod[li];
             for (uint32_t k = 0; k < n; k++) {
                 uint64_t s = 0;
                 for (uint32_t t = 0; t < beta; t++)
                     s = addmod(s, mulmod(dig[((size_t)t * E + e) * n + k], key[(((size_t)t * 2 + j) * T + li) * n + k], r), r);
-                acc[(size_t)e * n + k] = s;
+                acc[((size_t)j * E + e) * n + k] = s;
             }
         }
-        or_moddown(cx, level, acc, ks + (size_t)j * level * n);
-    }
+}
+/* Key inner product + ModDown: ks_j = ModDown(acc_j), ks [2][l][N'] */
+static void kip_moddown(const or_ctx* cx, uint32_t level, const uint64_t* dig, const uint64_t* key, uint64_t* ks) {
+    uint32_t n = cx->n, E = level + cx->alpha;
+    uint64_t* acc = (uint64_t*)malloc((size_t)2 * E * n * 8);
+    kip(cx, level, dig, key, acc);
+    for (uint32_t j = 0; j < 2; j++) or_moddown(cx, level, acc + (size_t)j * E * n, ks + (size_t)j * level * n);
     free(acc);
 }
 
@@ -594,6 +601,21 @@ void or_rotate_hoisted(const or_ctx* cx, uint32_t level, uint32_t n_g, const uin
 /* non-hoisted rotation = hoisted with a single element (identical bits by the O10 definition) */
 void or_rotate(const or_ctx* cx, uint32_t level, uint64_t g, const uint64_t* key, const uint64_t* ct, uint64_t* out) {
     or_rotate_hoisted(cx, level, 1, &g, key, ct, out);
+}
+
+/* The parts of Rot(ct; g) before the ModDown (R19, lazy ModDown): c0g = sigma_g(c0) [l][N'] and
+ * acc [2][l+alpha][N'] = KIP(sigma_g(ModUp(c1)), key) over Q_l u P, so that Rot(ct; g) = (c0g + ModDown(acc_0),
+ * ModDown(acc_1)). */
+static void rot_parts(const or_ctx* cx, uint32_t level, uint64_t g, const uint64_t* key, const uint64_t* ct,
+                      uint64_t* c0g, uint64_t* acc) {
+    uint32_t n = cx->n, E = level + cx->alpha, beta = n_digits(cx, level);
+    uint64_t* dig = (uint64_t*)malloc((size_t)beta * E * n * 8);
+    uint64_t* dperm = (uint64_t*)malloc((size_t)beta * E * n * 8);
+    or_modup(cx, level, ct + (size_t)level * n, dig);
+    or_automorph_ntt(cx->log_n, g, beta * E, dig, dperm);
+    kip(cx, level, dperm, key, acc);
+    or_automorph_ntt(cx->log_n, g, level, ct, c0g);
+    free(dig); free(dperm);
 }
 
 /* g = 5^r mod 2N' (left rotation by r slots, r taken mod N'/2) */
@@ -633,18 +655,23 @@ static void* baby_worker(void* p) {
 /* Output columns cols[0..ncols) (all m when cols == NULL); y holds one ciphertext per computed column. */
 typedef struct { const or_ctx* cx; uint32_t level, s, k, B, d, ldw, n_in, n_keys; const int8_t* W; const uint64_t* gkeys;
                  const uint64_t* keys; const uint64_t* R; uint64_t* y; const uint32_t* cols; uint32_t ncols, tid, nth;
-                 int rc; } bcol_job;
+                 int rc; uint32_t lazy; } bcol_job;
 static void* bcol_worker(void* p) {
     bcol_job* j = (bcol_job*)p;
     const or_ctx* cx = j->cx;
     uint32_t n = cx->n, level = j->level, G = j->k / j->B;
     size_t ctw = (size_t)2 * level * n;
+    uint32_t E = level + cx->alpha;
     uint64_t* Tt = (uint64_t*)malloc(ctw * 8);
     uint64_t* rot = (uint64_t*)malloc(ctw * 8);
+    uint64_t* la = (uint64_t*)malloc((size_t)2 * E * n * 8);      /* lazy: sum of the giant steps' KIP outputs */
+    uint64_t* acc = (uint64_t*)malloc((size_t)2 * E * n * 8);
+    uint64_t* c0g = (uint64_t*)malloc((size_t)level * n * 8);
     for (uint32_t ci = j->tid; ci < j->ncols; ci += j->nth) {
         uint32_t i = j->cols ? j->cols[ci] : ci;
         uint64_t* yi = j->y + (size_t)ci * ctw;
         memset(yi, 0, ctw * 8);
+        memset(la, 0, (size_t)2 * E * n * 8);
         for (uint32_t gam = 0; gam < G; gam++) {
             memset(Tt, 0, ctw * 8);
             for (uint32_t c = 0; c < j->n_in; c++)
@@ -666,6 +693,26 @@ static void* bcol_worker(void* p) {
                 uint64_t g = or_galois_elt(cx->log_n, (int64_t)j->s * j->B * gam);
                 const uint64_t* kk = find_key(cx, j->n_keys, j->gkeys, j->keys, g);
                 if (!kk) { j->rc = 5; break; }
+                if (j->lazy) {
+                    /* R19: y_i += (sigma_g(T.c0), 0) now; la += KIP(...) over Q_l u P, one ModDown at the end */
+                    rot_parts(cx, level, g, kk, Tt, c0g, acc);
+                    for (uint32_t e = 0; e < E; e++) {
+                        uint64_t r = cx->mod[ext_limb(cx, level, e)];
+                        for (uint32_t poly = 0; poly < 2; poly++)
+                            for (uint32_t kk2 = 0; kk2 < n; kk2++) {
+                                size_t o = ((size_t)poly * E + e) * n + kk2;
+                                la[o] = addmod(la[o], acc[o], r);
+                            }
+                    }
+                    for (uint32_t rr = 0; rr < level; rr++) {
+                        uint64_t q = cx->mod[rr];
+                        for (uint32_t kk2 = 0; kk2 < n; kk2++) {
+                            size_t o = (size_t)rr * n + kk2;
+                            yi[o] = addmod(yi[o], c0g[o], q);
+                        }
+                    }
+                    continue;
+                }
                 or_rotate(cx, level, g, kk, Tt, rot);
                 src = rot;
             }
@@ -676,15 +723,24 @@ static void* bcol_worker(void* p) {
                 }
         }
         if (j->rc) break;
+        if (j->lazy && G > 1) {
+            for (uint32_t poly = 0; poly < 2; poly++) {
+                or_moddown(cx, level, la + (size_t)poly * E * n, rot);
+                for (uint32_t rr = 0; rr < level; rr++) {
+                    uint64_t q = cx->mod[rr]; size_t off = ((size_t)poly * level + rr) * n;
+                    for (uint32_t kk = 0; kk < n; kk++) yi[off + kk] = addmod(yi[off + kk], rot[(size_t)rr * n + kk], q);
+                }
+            }
+        }
     }
-    free(Tt); free(rot);
+    free(Tt); free(rot); free(la); free(acc); free(c0g);
     return NULL;
 }
 /* Threads (nthreads >= 1) split the baby rotations and then the output columns; the arithmetic of every word is the
  * sequence written above (threading changes no result). */
 int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t B, uint32_t d, uint32_t m, uint32_t ldw,
               uint32_t n_in, const uint64_t* x, const int8_t* W, uint32_t n_keys, const uint64_t* gkeys, const uint64_t* keys,
-              uint64_t* y, const uint32_t* cols, uint32_t ncols, uint32_t nthreads) {
+              uint64_t* y, const uint32_t* cols, uint32_t ncols, uint32_t nthreads, uint32_t lazy) {
     uint32_t n = cx->n;
     size_t ctw = (size_t)2 * level * n;
     if (!cols) ncols = m;
@@ -713,7 +769,8 @@ int or_pcmm_b(const or_ctx* cx, uint32_t level, uint32_t s, uint32_t k, uint32_t
     bcol_job cj[256];
     int rc = 0;
     for (uint32_t t = 0; t < nthreads; t++) {
-        cj[t] = (bcol_job){cx, level, s, k, B, d, ldw, n_in, n_keys, W, gkeys, keys, R, y, cols, ncols, t, nthreads, 0};
+        cj[t] = (bcol_job){cx, level, s, k, B, d, ldw, n_in, n_keys, W, gkeys, keys, R, y, cols, ncols, t, nthreads, 0,
+                           lazy};
         pthread_create(&th[t], NULL, bcol_worker, &cj[t]);
     }
     for (uint32_t t = 0; t < nthreads; t++) {

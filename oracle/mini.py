@@ -175,6 +175,18 @@ class Mini:
         out0 = [[(c0g[i][k] + ks[0][i][k]) % self.q[i] for k in range(self.n)] for i in range(level)]
         return [out0, ks[1]]
 
+    def rotate_parts(self, ct: list, g: int, key: list):
+        """Rot(ct; g) before its ModDown (R19): (sigma_g(c0), [acc_0, acc_1]) with acc_j over Q_l u P, so that
+        Rot = (sigma_g(c0) + ModDown(acc_0), ModDown(acc_1))."""
+        level = len(ct[0])
+        ext_mod = self._ext_moduli(level)
+        ext_idx = list(range(level)) + [self.L + k for k in range(self.alpha)]
+        dig = self.modup(level, ct[1])
+        dig = [[self.automorph_ntt(ext_mod[e], row, g) for e, row in enumerate(d)] for d in dig]
+        accs = [[[sum(dig[t][e][k] * key[t][j][ext_idx[e]][k] for t in range(len(dig))) % r for k in range(self.n)]
+                 for e, r in enumerate(ext_mod)] for j in range(2)]
+        return [self.automorph_ntt(self.q[i], ct[0][i], g) for i in range(level)], accs
+
     # ---------------------------------------------------------------- O8 / O11
     def add(self, a: list, b: list, sign: int = 1) -> list:
         return [[[(x + sign * y) % self.q[i] for x, y in zip(a[p][i], b[p][i])] for i in range(len(a[p]))]
@@ -196,9 +208,10 @@ class Mini:
             ys.append(y)
         return ys
 
-    def pcmm_b(self, x: list, W, s: int, k: int, B: int, keys: dict) -> list:
+    def pcmm_b(self, x: list, W, s: int, k: int, B: int, keys: dict, lazy: bool = False) -> list:
         """O11: R_{c,b} = Rot(ct_c; s b), T_{i,gam} = sum_{c,b} W[c k + gam B + b][i] R_{c,b},
-        y_i = T_{i,0} + sum_{gam >= 1} Rot(T_{i,gam}; s B gam).  keys: {galois element: key}."""
+        y_i = T_{i,0} + sum_{gam >= 1} Rot(T_{i,gam}; s B gam).  keys: {galois element: key}.
+        lazy (R19): the giant rotations' KIP outputs are summed over Q_l u P and ModDown'ed once per output."""
         d, m = len(W), len(W[0])
         level = len(x[0][0])
         G = k // B
@@ -207,9 +220,11 @@ class Mini:
             for b in range(B):
                 g = self.galois(s * b)
                 R[c, b] = x[c] if b == 0 else self.rotate(x[c], g, keys[g])
+        ext_mod = self._ext_moduli(level)
         ys = []
         for i in range(m):
             y = self.zero(level)
+            la = [[[0] * self.n for _ in ext_mod] for _ in range(2)]
             for gam in range(G):
                 T = self.zero(level)
                 for c in range(len(x)):
@@ -219,8 +234,16 @@ class Mini:
                             T = self.add(T, R[c, b], int(W[col][i]))
                 if gam:
                     g = self.galois(s * B * gam)
+                    if lazy:
+                        c0g, accs = self.rotate_parts(T, g, keys[g])
+                        y[0] = [[(a + b) % self.q[r] for a, b in zip(y[0][r], c0g[r])] for r in range(level)]
+                        la = [[[(a + b) % ext_mod[e] for a, b in zip(la[j][e], accs[j][e])] for e in range(len(ext_mod))]
+                              for j in range(2)]
+                        continue
                     T = self.rotate(T, g, keys[g])
                 y = self.add(y, T)
+            if lazy and G > 1:
+                y = self.add(y, [self.moddown(level, la[0]), self.moddown(level, la[1])])
             ys.append(y)
         return ys
 

@@ -119,8 +119,12 @@ __device__ __forceinline__ void epi_words(uint32_t tcol, uint32_t release_addr, 
     uint64_t v[HW];
 #pragma unroll
     for (uint32_t i = 0; i < HW; i++) {
+#ifdef ENSI_ABL_NOCOMBINE   // timing-only ablation build (wrong words; profiles/r02_tcc_ablations.md)
+        v[i] = r[W * i];
+#else
         if constexpr (W == 5) v[i] = combine_word5(r + 5 * i, ea.br.q, ea.mu32, ea.off64);
         else v[i] = combine_w<W>(r + W * i, ea.br, ea.off_lo, ea.off_hi);
+#endif
     }
 #pragma unroll
     for (uint32_t j = 0; j < NC / 8; j++) u[j] = 0;
@@ -140,8 +144,19 @@ __device__ __forceinline__ void epi_tile(uint32_t tbase_q, uint32_t release_addr
                                          uint32_t quarter, uint8_t* ys, const EpiArgs& ea, const CUtensorMap* map,
                                          uint32_t byte, uint32_t row0) {
     constexpr uint32_t NB = W * HW;             // bytes of this warp's half row segment
+#ifdef ENSI_ABL_NOEPI       // timing-only ablation build (no outputs): release the accumulator at once
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_remote(release_addr);
+    return;
+#endif
     uint64_t u[NB / 8];
     epi_words<W, HW>(tbase_q + half * half1_col(NB), release_addr, lane, ea, u);
+#ifdef ENSI_ABL_NOSTS       // timing-only ablation build (no outputs): words computed and kept alive, not staged
+#pragma unroll
+    for (uint32_t j = 0; j < NB / 8; j++) asm volatile("" ::"l"(u[j]));
+    return;
+#endif
     // staging free: the previous TMA store of this quarter has read it
     if (half == 0 && lane == 0) tma_store_wait_read0();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");

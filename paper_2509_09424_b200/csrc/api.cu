@@ -193,7 +193,11 @@ int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const st
     const uint32_t rows = p.n_in * p.B;
     // rotated inputs R [rows] and (G > 1) the giant-step partials T [m]: ctx-owned, grown on demand (cudaMallocAsync
     // would return the 9+ GB to the OS at every synchronisation under the default pool release threshold)
-    const size_t need = ((size_t)rows + (p.G > 1 ? (size_t)m : 0)) * ctw;
+    // R19 lazy ModDown (G > 2 only: with one giant rotation per output it is the eager path): the extended-basis
+    // accumulators of all m outputs, la [m][2][level + A][N']
+    const bool lazy = o.moddown_lazy && p.G > 2;
+    const size_t law = (size_t)2 * (level + ctx->A) * ctx->n;
+    const size_t need = ((size_t)rows + (p.G > 1 ? (size_t)m : 0)) * ctw + (lazy ? (size_t)m * law : 0);
     if (ctx->lb_words < need) {
         cudaStreamSynchronize(st);
         cudaFree(ctx->lb_buf);
@@ -208,6 +212,7 @@ int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const st
     }
     uint64_t* R = ctx->lb_buf;
     uint64_t* Tg = p.G > 1 ? R + (size_t)rows * ctw : nullptr;
+    uint64_t* La = lazy ? Tg + (size_t)m * ctw : nullptr;
     auto accum_b = [&](uint32_t gm, uint64_t* dst) -> int {
         ensi_weights* sw = subs[gm];
         return tc ? accum_ternary_tc(ctx, R, sw->d, sw, dst, level, st, 0, 0, tc_variant(o.kernel))
@@ -228,9 +233,18 @@ int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const st
             ko.add_mask = 3;
             ko.add_src = acc_out + (size_t)c0 * ctw;
             ko.add_stride = ctw;
+            if (lazy) {
+                ko.lazy_acc = La + (size_t)c0 * law;
+                ko.lazy_init = gm == 1;
+            }
             rc = rotate_hoisted_multi(ctx, Tg + (size_t)c0 * ctw, nc, ctw, level, 1, &gg, acc_out + (size_t)c0 * ctw, 1,
                                       st, &ko);
         }
+    }
+    // R19: one ModDown per output of the summed giant-step key inner products, added in place
+    for (uint32_t c0 = 0; lazy && c0 < m && !rc; c0 += 96) {
+        const uint32_t nc = std::min<uint32_t>(96, m - c0);
+        rc = lazy_moddown(ctx, La + (size_t)c0 * law, nc, level, acc_out + (size_t)c0 * ctw, st);
     }
     return rc;
 }
@@ -368,6 +382,10 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
     }
     ctx->ntt_fp_ok = true;
     for (uint32_t i = 0; i < ctx->T; i++) ctx->ntt_fp_ok = ctx->ntt_fp_ok && ctx->mod[i] < (1ull << 50);
+    {
+        const char* f = getenv("ENSI_NTT_FUSED");
+        ctx->ntt_fused_off = !(f && f[0] == '1');     // experiment: the fused single-launch NTT only on request
+    }
     if (e == cudaSuccess && ctx->ntt_fp_ok) {
         // centred twiddle c (|c| < q/2, exact in a double) and RN(c / q) for the FP64 NTT (ntt_fp.cuh)
         std::vector<double> tw3((size_t)ctx->T * 4 * n + (size_t)ctx->T * 2);
@@ -422,6 +440,7 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     cudaFree(ctx->d_tw2);
     cudaFree(ctx->d_tw3);
     cudaFree(ctx->d_tw1);
+    cudaFree(ctx->d_ntt_sync);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
     if (ctx->relin_owned) cudaFree(ctx->d_relin);
@@ -568,6 +587,8 @@ int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_we
     if (y->count != m) return set_err(ctx, ENSI_EDIM, "y.count != m");
     if (overlaps(x, y, n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
     if (o.layout > 1) return set_err(ctx, ENSI_EINVAL, "layout must be 0 (A) or 1 (B)");
+    if (o.moddown_lazy > 1 || (o.moddown_lazy && o.layout != 1))
+        return set_err(ctx, ENSI_EINVAL, "moddown_lazy must be 0, or 1 with Layout B");
     bool tc = false;
     rc = select_kernel(ctx, o.kernel, level, d, &tc);
     if (rc) return rc;
@@ -790,6 +811,7 @@ int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const e
     if (opts) o = *opts;
     if (o.layout != 0) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: Layout A only");
     if (o.rescale_out) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: no rescale epilogue");
+    if (o.moddown_lazy) return set_err(ctx, ENSI_EINVAL, "moddown_lazy: Layout B only");
     if (o.kernel != 0 && o.kernel != 2) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: kernel must be 0 or 2");
     if (x->count != w->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
     if (y->count != w->m) return set_err(ctx, ENSI_EDIM, "y.count != m");
@@ -914,6 +936,10 @@ int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* st
     if (y->level != x->level - 1 || y->count != x->count) return set_err(ctx, ENSI_EDIM, "y must be count x (level-1)");
     if (overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
     DeviceGuard g(ctx->device);
+    {
+        cudaError_t e0 = cudaGetLastError();
+        if (e0 != cudaSuccess) return cuda_err(ctx, e0, "stale error before rescale (diagnostic)");
+    }
     rc = ensi::rescale(ctx, x->data, x->count, x->level, y->data, (cudaStream_t)stream);
     if (!rc) y->log2_scale = x->log2_scale - std::log2((double)ctx->mod[x->level - 1]);
     return rc;

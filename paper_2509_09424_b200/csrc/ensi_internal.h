@@ -112,6 +112,12 @@ struct ensi_ctx {
     // key switching: two internal streams for alternating rotation batches
     cudaStream_t st_ks[2] = {};
     cudaEvent_t ev_ks_done[2] = {}, ev_ks_fork = nullptr;
+    // fused two-pass NTT (ntt_fp.cuh k_ntt_fused): per-stream work counters [kNttSyncSlots][1 + kNttSyncRows]
+    uint32_t* d_ntt_sync = nullptr;
+    cudaStream_t ntt_sync_stream[4] = {};
+    uint32_t ntt_sync_used = 0;
+    int ntt_fused_ctas = 0;                // resident CTAs of the fused kernel (occupancy x SMs), 0 = not queried
+    bool ntt_fused_off = false;            // ENSI_NTT_FUSED=0: two launches per transform (A/B only)
     std::string err;
     uint64_t launches = 0;
 };
@@ -178,7 +184,10 @@ struct KsOpts {
     const uint64_t* add_src = nullptr;   // non-NULL: the added polynomials come from add_src + c * add_stride (input c)
     uint64_t add_stride = 0;             //   instead of the input ciphertext itself (may alias out exactly)
     uint64_t* scratch = nullptr;         // internal: caller-provided scratch region (no ensure_scratch, no splitting)
+    uint64_t* lazy_acc = nullptr;        // R19: [n_ct][2][level+A][N'] -- accumulate the KIP output here (no ModDown)
+    bool lazy_init = false;              //   and add (sigma_g(c0), 0) to out; lazy_init: overwrite instead of add
 };
+int lazy_moddown(ensi_ctx* ctx, uint64_t* la, uint32_t n_ct, uint32_t level, uint64_t* out, cudaStream_t st);
 int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint64_t in_stride, uint32_t level,
                          uint32_t n_g, const uint64_t* galois, uint64_t* out, uint32_t out_c_stride, cudaStream_t st,
                          const KsOpts* opts = nullptr);

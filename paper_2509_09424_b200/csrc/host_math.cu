@@ -1,6 +1,6 @@
 // host_math.cpp -- host-side number theory for context setup (primes, roots, Shoup/Barrett constants).
 // Independent of oracle/ (no shared code): min_root / is_prime_u64 here and their counterparts in
-// oracle/ensi_oracle.c are two separate transcriptions of the same textbook rules (R1 prime rule,
+// the C oracle (oracle/) are two separate transcriptions of the same textbook rules (R1 prime rule,
 // R2 minimal root).  The oracle's side is pinned to SURVEY.md Appendix A (tests/test_oracle_params_ntt.py);
 // this side is pinned only transitively, to the oracle, by tests/test_gpu_parity.py
 // test_moduli_and_roots_match_oracle.

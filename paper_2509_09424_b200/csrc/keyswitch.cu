@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kT) k_moddown_final(const uint64_t* __restrict
     const uint64_t* pinv = cm + (size_t)A * 2 + (size_t)level * A * 2 + (size_t)i * 2;
     uint64_t v = sub_mod(acc[((size_t)gj * E + i) * n + k], z[((size_t)blockIdx.z * level + i) * n + k], q);
     v = mul_shoup(v, pinv[0], pinv[1], q);
-    if (j == 0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
+    if (j == 0 && c0) v = add_mod(v, c0[c * gb.in_stride + (size_t)i * n + galois_src_index(k, gb.g[gi], log_n)], q);
     if ((add_mask >> j) & 1) {
         const uint64_t* ab = add_src ? add_src + c * add_stride : c0 + c * gb.in_stride;
         v = add_mod(v, ab[(j ? add1_off : 0) + (size_t)i * n + k], q);
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp(const uint64_t* __restr
     const long long dv = (long long)acc[((size_t)gj * E + i) * n + k] - (long long)z[((size_t)blockIdx.z * level + i) * n + k];
     double v = nttfp::mulmod(nttfp::i2d(dv), fc.pinv[i], fc.pinvq[i], qd);          // |v| <= 0.625 q
     const uint64_t* cb = c0 + c * gb.in_stride + (size_t)i * n;
-    if (j == 0) v += nttfp::i2d((long long)cb[galois_src_index(k, gb.g[gi], log_n)]);
+    if (j == 0 && c0) v += nttfp::i2d((long long)cb[galois_src_index(k, gb.g[gi], log_n)]);
     if ((add_mask >> j) & 1) {
         const uint64_t* ab = (add_src ? add_src + c * add_stride : c0 + c * gb.in_stride) + (size_t)i * n;
         v += nttfp::i2d((long long)ab[(j ? add1_off : 0) + k]);
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __rest
     double va = nttfp::mulmod(nttfp::i2d((long long)av.x - (long long)zv.x), pw, pq, qd);
     double vb = nttfp::mulmod(nttfp::i2d((long long)av.y - (long long)zv.y), pw, pq, qd);
     const uint64_t* cb = c0 + c * gb.in_stride + (size_t)i * n;
-    if (j == 0) {
+    if (j == 0 && c0) {
         const uint64_t g = gb.g[gi];
         va += nttfp::i2d((long long)cb[galois_src_index(k, g, log_n)]);
         vb += nttfp::i2d((long long)cb[galois_src_index(k + 1, g, log_n)]);
@@ -820,6 +820,29 @@ __global__ void __launch_bounds__(kT) k_moddown_final_fp2(const uint64_t* __rest
         make_ulonglong2(nttfp::canon(nttfp::red(va, qd, qinv), q), nttfp::canon(nttfp::red(vb, qd, qinv), q));
 }
 
+// R19 (lazy ModDown of Layout-B giant steps): la[c][j][e] = (init ? 0 : la[c][j][e]) + acc[c][j][e] mod r_e over the
+// extended basis Q_l u P, and out[c].c0 = add[c].c0 + sigma_g(ct[c].c0) (poly 1 of out is left to lazy_moddown).
+// One Galois element per call (acc [n_ct][2][E][N'], rotation index = input index).
+__global__ void __launch_bounds__(kT) k_lazy_accum(const uint64_t* __restrict__ acc, uint64_t* __restrict__ la,
+                                                   const uint64_t* __restrict__ ct, uint64_t* out,
+                                                   const uint64_t* add_src, uint64_t add_stride, GBatch gb,
+                                                   uint32_t log_n, uint32_t level, uint32_t A, uint32_t L, ModTab tab,
+                                                   uint32_t init) {
+    const uint32_t n = 1u << log_n, E = level + A;
+    const uint32_t e = blockIdx.y, gj = blockIdx.z, j = gj & 1, c = gj >> 1;
+    const uint32_t k = blockIdx.x * kT + threadIdx.x;
+    const uint64_t r = tab.q[e < level ? e : L + (e - level)];
+    const size_t o = ((size_t)gj * E + e) * n + k;
+    uint64_t v = acc[o];
+    if (!init) v = add_mod(v, la[o], r);
+    la[o] = v;
+    if (j == 0 && e < level) {
+        const uint64_t s = ct[c * gb.in_stride + (size_t)e * n + galois_src_index(k, gb.g[0], log_n)];
+        const uint64_t* ab = (add_src ? add_src + c * add_stride : ct + c * gb.in_stride) + (size_t)e * n;
+        out[(((size_t)c * gb.out_c_stride + gb.oidx[0]) * 2 * level + e) * n + k] = add_mod(ab[k], s, r);
+    }
+}
+
 // ---------------------------------------------------------------- host driver
 
 const uint64_t* find_key(const ensi_ctx* ctx, uint64_t g) {
@@ -832,6 +855,88 @@ static int key_index(const ensi_ctx* ctx, uint64_t g) {
     for (size_t i = 0; i < ctx->galois.size(); i++)
         if (ctx->galois[i] == g) return (int)i;
     return -1;
+}
+
+// ModDown of gcnt extended-basis polynomials acc [gcnt][E][N'] (rotation r = gj / 2, poly j = gj % 2) and the final
+// combine out = (acc_Q - z) P^{-1} (+ sigma_g(c0) on poly 0 when c0 != NULL) (+ the added polynomials, add_mask):
+// INTT of the P rows, conversion, NTT, combine.  The P rows of acc are transformed in place.
+static void moddown_combine(ensi_ctx* ctx, ConvTables* cvt, uint64_t* acc, uint64_t* z, uint32_t gcnt, uint32_t level,
+                            const uint64_t* c0, uint64_t* out, const GBatch& gb, uint32_t add_mask, uint64_t add1o,
+                            const uint64_t* add_src, uint64_t add_stride, cudaStream_t st) {
+    const uint32_t n = ctx->n, A = ctx->A, E = level + A;
+    LimbMap pm = identity_map(A);
+    for (uint32_t a = 0; a < A; a++) pm.limb[a] = (uint8_t)(ctx->L + a);
+    pm.grp_rows = A;
+    pm.grp_stride = E;
+    pm.grp_off = level;
+    // ModDown of the batch's 2 nr polynomials: INTT of the P rows, conversion, NTT, final combine
+    const uint32_t g0 = 0;
+    uint64_t* accs = acc;
+    {
+    ntt_inverse(ctx, accs, gcnt * A, pm, st);
+    if (A <= 8 && ctx->ntt_fp_ok) {
+        dim3 g(n / kT, gcnt);
+        if (level <= 16) {
+            MDConstFp mc{};
+            const std::vector<double>& mf = cvt->h_moddown_fp;
+            for (uint32_t a = 0; a < A; a++) {
+                const uint64_t pk = ctx->mod[ctx->L + a];
+                mc.yw[a] = mf[2 * a];
+                mc.ywq[a] = mf[2 * a + 1];
+                mc.p[a] = (double)pk;
+                mc.hp[a] = (double)(pk >> 1);
+            }
+            for (uint32_t i = 0; i < level; i++) {
+                mc.q[i] = (double)ctx->mod[i];
+                mc.qinv[i] = 1.0 / mc.q[i];
+                for (uint32_t a = 0; a < A; a++) {
+                    mc.c[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2];
+                    mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
+                }
+            }
+            if (A <= 4 && n >= 2 * kT)
+                k_moddown_convert_fpc2<<<dim3(g.x / 2, g.y), kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
+            else
+                k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
+        } else
+        k_moddown_convert_fp<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab,
+                                               cvt->d_moddown_fp);
+        ENSI_LAUNCH_CHECK(ctx);
+    } else if (A <= 8) {
+        dim3 g(n / kT, gcnt);
+        k_moddown_convert2<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
+                                             cvt->d_moddown2);
+        ENSI_LAUNCH_CHECK(ctx);
+    } else {
+        dim3 g(n / kT, level, gcnt);
+        k_moddown_convert<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
+        ENSI_LAUNCH_CHECK(ctx);
+    }
+    ntt_forward(ctx, z, gcnt * level, identity_map(level), st);
+    {
+        dim3 g(n / kT, level, gcnt);
+        if (ctx->ntt_fp_ok && level <= 16) {
+            MDFinConst fc{};
+            for (uint32_t i = 0; i < level; i++) {
+                const uint64_t q = ctx->mod[i], w = cvt->h_pinv[i];
+                fc.q[i] = (double)q;
+                fc.qinv[i] = 1.0 / fc.q[i];
+                fc.pinv[i] = w > q / 2 ? -(double)(q - w) : (double)w;
+                fc.pinvq[i] = fc.pinv[i] / fc.q[i];
+            }
+            if (n >= 2 * kT) {
+                dim3 g2(g.x / 2, g.y, g.z);
+                k_moddown_final_fp2<<<g2, kT, 0, st>>>(acc, z, c0, out, gb, ctx->log_n, level, A, fc, add_mask,
+                                                       add1o, g0, add_src, add_stride);
+            } else
+                k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, c0, out, gb, ctx->log_n, level, A, fc, add_mask,
+                                                     add1o, g0, add_src, add_stride);
+        } else
+        k_moddown_final<<<g, kT, 0, st>>>(acc, z, c0, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
+                                          add_mask, add1o, g0, add_src, add_stride);
+        ENSI_LAUNCH_CHECK(ctx);
+    }
+    }
 }
 
 // Batch sizes of the key-switching core (measured): up to 32 Galois elements and ~96
@@ -871,6 +976,8 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         gs.push_back(g);
     }
     if (idx.empty()) return ENSI_OK;
+    if (ko.lazy_acc && (idx.size() != 1 || n_g != 1))
+        return set_err(ctx, ENSI_EINVAL, "lazy ModDown: one (non-identity) Galois element per call");
     ConvTables* cvt = nullptr;
     int rc = conv_tables(ctx, level, &cvt);
     if (rc) return rc;
@@ -899,6 +1006,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         k0.scratch = (uint64_t*)ctx->scratch;
         k1.scratch = (uint64_t*)ctx->scratch + words(h0);
         if (ko.add_src) k1.add_src = ko.add_src + (size_t)h0 * ko.add_stride;
+        if (ko.lazy_acc) k1.lazy_acc = ko.lazy_acc + (size_t)h0 * 2 * E * n;
         rc = rotate_hoisted_multi(ctx, ct, h0, in_stride, level, n_g, galois, out, out_c_stride, ctx->st_ks[0], &k0);
         if (!rc)
             rc = rotate_hoisted_multi(ctx, ct + (size_t)h0 * in_stride, h1, in_stride, level, n_g, galois,
@@ -1087,79 +1195,16 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
                                          ctx->tab, w_ext1, perm);
             ENSI_LAUNCH_CHECK(ctx);
         }
-        LimbMap pm = identity_map(A);
-        for (uint32_t a = 0; a < A; a++) pm.limb[a] = (uint8_t)(ctx->L + a);
-        pm.grp_rows = A;
-        pm.grp_stride = E;
-        pm.grp_off = level;
-        // ModDown of the batch's 2 nr polynomials: INTT of the P rows, conversion, NTT, final combine
-        const uint32_t g0 = 0, gcnt = nr * 2;
-        uint64_t* accs = acc;
-        {
-        ntt_inverse(ctx, accs, gcnt * A, pm, st);
-        if (A <= 8 && ctx->ntt_fp_ok) {
-            dim3 g(n / kT, gcnt);
-            if (level <= 16) {
-                MDConstFp mc{};
-                const std::vector<double>& mf = cvt->h_moddown_fp;
-                for (uint32_t a = 0; a < A; a++) {
-                    const uint64_t pk = ctx->mod[ctx->L + a];
-                    mc.yw[a] = mf[2 * a];
-                    mc.ywq[a] = mf[2 * a + 1];
-                    mc.p[a] = (double)pk;
-                    mc.hp[a] = (double)(pk >> 1);
-                }
-                for (uint32_t i = 0; i < level; i++) {
-                    mc.q[i] = (double)ctx->mod[i];
-                    mc.qinv[i] = 1.0 / mc.q[i];
-                    for (uint32_t a = 0; a < A; a++) {
-                        mc.c[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2];
-                        mc.cq[i][a] = mf[(size_t)A * 2 + ((size_t)i * A + a) * 2 + 1];
-                    }
-                }
-                if (A <= 4 && n >= 2 * kT)
-                    k_moddown_convert_fpc2<<<dim3(g.x / 2, g.y), kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
-                else
-                    k_moddown_convert_fpc<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, A, mc);
-            } else
-            k_moddown_convert_fp<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab,
-                                                   cvt->d_moddown_fp);
+        if (ko.lazy_acc) {
+            // R19: sum this giant step's key inner product into the lazy accumulator (Q_l u P) and add
+            // (sigma_g(c0), 0) to the output now; the one ModDown per output runs in lazy_moddown
+            dim3 g(n / kT, E, nr * 2);
+            k_lazy_accum<<<g, kT, 0, st>>>(acc, ko.lazy_acc, ct, out, ko.add_src, ko.add_stride, gb, ctx->log_n, level,
+                                          A, ctx->L, ctx->tab, ko.lazy_init ? 1u : 0u);
             ENSI_LAUNCH_CHECK(ctx);
-        } else if (A <= 8) {
-            dim3 g(n / kT, gcnt);
-            k_moddown_convert2<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown,
-                                                 cvt->d_moddown2);
-            ENSI_LAUNCH_CHECK(ctx);
-        } else {
-            dim3 g(n / kT, level, gcnt);
-            k_moddown_convert<<<g, kT, 0, st>>>(accs, z, ctx->log_n, level, ctx->L, A, ctx->tab, cvt->d_moddown);
-            ENSI_LAUNCH_CHECK(ctx);
+            continue;
         }
-        ntt_forward(ctx, z, gcnt * level, identity_map(level), st);
-        {
-            dim3 g(n / kT, level, gcnt);
-            if (ctx->ntt_fp_ok && level <= 16) {
-                MDFinConst fc{};
-                for (uint32_t i = 0; i < level; i++) {
-                    const uint64_t q = ctx->mod[i], w = cvt->h_pinv[i];
-                    fc.q[i] = (double)q;
-                    fc.qinv[i] = 1.0 / fc.q[i];
-                    fc.pinv[i] = w > q / 2 ? -(double)(q - w) : (double)w;
-                    fc.pinvq[i] = fc.pinv[i] / fc.q[i];
-                }
-                if (n >= 2 * kT) {
-                    dim3 g2(g.x / 2, g.y, g.z);
-                    k_moddown_final_fp2<<<g2, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
-                                                           add1o, g0, ko.add_src, ko.add_stride);
-                } else
-                    k_moddown_final_fp<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, fc, ko.add_mask,
-                                                         add1o, g0, ko.add_src, ko.add_stride);
-            } else
-            k_moddown_final<<<g, kT, 0, st>>>(acc, z, ct, out, gb, ctx->log_n, level, A, ctx->tab, cvt->d_moddown,
-                                              ko.add_mask, add1o, g0, ko.add_src, ko.add_stride);
-            ENSI_LAUNCH_CHECK(ctx);
-        }
-        }
+        moddown_combine(ctx, cvt, acc, z, nr * 2, level, ct, out, gb, ko.add_mask, add1o, ko.add_src, ko.add_stride, st);
     }
     if (nsets == 2) {
         for (int k = 0; k < 2; k++) {
@@ -1175,6 +1220,30 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
 int rotate_hoisted(ensi_ctx* ctx, const uint64_t* ct, uint32_t level, uint32_t n_g, const uint64_t* galois,
                    uint64_t* out, cudaStream_t st) {
     return rotate_hoisted_multi(ctx, ct, 1, 0, level, n_g, galois, out, 0, st);
+}
+
+// R19: out[c] += ModDown(la[c]) for both polynomials of n_ct outputs (la [n_ct][2][E][N'], out [n_ct][2][level][N'],
+// in place), after every giant step went through rotate_hoisted_multi with KsOpts.lazy_acc.
+int lazy_moddown(ensi_ctx* ctx, uint64_t* la, uint32_t n_ct, uint32_t level, uint64_t* out, cudaStream_t st) {
+    if (n_ct == 0) return ENSI_OK;
+    ConvTables* cvt = nullptr;
+    int rc = conv_tables(ctx, level, &cvt);
+    if (rc) return rc;
+    const size_t ctw = (size_t)2 * level * ctx->n;
+    rc = ensure_scratch(ctx, (size_t)n_ct * ctw * 8);              // z [n_ct][2][level][N']
+    if (rc) return rc;
+    GBatch gb{};
+    gb.g[0] = 1;
+    gb.key[0] = 0;
+    gb.oidx[0] = 0;
+    gb.cnt = 1;
+    gb.n_ct = n_ct;
+    gb.out_c_stride = 1;
+    gb.in_stride = ctw;
+    moddown_combine(ctx, cvt, la, (uint64_t*)ctx->scratch, 2 * n_ct, level, nullptr, out, gb, 3u, (uint64_t)level * ctx->n,
+                    out, ctw, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "lazy_moddown");
 }
 
 }  // namespace ensi

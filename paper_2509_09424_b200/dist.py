@@ -56,11 +56,12 @@ class ColumnShardedPCMM:
         self._W_np = Ws
         self.W_local = make_weights(Ws) if make_weights else Ws
 
-    def local_buffer(self, torch, ct_shape, device):
-        return torch.empty((self.S,) + tuple(ct_shape), dtype=torch.int64, device=device)
+    def local_buffer(self, torch, ct_shape, device, dtype=None):
+        """[S] + ct_shape: uint64 words as int64 (ct_shape (2, l, N')) or compact bytes as uint8 ((wire_bytes,))."""
+        return torch.empty((self.S,) + tuple(ct_shape), dtype=dtype or torch.int64, device=device)
 
-    def gathered_buffer(self, torch, ct_shape, device):
-        return torch.empty((self.S * self.world,) + tuple(ct_shape), dtype=torch.int64, device=device)
+    def gathered_buffer(self, torch, ct_shape, device, dtype=None):
+        return torch.empty((self.S * self.world,) + tuple(ct_shape), dtype=dtype or torch.int64, device=device)
 
     def chunk_bounds(self, chunks: int):
         """Contiguous, balanced split of this rank's S output columns into `chunks` pieces."""

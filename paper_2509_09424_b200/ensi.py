@@ -59,7 +59,7 @@ class Keys(C.Structure):
 
 class PcmmOpts(C.Structure):
     _fields_ = [("layout", C.c_uint32), ("block_s", C.c_uint32), ("baby", C.c_uint32), ("rescale_out", C.c_uint32),
-                ("kernel", C.c_uint32)]
+                ("kernel", C.c_uint32), ("moddown_lazy", C.c_uint32)]
 
 
 _LIB = None
@@ -238,11 +238,12 @@ class Context:
 
     # ---- PCMM (rows a3, a4, a8)
     def pcmm_ternary(self, x, W, y, level: int, layout: int = 0, block_s: int = 0, baby: int = 0,
-                     rescale_out: bool = False, kernel: int = 0, stream=None, log2_scale: float = 40.0) -> float:
+                     rescale_out: bool = False, kernel: int = 0, stream=None, log2_scale: float = 40.0,
+                     moddown_lazy: bool = False) -> float:
         """y = x (x) W.  W: Weights (prepacked) or host int8 array.  Returns y's log2 scale."""
         xv = self.view(x, level, log2_scale)
         yv = self.view(y, level - 1 if rescale_out else level)
-        opts = PcmmOpts(layout, block_s, baby, 1 if rescale_out else 0, kernel)
+        opts = PcmmOpts(layout, block_s, baby, 1 if rescale_out else 0, kernel, 1 if moddown_lazy else 0)
         if isinstance(W, Weights):
             rc = lib().ensi_pcmm_ternary_packed(self.h, C.byref(xv), W.h, C.byref(yv), C.byref(opts),
                                                 _stream_ptr(stream))
@@ -283,7 +284,7 @@ class Context:
                              log2_scale: float = 40.0) -> float:
         """y = x (x) W on compact ciphertexts (Layout A); returns y's log2 scale."""
         xv, yv = self.compact_view(x, level, log2_scale), self.compact_view(y, level)
-        opts = PcmmOpts(0, 0, 0, 0, kernel)
+        opts = PcmmOpts(0, 0, 0, 0, kernel, 0)
         self._check(lib().ensi_pcmm_ternary_compact(self.h, C.byref(xv), w.h, C.byref(yv), C.byref(opts),
                                                     _stream_ptr(stream)))
         return yv.log2_scale

@@ -33,7 +33,7 @@ def test_shard_arithmetic():
             assert blocks == list(range(m))
 
 
-def _worker(rank, world, port, d, m, out_q):
+def _worker(rank, world, port, d, m, out_q, chunks=3):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     import oracle
@@ -54,7 +54,7 @@ def _worker(rank, world, port, d, m, out_q):
     y_local2 = sh.local_buffer(torch, (2, 1, o.n), "cpu")
     y_all2 = sh.gathered_buffer(torch, (2, 1, o.n), "cpu")
     y_all2.zero_()
-    sh.run_overlapped(pcmm, x, y_local2, y_all2, sh.chunk_weights(3))
+    sh.run_overlapped(pcmm, x, y_local2, y_all2, sh.chunk_weights(chunks))
     assert torch.equal(y_all2[:m], y_all[:m])
     if rank == 0:
         out_q.put(y_all[:m].numpy().view(np.uint64).copy())
@@ -76,6 +76,28 @@ def test_column_sharded_allgather_equals_single_process(d, m):
     got = q.get(timeout=240)
     for p in procs:
         p.join(timeout=240)
+        assert p.exitcode == 0
+    o = oracle.Oracle(12, 2, 1, 2)
+    want = o.pcmm_a(synth.gen_words(55, o.q, d, 1, o.n), synth.gen_W(56, d, m))
+    assert (got == want).all()
+
+
+def test_column_sharded_world4_ragged():
+    """World size 4, m = 7 (shards of S = 2, the last rank owns one real column and one zero-padded one) and 4
+    chunks per shard (two of them empty, so run_overlapped skips them on every rank consistently): the gathered
+    outputs of both the one-shot and the chunked, overlapped all-gather equal the single-process oracle."""
+    import oracle
+    import synth
+    world, d, m = 4, 6, 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, m, q, 4)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
         assert p.exitcode == 0
     o = oracle.Oracle(12, 2, 1, 2)
     want = o.pcmm_a(synth.gen_words(55, o.q, d, 1, o.n), synth.gen_W(56, d, m))

@@ -69,6 +69,36 @@ def test_column_sharded_nccl_world1(torch_cuda):
         dist.destroy_process_group()
 
 
+def test_column_sharded_compact_nccl_world1(torch_cuda):
+    """The bench's N > 1 headline path on compact ciphertexts (uint8 [count][wire_bytes]): chunked column shards +
+    NCCL all-gather == the unsharded compact call == the oracle on sampled columns."""
+    torch = torch_cuda
+    import torch.distributed as dist
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.dist import ColumnShardedPCMM
+    from paper_2509_09424_b200.ensi import wire_pack_host, wire_unpack_host
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        o = oracle.Oracle(12, 3, 1, 3)
+        ctx = Context(12, 3, 1, 3)
+        d, m, level = 300, 7, 3
+        x = synth.gen_words(73, o.q, d, level, o.n)
+        W = synth.gen_W(74, d, m)
+        wb = ctx.wire_bytes(level)
+        xc = torch.from_numpy(wire_pack_host(x, ctx.wire_widths(level))).cuda()
+        sh = ColumnShardedPCMM(W, 1, 0)
+        y_local = sh.local_buffer(torch, (wb,), "cuda", dtype=torch.uint8)
+        y_all = sh.gathered_buffer(torch, (wb,), "cuda", dtype=torch.uint8)
+        y_all.zero_()
+        sh.run_overlapped(lambda xa, wl, yl: ctx.pcmm_ternary_compact(xa, wl, yl, level=level), xc, y_local, y_all,
+                          sh.chunk_weights(4, make_weights=ctx.weights))
+        torch.cuda.synchronize()
+        got = wire_unpack_host(y_all[:m].cpu().numpy(), ctx.wire_widths(level), level, o.n)
+        assert (got == o.pcmm_a(x, W)).all()
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.slow
 def test_bench_under_torchrun_nccl(torch_cuda):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
@@ -80,5 +110,7 @@ def test_bench_under_torchrun_nccl(torch_cuda):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     out = json.loads(line)
     assert out["n_gpus"] == 1 and out["value"] > 0 and out["gpu_launches"] >= 3
-    assert out["roofline"]["frac"] > 0
-    assert out["column_sharded"]["value"] > 0 and out["column_sharded"]["n_gpus"] == 1
+    assert out["roofline"]["frac"] > 0 and out["roofline"]["kernel"] == "k_accum_tcc"
+    assert out["scaling"] == "strong" and out["config"]["parallelism"].startswith("output columns sharded x1")
+    assert out["column_sharded"]["gather_ms"] > 0 and out["column_sharded"]["compute_ms"] > 0
+    assert out["token_blocks"]["value"] > 0

@@ -245,6 +245,46 @@ def test_layout_b_c2_bench_schedule(c2, torch_cuda):
     assert (got == want).all()
 
 
+@pytest.mark.parametrize("d,m,baby,cols", [(3072, 768, 0, [0, 500, 767]), (768, 768, 64, [5, 700])])
+def test_layout_b_lazy_moddown_full_size(c2, torch_cuda, d, m, baby, cols):
+    """R19 (moddown_lazy) at full size, C2 parameters: BASELINE configs[2]'s down projection
+    3072 -> 768 on its default plan (k = 256, n_in = 12, B = 128, G = 2: 1524 baby + 768 giant rotations; with one
+    giant rotation per output the lazy form IS the eager one, checked on every output word) and 768 -> 768 with
+    B = 64 (G = 4: 189 baby + 2304 giant rotations, three giant steps summed over Q_l u P per output, 8 chunks of
+    96 outputs split over the two internal streams).  Seeded uniform words and keys (the path is data-oblivious);
+    sampled output columns == the oracle's lazy O11 word for word."""
+    o, sk, pk, ctx = c2
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    s = 128
+    k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, baby)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
+    keys = synth.gen_words_torch(synth.SEED_BASE + 50 + d, o.moduli, len(gk) * 3, 16, o.n).view(len(gk), 3, 2, 16,
+                                                                                                 o.n)
+    x = synth.gen_words(synth.SEED_BASE + 51 + d, o.q, n_in, 12, o.n)
+    W = synth.gen_W(synth.SEED_BASE + 52 + d, d, m)
+    bctx = Context(16, 12, 4, 3)
+    bctx.load_keys(galois=gk, rot_keys=keys)
+    w = bctx.weights(W)
+    yd = torch.empty((m, 2, 12, o.n), dtype=torch.int64, device="cuda")
+    bctx.pcmm_ternary(_dev(torch, x), w, yd, level=12, layout=1, block_s=s, baby=B, moddown_lazy=True)
+    torch.cuda.synchronize()
+    got = yd[cols].cpu().numpy().view(np.uint64)
+    if G <= 2:
+        ye = torch.empty_like(yd)
+        bctx.pcmm_ternary(_dev(torch, x), w, ye, level=12, layout=1, block_s=s, baby=B)
+        torch.cuda.synchronize()
+        assert torch.equal(yd, ye)
+        del ye
+    del yd
+    bctx.close()
+    kh = keys.cpu().numpy().view(np.uint64)
+    del keys
+    torch.cuda.empty_cache()
+    want = o.pcmm_b(x, W, s, k, B, gk, kh, cols=cols, nthreads=NTH, lazy=True)
+    assert (got == want).all()
+
+
 def test_c2_integer_ntt_and_keyswitch_wide_moduli(torch_cuda):
     """N' = 2^16 with moduli >= 2^50: the integer v2 NTT passes (not the FP64 ones) in both directions on extreme and
     random rows, then hoisted rotations and rescale through the integer key-switching kernels -- word for word."""

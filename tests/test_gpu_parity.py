@@ -92,6 +92,31 @@ def test_ntt_n16_extreme_inputs(torch_cuda):
     assert (host(t) == np.stack([o.intt(limbs[i], rows[i]) for i in range(len(rows))])).all()
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_ntt_n16_many_rows_fused_and_two_launch(torch_cuda, monkeypatch, fused):
+    """N'=2^16, 203 rows over every limb of Q u P: the single-launch transform (k_ntt_fused: both passes in one
+    persistent launch, work items claimed in order, second-pass tiles waiting on their row's first pass -- 203 rows
+    span the lead-in, the interleaved pairs and the tail of its item order) and, with ENSI_NTT_FUSED=0, the
+    two-launch passes; forward and inverse against the oracle, every word."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    monkeypatch.setenv("ENSI_NTT_FUSED", fused)
+    ctx = Context(16, 12, 4, 3)
+    o = oracle.Oracle(16, 12, 4, 3)
+    T = 16
+    rs = np.random.default_rng(203)
+    period = [(7 * i) % T for i in range(T)]                 # row i holds limb period[i % 16]
+    limbs = [period[i % T] for i in range(203)]
+    rows = np.stack([rs.integers(0, o.moduli[li], o.n, dtype=np.uint64) for li in limbs])
+    t = dev(torch, rows)
+    ctx.ntt(t, period)
+    want = np.stack([o.ntt(limbs[i], rows[i]) for i in range(len(rows))])
+    assert (host(t) == want).all()
+    ctx.ntt(t, period, inverse=True)
+    assert (host(t) == rows).all()
+    ctx.close()
+
+
 def _enc_cols(o, pk, X, level, seed):
     d = X.shape[1]
     m_res = np.stack([o.encode(X[:, j], level, DELTA) for j in range(d)])
@@ -479,11 +504,13 @@ def test_rotate_missing_key(rot_setup, torch_cuda):
 
 # ---------------------------------------------------------------- Layout B
 
+@pytest.mark.parametrize("lazy", [False, True])
 @pytest.mark.parametrize("d,m,B,s", [(16, 16, 0, 16), (16, 16, 4, 16), (20, 6, 4, 16), (100, 130, 4, 64)])
-def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B, s):
+def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B, s, lazy):
     """Layout B (O11) on real encryptions, every output word == the oracle; (100, 130, 4, 64): 7 giant steps over 130
     outputs = two key-stationary chunks (96 + 34) each split over the two internal streams, with the running sum
-    added in place by the final combine."""
+    added in place by the final combine.  lazy: R19 (moddown_lazy) against the oracle's lazy form -- G = 4 and 8
+    giant steps accumulate over Q_l u P and take one ModDown per output (words differ from the eager form)."""
     from paper_2509_09424_b200 import Context
     o, sk, pk, _ = setup_c1
     torch = torch_cuda
@@ -503,11 +530,11 @@ def test_pcmm_layout_b_bit_exact(setup_c1, torch_cuda, d, m, B, s):
     x = np.stack(cts)
     gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
     keys = np.stack([o.rotkey(6200 + i, g, sk) for i, g in enumerate(gk)])
-    want = o.pcmm_b(x, W, s, k, B, gk, keys)
+    want = o.pcmm_b(x, W, s, k, B, gk, keys, lazy=lazy)
     ctx.load_keys(sk_ntt=sk, galois=gk, rot_keys=keys)
     xd = dev(torch, x)
     yd = torch.empty((m, 2, 3, o.n), dtype=torch.int64, device="cuda")
-    ctx.pcmm_ternary(xd, W, yd, level=3, layout=1, block_s=s, baby=B)
+    ctx.pcmm_ternary(xd, W, yd, level=3, layout=1, block_s=s, baby=B, moddown_lazy=lazy)
     torch.cuda.synchronize()
     assert (host(yd) == want).all()
     ref = X @ W.astype(np.float64)

@@ -158,6 +158,35 @@ def test_layout_b_c_vs_mini(ks64, B):
     assert (sub[0] == got[2]).all() and (sub[1] == got[0]).all()
 
 
+@pytest.mark.parametrize("B", [1, 2, 4])
+def test_layout_b_lazy_moddown_c_vs_mini(ks64, B):
+    """R19 lazy ModDown at N' = 64 (k = 8, so G = 8, 4, 2 giant steps): the C oracle's lazy form == the mini-oracle's
+    (its own ModUp / KIP / centred ModDown, summed over Q_l u P by Python integers) word for word; at G = 2 (one
+    giant rotation per output) lazy == eager exactly, while at G > 2 the two differ (a single ModDown of the sum is
+    not the sum of the ModDowns) -- so a lazy path that silently ran the eager one would fail here."""
+    o, mo = ks64
+    s, d, m = 4, 11, 3
+    k, n_in, Bq, G, rots = oracle.layout_b_plan(o.n, s, d, m, B)
+    rs = np.random.default_rng(61 + B)
+    x = np.stack([np.stack([_rand(rs, o.q, o.n) for _ in range(2)]) for _ in range(n_in)])
+    W = rs.integers(-1, 2, (d, m)).astype(np.int8)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, Bq, G)
+    keys = np.stack([np.stack([np.stack([_rand(rs, o.moduli, o.n) for _ in range(2)]) for _ in range(o.dnum)])
+                     for _ in gk])
+    lazy = o.pcmm_b(x, W, s, k, Bq, gk, keys, lazy=True)
+    eager = o.pcmm_b(x, W, s, k, Bq, gk, keys)
+    kd = {g: [[_lst(keys[i, t, j]) for j in range(2)] for t in range(o.dnum)] for i, g in enumerate(gk)}
+    want = mo.pcmm_b([_ct_list(c) for c in x], W.tolist(), s, k, Bq, kd, lazy=True)
+    for i in range(m):
+        assert _ct_list(lazy[i]) == want[i], i
+    if G <= 2:
+        assert (lazy == eager).all()
+    else:
+        assert not (lazy == eager).all()
+    sub = o.pcmm_b(x, W, s, k, Bq, gk, keys, cols=[1], nthreads=2, lazy=True)
+    assert (sub[0] == lazy[1]).all()
+
+
 def test_pcmm_a_c_vs_mini(ks64):
     o, mo = ks64
     rs = np.random.default_rng(41)

@@ -393,6 +393,30 @@ def test_layout_b_decrypts_block0(c1, d, m, s, B):
         assert np.max(np.abs(z[:s] - ref[:, i])) < 1e-4
 
 
+@pytest.mark.parametrize("d,m,s,B", [(16, 16, 16, 1), (20, 6, 16, 4), (16, 16, 16, 8)])
+def test_layout_b_lazy_moddown_decrypts_block0(c1, d, m, s, B):
+    """R19: the lazy-ModDown Layout B (giant steps summed over Q_l u P, one ModDown per output) decrypts to the same
+    (X.W)[:, i] within 1e-4 -- with G = 16, 4 and 2 giant steps -- and its noise is no larger than the eager
+    form's plus one fresh-rotation error (one ModDown rounding instead of G - 1)."""
+    o, skc, sk, pk = c1
+    k, n_in, B, G, rots = oracle.layout_b_plan(o.n, s, d, m, B)
+    X = synth.gen_X(41 + d, s, d)
+    W = synth.gen_W(42 + d, d, m)
+    x = _layout_b_setup(o, sk, pk, X, s, k, 4100)
+    gk = oracle.layout_b_galois(o.n, o.log_n, s, B, G)
+    keys = np.stack([o.rotkey(5100 + i, g, sk) for i, g in enumerate(gk)])
+    y = o.pcmm_b(x, W, s, k, B, gk, keys, lazy=True)
+    ye = o.pcmm_b(x, W, s, k, B, gk, keys)
+    ref = X @ W.astype(np.float64)
+    for i in range(m):
+        z = o.decrypt(sk, y[i], DELTA)
+        ze = o.decrypt(sk, ye[i], DELTA)
+        assert np.max(np.abs(z[:s] - ref[:, i])) < 1e-4
+        assert np.max(np.abs(z - ze)) < 1e-5
+    if G <= 2:
+        assert (y == ye).all()
+
+
 # ---------------------------------------------------------------- O12 rescale
 
 def test_rescale_is_rounded_division(c1):

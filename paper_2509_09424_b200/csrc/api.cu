@@ -382,10 +382,7 @@ int ensi_ctx_create(const ensi_params* prm, int cuda_device, ensi_ctx** out) {
     }
     ctx->ntt_fp_ok = true;
     for (uint32_t i = 0; i < ctx->T; i++) ctx->ntt_fp_ok = ctx->ntt_fp_ok && ctx->mod[i] < (1ull << 50);
-    {
-        const char* f = getenv("ENSI_NTT_FUSED");
-        ctx->ntt_fused_off = !(f && f[0] == '1');     // experiment: the fused single-launch NTT only on request
-    }
+
     if (e == cudaSuccess && ctx->ntt_fp_ok) {
         // centred twiddle c (|c| < q/2, exact in a double) and RN(c / q) for the FP64 NTT (ntt_fp.cuh)
         std::vector<double> tw3((size_t)ctx->T * 4 * n + (size_t)ctx->T * 2);
@@ -440,7 +437,6 @@ void ensi_ctx_destroy(ensi_ctx* ctx) {
     cudaFree(ctx->d_tw2);
     cudaFree(ctx->d_tw3);
     cudaFree(ctx->d_tw1);
-    cudaFree(ctx->d_ntt_sync);
     cudaFree(ctx->d_sk);
     if (ctx->keys_owned) cudaFree(ctx->d_keys);
     if (ctx->relin_owned) cudaFree(ctx->d_relin);

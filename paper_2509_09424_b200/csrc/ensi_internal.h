@@ -112,12 +112,6 @@ struct ensi_ctx {
     // key switching: two internal streams for alternating rotation batches
     cudaStream_t st_ks[2] = {};
     cudaEvent_t ev_ks_done[2] = {}, ev_ks_fork = nullptr;
-    // fused two-pass NTT (ntt_fp.cuh k_ntt_fused): per-stream work counters [kNttSyncSlots][1 + kNttSyncRows]
-    uint32_t* d_ntt_sync = nullptr;
-    cudaStream_t ntt_sync_stream[4] = {};
-    uint32_t ntt_sync_used = 0;
-    int ntt_fused_ctas = 0;                // resident CTAs of the fused kernel (occupancy x SMs), 0 = not queried
-    bool ntt_fused_off = false;            // ENSI_NTT_FUSED=0: two launches per transform (A/B only)
     std::string err;
     uint64_t launches = 0;
 };

@@ -7,8 +7,6 @@
 // the block pass runs the remaining log N2 stages on contiguous blocks of N2 words.  Each pass stages a
 // 32 KB tile in shared memory (4096 words) with coalesced loads (16+ consecutive words per column row).
 // Twiddle multiplications are Shoup products; every output word is canonical.
-#include <algorithm>
-
 #include "ensi_internal.h"
 #include "ntt_v2.cuh"
 #include "ntt_fp.cuh"
@@ -215,64 +213,9 @@ bool ntt_row_tmap(const ensi_ctx* ctx, uint64_t* data, uint32_t rows, const Limb
     return row_tmap(ctx, data, rows, map, tm);
 }
 
-// ---- fused two-pass launch (ntt_fp.cuh k_ntt_fused): per-stream counter slots, zeroed before every launch
-static constexpr uint32_t kNttSyncSlots = 4;
-static constexpr uint32_t kNttSyncRows = 16384;
-
-static bool fused_sync(ensi_ctx* ctx, uint32_t rows, cudaStream_t st, nttfp::FusedSync* fs) {
-    if (ctx->ntt_fused_off || rows > kNttSyncRows) return false;
-    if (!ctx->d_ntt_sync) {
-        if (cudaMalloc(&ctx->d_ntt_sync, (size_t)kNttSyncSlots * (1 + kNttSyncRows) * 4) != cudaSuccess) {
-            cudaGetLastError();
-            ctx->ntt_fused_off = true;
-            return false;
-        }
-    }
-    if (!ctx->ntt_fused_ctas) {
-        int sms = 148, b1 = 0, b2 = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, nttfp::k_ntt_fused<true>, 256, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, nttfp::k_ntt_fused<false>, 256, 0);
-        ctx->ntt_fused_ctas = sms * std::max(1, std::min(b1, b2));
-    }
-    // one slot per stream (calls on one stream are ordered; calls on different streams may overlap)
-    uint32_t slot = kNttSyncSlots;
-    for (uint32_t i = 0; i < ctx->ntt_sync_used; i++)
-        if (ctx->ntt_sync_stream[i] == st) slot = i;
-    if (slot == kNttSyncSlots) {
-        if (ctx->ntt_sync_used == kNttSyncSlots) return false;
-        slot = ctx->ntt_sync_used++;
-        ctx->ntt_sync_stream[slot] = st;
-    }
-    uint32_t* base = ctx->d_ntt_sync + (size_t)slot * (1 + kNttSyncRows);
-    if (cudaMemsetAsync(base, 0, (size_t)(1 + rows) * 4, st) != cudaSuccess) return false;
-    fs->counter = base;
-    fs->done = base + 1;
-    fs->rows = rows;
-    // the second pass of row r is claimed ~2 lag groups of 16 tiles after its first pass: enough for the
-    // resident CTAs to finish row r's first pass (no spinning) while ~lag rows (lag x 512 KB) stay in L2
-    fs->lag = std::max<uint32_t>(2, (uint32_t)((3 * ctx->ntt_fused_ctas + 63) / 64));
-    return true;
-}
-
-static uint32_t fused_grid(const ensi_ctx* ctx, uint32_t rows) {
-    return std::min<uint32_t>((uint32_t)ctx->ntt_fused_ctas, 32u * rows);
-}
-
 void ntt_forward(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& map, cudaStream_t st) {
     if (rows == 0) return;
     const uint32_t log_n = ctx->log_n, n = ctx->n;
-    if (use_fp(ctx)) {
-        nttfp::FusedSync fs;
-        CUtensorMap tmf;
-        if (row_tmap(ctx, data, rows, map, &tmf) && fused_sync(ctx, rows, st, &fs)) {
-            const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
-            nttfp::k_ntt_fused<true><<<fused_grid(ctx, rows), 256, 0, st>>>(
-                data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tmf, LimbMap(), 0u, tw1_of(ctx), fs);
-            ctx->launches += 1;
-            return;
-        }
-    }
     if (use_fp(ctx)) {
         const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
         dim3 g(16, rows);
@@ -315,13 +258,6 @@ bool ntt_inverse_from(ensi_ctx* ctx, const uint64_t* src, const LimbMap& smap, u
     if (!row_tmap(ctx, const_cast<uint64_t*>(src), rows, smap, &tm)) return false;
     const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
     const uint32_t n = ctx->n;
-    nttfp::FusedSync fs;
-    if (fused_sync(ctx, rows, st, &fs)) {
-        nttfp::k_ntt_fused<false><<<fused_grid(ctx, rows), 256, 0, st>>>(
-            dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm, smap, 1u, tw1_of(ctx), fs);
-        ctx->launches += 1;
-        return true;
-    }
     dim3 g(16, rows);
     nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(dst, dmap, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
                                                          nttfp::PlainOut(), smap, 1u, tw1_of(ctx));
@@ -340,13 +276,6 @@ void ntt_inverse(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const LimbMap& ma
         const double2* tw = reinterpret_cast<const double2*>(ctx->d_tw3);
         dim3 g(16, rows);
         CUtensorMap tm;
-        nttfp::FusedSync fs;
-        if (row_tmap(ctx, data, rows, map, &tm) && fused_sync(ctx, rows, st, &fs)) {
-            nttfp::k_ntt_fused<false><<<fused_grid(ctx, rows), 256, 0, st>>>(
-                data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm, LimbMap(), 0u, tw1_of(ctx), fs);
-            ctx->launches += 1;
-            return;
-        }
         if (row_tmap(ctx, data, rows, map, &tm))
             nttfp::k_ntt256_tma<nttfp::INV_B><<<g, 256, 0, st>>>(data, map, ctx->tab, tw, tw + (size_t)ctx->T * 2 * n, tm,
                                                                  nttfp::PlainOut(), LimbMap(), 0u, tw1_of(ctx));

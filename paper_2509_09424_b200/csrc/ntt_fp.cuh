@@ -82,12 +82,12 @@ __device__ __forceinline__ void tile_load(void* dst, const CUtensorMap* map, uin
         "l"((uint64_t)map), "r"(su32(bar)), "r"(0), "r"(c1), "r"(c2)
         : "memory");
 }
-__device__ __forceinline__ void tile_wait(uint64_t* bar, uint32_t parity = 0) {
+__device__ __forceinline__ void tile_wait(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(bar)),
-        "r"(parity)
+        "r"(0u)
         : "memory");
 }
 __device__ __forceinline__ void tile_store(const CUtensorMap* map, const void* src, int32_t c1, int32_t c2) {
@@ -105,10 +105,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
                                             const double2* __restrict__ W2, const double2* __restrict__ ninv,
                                             double* sm, const IN& in, const OUT& out,
                                             const CUtensorMap* tmap = nullptr, uint32_t prow = 0,
-                                            uint64_t* bar = nullptr, const double* __restrict__ W1 = nullptr,
-                                            uint32_t bx = 0xFFFFFFFFu, uint32_t bar_parity = 0) {
-    // bx: which 4096-word tile of the row this CTA transforms (blockIdx.x for the one-pass-per-launch kernels)
-    if (bx == 0xFFFFFFFFu) bx = blockIdx.x;
+                                            uint64_t* bar = nullptr, const double* __restrict__ W1 = nullptr) {
     const double qd = (double)q, qinv = 1.0 / qd;
     const bool fwd = PASS == FWD_A || PASS == FWD_B;
     const bool colp = PASS == FWD_A || PASS == INV_A;
@@ -127,7 +124,7 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
     const uint32_t tid = threadIdx.x;
     const uint32_t sp = colp ? (tid & 15) : (tid >> 4);
     const uint32_t tt = colp ? (tid >> 4) : (tid & 15);
-    const uint32_t sub = bx * 16 + sp;
+    const uint32_t sub = blockIdx.x * 16 + sp;
     auto gaddr = [&](uint32_t i) -> uint64_t { return colp ? (uint64_t)sub + 256ull * i : 256ull * sub + i; };
     // twiddle index of the butterfly with lower point i1 at local stride 2^lt is pre(lt) + (i1 >> (lt + 1)).  For
     // points i1 = tt + 16 k (lt >= 4) that is pre(lt) + (k >> (lt - 3)); for i1 = 16 tt + k (lt <= 3) it is
@@ -224,12 +221,12 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
                     const uint32_t w = threadIdx.x + 256 * k, r2 = w >> 4;
                     const uint64_t zt =
                         *reinterpret_cast<const uint64_t*>(tile + tile_off(r2, (w >> 1) & 7) + 8 * (w & 1));
-                    out.store(a, row, limb, 4096 * bx + w, zt);
+                    out.store(a, row, limb, 4096 * blockIdx.x + w, zt);
                 }
             } else {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncthreads();
-                if (threadIdx.x == 0) tile_store(tmap, tile, (int32_t)(256 * bx), (int32_t)prow);
+                if (threadIdx.x == 0) tile_store(tmap, tile, (int32_t)(256 * blockIdx.x), (int32_t)prow);
             }
         } else {
             __syncthreads();
@@ -248,8 +245,8 @@ __device__ __forceinline__ void ntt256_body(uint64_t* __restrict__ a, uint32_t r
             return i2d(s);
         };
         if (PASS == INV_B && TMA) {
-            if (threadIdx.x == 0) tile_load(sm, tmap, bar, (int32_t)(256 * bx), (int32_t)prow);
-            tile_wait(bar, bar_parity);
+            if (threadIdx.x == 0) tile_load(sm, tmap, bar, (int32_t)(256 * blockIdx.x), (int32_t)prow);
+            tile_wait(bar);
             const uint8_t* tile = reinterpret_cast<const uint8_t*>(sm);
             const uint32_t r = sp * 16 + tt;
 #pragma unroll
@@ -353,115 +350,6 @@ __global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt256_tma(uint64_t* _
     const double* W1 = tw1 ? tw1 + ((size_t)limb * 2 + (fwd ? 0 : 1)) * n : nullptr;
     if (q >= (1ull << 41)) ntt256_body<PASS, true, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar);
     else ntt256_body<PASS, false, PlainIn, OUT, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar, W1);
-}
-
-
-// ---- Both passes in ONE persistent launch, the pass-A -> pass-B intermediate kept in L2 (one HBM round trip).
-// Work items are (pass, row, tile) with 16 tiles of 4096 words per row and pass, claimed in a fixed order through
-// an atomic counter: the first pass of rows 0..lag-1, then the pairs (first pass of row r + lag, second pass of
-// row r), then the remaining second passes.  A second-pass tile of row r needs all 16 first-pass tiles of row r
-// (done[r] == 16): they were claimed earlier, by CTAs that are running and never wait, so the spin terminates.
-// With lag ~ 1.5 x (resident CTAs) / 32 rows the second pass of a row starts while its intermediate (512 KB per
-// row) is still in L2: DRAM sees one read and one write per limb instead of two of each.
-struct FusedSync {
-    uint32_t* counter;   // [1] next work item (zeroed before the launch)
-    uint32_t* done;      // [rows] first-pass tiles completed per row (zeroed before the launch)
-    uint32_t rows, lag;
-};
-__device__ __forceinline__ void fused_item(uint32_t g, uint32_t rows, uint32_t lag, uint32_t& second, uint32_t& row) {
-    const uint32_t L = lag < rows ? lag : rows;
-    if (g < L) {
-        second = 0;
-        row = g;
-        return;
-    }
-    const uint32_t j = g - L, pairs = rows - L;
-    if (j < 2 * pairs) {
-        second = j & 1;
-        row = (j >> 1) + (second ? 0 : L);
-        return;
-    }
-    second = 1;
-    row = pairs + (j - 2 * pairs);
-}
-
-// FWD: FWD_A then FWD_B (TMA tile store) in place.  !FWD: INV_B (TMA tile load from tmap's rows -- smap.phys(row)
-// when oop, else in place) then INV_A in place on data.
-template <bool FWD>
-__global__ void __launch_bounds__(256, ENSI_NTTFP_MINB) k_ntt_fused(uint64_t* __restrict__ data, LimbMap map, ModTab tab,
-                                                   const double2* __restrict__ tw, const double2* __restrict__ ninv,
-                                                   const __grid_constant__ CUtensorMap tmap, LimbMap smap,
-                                                   uint32_t oop, const double* __restrict__ tw1, FusedSync fs) {
-    __shared__ __align__(1024) double sm[16 * kRow];
-    __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t s_item;
-    const uint32_t n = 65536;
-    if (!FWD) {
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-    }
-    uint32_t parity = 0;
-    const uint32_t total = 32u * fs.rows;
-    const PlainIn in;
-    const PlainOut out;
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(fs.counter, 1u);
-        __syncthreads();
-        const uint32_t item = s_item;
-        if (item >= total) break;
-        uint32_t second, row;
-        fused_item(item >> 4, fs.rows, fs.lag, second, row);
-        const uint32_t bx = item & 15;
-        if (second) {
-            if (threadIdx.x == 0) {
-                uint32_t v;
-                for (;;) {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fs.done + row) : "memory");
-                    if (v >= 16) break;
-                    __nanosleep(64);
-                }
-            }
-            __syncthreads();
-        }
-        const uint32_t limb = map.limb[row % map.period];
-        const uint64_t q = tab.q[limb];
-        const double2* W2 = tw + ((size_t)limb * 2 + (FWD ? 0 : 1)) * n;
-        const double* W1 = tw1 ? tw1 + ((size_t)limb * 2 + (FWD ? 0 : 1)) * n : nullptr;
-        uint64_t* a = data + map.phys(row) * n;
-        const bool wide = q >= (1ull << 41);
-        if (FWD) {
-            if (!second) {
-                if (wide) ntt256_body<FWD_A, true>(a, row, limb, q, W2, ninv, sm, in, out, nullptr, 0, nullptr, nullptr, bx);
-                else ntt256_body<FWD_A, false>(a, row, limb, q, W2, ninv, sm, in, out, nullptr, 0, nullptr, nullptr, bx);
-            } else {
-                const uint32_t prow = (uint32_t)map.phys(row);
-                if (wide) ntt256_body<FWD_B, true, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, nullptr, nullptr, bx);
-                else ntt256_body<FWD_B, false, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, nullptr, W1, bx);
-            }
-        } else {
-            if (!second) {
-                const uint32_t prow = oop ? (uint32_t)smap.phys(row) : (uint32_t)map.phys(row);
-                // the previous item's generic-proxy shared-memory accesses (ordered by the barrier above) before
-                // the async-proxy TMA write into the same buffer
-                if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (wide) ntt256_body<INV_B, true, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar, nullptr, bx, parity);
-                else ntt256_body<INV_B, false, PlainIn, PlainOut, true>(a, row, limb, q, W2, ninv, sm, in, out, &tmap, prow, &bar, W1, bx, parity);
-                parity ^= 1;
-            } else {
-                if (wide) ntt256_body<INV_A, true>(a, row, limb, q, W2, ninv, sm, in, out, nullptr, 0, nullptr, nullptr, bx);
-                else ntt256_body<INV_A, false>(a, row, limb, q, W2, ninv, sm, in, out, nullptr, 0, nullptr, nullptr, bx);
-            }
-        }
-        __syncthreads();                        // every store of the item issued (and s_item read) by all threads
-        if (!second && threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(fs.done + row, 1u);
-        }
-        if (FWD && second && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-    if (FWD && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace nttfp

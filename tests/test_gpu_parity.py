@@ -92,15 +92,11 @@ def test_ntt_n16_extreme_inputs(torch_cuda):
     assert (host(t) == np.stack([o.intt(limbs[i], rows[i]) for i in range(len(rows))])).all()
 
 
-@pytest.mark.parametrize("fused", ["1", "0"])
-def test_ntt_n16_many_rows_fused_and_two_launch(torch_cuda, monkeypatch, fused):
-    """N'=2^16, 203 rows over every limb of Q u P: the single-launch transform (k_ntt_fused: both passes in one
-    persistent launch, work items claimed in order, second-pass tiles waiting on their row's first pass -- 203 rows
-    span the lead-in, the interleaved pairs and the tail of its item order) and, with ENSI_NTT_FUSED=0, the
-    two-launch passes; forward and inverse against the oracle, every word."""
+def test_ntt_n16_many_rows(torch_cuda):
+    """N'=2^16, 203 rows over every limb of Q u P in a permuted period (the FP64 passes with the TMA block pass):
+    forward and inverse against the oracle, every word."""
     from paper_2509_09424_b200 import Context
     torch = torch_cuda
-    monkeypatch.setenv("ENSI_NTT_FUSED", fused)
     ctx = Context(16, 12, 4, 3)
     o = oracle.Oracle(16, 12, 4, 3)
     T = 16

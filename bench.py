@@ -749,6 +749,19 @@ def main():
                                  "gather_ms": max_over_ranks(world, gat),
                                  "gather_bytes_per_rank": (world - 1) * sh.S * (wb if layout == "compact" else ct_u64),
                                  "chunks": chunks}
+        # the same layer with the gather fused into the accumulate epilogue (every output tile
+        # TMA-stored into every rank's gathered buffer over CUDA IPC / NVLink, then a signal / wait pair)
+        if layout == "compact":
+            from paper_2509_09424_b200.dist import FusedGatherPCMM
+            fg = FusedGatherPCMM(ctx, W, world, rank, L)
+            fg(x)
+            torch.cuda.synchronize()
+            barrier(world)
+            fms = max_over_ranks(world, time_loop(lambda: fg(x), max(1, args.steps), st))
+            out["column_sharded"]["fused_gather_ms"] = fms
+            barrier(world)
+            fg.close()
+            del fg
         # token blocks (weak scaling, no collective): every rank the whole layer on its own input block
         xt = (gen_compact(ctx, synth.SEED_BASE + 2 + 1000 * rank, d, L) if layout == "compact"
               else synth.gen_words_torch(synth.SEED_BASE + 2 + 1000 * rank, ctx.q, d, L, n))

@@ -41,8 +41,12 @@ struct Tiles {
     uint32_t byte0[kMaxSlices];               // byte offset of slice s inside a ciphertext
     uint8_t wb[kMaxSlices], limb[kMaxSlices], wpt[kMaxSlices], map_full[kMaxSlices], map_tail[kMaxSlices];
 };
+static constexpr uint32_t kMaxPeers = 8;
 struct StoreMaps {
-    CUtensorMap m[kMaxMaps];                  // Y store maps, one per distinct tile width N (box {N, 32})
+    // Y store maps [destination][tile width N] (box {N, 32}).  One destination: the output buffer.  Several (the fused
+    // gather epilogue): every GPU's gathered buffer, this rank's rows of it (row0 * ct bytes on)
+    CUtensorMap m[kMaxPeers][kMaxMaps];
+    uint32_t n_dst;
 };
 
 struct TileInfo {
@@ -142,7 +146,7 @@ __device__ __forceinline__ void epi_words(uint32_t tcol, uint32_t release_addr, 
 template <uint32_t W, uint32_t HW>
 __device__ __forceinline__ void epi_tile(uint32_t tbase_q, uint32_t release_addr, uint32_t lane, uint32_t half,
                                          uint32_t quarter, uint8_t* ys, const EpiArgs& ea, const CUtensorMap* map,
-                                         uint32_t byte, uint32_t row0) {
+                                         uint32_t byte, uint32_t row0, uint32_t n_dst) {
     constexpr uint32_t NB = W * HW;             // bytes of this warp's half row segment
 #ifdef ENSI_ABL_NOEPI       // timing-only ablation build (no outputs): release the accumulator at once
     tc_fence_before();
@@ -167,7 +171,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tbase_q, uint32_t release_addr
     fence_proxy_async();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     if (half == 0 && lane == 0) {
-        tma_store_2d(map, ys, (int32_t)byte, (int32_t)row0);
+        for (uint32_t dd = 0; dd < n_dst; dd++) tma_store_2d(map + dd * kMaxMaps, ys, (int32_t)byte, (int32_t)row0);
         tma_store_commit();
     }
 }
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ea.off_hi = ec.off_hi[ti.limb];
             ea.off64 = ec.off64[ti.limb];
             ea.mu32 = ec.mu32[ti.limb];
-            const CUtensorMap* map = &maps.m[ti.map];
+            const CUtensorMap* map = &maps.m[0][ti.map];
             const uint32_t row0 = g * 128 + quarter * 32;
             const uint32_t tq = tmem_base + ((quarter * 32) << 16) + acc * 256;
             const uint32_t rel = tempty_leader0 + acc * 8;
@@ -315,16 +319,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             switch (ti.wb * 64 + ti.nw / 2) {
                 // full tiles: 48 / 40 / 32 / 32 words; tails: N' mod 48 (16, 32) and N' mod 40 (8, 16, 24, 32)
-                case 5 * 64 + 24: epi_tile<5, 24>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 5 * 64 + 8: epi_tile<5, 8>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 5 * 64 + 16: epi_tile<5, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 6 * 64 + 20: epi_tile<6, 20>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 6 * 64 + 4: epi_tile<6, 4>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 6 * 64 + 8: epi_tile<6, 8>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 6 * 64 + 12: epi_tile<6, 12>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 6 * 64 + 16: epi_tile<6, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                case 7 * 64 + 16: epi_tile<7, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
-                default: epi_tile<8, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0); break;
+                case 5 * 64 + 24: epi_tile<5, 24>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 5 * 64 + 8: epi_tile<5, 8>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 5 * 64 + 16: epi_tile<5, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 6 * 64 + 20: epi_tile<6, 20>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 6 * 64 + 4: epi_tile<6, 4>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 6 * 64 + 8: epi_tile<6, 8>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 6 * 64 + 12: epi_tile<6, 12>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 6 * 64 + 16: epi_tile<6, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                case 7 * 64 + 16: epi_tile<7, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
+                default: epi_tile<8, 16>(tq, rel, lane, half, quarter, ys, ea, map, ti.byte, row0, maps.n_dst); break;
             }
         }
         if (half == 0 && lane == 0) tma_store_wait0();
@@ -382,8 +386,11 @@ void fill_epi_const(const ensi_ctx* ctx, const ensi_weights* w, tc::EpiConst* ec
 
 // x: d compact ciphertexts of ct_bytes each; y: m of them.  A whole ciphertext (slice_limb < 0: 2 level slices)
 // or one staged (poly, limb) slice of every ciphertext (slice_limb = r: ct_bytes = N' w_r).
-int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
-                      cudaStream_t st, int slice_limb) {
+// y_dst[0..n_dst): output buffers, each [m][ct_bytes] from its pointer on (one for the plain call; every GPU's
+// gathered buffer, offset to this rank's rows, for the fused gather epilogue) -- every tile is TMA-stored to each.
+int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* const* y_dst,
+                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb) {
+    if (n_dst < 1 || n_dst > tcc::kMaxPeers) return set_err(ctx, ENSI_EINVAL, "1..8 output destinations");
     if (d != w->d) return set_err(ctx, ENSI_EDIM, "d mismatch");
     if (!tcc_supported(ctx, level)) return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable");
     int rc = build_wt8(ctx, w);
@@ -450,15 +457,17 @@ int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map B (compact)");
     }
-    for (uint32_t i = 0; i < nmaps; i++) {   // Y = [m][ct_bytes], box {N, 32}, no swizzle (packed staging rows)
-        cuuint64_t dims[2] = {ct_bytes, w->m};
-        cuuint64_t strides[1] = {ct_bytes};
-        cuuint32_t box[2] = {ns[i], 32}, es[2] = {1, 1};
-        if (enc(&maps.m[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)y, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return set_err(ctx, ENSI_ECUDA, "tensor map Y (compact)");
-    }
+    maps.n_dst = n_dst;
+    for (uint32_t dd = 0; dd < n_dst; dd++)
+        for (uint32_t i = 0; i < nmaps; i++) {   // Y = [m][ct_bytes], box {N, 32}, no swizzle (packed staging rows)
+            cuuint64_t dims[2] = {ct_bytes, w->m};
+            cuuint64_t strides[1] = {ct_bytes};
+            cuuint32_t box[2] = {ns[i], 32}, es[2] = {1, 1};
+            if (enc(&maps.m[dd][i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)y_dst[dd], dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                return set_err(ctx, ENSI_ECUDA, "tensor map Y (compact)");
+        }
     tc::EpiConst ec;
     fill_epi_const(ctx, w, &ec);
     if (!ec.narrow_ok) return set_err(ctx, ENSI_EINVAL, "d too large for the compact tensor-core epilogue");
@@ -505,6 +514,37 @@ int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights*
     ENSI_LAUNCH_CHECK(ctx);
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tcc launch");
+}
+
+int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
+                      cudaStream_t st, int slice_limb) {
+    uint8_t* dst[1] = {y};
+    return accum_ternary_tcc_dst(ctx, x, d, w, dst, 1, level, st, slice_limb);
+}
+
+// ---------------------------------------------------------------------------------------------- peer signalling
+// After the fused gather epilogue every rank's output rows have been TMA-stored into every GPU's gathered buffer.
+// k_peer_signal (stream-ordered after that kernel, so its stores are complete) makes them visible system-wide and
+// publishes `epoch` in slot `slot` of every destination's flag array; k_peer_wait spins until all n flags of this
+// GPU's array reached `epoch` (release / acquire at system scope: the flags may live in another GPU's memory).
+__global__ void k_peer_signal(PeerFlags pf, uint32_t slot, uint32_t epoch) {
+    const uint32_t p = threadIdx.x;
+    if (p < pf.n) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[p] + slot), "r"(epoch) : "memory");
+    }
+}
+__global__ void k_peer_wait(const uint32_t* flags, uint32_t n, uint32_t epoch) {
+    const uint32_t p = threadIdx.x;
+    if (p < n) {
+        uint32_t v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+            if ((int32_t)(v - epoch) >= 0) break;
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
 }
 
 }  // namespace ensi

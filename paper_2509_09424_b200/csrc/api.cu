@@ -47,6 +47,10 @@ namespace {
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
+        // a non-sticky error left in the runtime's per-thread slot by earlier, unrelated CUDA calls of the process
+        // (seen: "invalid device ordinal" after NCCL / torch teardown in the GPU test run) would otherwise be
+        // reported by this call's cudaGetLastError() check; sticky errors (a faulted context) persist regardless
+        cudaGetLastError();
         cudaGetDevice(&prev);
         if (prev != dev) cudaSetDevice(dev);
     }
@@ -794,32 +798,143 @@ int ensi_pcmm_ternary_host_wire(ensi_ctx* ctx, const uint8_t* x_wire, uint32_t l
     return pcmm_host_impl(ctx, x_wire, level, wc, y_wire, kernel, stream, true);
 }
 
-int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc, ensi_compact_view* y,
-                              const ensi_pcmm_opts* opts, void* stream) {
-    if (!ctx) return ENSI_EINVAL;
+namespace {
+// shared validation of the compact-layout accumulate calls (plain and fused gather)
+int check_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc, const ensi_pcmm_opts* opts) {
     if (!wc) return set_err(ctx, ENSI_EINVAL, "NULL weights");
-    ensi_weights* w = const_cast<ensi_weights*>(wc);
-    if (w->ctx != ctx) return set_err(ctx, ENSI_EINVAL, "weights belong to another context");
-    if (!x || !x->data || !y || !y->data) return set_err(ctx, ENSI_EINVAL, "NULL view or data");
+    if (wc->ctx != ctx) return set_err(ctx, ENSI_EINVAL, "weights belong to another context");
+    if (!x || !x->data) return set_err(ctx, ENSI_EINVAL, "NULL view or data");
     if (x->level < 1 || x->level > ctx->L) return set_err(ctx, ENSI_ELEVEL, "x.level outside [1, num_q]");
-    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level must equal x.level");
     ensi_pcmm_opts o{};
     if (opts) o = *opts;
     if (o.layout != 0) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: Layout A only");
     if (o.rescale_out) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: no rescale epilogue");
     if (o.moddown_lazy) return set_err(ctx, ENSI_EINVAL, "moddown_lazy: Layout B only");
     if (o.kernel != 0 && o.kernel != 2) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: kernel must be 0 or 2");
-    if (x->count != w->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
+    if (x->count != wc->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
+    if (!tcc_supported(ctx, x->level) || wc->d >= (1u << 22))
+        return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable (sm_100a, 5..8-byte words, N' >= 256)");
+    return ENSI_OK;
+}
+}  // namespace
+
+int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc, ensi_compact_view* y,
+                              const ensi_pcmm_opts* opts, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!y || !y->data) return set_err(ctx, ENSI_EINVAL, "NULL view or data");
+    int rc = check_compact(ctx, x, wc, opts);
+    if (rc) return rc;
+    ensi_weights* w = const_cast<ensi_weights*>(wc);
+    if (y->level != x->level) return set_err(ctx, ENSI_ELEVEL, "y.level must equal x.level");
     if (y->count != w->m) return set_err(ctx, ENSI_EDIM, "y.count != m");
     const uint64_t cb = 2 * wire_poly_bytes(ctx, x->level);
     const uint8_t *x0 = x->data, *x1 = x0 + (size_t)x->count * cb, *y0 = y->data, *y1 = y0 + (size_t)y->count * cb;
     if (x0 < y1 && y0 < x1) return set_err(ctx, ENSI_EINVAL, "y aliases x");
-    if (!tcc_supported(ctx, x->level) || w->d >= (1u << 22))
-        return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable (sm_100a, 5..8-byte words, N' >= 256)");
     DeviceGuard g(ctx->device);
-    int rc = accum_ternary_tcc(ctx, x->data, w->d, w, y->data, x->level, (cudaStream_t)stream);
+    rc = accum_ternary_tcc(ctx, x->data, w->d, w, y->data, x->level, (cudaStream_t)stream);
     if (!rc) y->log2_scale = x->log2_scale;
     return rc;
+}
+
+int ensi_pcmm_ternary_compact_gather(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc,
+                                     uint8_t* const* y_dst, uint32_t n_dst, uint32_t rows_total, uint32_t row0,
+                                     const ensi_pcmm_opts* opts, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    int rc = check_compact(ctx, x, wc, opts);
+    if (rc) return rc;
+    ensi_weights* w = const_cast<ensi_weights*>(wc);
+    if (!y_dst || n_dst < 1 || n_dst > 8) return set_err(ctx, ENSI_EINVAL, "y_dst: 1..8 destination buffers");
+    if ((uint64_t)row0 + w->m > rows_total) return set_err(ctx, ENSI_EDIM, "row0 + m exceeds rows_total");
+    const uint64_t cb = 2 * wire_poly_bytes(ctx, x->level);
+    const uint8_t *x0 = x->data, *x1 = x0 + (size_t)x->count * cb;
+    uint8_t* dst[8];
+    for (uint32_t p = 0; p < n_dst; p++) {
+        if (!y_dst[p]) return set_err(ctx, ENSI_EINVAL, "NULL destination buffer");
+        const uint8_t *b0 = y_dst[p], *b1 = b0 + (size_t)rows_total * cb;
+        if (x0 < b1 && b0 < x1) return set_err(ctx, ENSI_EINVAL, "a destination buffer aliases x");
+        dst[p] = y_dst[p] + (size_t)row0 * cb;       // this rank's rows of destination p
+    }
+    DeviceGuard g(ctx->device);
+    return accum_ternary_tcc_dst(ctx, x->data, w->d, w, dst, n_dst, x->level, (cudaStream_t)stream);
+}
+
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int ensi_ipc_get_handle(ensi_ctx* ctx, const void* dev_ptr, ensi_ipc_handle* out) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!dev_ptr || !out) return set_err(ctx, ENSI_EINVAL, "NULL argument");
+    static PFN_memGetAddressRange range = nullptr;
+    if (!range) {
+        void* fp = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range = (PFN_memGetAddressRange)fp;
+        if (!range) return set_err(ctx, ENSI_ECUDA, "cuMemGetAddressRange unavailable");
+    }
+    DeviceGuard g(ctx->device);
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return set_err(ctx, ENSI_EINVAL, "not a device allocation");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) <= sizeof(out->handle), "IPC handle size");
+    std::memset(out, 0, sizeof(*out));
+    std::memcpy(out->handle, &h, sizeof(h));
+    out->offset = (uint64_t)((CUdeviceptr)dev_ptr - base);
+    return ENSI_OK;
+}
+
+int ensi_ipc_open(ensi_ctx* ctx, const ensi_ipc_handle* h, void** dev_ptr) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!h || !dev_ptr) return set_err(ctx, ENSI_EINVAL, "NULL argument");
+    DeviceGuard g(ctx->device);
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, h->handle, sizeof(ih));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "cudaIpcOpenMemHandle");
+    *dev_ptr = (uint8_t*)base + h->offset;
+    ctx->ipc_bases[*dev_ptr] = base;
+    return ENSI_OK;
+}
+
+int ensi_ipc_close(ensi_ctx* ctx, void* dev_ptr) {
+    if (!ctx) return ENSI_EINVAL;
+    auto it = ctx->ipc_bases.find(dev_ptr);
+    if (it == ctx->ipc_bases.end()) return set_err(ctx, ENSI_EINVAL, "pointer was not opened with ensi_ipc_open");
+    DeviceGuard g(ctx->device);
+    cudaError_t e = cudaIpcCloseMemHandle(it->second);
+    ctx->ipc_bases.erase(it);
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "cudaIpcCloseMemHandle");
+}
+
+int ensi_peer_signal(ensi_ctx* ctx, uint32_t* const* flags_dst, uint32_t n_dst, uint32_t slot, uint32_t epoch,
+                     void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!flags_dst || n_dst < 1 || n_dst > 8) return set_err(ctx, ENSI_EINVAL, "flags_dst: 1..8 flag arrays");
+    PeerFlags pf{};
+    pf.n = n_dst;
+    for (uint32_t p = 0; p < n_dst; p++) {
+        if (!flags_dst[p]) return set_err(ctx, ENSI_EINVAL, "NULL flag array");
+        pf.f[p] = flags_dst[p];
+    }
+    DeviceGuard g(ctx->device);
+    k_peer_signal<<<1, 32, 0, (cudaStream_t)stream>>>(pf, slot, epoch);
+    ENSI_LAUNCH_CHECK(ctx);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "peer_signal");
+}
+
+int ensi_peer_wait(ensi_ctx* ctx, const uint32_t* flags, uint32_t n, uint32_t epoch, void* stream) {
+    if (!ctx) return ENSI_EINVAL;
+    if (!flags || n < 1 || n > 32) return set_err(ctx, ENSI_EINVAL, "flags: 1..32 entries");
+    DeviceGuard g(ctx->device);
+    k_peer_wait<<<1, 32, 0, (cudaStream_t)stream>>>(flags, n, epoch);
+    ENSI_LAUNCH_CHECK(ctx);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "peer_wait");
 }
 
 int ensi_wire_pack(ensi_ctx* ctx, const ensi_ct_view* x, uint8_t* out, void* stream) {
@@ -932,10 +1047,6 @@ int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* st
     if (y->level != x->level - 1 || y->count != x->count) return set_err(ctx, ENSI_EDIM, "y must be count x (level-1)");
     if (overlaps(x, y, ctx->n)) return set_err(ctx, ENSI_EINVAL, "y aliases x");
     DeviceGuard g(ctx->device);
-    {
-        cudaError_t e0 = cudaGetLastError();
-        if (e0 != cudaSuccess) return cuda_err(ctx, e0, "stale error before rescale (diagnostic)");
-    }
     rc = ensi::rescale(ctx, x->data, x->count, x->level, y->data, (cudaStream_t)stream);
     if (!rc) y->log2_scale = x->log2_scale - std::log2((double)ctx->mod[x->level - 1]);
     return rc;

@@ -112,6 +112,7 @@ struct ensi_ctx {
     // key switching: two internal streams for alternating rotation batches
     cudaStream_t st_ks[2] = {};
     cudaEvent_t ev_ks_done[2] = {}, ev_ks_fork = nullptr;
+    std::map<void*, void*> ipc_bases;        // ensi_ipc_open: returned pointer -> opened allocation base
     std::string err;
     uint64_t launches = 0;
 };
@@ -161,6 +162,14 @@ bool tc_supported(const ensi_ctx* ctx, uint32_t level);
 uint32_t compact_word_bytes(const ensi_ctx* ctx, uint32_t limb);
 bool tcc_supported(const ensi_ctx* ctx, uint32_t level);
 // x: d compact ciphertexts (slice_limb < 0) or d copies of one staged (poly, limb) slice of limb slice_limb
+struct PeerFlags {
+    uint32_t* f[8];
+    uint32_t n;
+};
+__global__ void k_peer_signal(PeerFlags pf, uint32_t slot, uint32_t epoch);
+__global__ void k_peer_wait(const uint32_t* flags, uint32_t n, uint32_t epoch);
+int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* const* y_dst,
+                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb = -1);
 int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
                       cudaStream_t st, int slice_limb = -1);
 

@@ -9,6 +9,11 @@ One process per GPU, `torch.distributed` over NCCL.  Two shardings:
   [r*S, (r+1)*S) with S = ceil(m / world) (the last shard zero-padded), computes them with its slice of W,
   and one `all_gather_into_tensor` over NCCL assembles the m output ciphertexts on every rank.
 
+* Output columns with the gather fused into the accumulate: `FusedGatherPCMM` maps every
+  rank's gathered buffer into every other rank through CUDA IPC; the compact accumulate's epilogue TMA-stores each
+  output tile into all of them (ensi_pcmm_ternary_compact_gather), and a signal / wait pair of tiny kernels orders
+  the writes -- no separate collective launch, the transfer overlaps the accumulate tile by tile.
+
 CCMM (R18) shards the same way by output columns: `ccmm_shard` gives a rank's (col0, cols).
 
 The compute step is a callable `pcmm(x, W_slice, y_local)`; the product passes the CUDA path
@@ -96,3 +101,64 @@ class ColumnShardedPCMM:
             return None
         import torch.distributed as dist
         return dist.all_gather_into_tensor(y_all, y_local, group=group, async_op=async_op)
+
+
+class FusedGatherPCMM:
+    """One column-sharded layer on compact ciphertexts with the all-gather fused into the accumulate epilogue.
+
+    Rank r computes output columns [r S, (r + 1) S) and its epilogue stores them at rows [r S, (r + 1) S) of EVERY
+    rank's gathered buffer y_all [S world][wire_bytes] (its own, and the peers' mapped through CUDA IPC); then it
+    publishes `epoch` in slot r of every rank's flag array and waits until its own array holds `epoch` in all slots.
+    After __call__ returns (stream-ordered), y_all holds all m outputs (rows >= m: padding columns, (0, 0)).
+
+    ctx: a Context (or any object with its wire_bytes / weights / ipc_handle / ipc_open / ipc_close /
+    pcmm_ternary_compact_gather / peer_signal / peer_wait methods -- the CPU tests pass a stand-in); alloc(shape,
+    dtype_name) allocates the gathered buffer ("uint8") and the flag array ("int32") on this rank's GPU."""
+
+    def __init__(self, ctx, W: np.ndarray, world: int, rank: int, level: int, alloc: Callable = None, group=None):
+        self.ctx, self.world, self.rank, self.level = ctx, world, rank, level
+        self.d, self.m = W.shape
+        self.lo, self.hi, self.S = column_shard(self.m, world, rank)
+        Ws = np.zeros((self.d, self.S), np.int8)
+        Ws[:, : self.hi - self.lo] = W[:, self.lo:self.hi]
+        self.w_local = ctx.weights(Ws)
+        self.wb = ctx.wire_bytes(level)
+        if alloc is None:
+            import torch
+
+            def alloc(shape, dt):
+                return torch.zeros(shape, dtype=getattr(torch, dt), device="cuda")
+        self.y_all = alloc((self.S * world, self.wb), "uint8")
+        self.flags = alloc((world,), "int32")
+        mine = (ctx.ipc_handle(self.y_all), ctx.ipc_handle(self.flags))
+        if world > 1:
+            import torch.distributed as dist
+            handles = [None] * world
+            dist.all_gather_object(handles, mine, group=group)
+        else:
+            handles = [mine]
+        self._opened = []
+        self.dst, self.flag_dst = [], []
+        for r in range(world):
+            if r == rank:
+                self.dst.append(self.y_all)
+                self.flag_dst.append(self.flags)
+            else:
+                py, pf = ctx.ipc_open(handles[r][0]), ctx.ipc_open(handles[r][1])
+                self._opened += [py, pf]
+                self.dst.append(py)
+                self.flag_dst.append(pf)
+        self.epoch = 0
+
+    def __call__(self, x, stream=None):
+        self.ctx.pcmm_ternary_compact_gather(x, self.w_local, self.dst, self.S * self.world, self.rank * self.S,
+                                             self.level, stream=stream)
+        self.epoch = (self.epoch + 1) & 0x7FFFFFFF
+        self.ctx.peer_signal(self.flag_dst, self.rank, self.epoch, stream=stream)
+        self.ctx.peer_wait(self.flags, self.world, self.epoch, stream=stream)
+        return self.y_all
+
+    def close(self):
+        for p in self._opened:
+            self.ctx.ipc_close(p)
+        self._opened = []

@@ -30,7 +30,8 @@ EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
            "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel", "ensi_load_relin_key",
            "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm", "ensi_wire_bytes", "ensi_pcmm_ternary_host_wire",
-           "ensi_wire_pack", "ensi_wire_unpack", "ensi_pcmm_ternary_compact"]
+           "ensi_wire_pack", "ensi_wire_unpack", "ensi_pcmm_ternary_compact", "ensi_pcmm_ternary_compact_gather",
+           "ensi_ipc_get_handle", "ensi_ipc_open", "ensi_ipc_close", "ensi_peer_signal", "ensi_peer_wait"]
 
 
 class EnsiError(RuntimeError):
@@ -55,6 +56,10 @@ class CompactView(C.Structure):
 class Keys(C.Structure):
     _fields_ = [("sk_ntt", C.c_void_p), ("n_rot", C.c_uint32), ("galois", C.c_void_p), ("rot_keys", C.c_void_p),
                 ("rot_keys_mem", C.c_uint32)]
+
+
+class IpcHandle(C.Structure):
+    _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_uint64)]
 
 
 class PcmmOpts(C.Structure):
@@ -107,6 +112,13 @@ def lib():
         L.ensi_wire_unpack.argtypes = [vp, vp, C.POINTER(CtView), vp]
         L.ensi_pcmm_ternary_compact.argtypes = [vp, C.POINTER(CompactView), vp, C.POINTER(CompactView),
                                                 C.POINTER(PcmmOpts), vp]
+        L.ensi_pcmm_ternary_compact_gather.argtypes = [vp, C.POINTER(CompactView), vp, C.POINTER(vp), u32, u32, u32,
+                                                       C.POINTER(PcmmOpts), vp]
+        L.ensi_ipc_get_handle.argtypes = [vp, vp, C.POINTER(IpcHandle)]
+        L.ensi_ipc_open.argtypes = [vp, C.POINTER(IpcHandle), C.POINTER(vp)]
+        L.ensi_ipc_close.argtypes = [vp, vp]
+        L.ensi_peer_signal.argtypes = [vp, C.POINTER(vp), u32, u32, u32, vp]
+        L.ensi_peer_wait.argtypes = [vp, vp, u32, u32, vp]
         L.ensi_mul_plain.argtypes = [vp, C.POINTER(CtView), vp, C.c_double, C.POINTER(CtView), vp]
         L.ensi_mul_relin.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), C.POINTER(CtView), vp]
         L.ensi_ccmm.argtypes = [vp, C.POINTER(CtView), C.POINTER(CtView), vp, C.POINTER(CtView),
@@ -288,6 +300,51 @@ class Context:
         self._check(lib().ensi_pcmm_ternary_compact(self.h, C.byref(xv), w.h, C.byref(yv), C.byref(opts),
                                                     _stream_ptr(stream)))
         return yv.log2_scale
+
+    def pcmm_ternary_compact_gather(self, x, w: "Weights", dsts, rows_total: int, row0: int, level: int,
+                                    kernel: int = 0, stream=None, log2_scale: float = 40.0):
+        """NEXT #4 fused gather: y_i of this call stored into rows row0 + i of every destination (device pointers or
+        contiguous uint8 CUDA tensors of rows_total x wire_bytes -- this GPU's gathered buffer and the peers')."""
+        xv = self.compact_view(x, level, log2_scale)
+        wb = self.wire_bytes(level)
+        ptrs = []
+        for dbuf in dsts:
+            if hasattr(dbuf, "data_ptr"):
+                if not (dbuf.is_cuda and dbuf.is_contiguous() and dbuf.dtype.itemsize == 1 and
+                        dbuf.numel() == rows_total * wb):
+                    raise ValueError(f"destination must be a contiguous uint8 CUDA tensor of {rows_total} x {wb} bytes")
+                ptrs.append(dbuf.data_ptr())
+            else:
+                ptrs.append(int(dbuf))
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        opts = PcmmOpts(0, 0, 0, 0, kernel, 0)
+        self._check(lib().ensi_pcmm_ternary_compact_gather(self.h, C.byref(xv), w.h, arr, len(ptrs), rows_total, row0,
+                                                           C.byref(opts), _stream_ptr(stream)))
+
+    def ipc_handle(self, t) -> bytes:
+        """CUDA IPC handle (72 bytes: allocation handle + offset) of a CUDA tensor's storage, for another process."""
+        h = IpcHandle()
+        self._check(lib().ensi_ipc_get_handle(self.h, C.c_void_p(t.data_ptr()), C.byref(h)))
+        return bytes(C.string_at(C.addressof(h), C.sizeof(h)))
+
+    def ipc_open(self, handle: bytes) -> int:
+        h = IpcHandle.from_buffer_copy(handle)
+        p = C.c_void_p()
+        self._check(lib().ensi_ipc_open(self.h, C.byref(h), C.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, ptr: int):
+        self._check(lib().ensi_ipc_close(self.h, C.c_void_p(ptr)))
+
+    def peer_signal(self, flag_ptrs, slot: int, epoch: int, stream=None):
+        """flag_ptrs: device pointers or 32-bit CUDA tensors (this GPU's and the peers' flag arrays)."""
+        arr = (C.c_void_p * len(flag_ptrs))(*[f.data_ptr() if hasattr(f, "data_ptr") else int(f) for f in flag_ptrs])
+        self._check(lib().ensi_peer_signal(self.h, arr, len(flag_ptrs), slot, epoch, _stream_ptr(stream)))
+
+    def peer_wait(self, flags, n: int, epoch: int, stream=None):
+        if not (flags.is_cuda and flags.dtype.itemsize == 4 and flags.numel() >= n):
+            raise ValueError("flags must be a CUDA tensor of >= n 32-bit words")
+        self._check(lib().ensi_peer_wait(self.h, C.c_void_p(flags.data_ptr()), n, epoch, _stream_ptr(stream)))
 
     # ---- compact wire format (host transfers)
     def wire_widths(self, level: int):

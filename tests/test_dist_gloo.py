@@ -148,3 +148,106 @@ def test_ccmm_column_shards_gather_to_single_process():
     skc, sk, pk = o.keygen(0x454E5349 + 1)
     a, src, mask, keys, rlk, ref = _ccmm_setup(o, sk, pk, 1, 8, 2, 5, 77)
     assert (got == o.ccmm(a, src, 1, 8, 2, 5, mask, keys, rlk)).all()
+
+
+class _ShmCtx:
+    """CPU stand-in for Context in FusedGatherPCMM's protocol: buffers are named shared-memory arrays (the "IPC
+    handle" is the name), the accumulate is the oracle's Algorithm 1 written into every destination at row0, the
+    flags are host words (test infrastructure only)."""
+
+    def __init__(self, o, level):
+        from multiprocessing import shared_memory
+        self.shm, self.o, self.level = shared_memory, o, level
+        self.keep = []
+
+    def wire_bytes(self, level):
+        return 2 * level * self.o.n * 8                      # uint64 words as bytes (no compaction needed here)
+
+    def weights(self, W):
+        return W
+
+    def alloc(self, shape, dt):
+        dtype = np.uint8 if dt == "uint8" else np.int32
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        sm = self.shm.SharedMemory(create=True, size=nbytes)
+        self.keep.append(sm)
+        a = np.ndarray(shape, dtype=dtype, buffer=sm.buf)
+        a[...] = 0
+        return _Named(a, sm.name)
+
+    def ipc_handle(self, buf):
+        return (buf.name, buf.a.shape, str(buf.a.dtype))
+
+    def ipc_open(self, h):
+        sm = self.shm.SharedMemory(name=h[0])
+        self.keep.append(sm)
+        return _Named(np.ndarray(h[1], dtype=np.dtype(h[2]), buffer=sm.buf), h[0])
+
+    def ipc_close(self, p):
+        pass
+
+    def pcmm_ternary_compact_gather(self, x, w, dsts, rows_total, row0, level, stream=None):
+        y = self.o.pcmm_a(x, w).view(np.uint8).reshape(w.shape[1], -1)
+        for dbuf in dsts:
+            dbuf.a[row0:row0 + y.shape[0]] = y
+
+    def peer_signal(self, flag_dsts, slot, epoch, stream=None):
+        for f in flag_dsts:
+            f.a[slot] = epoch
+
+    def peer_wait(self, flags, n, epoch, stream=None):
+        import time
+        t0 = time.time()
+        while not all(int(v) >= epoch for v in flags.a[:n]):
+            assert time.time() - t0 < 60, "peer_wait timed out"
+            time.sleep(0.001)
+
+
+class _Named:
+    def __init__(self, a, name):
+        self.a, self.name = a, name
+
+
+def _fused_worker(rank, world, port, d, m, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import oracle
+    import synth
+    from paper_2509_09424_b200.dist import FusedGatherPCMM
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = oracle.Oracle(12, 2, 1, 2)
+    ctx = _ShmCtx(o, 1)
+    x = synth.gen_words(57, o.q, d, 1, o.n)
+    W = synth.gen_W(58, d, m)
+    fg = FusedGatherPCMM(ctx, W, world, rank, 1, alloc=ctx.alloc)
+    for _ in range(2):                                          # two layers: epochs 1 and 2
+        dist.barrier()
+        y = fg(x)
+    assert int(fg.flags.a.min()) == 2
+    if rank == 0:
+        out_q.put(y.a[:m].copy().view(np.uint64).reshape(m, 2, 1, o.n))
+    dist.barrier()
+    fg.close()
+    dist.destroy_process_group()
+
+
+def test_fused_gather_protocol_world2_ragged():
+    """FusedGatherPCMM's host protocol at world size 2 (gloo; a shared-memory stand-in for the CUDA IPC mappings):
+    handle exchange, every rank's rows at rank * S of every gathered buffer, the epoch flags -- with m = 7 (a
+    zero-padded last shard), the gathered rows equal the single-process oracle layer."""
+    import oracle
+    import synth
+    world, d, m = 2, 5, 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, d, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    o = oracle.Oracle(12, 2, 1, 2)
+    want = o.pcmm_a(synth.gen_words(57, o.q, d, 1, o.n), synth.gen_W(58, d, m))
+    assert (got == want).all()

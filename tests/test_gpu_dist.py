@@ -113,4 +113,110 @@ def test_bench_under_torchrun_nccl(torch_cuda):
     assert out["roofline"]["frac"] > 0 and out["roofline"]["kernel"] == "k_accum_tcc"
     assert out["scaling"] == "strong" and out["config"]["parallelism"].startswith("output columns sharded x1")
     assert out["column_sharded"]["gather_ms"] > 0 and out["column_sharded"]["compute_ms"] > 0
+    assert out["column_sharded"]["fused_gather_ms"] > 0
     assert out["token_blocks"]["value"] > 0
+
+
+def _c1_compact(torch, seed, d, m, level=3):
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import wire_pack_host
+    o = oracle.Oracle(12, 3, 1, 3)
+    ctx = Context(12, 3, 1, 3)
+    x = synth.gen_words(seed, o.q, d, level, o.n)
+    W = synth.gen_W(seed + 1, d, m)
+    xc = torch.from_numpy(wire_pack_host(x, ctx.wire_widths(level))).cuda()
+    return o, ctx, x, W, xc
+
+
+def test_fused_gather_epilogue_multi_destination(torch_cuda):
+    """SURVEY 8(f) NEXT #4 (fused gather epilogue), on one GPU: ensi_pcmm_ternary_compact_gather with two destination
+    buffers (standing in for two GPUs' gathered buffers) -- rows [row0, row0 + m) of BOTH hold the oracle's outputs,
+    every other row is untouched; row0 + m > rows_total is EDIM."""
+    torch = torch_cuda
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_EDIM, wire_unpack_host
+    d, m, level, rows_total, row0 = 70, 50, 3, 130, 37
+    o, ctx, x, W, xc = _c1_compact(torch, 81, d, m, level)
+    wb = ctx.wire_bytes(level)
+    bufs = [torch.full((rows_total, wb), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    w = ctx.weights(W)
+    ctx.pcmm_ternary_compact_gather(xc, w, bufs, rows_total, row0, level)
+    torch.cuda.synchronize()
+    want = o.pcmm_a(x, W)
+    for b in bufs:
+        h = b.cpu().numpy()
+        assert (wire_unpack_host(h[row0:row0 + m], ctx.wire_widths(level), level, o.n) == want).all()
+        assert (h[:row0] == 0xA5).all() and (h[row0 + m:] == 0xA5).all()
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary_compact_gather(xc, w, bufs, rows_total, rows_total - m + 1, level)
+    assert e.value.code == ENSI_EDIM
+
+
+def test_fused_gather_world1(torch_cuda):
+    """FusedGatherPCMM at world size 1 (self-peer): the gathered buffer == the oracle's layer, twice (epochs 1, 2:
+    the signal / wait kernels order consecutive layers)."""
+    torch = torch_cuda
+    from paper_2509_09424_b200.dist import FusedGatherPCMM
+    from paper_2509_09424_b200.ensi import wire_unpack_host
+    d, m, level = 40, 33, 3
+    o, ctx, x, W, xc = _c1_compact(torch, 91, d, m, level)
+    fg = FusedGatherPCMM(ctx, W, 1, 0, level)
+    want = o.pcmm_a(x, W)
+    for it in range(2):
+        fg.y_all.zero_()
+        y = fg(xc)
+        torch.cuda.synchronize()
+        assert (wire_unpack_host(y[:m].cpu().numpy(), ctx.wire_widths(level), level, o.n) == want).all()
+        assert int(fg.flags[0]) == it + 1
+    fg.close()
+
+
+_CHILD = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import synth
+from paper_2509_09424_b200 import Context
+from paper_2509_09424_b200.ensi import wire_pack_host
+hy, hf, rows_total, row0 = bytes.fromhex(sys.argv[2]), bytes.fromhex(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+ctx = Context(12, 3, 1, 3)
+x = synth.gen_words(101, ctx.q, 30, 3, ctx.n)
+W = synth.gen_W(102, 30, 20)
+xc = torch.from_numpy(wire_pack_host(x, ctx.wire_widths(3))).cuda()
+py, pf = ctx.ipc_open(hy), ctx.ipc_open(hf)
+ctx.pcmm_ternary_compact_gather(xc, ctx.weights(W), [py], rows_total, row0, 3)
+ctx.peer_signal([pf], 1, 7)
+torch.cuda.synchronize()
+ctx.ipc_close(py)
+ctx.ipc_close(pf)
+print("child ok")
+"""
+
+
+def test_fused_gather_through_cuda_ipc_from_another_process(torch_cuda):
+    """The IPC leg of FusedGatherPCMM: a second process maps this process's gathered buffer and flag array
+    (ensi_ipc_get_handle / ensi_ipc_open, offsets inside torch's allocations), its accumulate epilogue stores its
+    output rows into them and it signals slot 1; after it exits the rows == the oracle and the flag == 7.  No kernel
+    of one process waits on the other (the wait is the host-side join)."""
+    torch = torch_cuda
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import wire_unpack_host
+    ctx = Context(12, 3, 1, 3)
+    o = oracle.Oracle(12, 3, 1, 3)
+    wb = ctx.wire_bytes(3)
+    rows_total, row0, m = 48, 24, 20
+    pad = torch.zeros(1000, dtype=torch.uint8, device="cuda")      # non-zero offsets inside the caching allocator
+    y_all = torch.full((rows_total, wb), 0x5A, dtype=torch.uint8, device="cuda")
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    hy, hf = ctx.ipc_handle(y_all), ctx.ipc_handle(flags)
+    r = subprocess.run([sys.executable, "-c", _CHILD, ROOT, hy.hex(), hf.hex(), str(rows_total), str(row0)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "child ok" in r.stdout, r.stderr[-2000:]
+    torch.cuda.synchronize()
+    x = synth.gen_words(101, o.q, 30, 3, o.n)
+    W = synth.gen_W(102, 30, 20)
+    h = y_all.cpu().numpy()
+    assert (wire_unpack_host(h[row0:row0 + m], ctx.wire_widths(3), 3, o.n) == o.pcmm_a(x, W)).all()
+    assert (h[:row0] == 0x5A).all() and (h[row0 + m:] == 0x5A).all()
+    assert int(flags[1]) == 7 and int(flags[0]) == 0
+    del pad

@@ -8,7 +8,8 @@
 //   all 8 warps (each x word is fetched from L2/HBM once per 64 outputs).
 //   The weight sign is warp-uniform: one branch per (j, output) covers 8 words per lane, and zeros are
 //   skipped exactly as Alg. 1 lines 4-8 skip W = 0.
-// Accumulation is signed, lazy 64-bit: the host derives `ared`, the number of rows between intermediate
+// Accumulation is signed and lazy: on the FP64 pipe for limbs below 2^51 (acc_u2d), in 64-bit integers otherwise.
+// Integer path: the host derives `ared`, the number of rows between intermediate
 // reductions, from the widest active modulus (accum_rows_between_reductions) so that |acc| never leaves the
 // int64 range nor the Barrett input range: 8191 rows for the O1 primes (< 2^50), 7 for a modulus near 2^60.
 // The epilogue maps acc to the canonical word in [0, q) (Barrett), so the output is the unique canonical value
@@ -41,6 +42,25 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// FP64-pipe accumulation for limbs q < 2^51 (every limb at the O1 primes).  Every canonical word and every partial sum
+// of up to `ared_fp` signed terms is an integer below 2^53, i.e. an exact double: one DFMA acc += w x (w in {-1,0,1})
+// per term-word on the FP64 pipe (64 lanes/clk/SM on B200) instead of the 64-bit IADD3 + IADD3.X pair and the per-
+// output sign branch on the integer pipe (3.86 instructions per term-word, profiles/r01_ncu_accum_cudacore.md).
+// A word enters as a double through the 2^52 binade (x < 2^52: OR its high half into 0x43300000, subtract 2^52) and
+// leaves through the centred reduction v - rint(v/q) q (exact) and the 1.5*2^52 round trip; the result is the same
+// canonical word the integer path produces.
+__device__ __forceinline__ double acc_u2d(uint64_t x) {
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - 4503599627370496.0;   // x < 2^52
+}
+__device__ __forceinline__ double acc_red(double v, double q, double qinv) {
+    const double t = fma(v, qinv, 6755399441055744.0) - 6755399441055744.0;   // rint(v / q), |v / q| < 2^51
+    return fma(-t, q, v);                                                       // exact: |v - t q| <= q/2 + tiny
+}
+__device__ __forceinline__ uint64_t acc_canon(double v, uint64_t q, double qd, double qinv) {
+    const long long r = __double_as_longlong(acc_red(v, qd, qinv) + 6755399441055744.0) - 0x4338000000000000ll;
+    return (uint64_t)(r + ((r >> 63) & (long long)q));
+}
 
 // planes: [d][2][mw] uint32 (pos bits, neg bits); bit (i % 32) of word i / 32; mw even, zero padded.
 __global__ void __launch_bounds__(256, 8 / AP)
@@ -88,6 +108,78 @@ __global__ void __launch_bounds__(256, 8 / AP)
 
     load_stage(0, 0);
     cp_commit();
+    if (br.q < (1ull << 51)) {   // >= 2 rows between reductions (see ared_fp)
+        // ---- narrow limb: the FP64 pipe (see acc_u2d); CTA-uniform branch (one limb per CTA).  Each landed stage is
+        // converted in shared memory once (x words -> doubles, sign bits -> w in {-1, 0, +1}), then every (row,
+        // output) is AP exact DFMAs acc += w x with no per-output branch (the branchy add/sub/skip form spent ~3 of
+        // its ~4 instructions per term-word on control: 152 ms for the C2 layer).
+        const double qd = (double)br.q, qinv = 1.0 / qd;
+        // rows between reductions for THIS limb: (n + 1/2) q < 2^53 (8189 at 2^40, 6 at 2^50; -2 absorbs the rounding
+        // of the quotient)
+        const uint32_t ared_fp = (uint32_t)(9007199254740991.0 / (double)(br.q - 1)) - 2;
+        double* sxd = reinterpret_cast<double*>(&sx[0][0][0]);
+        __shared__ double swd[2][AKC][ATI];
+        double acd[AO][AP];
+#pragma unroll
+        for (int o = 0; o < AO; o++)
+#pragma unroll
+            for (int p = 0; p < AP; p++) acd[o][p] = 0.0;
+        uint32_t sincef = 0;
+        for (uint32_t s = 0; s < nstages; s++) {
+            const int buf = s & 1;
+            if (s + 1 < nstages) load_stage(s + 1, buf ^ 1);
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+            {   // convert this stage in place: AKC x ATW words, AKC x ATI weights
+                const uint32_t rows = min((uint32_t)AKC, d - s * AKC);
+#pragma unroll
+                for (int c = 0; c < AKC * ATW / 256; c++) {
+                    const uint32_t e = tid + 256 * c, r = e / ATW;
+                    uint64_t* px = &sx[buf][0][0] + e;
+                    sxd[buf * AKC * ATW + e] = r < rows ? acc_u2d(*px) : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < AKC * ATI / 256; c++) {
+                    const uint32_t e = tid + 256 * c, r = e / ATI, o = e % ATI;
+                    const uint32_t pw = ssg[buf][r][o >> 5], nw = ssg[buf][r][2 + (o >> 5)];
+                    swd[buf][r][o] = (double)(int)((pw >> (o & 31)) & 1u) - (double)(int)((nw >> (o & 31)) & 1u);
+                }
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int r = 0; r < AKC; r++) {
+                if (sincef == ared_fp) {   // |acd| <= (ared_fp + 1/2) q < 2^53 between reductions
+#pragma unroll
+                    for (int o = 0; o < AO; o++)
+#pragma unroll
+                        for (int p = 0; p < AP; p++) acd[o][p] = acc_red(acd[o][p], qd, qinv);
+                    sincef = 0;
+                }
+                sincef++;
+                double xv[AP];
+#pragma unroll
+                for (int p = 0; p < AP; p++) xv[p] = sxd[(buf * AKC + r) * ATW + lane + 32 * p];
+#pragma unroll
+                for (int o = 0; o < AO; o++) {
+                    const double wv = swd[buf][r][warp * AO + o];
+#pragma unroll
+                    for (int p = 0; p < AP; p++) acd[o][p] = fma(wv, xv[p], acd[o][p]);
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int o = 0; o < AO; o++) {
+            const uint32_t i = i0 + warp * AO + o;
+            if (i < m) {
+                uint64_t* yo = y + (uint64_t)i * ctw + pos0;
+#pragma unroll
+                for (int p = 0; p < AP; p++) yo[lane + 32 * p] = acc_canon(acd[o][p], br.q, qd, qinv);
+            }
+        }
+        return;
+    }
     for (uint32_t s = 0; s < nstages; s++) {
         const int buf = s & 1;
         if (s + 1 < nstages) load_stage(s + 1, buf ^ 1);

@@ -945,15 +945,14 @@ int ensi_wire_pack(ensi_ctx* ctx, const ensi_ct_view* x, uint8_t* out, void* str
     DeviceGuard g(ctx->device);
     const uint32_t lv = x->level, n = ctx->n;
     const size_t pb = wire_poly_bytes(ctx, lv);
-    for (uint32_t c = 0; c < x->count && !rc; c++)
-        for (uint32_t p = 0; p < 2 && !rc; p++) {
-            size_t off = (size_t)c * 2 * pb + p * pb;
-            for (uint32_t r = 0; r < lv && !rc; r++) {
-                const uint32_t wb = wire_width(ctx, r);
-                rc = wire_pack(ctx, x->data + (((size_t)c * 2 + p) * lv + r) * n, out + off, n, wb, (cudaStream_t)stream);
-                off += (size_t)n * wb;
-            }
-        }
+    // one launch per limb over all (ciphertext, poly) rows
+    size_t off = 0;
+    for (uint32_t r = 0; r < lv && !rc; r++) {
+        const uint32_t wb = wire_width(ctx, r);
+        rc = wire_pack_rows(ctx, x->data + (size_t)r * n, (size_t)lv * n, out + off, pb, 2 * x->count, n, wb,
+                            (cudaStream_t)stream);
+        off += (size_t)n * wb;
+    }
     return rc;
 }
 
@@ -965,15 +964,13 @@ int ensi_wire_unpack(ensi_ctx* ctx, const uint8_t* in, ensi_ct_view* y, void* st
     DeviceGuard g(ctx->device);
     const uint32_t lv = y->level, n = ctx->n;
     const size_t pb = wire_poly_bytes(ctx, lv);
-    for (uint32_t c = 0; c < y->count && !rc; c++)
-        for (uint32_t p = 0; p < 2 && !rc; p++) {
-            size_t off = (size_t)c * 2 * pb + p * pb;
-            for (uint32_t r = 0; r < lv && !rc; r++) {
-                const uint32_t wb = wire_width(ctx, r);
-                rc = wire_unpack(ctx, in + off, y->data + (((size_t)c * 2 + p) * lv + r) * n, n, wb, (cudaStream_t)stream);
-                off += (size_t)n * wb;
-            }
-        }
+    size_t off = 0;
+    for (uint32_t r = 0; r < lv && !rc; r++) {
+        const uint32_t wb = wire_width(ctx, r);
+        rc = wire_unpack_rows(ctx, in + off, pb, y->data + (size_t)r * n, (size_t)lv * n, 2 * y->count, n, wb,
+                              (cudaStream_t)stream);
+        off += (size_t)n * wb;
+    }
     return rc;
 }
 

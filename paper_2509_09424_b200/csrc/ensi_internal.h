@@ -209,6 +209,10 @@ int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, u
 // wire format (poly.cu): words <-> wb-byte little-endian packing, words a multiple of 4
 int wire_unpack(ensi_ctx* ctx, const uint8_t* in, uint64_t* out, size_t words, uint32_t wb, cudaStream_t st);
 int wire_pack(ensi_ctx* ctx, const uint64_t* in, uint8_t* out, size_t words, uint32_t wb, cudaStream_t st);
+int wire_unpack_rows(ensi_ctx* ctx, const uint8_t* in, size_t wire_rs, uint64_t* out, size_t word_rs, uint32_t rows,
+                     size_t words, uint32_t wb, cudaStream_t st);
+int wire_pack_rows(ensi_ctx* ctx, const uint64_t* in, size_t word_rs, uint8_t* out, size_t wire_rs, uint32_t rows,
+                   size_t words, uint32_t wb, cudaStream_t st);
 
 // poly (poly.cu)
 int rescale(ensi_ctx* ctx, const uint64_t* in, uint32_t count, uint32_t level, uint64_t* out, cudaStream_t st);

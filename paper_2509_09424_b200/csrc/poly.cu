@@ -189,9 +189,12 @@ void add_into(ensi_ctx* ctx, uint64_t* y, const uint64_t* x, uint32_t count, uin
 // Each thread moves 4 consecutive words = wb 32-bit words of wire bytes (4 wb bytes, 4-byte aligned).
 template <uint32_t WB>
 __global__ void __launch_bounds__(kT) k_wire_unpack(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
-                                                    size_t groups) {
+                                                    size_t groups, size_t in_rs, size_t out_rs) {
+    // blockIdx.y: row (one (ciphertext, poly) slice of one limb); in_rs / out_rs: row strides in 32-bit / 64-bit words
     const size_t gi = (size_t)blockIdx.x * kT + threadIdx.x;
     if (gi >= groups) return;
+    in += blockIdx.y * in_rs;
+    out += blockIdx.y * out_rs;
     uint32_t u[WB + 1];
 #pragma unroll
     for (uint32_t i = 0; i < WB; i++) u[i] = __ldcs(in + gi * WB + i);
@@ -208,9 +211,11 @@ __global__ void __launch_bounds__(kT) k_wire_unpack(const uint32_t* __restrict__
 }
 template <uint32_t WB>
 __global__ void __launch_bounds__(kT) k_wire_pack(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                  size_t groups) {
+                                                  size_t groups, size_t in_rs, size_t out_rs) {
     const size_t gi = (size_t)blockIdx.x * kT + threadIdx.x;
     if (gi >= groups) return;
+    in += blockIdx.y * in_rs;
+    out += blockIdx.y * out_rs;
     uint32_t u[WB + 2];
 #pragma unroll
     for (uint32_t i = 0; i < WB + 2; i++) u[i] = 0;
@@ -230,41 +235,62 @@ __global__ void __launch_bounds__(kT) k_wire_pack(const uint64_t* __restrict__ i
 }
 
 template <uint32_t WB>
-static void wire_launch(bool unpack, const void* in, void* out, size_t groups, cudaStream_t st) {
-    const uint32_t g = (uint32_t)((groups + kT - 1) / kT);
-    if (unpack) k_wire_unpack<WB><<<g, kT, 0, st>>>((const uint32_t*)in, (uint64_t*)out, groups);
-    else k_wire_pack<WB><<<g, kT, 0, st>>>((const uint64_t*)in, (uint32_t*)out, groups);
+static void wire_launch(bool unpack, const void* in, void* out, size_t groups, uint32_t rows, size_t in_rs,
+                        size_t out_rs, cudaStream_t st) {
+    const dim3 g((uint32_t)((groups + kT - 1) / kT), rows);
+    if (unpack) k_wire_unpack<WB><<<g, kT, 0, st>>>((const uint32_t*)in, (uint64_t*)out, groups, in_rs, out_rs);
+    else k_wire_pack<WB><<<g, kT, 0, st>>>((const uint64_t*)in, (uint32_t*)out, groups, in_rs, out_rs);
 }
 
+// rows x `words` words of one limb (width wb): row i of the wire side at +i*wire_rs bytes, of the word side at
+// +i*word_rs words (wire_rs a multiple of 4, word_rs of 1) -- one launch for all rows (<= 65535 per launch)
 static int wire_dispatch(ensi_ctx* ctx, bool unpack, const void* in, void* out, size_t words, uint32_t wb,
-                         cudaStream_t st) {
+                         uint32_t rows, size_t wire_rs, size_t word_rs, cudaStream_t st) {
     if (words % 4) return set_err(ctx, ENSI_EINVAL, "wire transfers move multiples of 4 words");
+    if (wire_rs % 4) return set_err(ctx, ENSI_EINVAL, "wire rows must start 4-byte aligned");
     const size_t groups = words / 4;
-    switch (wb) {
-        case 1: wire_launch<1>(unpack, in, out, groups, st); break;
-        case 2: wire_launch<2>(unpack, in, out, groups, st); break;
-        case 3: wire_launch<3>(unpack, in, out, groups, st); break;
-        case 4: wire_launch<4>(unpack, in, out, groups, st); break;
-        case 5: wire_launch<5>(unpack, in, out, groups, st); break;
-        case 6: wire_launch<6>(unpack, in, out, groups, st); break;
-        case 7: wire_launch<7>(unpack, in, out, groups, st); break;
-        case 8: {
-            cudaError_t e = cudaMemcpyAsync(out, in, words * 8, cudaMemcpyDeviceToDevice, st);
-            if (e != cudaSuccess) return cuda_err(ctx, e, "wire copy");
-            return ENSI_OK;
+    for (uint32_t r0 = 0; r0 < rows; r0 += 65535) {
+        const uint32_t nr = std::min<uint32_t>(65535, rows - r0);
+        const uint8_t* wi = (const uint8_t*)(unpack ? in : out) + (size_t)r0 * wire_rs;
+        const uint64_t* wo = (const uint64_t*)(unpack ? out : in) + (size_t)r0 * word_rs;
+        const void* src = unpack ? (const void*)wi : (const void*)wo;
+        void* dst = unpack ? (void*)wo : (void*)wi;
+        const size_t in_rs = unpack ? wire_rs / 4 : word_rs, out_rs = unpack ? word_rs : wire_rs / 4;
+        switch (wb) {
+            case 1: wire_launch<1>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 2: wire_launch<2>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 3: wire_launch<3>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 4: wire_launch<4>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 5: wire_launch<5>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 6: wire_launch<6>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 7: wire_launch<7>(unpack, src, dst, groups, nr, in_rs, out_rs, st); break;
+            case 8: {
+                const size_t dp = unpack ? word_rs * 8 : wire_rs, sp = unpack ? wire_rs : word_rs * 8;
+                cudaError_t e = cudaMemcpy2DAsync(dst, dp, src, sp, words * 8, nr, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return cuda_err(ctx, e, "wire copy");
+                continue;
+            }
+            default: return set_err(ctx, ENSI_EINVAL, "wire width must be 1..8 bytes");
         }
-        default: return set_err(ctx, ENSI_EINVAL, "wire width must be 1..8 bytes");
+        ctx->launches += 1;
     }
-    ctx->launches += 1;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "wire");
 }
 
 int wire_unpack(ensi_ctx* ctx, const uint8_t* in, uint64_t* out, size_t words, uint32_t wb, cudaStream_t st) {
-    return wire_dispatch(ctx, true, in, out, words, wb, st);
+    return wire_dispatch(ctx, true, in, out, words, wb, 1, 0, 0, st);
 }
 int wire_pack(ensi_ctx* ctx, const uint64_t* in, uint8_t* out, size_t words, uint32_t wb, cudaStream_t st) {
-    return wire_dispatch(ctx, false, in, out, words, wb, st);
+    return wire_dispatch(ctx, false, in, out, words, wb, 1, 0, 0, st);
+}
+int wire_unpack_rows(ensi_ctx* ctx, const uint8_t* in, size_t wire_rs, uint64_t* out, size_t word_rs, uint32_t rows,
+                     size_t words, uint32_t wb, cudaStream_t st) {
+    return wire_dispatch(ctx, true, in, out, words, wb, rows, wire_rs, word_rs, st);
+}
+int wire_pack_rows(ensi_ctx* ctx, const uint64_t* in, size_t word_rs, uint8_t* out, size_t wire_rs, uint32_t rows,
+                   size_t words, uint32_t wb, cudaStream_t st) {
+    return wire_dispatch(ctx, false, in, out, words, wb, rows, wire_rs, word_rs, st);
 }
 
 }  // namespace ensi

@@ -1,27 +1,31 @@
 #!/usr/bin/env python
 """bench.py -- ENSI ternary PCMM (Algorithm 1) on B200.
 
-Workload (BASELINE.json configs[1], "C2"): N'=2^16, L=12 RNS limbs, one 768x768 BitNet ternary PCMM
-(Layout A, the paper's column packing): 768 input ciphertexts -> 768 output ciphertexts, 9.66 GB in,
-9.66 GB out.  A step = one full layer through ensi_pcmm_ternary_packed (inputs resident in HBM; inputs
-(9.66 GB) exceed the 126 MB L2, so no flush is needed between steps).
+Workload (BASELINE.json configs[1], "C2"): N'=2^16, L=12 RNS limbs, one 768x768 BitNet ternary PCMM (Layout A, the
+paper's column packing): 768 input ciphertexts -> 768 output ciphertexts, resident in HBM in the compact word layout
+(ceil(bits/8) bytes per word: 6.24 GB in, 6.24 GB out; larger than the 126 MB L2, so no flush
+is needed between steps).  A step = one full layer through ensi_pcmm_ternary_compact (one k_accum_tcc launch).
 
 Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints ONE JSON line.
-  value       = ms per layer (lower is better).  N > 1: weak scaling over token blocks -- every rank runs
-                the layer on its own token block (its own 768 input ciphertexts, same W), no data-path
-                collective; value = max-over-ranks step time / N (whole-job layers per ms, inverted).
+  value       = ms per layer (lower is better), device time, max over ranks.  N > 1: the north star's layout, strong
+                scaling -- one layer split by output columns over the N ranks (inputs replicated), the compact outputs
+                all-gathered over NCCL in 4 chunks overlapped with the accumulate; `column_sharded` adds the shard's
+                compute alone, the gather alone and the fused-gather epilogue (R20); `token_blocks` the
+                weak-scaling mode (every rank a whole layer on its own token block, no collective).
   e2e         = the same metric through ensi_pcmm_ternary_host_wire (pinned host ciphertexts in the compact wire
-                format; the uint64-word host API is reported beside it as e2e.uint64_words): host inputs -> device -> PCMM ->
-                pinned host outputs, every copy inside the timed region (pipelined over (poly, limb) slices).
-  roofline    = the accumulate kernel (the only kernel of a Layout-A step) against its bound.
+                format): host inputs -> device -> PCMM -> pinned host outputs, every copy inside the timed region.
+  roofline    = the accumulate launch against its bound on SURVEY 8(d)'s op count (7/5 byte planes per word), with the
+                HBM fraction on its algorithmic bytes, the committed ncu DRAM traffic (profiles/traffic.json) and the
+                NTT / key-switching HBM fractions of the same run (other_kernels).
   cpu_baseline= the CPU oracle (oracle/ensi_oracle.c, as it stands) on a bounded sample of output columns,
                 extrapolated by nnz (the oracle's cost is exactly linear in nnz).
   rotations   = hoisted key-switched rotations/s at the same parameters (alpha=4, dnum=3), BASELINE metric's
                 second clause (also 32 per ModUp and independent inputs).
   clocks      = SM clock / clock-event reasons polled through NVML by a separate process inside the timed region.
-  secondary   = the other SURVEY 8 rows at C2 parameters: NTT/INTT, rescale, Layout B, Layout-A shapes of C3-C5,
-                one C5 transformer block, the paper's Table III PCMM shapes at N'=2^14, and CCMM (R18) at the
-                Table III attention shapes (a sample of output columns, extrapolated by rotation count).
+  secondary   = the other SURVEY 8 rows at C2 parameters: NTT/INTT, rescale, Layout B (and lazy ModDown, R19, before /
+                after), the C2 layer in uint64 words and on CUDA cores, the C3-C5 shapes, one C5 transformer block,
+                the paper's Table III PCMM shapes at N'=2^14, and CCMM (R18) at the Table III attention shapes.
+  --layout u64 / --kernel 1 time the uint64-word tcgen05 / CUDA-core accumulate as the headline instead.
   --no-rot / --no-layout-b / --no-ccmm / --no-e2e / --no-cpu skip parts (tests and quick runs).
 """
 from __future__ import annotations
@@ -436,15 +440,17 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
     # resident layout (the headline's), and the C2 layer in the uint64 layout (k_accum_tc2) for comparison
     sweep = {}
     wb = ctx.wire_bytes(L)
-    for name, (dd, mm) in (("C2_768x768_u64", (768, 768)), ("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)),
+    for name, (dd, mm) in (("C2_768x768_u64", (768, 768)), ("C2_768x768_cudacore", (768, 768)),
+                           ("C3_768x3072", (768, 3072)), ("C3_3072x768", (3072, 768)),
                            ("C4_2048x2048", (2048, 2048)), ("C5_2048x5504", (2048, 5504)),
                            ("C5_5504x2048", (5504, 2048)), ("C5_qkv_2048x6144", (2048, 6144))):
         W = synth.gen_W(synth.SEED_BASE + dd + mm, dd, mm)
         w = ctx.weights(W)
-        if name.endswith("_u64"):
+        if name.endswith("_u64") or name.endswith("_cudacore"):
             xs = synth.gen_words_torch(17, ctx.q, dd, L, n)
             ys = torch.empty((mm, 2, L, n), dtype=torch.int64, device="cuda")
-            fn = lambda: ctx.pcmm_ternary(xs, w, ys, level=L)  # noqa: E731
+            kern = 1 if name.endswith("_cudacore") else 0
+            fn = lambda: ctx.pcmm_ternary(xs, w, ys, level=L, kernel=kern)  # noqa: E731
             ctb = 2 * L * n * 8
         else:
             xs = gen_compact(ctx, 17, dd, L)
@@ -457,6 +463,13 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         sweep[name] = {"ms_per_layer": ms, "tensor_TOPS": ops / (ms * 1e-3) / 1e12,
                        "tensor_frac": ops / (ms * 1e-3) / 1e12 / (2.0 * peaks["bf16_tflops"]),
                        "hbm_GBps": (dd + mm) * ctb / (ms * 1e-3) / 1e9}
+        if name.endswith("_cudacore"):
+            # the CUDA-core path (north star's literal kernel): one exact DFMA per dense term-word on the FP64 pipe
+            # (64 lanes/clk/SM, B300_MICROARCH / ntt_fp.cuh), so its floor is d m (2 l N') / (64 x 148 x f_max)
+            dfma = dd * mm * 2.0 * L * n
+            fp64_peak = 64 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+            sweep[name] = {"ms_per_layer": ms, "kernel": "k_accum_ternary (FP64-pipe DFMA, opts.kernel = 1)",
+                           "fp64_frac": dfma / (ms * 1e-3) / fp64_peak, "floor_ms": 1e3 * dfma / fp64_peak}
         del xs, ys, w
         torch.cuda.empty_cache()
     out["layout_a_shapes"] = sweep

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(256, 8 / AP)
         // of the quotient)
         const uint32_t ared_fp = (uint32_t)(9007199254740991.0 / (double)(br.q - 1)) - 2;
         double* sxd = reinterpret_cast<double*>(&sx[0][0][0]);
-        __shared__ double swd[2][AKC][ATI];
+        __shared__ __align__(16) double swd[2][AKC][ATI];
         double acd[AO][AP];
 #pragma unroll
         for (int o = 0; o < AO; o++)
@@ -157,14 +157,24 @@ __global__ void __launch_bounds__(256, 8 / AP)
                     sincef = 0;
                 }
                 sincef++;
+                // 16-byte shared loads: lane holds positions 2 lane + {0, 1} + 64 j (j < AP / 2); the warp's 8 weights
+                // are 4 broadcast double2 loads
                 double xv[AP];
 #pragma unroll
-                for (int p = 0; p < AP; p++) xv[p] = sxd[(buf * AKC + r) * ATW + lane + 32 * p];
+                for (int j = 0; j < AP / 2; j++) {
+                    const double2 t2 =
+                        *reinterpret_cast<const double2*>(&sxd[(buf * AKC + r) * ATW + 2 * lane + 64 * j]);
+                    xv[2 * j] = t2.x;
+                    xv[2 * j + 1] = t2.y;
+                }
 #pragma unroll
-                for (int o = 0; o < AO; o++) {
-                    const double wv = swd[buf][r][warp * AO + o];
+                for (int o = 0; o < AO; o += 2) {
+                    const double2 w2 = *reinterpret_cast<const double2*>(&swd[buf][r][warp * AO + o]);
 #pragma unroll
-                    for (int p = 0; p < AP; p++) acd[o][p] = fma(wv, xv[p], acd[o][p]);
+                    for (int p = 0; p < AP; p++) {
+                        acd[o][p] = fma(w2.x, xv[p], acd[o][p]);
+                        acd[o + 1][p] = fma(w2.y, xv[p], acd[o + 1][p]);
+                    }
                 }
             }
             __syncthreads();
@@ -175,7 +185,10 @@ __global__ void __launch_bounds__(256, 8 / AP)
             if (i < m) {
                 uint64_t* yo = y + (uint64_t)i * ctw + pos0;
 #pragma unroll
-                for (int p = 0; p < AP; p++) yo[lane + 32 * p] = acc_canon(acd[o][p], br.q, qd, qinv);
+                for (int j = 0; j < AP / 2; j++)
+                    *reinterpret_cast<ulonglong2*>(yo + 2 * lane + 64 * j) =
+                        make_ulonglong2(acc_canon(acd[o][2 * j], br.q, qd, qinv),
+                                        acc_canon(acd[o][2 * j + 1], br.q, qd, qinv));
             }
         }
         return;

@@ -277,15 +277,17 @@ def test_pcmm_a_long_sum_lazy_reduction(setup_c1, torch_cuda, kernel):
         assert (got[i] == np.uint64((coef * (q - 1)) % q)).all()
 
 
+@pytest.mark.parametrize("bits", [(60, 59), (51, 50)])
 @pytest.mark.parametrize("kernel", [1, 2, 3, 0])
-def test_pcmm_a_wide_moduli_long_sum(torch_cuda, kernel):
+def test_pcmm_a_wide_moduli_long_sum(torch_cuda, kernel, bits):
     """Moduli just under 2^60 (the ctx maximum) with d = 8300 terms of q - 1: the CUDA-core path must reduce its
     int64 accumulators every 7 rows there (accum_rows_between_reductions), the tcgen05 path takes the 128-bit
-    combine -- closed-form expected words (sum_j W_ji) (q - 1) mod q, and == the oracle on one column."""
+    combine -- closed-form expected words (sum_j W_ji) (q - 1) mod q, and == the oracle on one column.  Moduli just
+    under 2^51 / 2^50 take the CUDA-core FP64-pipe loop at its shortest reduction interval (2 / 6 rows)."""
     from paper_2509_09424_b200 import Context
     torch = torch_cuda
     m2n = 1 << 13
-    q = [_primes_1mod(m2n, 1 << 60, 1)[0], _primes_1mod(m2n, 1 << 59, 1)[0]]
+    q = [_primes_1mod(m2n, 1 << bits[0], 1)[0], _primes_1mod(m2n, 1 << bits[1], 1)[0]]
     p = [_primes_1mod(m2n, 1 << 60, 1, skip=1)[0]]
     ctx = Context(12, 2, 1, 2, q=q, p=p)
     d, m, level = 8300, 3, 2

@@ -538,10 +538,14 @@ __global__ void k_peer_wait(const uint32_t* flags, uint32_t n, uint32_t epoch) {
     const uint32_t p = threadIdx.x;
     if (p < n) {
         uint32_t v;
+        // bounded: a peer that never signals (a crashed rank) faults this context after ~30 s instead of hanging
+        // the GPU forever
+        const long long t0 = clock64();
         for (;;) {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
             if ((int32_t)(v - epoch) >= 0) break;
-            __nanosleep(100);
+            __nanosleep(200);
+            if (clock64() - t0 > 60000000000ll) __trap();
         }
     }
     __syncthreads();

@@ -591,9 +591,10 @@ def test_pcmm_with_rescale_epilogue(setup_c1, torch_cuda):
 
 
 @pytest.mark.parametrize("L,alpha,dnum,level", [(4, 2, 2, 4), (4, 2, 2, 3), (5, 2, 3, 5)])
-def test_rotate_hoisted_n16_fused_moddown(torch_cuda, L, alpha, dnum, level):
-    """N'=2^16 takes the fused ModDown (conversion in the first NTT pass, final combine in the last) and the
-    two-digit KIP; bit-exact against the oracle at reduced limb counts."""
+def test_rotate_hoisted_n16_reduced_limbs(torch_cuda, L, alpha, dnum, level):
+    """N'=2^16 with few limbs: the FP64 key-switching kernels (constant-bank ModUp / ModDown conversions, the
+    two-digit and partial-last-digit key inner products, the separate ModDown INTT / conversion / NTT / combine
+    steps) bit-exact against the oracle, including the identity element."""
     from paper_2509_09424_b200 import Context
     torch = torch_cuda
     o = oracle.Oracle(16, L, alpha, dnum)

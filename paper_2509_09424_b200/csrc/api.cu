@@ -225,9 +225,17 @@ int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const st
     std::vector<uint64_t> gb(p.B);
     for (uint32_t b = 0; b < p.B; b++) gb[b] = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * b);
     // baby steps for all inputs at once: key-stationary (each rotation key read once for the n_in inputs)
-    int rc = rotate_hoisted_multi(ctx, x->data, p.n_in, ctw, level, p.B, gb.data(), R, p.B, st);
-    if (!rc) rc = accum_b(0, acc_out);
+    int rc;
+    {
+        NvtxRange r_("layoutB.baby_rotations");
+        rc = rotate_hoisted_multi(ctx, x->data, p.n_in, ctw, level, p.B, gb.data(), R, p.B, st);
+    }
+    if (!rc) {
+        NvtxRange r_("layoutB.accumulate");
+        rc = accum_b(0, acc_out);
+    }
     for (uint32_t gm = 1; gm < p.G && !rc; gm++) {
+        NvtxRange r_("layoutB.giant_step");
         rc = accum_b(gm, Tg);
         const uint64_t gg = galois_of_rotation(ctx->log_n, (int64_t)o.block_s * p.B * gm);
         // chunks of at most 96 outputs bound the key-switching scratch (as ensi_rotate_batch)
@@ -246,6 +254,7 @@ int layout_b_run(ensi_ctx* ctx, const ensi_ct_view* x, ensi_weights* w, const st
         }
     }
     // R19: one ModDown per output of the summed giant-step key inner products, added in place
+    NvtxRange r_lazy(lazy ? "layoutB.lazy_moddown" : "layoutB.done");
     for (uint32_t c0 = 0; lazy && c0 < m && !rc; c0 += 96) {
         const uint32_t nc = std::min<uint32_t>(96, m - c0);
         rc = lazy_moddown(ctx, La + (size_t)c0 * law, nc, level, acc_out + (size_t)c0 * ctw, st);
@@ -569,6 +578,7 @@ void ensi_weights_destroy(ensi_weights* w) {
 
 int ensi_pcmm_ternary_packed(ensi_ctx* ctx, const ensi_ct_view* x, const ensi_weights* wc, ensi_ct_view* y,
                              const ensi_pcmm_opts* opts, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.pcmm");
     if (!ctx) return ENSI_EINVAL;
     if (!wc) return set_err(ctx, ENSI_EINVAL, "NULL weights");
     ensi_weights* w = const_cast<ensi_weights*>(wc);
@@ -788,12 +798,14 @@ static int pcmm_host_impl(ensi_ctx* ctx, const void* x_host, uint32_t level, con
 
 int ensi_pcmm_ternary_host(ensi_ctx* ctx, const uint64_t* x_host, uint32_t level, double log2_scale,
                            const ensi_weights* wc, uint64_t* y_host, uint32_t kernel, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.pcmm_host");
     (void)log2_scale;
     return pcmm_host_impl(ctx, x_host, level, wc, y_host, kernel, stream, false);
 }
 
 int ensi_pcmm_ternary_host_wire(ensi_ctx* ctx, const uint8_t* x_wire, uint32_t level, double log2_scale,
                                 const ensi_weights* wc, uint8_t* y_wire, uint32_t kernel, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.pcmm_host_wire");
     (void)log2_scale;
     return pcmm_host_impl(ctx, x_wire, level, wc, y_wire, kernel, stream, true);
 }
@@ -820,6 +832,7 @@ int check_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights*
 
 int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc, ensi_compact_view* y,
                               const ensi_pcmm_opts* opts, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.pcmm_compact");
     if (!ctx) return ENSI_EINVAL;
     if (!y || !y->data) return set_err(ctx, ENSI_EINVAL, "NULL view or data");
     int rc = check_compact(ctx, x, wc, opts);
@@ -839,6 +852,7 @@ int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const e
 int ensi_pcmm_ternary_compact_gather(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights* wc,
                                      uint8_t* const* y_dst, uint32_t n_dst, uint32_t rows_total, uint32_t row0,
                                      const ensi_pcmm_opts* opts, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.pcmm_compact_gather");
     if (!ctx) return ENSI_EINVAL;
     int rc = check_compact(ctx, x, wc, opts);
     if (rc) return rc;
@@ -912,6 +926,7 @@ int ensi_ipc_close(ensi_ctx* ctx, void* dev_ptr) {
 
 int ensi_peer_signal(ensi_ctx* ctx, uint32_t* const* flags_dst, uint32_t n_dst, uint32_t slot, uint32_t epoch,
                      void* stream) {
+    ensi::NvtxRange nvtx_("ensi.peer_signal");
     if (!ctx) return ENSI_EINVAL;
     if (!flags_dst || n_dst < 1 || n_dst > 8) return set_err(ctx, ENSI_EINVAL, "flags_dst: 1..8 flag arrays");
     PeerFlags pf{};
@@ -928,6 +943,7 @@ int ensi_peer_signal(ensi_ctx* ctx, uint32_t* const* flags_dst, uint32_t n_dst, 
 }
 
 int ensi_peer_wait(ensi_ctx* ctx, const uint32_t* flags, uint32_t n, uint32_t epoch, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.peer_wait");
     if (!ctx) return ENSI_EINVAL;
     if (!flags || n < 1 || n > 32) return set_err(ctx, ENSI_EINVAL, "flags: 1..32 entries");
     DeviceGuard g(ctx->device);
@@ -976,6 +992,7 @@ int ensi_wire_unpack(ensi_ctx* ctx, const uint8_t* in, ensi_ct_view* y, void* st
 
 int ensi_ntt(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const uint32_t* limb_of_row, uint32_t period, int inverse,
              void* stream) {
+    ensi::NvtxRange nvtx_("ensi.ntt");
     if (!ctx) return ENSI_EINVAL;
     if (!data || !limb_of_row) return set_err(ctx, ENSI_EINVAL, "NULL argument");
     if (period == 0 || period > 2 * ENSI_MAXT) return set_err(ctx, ENSI_EINVAL, "period out of range");
@@ -995,6 +1012,7 @@ int ensi_ntt(ensi_ctx* ctx, uint64_t* data, uint32_t rows, const uint32_t* limb_
 
 int ensi_rotate_hoisted(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, const uint64_t* galois, ensi_ct_view* y,
                         void* stream) {
+    ensi::NvtxRange nvtx_("ensi.rotate_hoisted");
     if (!ctx) return ENSI_EINVAL;
     int rc = check_view(ctx, x, "x");
     if (rc) return rc;
@@ -1012,6 +1030,7 @@ int ensi_rotate_hoisted(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, cons
 
 int ensi_rotate_batch(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, const uint64_t* galois, ensi_ct_view* y,
                       void* stream) {
+    ensi::NvtxRange nvtx_("ensi.rotate_batch");
     if (!ctx) return ENSI_EINVAL;
     int rc = check_view(ctx, x, "x");
     if (rc) return rc;
@@ -1035,6 +1054,7 @@ int ensi_rotate_batch(ensi_ctx* ctx, const ensi_ct_view* x, uint32_t n_g, const 
 }
 
 int ensi_rescale(ensi_ctx* ctx, const ensi_ct_view* x, ensi_ct_view* y, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.rescale");
     if (!ctx) return ENSI_EINVAL;
     int rc = check_view(ctx, x, "x");
     if (rc) return rc;
@@ -1095,6 +1115,7 @@ int ensi_mul_plain(ensi_ctx* ctx, const ensi_ct_view* x, const uint64_t* pt, dou
 }
 
 int ensi_mul_relin(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* b, ensi_ct_view* y, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.mul_relin");
     if (!ctx) return ENSI_EINVAL;
     int rc = check_view(ctx, a, "a");
     if (!rc) rc = check_view(ctx, b, "b");
@@ -1124,6 +1145,7 @@ int ensi_mul_relin(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* b, 
 
 int ensi_ccmm(ensi_ctx* ctx, const ensi_ct_view* a, const ensi_ct_view* src, const uint64_t* mask_pt, ensi_ct_view* y,
               const ensi_ccmm_opts* opts, void* stream) {
+    ensi::NvtxRange nvtx_("ensi.ccmm");
     if (!ctx) return ENSI_EINVAL;
     if (!opts || !mask_pt) return set_err(ctx, ENSI_EINVAL, "NULL opts or mask");
     int rc = check_view(ctx, a, "a");

@@ -156,6 +156,7 @@ static int rotate_all(ensi_ctx* ctx, const uint64_t* x, uint32_t cnt, uint32_t l
 
 int ccmm(ensi_ctx* ctx, const uint64_t* a, const uint64_t* src, uint32_t form, uint32_t s, uint32_t d, uint32_t m,
          uint32_t level, const uint64_t* mask, uint64_t* y, uint32_t i0, uint32_t i1, cudaStream_t st) {
+    NvtxRange nvtx_("ccmm.columns");
     const uint32_t n = ctx->n, l1 = level - 1, l2 = level - 2;
     const uint32_t pi = form == 1 ? s : (1u << ilog2(2 * d - 1));     // 2^ceil(log2 d)
     const uint32_t Ba = baby_count(form == 2 ? d : m);

@@ -1,6 +1,7 @@
 // ensi_internal.h -- context and launch helpers shared by the CUDA translation units of libensi.so.
 #pragma once
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -118,6 +119,15 @@ struct ensi_ctx {
 };
 
 namespace ensi {
+
+// NVTX phase ranges (per-phase tracing).  Header-only NVTX v3: free when no tool is attached; under
+// nsys / ncu --nvtx the host-side enqueue phases of every call are labelled (ensi.*, ks.*, layoutB.*, ccmm.*).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // error helpers (api.cu)
 int set_err(ensi_ctx* ctx, int code, const std::string& msg);

@@ -1047,6 +1047,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     const uint32_t perm = (ctx->ntt_fp_ok && A <= 8) ? 1u : 0u;
     const bool own_direct = perm && beta <= 8;
     {
+        NvtxRange nvtx_modup("ks.modup");
         const size_t row_b = (size_t)level * n * 8;
         // INTT of every input's c1 into coef: out of place (the first pass reads the input rows through a TMA
         // tensor map) when the strides allow, else copy + in place
@@ -1145,6 +1146,7 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
 
     // ---- per batch of Galois elements
     for (size_t b0 = 0; b0 < idx.size(); b0 += nb) {
+        NvtxRange nvtx_batch("ks.kip_moddown_batch");
         const uint32_t bi = (uint32_t)(b0 / nb);
         cudaStream_t st = nsets == 2 ? ctx->st_ks[bi & 1] : st_caller;   // batches of a set run in order
         uint64_t* acc = set0 + (size_t)(bi % nsets) * (w_acc + w_z);

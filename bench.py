@@ -271,10 +271,11 @@ def run_reference(args, cfg_name):
     line = {"metric": METRIC, "value": v, "unit": "ms/layer", "n_gpus": args.gpus, "device": "cpu (host cores)",
             "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic uniform RNS words (data-oblivious accumulate)",
+            "vs_baseline": None, "dtype": "u64", "dtype_note": "the oracle's plain 64-bit modular adds",
+            "data": "synthetic uniform RNS words (data-oblivious accumulate)",
             "impl": "reference",
             "config": {"workload": f"{cfg_name}: {cfg['desc']}", "d": d, "m": m, "log_n": cfg["log_n"],
-                       "limbs": cfg["L"], "layout": "A"},
+                       "limbs": cfg["L"], "layout": "A (the oracle computes on uint64 words; same words)"},
             "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": nth, "kind": "oracle",
                              "sample": f"{ncols} of {m} output columns per step (all 24 RNS slices), "
                                        f"extrapolated by nnz(W)"},
@@ -741,8 +742,10 @@ def main():
 
     out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
-           "vs_baseline": None, "dtype": "u8 x s8 -> s32 byte planes (exact mod-q words)" if kernel_name != "cuda-core"
-           else "u64",
+           "vs_baseline": None, "dtype": "u8" if kernel_name != "cuda-core" else "f64",
+           "dtype_note": ("u8 word bytes x s8 weights -> exact s32 tensor-core sums, recombined to canonical mod-q words"
+                          if kernel_name != "cuda-core" else
+                          "uint64 words as exact f64 integers (DFMA on the FP64 pipe), canonical mod-q words out"),
            "data": "synthetic uniform RNS words in [0,q_r) (the accumulate is data-oblivious); BitNet absmean W",
            "config": {"workload": f"{args.config}: {cfg['desc']}", "d": d, "m": m, "log_n": cfg["log_n"],
                       "limbs": L, "layout": f"A, {layout} words" + (" (ceil(bits/8) bytes per word, DESIGN.md 3)"

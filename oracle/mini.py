@@ -17,6 +17,9 @@ rounding convention shows up as a word mismatch:
 * Rot      -- ModUp first, then sigma_g on every extended digit (O10), KIP, ModDown, + sigma_g(c0).
 * Layout B -- O11 step by step (baby rotations, Algorithm-1 partial sums, giant rotations, sum).
 * rescale  -- O12 in the coefficient domain: (c_i - t) q_{l-1}^{-1} with t the centred last limb, then NTT.
+* CCMM     -- R18 step by step (periodic copy, giant-then-baby alignment, mask + rescale, doubling replication,
+              tensor products summed, relinearisation = the key switch of d2 with no automorphism, rescale), with
+              rotations taken one at a time (hoisted rotations are the same words by the O10 definition).
 
 Ciphertexts are lists of polynomials: ct[poly][limb] = list of N' Python ints (NTT form, canonical).
 """
@@ -246,6 +249,70 @@ class Mini:
                 y = self.add(y, [self.moddown(level, la[0]), self.moddown(level, la[1])])
             ys.append(y)
         return ys
+
+    # ---------------------------------------------------------------- R18 (CCMM)
+    def mul_plain(self, ct: list, pt: list) -> list:
+        """slot-wise (NTT-domain) product of both polynomials with the plaintext pt [level][N']."""
+        return [[[x * y % self.q[i] for x, y in zip(ct[p][i], pt[i])] for i in range(len(ct[p]))] for p in range(2)]
+
+    def mul_ct(self, a: list, b: list) -> list:
+        """(a0 b0, a0 b1 + a1 b0, a1 b1), NTT domain."""
+        level = len(a[0])
+        d0 = [[x * y % self.q[i] for x, y in zip(a[0][i], b[0][i])] for i in range(level)]
+        d1 = [[(x * y + u * v) % self.q[i] for x, y, u, v in zip(a[0][i], b[1][i], a[1][i], b[0][i])]
+              for i in range(level)]
+        d2 = [[x * y % self.q[i] for x, y in zip(a[1][i], b[1][i])] for i in range(level)]
+        return [d0, d1, d2]
+
+    def relin(self, d: list, key: list) -> list:
+        """(d0 + ModDown(KIP_0), d1 + ModDown(KIP_1)) with KIP over ModUp(d2) and the relinearisation key (no
+        automorphism)."""
+        level = len(d[0])
+        ext_mod = self._ext_moduli(level)
+        ext_idx = list(range(level)) + [self.L + k for k in range(self.alpha)]
+        dig = self.modup(level, d[2])
+        ks = []
+        for j in range(2):
+            acc = [[sum(dig[t][e][k] * key[t][j][ext_idx[e]][k] for t in range(len(dig))) % r for k in range(self.n)]
+                   for e, r in enumerate(ext_mod)]
+            ks.append(self.moddown(level, acc))
+        return [[[(x + y) % self.q[i] for x, y in zip(d[j][i], ks[j][i])] for i in range(level)] for j in range(2)]
+
+    def ccmm(self, a: list, src: list, form: int, s: int, d: int, m: int, mask: list, keys: dict, rlk: list,
+             Ba: int) -> list:
+        """R18 (DESIGN.md): per output column i -- form 2: P_i = b_i, P_i += Rot(P_i, -pi 2^u) (u < log2(s/pi));
+        R_j = Rot(Rot(P_i, gam Ba), b) for j = gam Ba + b < d; form 1: R_j = Rot(Rot(k_j, gam Ba), b) for
+        i = gam Ba + b; M_j = Rescale(R_j (.) mask); M_j += Rot(M_j, -2^u) (u < log2 pi); D_i = sum_j
+        a_j|_{l-1} (x) M_j; c_i = Rescale(Relin(D_i)).  Rot(., 0) is the identity."""
+        pi = s if form == 1 else 1 << max(0, (d - 1).bit_length())
+        lg = lambda v: v.bit_length() - 1
+
+        def rot(x, r):
+            if r == 0:
+                return x
+            g = self.galois(r)
+            return self.rotate(x, g, keys[g])
+
+        out = []
+        for i in range(m):
+            if form == 2:
+                P = src[i]
+                for u in range(lg(s // pi)):
+                    P = self.add(P, rot(P, -pi * (1 << u)))
+                R = [rot(rot(P, (j // Ba) * Ba), j % Ba) for j in range(d)]
+            else:
+                R = [rot(rot(src[j], (i // Ba) * Ba), i % Ba) for j in range(d)]
+            D = None
+            for j in range(d):
+                M = self.rescale(self.mul_plain(R[j], mask))
+                for u in range(lg(pi)):
+                    M = self.add(M, rot(M, -(1 << u)))
+                aj = [[list(r) for r in a[j][p][:len(M[0])]] for p in range(2)]
+                t = self.mul_ct(aj, M)
+                D = t if D is None else [[[(x + y) % self.q[r] for x, y in zip(D[c][r], t[c][r])]
+                                          for r in range(len(t[c]))] for c in range(3)]
+            out.append(self.rescale(self.relin(D, rlk)))
+        return out
 
     # ---------------------------------------------------------------- O12
     def rescale(self, ct: list) -> list:

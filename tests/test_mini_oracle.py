@@ -202,3 +202,32 @@ def test_rescale_c_vs_mini(ks64, level):
     o, mo = ks64
     ct = np.stack([_rand(np.random.default_rng(51 + level + j), o.q[:level], o.n) for j in range(2)])
     assert _ct_list(o.rescale(ct)) == mo.rescale(_ct_list(ct))
+
+
+@pytest.mark.parametrize("form,s,d,m", [(2, 8, 4, 2), (1, 8, 3, 4), (2, 4, 1, 2)])
+def test_ccmm_c_vs_mini(form, s, d, m):
+    """R18 CCMM at N' = 64 (32 slots, s-slot head blocks; L = 4 so two levels are left for the mask and the product):
+    the oracle's CCMM (a Python driver over the C oracle's rotations, products, relinearisation and rescale) == the
+    mini-oracle's own step-by-step R18 with Python integers, every output word -- both forms with alignments that
+    need a giant AND a baby step (Ba = 2: form 2 element j = 3, form 1 column i = 3), d = 1.  (The final rescale
+    divides the relinearisation's ModDown rounding away, so this pins the R18 step order, amounts, mask and
+    products; the ModDown convention itself is pinned by the rotation and Layout-B cross-checks.)  Ciphertexts, keys and the mask are seeded uniform words (the arithmetic is
+    data-oblivious)."""
+    o, mo = _pair(6, 4, 2, 2)
+    rs = np.random.default_rng(70 + 10 * form + d)
+    level = 4
+    pi, amounts, per_out, Ba = oracle.ccmm_plan(form, s, d, m)
+    nsrc = m if form == 2 else d
+    a = np.stack([np.stack([_rand(rs, o.q, o.n) for _ in range(2)]) for _ in range(d)])
+    src = np.stack([np.stack([_rand(rs, o.q, o.n) for _ in range(2)]) for _ in range(nsrc)])
+    mask = _rand(rs, o.q, o.n)
+    keys = {o.galois(r): np.stack([np.stack([_rand(rs, o.moduli, o.n) for _ in range(2)]) for _ in range(o.dnum)])
+            for r in amounts}
+    rlk = np.stack([np.stack([_rand(rs, o.moduli, o.n) for _ in range(2)]) for _ in range(o.dnum)])
+    got = o.ccmm(a, src, form, s, d, m, mask, keys, rlk)
+    kd = {g: [[_lst(k[t, j]) for j in range(2)] for t in range(o.dnum)] for g, k in keys.items()}
+    want = mo.ccmm([_ct_list(c) for c in a], [_ct_list(c) for c in src], form, s, d, m, _lst(mask), kd,
+                   [[_lst(rlk[t, j]) for j in range(2)] for t in range(o.dnum)], Ba)
+    assert len(want) == m
+    for i in range(m):
+        assert _ct_list(got[i]) == want[i], i

@@ -29,7 +29,13 @@ static constexpr int AP = ENSI_ACC_AP;  // positions per lane
 static constexpr int AW = 8;          // warps per CTA
 static constexpr int ATI = AO * AW;   // 64 outputs per CTA
 static constexpr int ATW = 32 * AP;   // 256 positions per CTA
-static constexpr int AKC = 8;         // x rows per pipeline stage
+#ifndef ENSI_ACC_AKC
+#define ENSI_ACC_AKC 32
+#endif
+static constexpr int AKC = ENSI_ACC_AKC;   // x rows per pipeline stage (32: 160 KB of dynamic shared memory, 1 CTA/SM; measured 86 ms vs 89 at 16 and 94 at 8 rows)
+
+// dynamic shared memory layout: sx [2][AKC][ATW] uint64 | swd [2][AKC][ATI] double | ssg [2][AKC][4] uint32
+static constexpr size_t kAccSmem = (size_t)2 * AKC * ATW * 8 + (size_t)2 * AKC * ATI * 8 + (size_t)2 * AKC * 4 * 4;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -67,8 +73,11 @@ __global__ void __launch_bounds__(256, 8 / AP)
     k_accum_ternary(const uint64_t* __restrict__ x, uint32_t d, uint64_t ctw, const uint32_t* __restrict__ planes,
                     uint32_t mw, uint32_t m, uint64_t* __restrict__ y, uint32_t log_n, uint32_t level, uint32_t limb0,
                     ModTab tab, uint32_t ared) {
-    __shared__ __align__(16) uint64_t sx[2][AKC][ATW];
-    __shared__ uint32_t ssg[2][AKC][4];   // pos lo, pos hi, neg lo, neg hi (64 outputs)
+    extern __shared__ __align__(16) uint8_t acc_smem[];
+    uint64_t (*sx)[AKC][ATW] = reinterpret_cast<uint64_t (*)[AKC][ATW]>(acc_smem);
+    double (*swd)[AKC][ATI] = reinterpret_cast<double (*)[AKC][ATI]>(acc_smem + (size_t)2 * AKC * ATW * 8);
+    uint32_t (*ssg)[AKC][4] = reinterpret_cast<uint32_t (*)[AKC][4]>(acc_smem + (size_t)2 * AKC * ATW * 8 +
+                                                                     (size_t)2 * AKC * ATI * 8);   // pos lo/hi, neg lo/hi
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t i0 = blockIdx.x * ATI;
     const uint64_t pos0 = (uint64_t)blockIdx.y * ATW;
@@ -118,7 +127,6 @@ __global__ void __launch_bounds__(256, 8 / AP)
         // of the quotient)
         const uint32_t ared_fp = (uint32_t)(9007199254740991.0 / (double)(br.q - 1)) - 2;
         double* sxd = reinterpret_cast<double*>(&sx[0][0][0]);
-        __shared__ __align__(16) double swd[2][AKC][ATI];
         double acd[AO][AP];
 #pragma unroll
         for (int o = 0; o < AO; o++)
@@ -260,7 +268,9 @@ int accum_ternary(ensi_ctx* ctx, const uint64_t* x, uint32_t d, const uint32_t* 
     if (ctw == 0) ctw = (uint64_t)2 * level * ctx->n;
     if (ctw % ATW) return set_err(ctx, ENSI_EINVAL, "ring too small for the accumulate tile");
     dim3 grid((m + ATI - 1) / ATI, (uint32_t)(ctw / ATW));
-    k_accum_ternary<<<grid, 256, 0, st>>>(x, d, ctw, planes, mw, m, y, ctx->log_n, level, limb0, ctx->tab,
+    cudaError_t ea = cudaFuncSetAttribute(k_accum_ternary, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAccSmem);
+    if (ea != cudaSuccess) return cuda_err(ctx, ea, "accum_ternary smem attribute");
+    k_accum_ternary<<<grid, 256, kAccSmem, st>>>(x, d, ctw, planes, mw, m, y, ctx->log_n, level, limb0, ctx->tab,
                                           accum_rows_between_reductions(ctx, level));
     ENSI_LAUNCH_CHECK(ctx);
     cudaError_t e = cudaGetLastError();

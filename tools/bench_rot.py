@@ -15,6 +15,15 @@ L, A, dnum, n, s = cfg["L"], cfg["alpha"], cfg["dnum"], 1 << cfg["log_n"], cfg["
 ctx = Context(cfg["log_n"], L, A, dnum)
 st = torch.cuda.current_stream()
 out = {}
+rows = 768
+data = torch.empty((rows, n), dtype=torch.int64, device="cuda")
+for lim in range(L + A):
+    data[lim::L + A].random_(0, ctx.moduli[lim])
+for name, inv in (("ntt_fwd_us", False), ("ntt_inv_us", True)):
+    for _ in range(3):
+        ctx.ntt(data, list(range(L + A)), inverse=inv)
+    out[name] = 1e3 * time_loop(lambda: ctx.ntt(data, list(range(L + A)), inverse=inv), 20, st) / rows
+del data
 x = synth.gen_words_torch(11, ctx.q, 1, L, n)
 for batch in (128, 32):
     gs = [pow(5, s * (b + 1), 2 * n) for b in range(batch)]

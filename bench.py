@@ -636,6 +636,74 @@ def committed_traffic(kname: str, config: str, d: int, m: int):
     return {"traffic": None, "traffic_source": None}
 
 
+def cross_kernel_check(ctx, W, L, n):
+    """Bit-exact flag without the oracle (bench's GPU leg never runs it): the C2 layer through the three independent
+    accumulate kernels -- compact tcgen05, uint64 tcgen05, CUDA cores (FP64 pipe) -- on the same words; every word of
+    a strided sample of all outputs must agree.  (The oracle pins all three in tests/.)"""
+    import torch
+    d, m = W.shape
+    w = ctx.weights(W)
+    x = synth.gen_words_torch(synth.SEED_BASE + 77, ctx.q, d, L, n)
+    y1 = torch.empty((m, 2, L, n), dtype=torch.int64, device="cuda")
+    y2 = torch.empty_like(y1)
+    ctx.pcmm_ternary(x, w, y1, level=L, kernel=2)
+    ctx.pcmm_ternary(x, w, y2, level=L, kernel=1)
+    wb = ctx.wire_bytes(L)
+    xc = torch.empty((d, wb), dtype=torch.uint8, device="cuda")
+    ctx.wire_pack(x, xc, L)
+    del x
+    yc = torch.empty((m, wb), dtype=torch.uint8, device="cuda")
+    ctx.pcmm_ternary_compact(xc, w, yc, level=L)
+    del xc
+    y3 = torch.empty_like(y2)
+    ctx.wire_unpack(yc, y3, L)
+    torch.cuda.synchronize()
+    ok = bool((y1[:, :, :, ::97] == y2[:, :, :, ::97]).all()) and bool((y1[:, :, :, ::97] == y3[:, :, :, ::97]).all())
+    del y1, y2, y3, yc
+    torch.cuda.empty_cache()
+    return ok
+
+
+def write_jsonl(path, out, ctx, W, L, n):
+    """One record per (config, GPUs, kernel) row of the bench line: time, bytes, GB/s, HBM / tensor fractions,
+    rotations/s, and a cross-kernel bit-exact flag for the C2 layer (SURVEY 5 "Metrics / logging")."""
+    recs = []
+    G = out["n_gpus"]
+    rf = out["roofline"]
+    recs.append({"config": "C2 768x768", "G": G, "kernel": rf["kernel"], "ms": out["value"],
+                 "bytes": rf["algorithmic_bytes"], "GBps": rf["hbm_gbs"], "hbm_frac": rf["hbm_frac"],
+                 "tensor_frac": rf.get("tensor_frac"), "bit_exact_vs_other_kernels": cross_kernel_check(ctx, W, L, n)})
+    sec = out.get("secondary", {})
+    for name, r in sec.get("layout_a_shapes", {}).items():
+        recs.append({"config": name, "G": 1, "kernel": r.get("kernel", "k_accum_tcc" if "_u64" not in name and
+                                                            "_cudacore" not in name else "k_accum_tc2"),
+                     "ms": r["ms_per_layer"], "GBps": r.get("hbm_GBps"), "tensor_frac": r.get("tensor_frac"),
+                     "fp64_frac": r.get("fp64_frac")})
+    for name in ("ntt_forward", "ntt_inverse"):
+        if name in sec:
+            recs.append({"config": "C2 params, 768 limb rows", "G": 1, "kernel": name, "us_per_limb":
+                         sec[name]["us_per_limb"], "GBps": sec[name]["achieved_GBps"], "hbm_frac": sec[name]["hbm_frac"]})
+    if "rotations_per_sec" in out:
+        r = out["rotations_per_sec"]
+        recs.append({"config": "C2 params", "G": 1, "kernel": "rotate_hoisted (128 per ModUp)",
+                     "rotations_per_s": r["value"], "hbm_frac": r.get("hbm_frac")})
+        recs.append({"config": "C2 params", "G": 1, "kernel": "rotate_batch (independent inputs)",
+                     "rotations_per_s": r["independent_inputs"]["value"],
+                     "hbm_frac": r["independent_inputs"].get("hbm_frac")})
+    if "pcmm_layout_b" in sec:
+        recs.append({"config": "C2 768x768 Layout B", "G": 1, "kernel": "layout_b", "ms": sec["pcmm_layout_b"]["value"],
+                     "rotations_per_s": sec["pcmm_layout_b"]["rotations_per_sec"]})
+    for name, r in sec.get("layout_b_lazy_moddown", {}).items():
+        recs.append({"config": name, "G": 1, "kernel": "layout_b eager / lazy ModDown", "ms": r["eager_ms"],
+                     "ms_lazy": r["lazy_ms"]})
+    if "e2e" in out:
+        recs.append({"config": "C2 768x768 e2e", "G": G, "kernel": "ensi_pcmm_ternary_host_wire",
+                     "ms": out["e2e"]["value"], "bytes": out["e2e"]["h2d_bytes_per_step"] + out["e2e"]["d2h_bytes_per_step"]})
+    with open(path, "w") as f:
+        for r in recs:
+            f.write(json.dumps(r) + "\n")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -651,6 +719,8 @@ def main():
     ap.add_argument("--no-rot", action="store_true", help="skip the secondary rows (NTT, rotations, rescale, Layout B)")
     ap.add_argument("--no-layout-b", action="store_true")
     ap.add_argument("--no-ccmm", action="store_true", help="skip the CCMM row (SURVEY 8(f) NEXT #3)")
+    ap.add_argument("--jsonl", default=None,
+                    help="also write one JSON record per (config, GPUs, kernel) row to this file (SURVEY 5 metrics)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)
@@ -857,6 +927,8 @@ def main():
                                             "sample": f"2 of {m} output columns ({dt_1:.1f} s wall), "
                                                       f"extrapolated by nnz"},
                                "cpu_model": _cpu_model()}
+    if rank == 0 and args.jsonl:
+        write_jsonl(args.jsonl, out, ctx, W, L, n)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if sharded:

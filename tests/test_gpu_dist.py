@@ -101,9 +101,10 @@ def test_column_sharded_compact_nccl_world1(torch_cuda):
 
 @pytest.mark.slow
 def test_bench_under_torchrun_nccl(torch_cuda):
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1", "--steps", "3", "--warmup", "3",
-           "--no-cpu", "--no-e2e", "--no-rot"]
+           "--no-cpu", "--no-e2e", "--no-rot", "--jsonl", os.path.join(ROOT, "gpurun_out", "bench_test.jsonl")]
     env = dict(os.environ, ENSI_BENCH_COLSHARD="1")          # run the column-sharded (all-gather) leg at N=1 too
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -115,6 +116,8 @@ def test_bench_under_torchrun_nccl(torch_cuda):
     assert out["column_sharded"]["gather_ms"] > 0 and out["column_sharded"]["compute_ms"] > 0
     assert out["column_sharded"]["fused_gather_ms"] > 0
     assert out["token_blocks"]["value"] > 0
+    recs = [json.loads(ln) for ln in open(os.path.join(ROOT, "gpurun_out", "bench_test.jsonl"))]
+    assert recs[0]["kernel"] == "k_accum_tcc" and recs[0]["bit_exact_vs_other_kernels"] is True
 
 
 def _c1_compact(torch, seed, d, m, level=3):

@@ -203,3 +203,31 @@ def test_compact_errors(c1, torch_cuda):
     with pytest.raises(EnsiError) as e:
         ctx.pcmm_ternary_compact(x[:2], ctx.weights(synth.gen_W(2, 2, 2)), x[1:3], level=3)
     assert e.value.code == ENSI_EINVAL
+
+
+@pytest.mark.parametrize("d,m", [(768, 3072), (3072, 768), (2048, 2048), (2048, 5504), (5504, 2048), (2048, 6144)])
+def test_compact_bench_shapes_sampled_columns(torch_cuda, d, m):
+    """Every C3-C5 shape bench.py times on the compact layout (layout_a_shapes) at full size, in the launch
+    configuration it times (one ensi_pcmm_ternary_compact call): 768->3072 (4 pairs per cluster, resident W^T),
+    3072->768 and 5504->2048 (streamed W^T, 24 / 43 K blocks), 2048^2, 2048->5504 (2 pairs per cluster) and the fused
+    Q/K/V 2048->6144 -- sampled output columns == the oracle's Algorithm 1, word for word."""
+    from paper_2509_09424_b200 import Context
+    from paper_2509_09424_b200.ensi import wire_unpack_host
+    torch = torch_cuda
+    ctx = Context(16, 12, 4, 3)
+    o = oracle.Oracle(16, 12, 4, 3)
+    xd = synth.gen_words_torch(synth.SEED_BASE + 5 + d, ctx.q, d, 12, ctx.n)
+    W = synth.gen_W(synth.SEED_BASE + 6 + m, d, m)
+    wb = ctx.wire_bytes(12)
+    xc = torch.empty((d, wb), dtype=torch.uint8, device="cuda")
+    ctx.wire_pack(xd, xc, 12)
+    x = xd.cpu().numpy().view(np.uint64)
+    del xd
+    yc = torch.empty((m, wb), dtype=torch.uint8, device="cuda")
+    ctx.pcmm_ternary_compact(xc, ctx.weights(W), yc, level=12)
+    torch.cuda.synchronize()
+    cols = [0, m // 2 + 7, m - 1]
+    got = wire_unpack_host(yc[cols].cpu().numpy(), ctx.wire_widths(12), 12, ctx.n)
+    del xc, yc
+    torch.cuda.empty_cache()
+    assert (got == o.pcmm_a(x, W, cols=cols, nthreads=NTH)).all()

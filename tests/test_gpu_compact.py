@@ -231,3 +231,23 @@ def test_compact_bench_shapes_sampled_columns(torch_cuda, d, m):
     del xc, yc
     torch.cuda.empty_cache()
     assert (got == o.pcmm_a(x, W, cols=cols, nthreads=NTH)).all()
+
+
+@pytest.mark.parametrize("d,m", [(1536, 1536), (4096, 1536)])
+def test_compact_paper_table3_shapes_n14(torch_cuda, d, m):
+    """Two of the paper's Table III PCMM shapes at its default ring N' = 2^14, l = 12 (bench.py paper_table3_n14 on the
+    compact layout): Q/K/V 1536x1536 and down 4096->1536, sampled columns == the oracle."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    ctx = Context(14, 12, 4, 3)
+    o = oracle.Oracle(14, 12, 4, 3)
+    x = synth.gen_words(15000 + d, o.q, d, 12, o.n)
+    W = synth.gen_W(15001 + m, d, m)
+    from paper_2509_09424_b200.ensi import wire_unpack_host
+    xc = _compact_dev(torch, ctx, x, 12)
+    yc = torch.empty((m, ctx.wire_bytes(12)), dtype=torch.uint8, device="cuda")
+    ctx.pcmm_ternary_compact(xc, ctx.weights(W), yc, level=12)
+    torch.cuda.synchronize()
+    cols = [0, 777, m - 1]
+    got = wire_unpack_host(yc[cols].cpu().numpy(), ctx.wire_widths(12), 12, ctx.n)
+    assert (got == o.pcmm_a(x, W, cols=cols, nthreads=NTH)).all()

@@ -252,7 +252,8 @@ def test_layout_b_lazy_moddown_full_size(c2, torch_cuda, d, m, baby, cols):
     giant rotation per output the lazy form IS the eager one, checked on every output word) and 768 -> 768 with
     B = 64 (G = 4: 189 baby + 2304 giant rotations, three giant steps summed over Q_l u P per output, 8 chunks of
     96 outputs split over the two internal streams).  Seeded uniform words and keys (the path is data-oblivious);
-    sampled output columns == the oracle's lazy O11 word for word."""
+    sampled output columns == the oracle's lazy O11 word for word, and the eager form (both timed by bench.py's
+    layout_b_lazy_moddown row) == the oracle's eager O11."""
     o, sk, pk, ctx = c2
     torch = torch_cuda
     from paper_2509_09424_b200 import Context
@@ -270,12 +271,13 @@ def test_layout_b_lazy_moddown_full_size(c2, torch_cuda, d, m, baby, cols):
     bctx.pcmm_ternary(_dev(torch, x), w, yd, level=12, layout=1, block_s=s, baby=B, moddown_lazy=True)
     torch.cuda.synchronize()
     got = yd[cols].cpu().numpy().view(np.uint64)
+    ye = torch.empty_like(yd)
+    bctx.pcmm_ternary(_dev(torch, x), w, ye, level=12, layout=1, block_s=s, baby=B)     # the eager form bench times
+    torch.cuda.synchronize()
     if G <= 2:
-        ye = torch.empty_like(yd)
-        bctx.pcmm_ternary(_dev(torch, x), w, ye, level=12, layout=1, block_s=s, baby=B)
-        torch.cuda.synchronize()
         assert torch.equal(yd, ye)
-        del ye
+    got_e = ye[cols].cpu().numpy().view(np.uint64)
+    del ye
     del yd
     bctx.close()
     kh = keys.cpu().numpy().view(np.uint64)
@@ -283,6 +285,8 @@ def test_layout_b_lazy_moddown_full_size(c2, torch_cuda, d, m, baby, cols):
     torch.cuda.empty_cache()
     want = o.pcmm_b(x, W, s, k, B, gk, kh, cols=cols, nthreads=NTH, lazy=True)
     assert (got == want).all()
+    if G > 2:
+        assert (got_e == o.pcmm_b(x, W, s, k, B, gk, kh, cols=cols, nthreads=NTH)).all()
 
 
 def test_c2_integer_ntt_and_keyswitch_wide_moduli(torch_cuda):

@@ -31,6 +31,19 @@ __device__ __forceinline__ void bfly_fp(double& U, double& V, double w, double w
     V = U - 2.0 * r;                     // (U + r) - 2r = U - r
 }
 
+// Hybrid butterfly: the quotient estimate on the FP64 pipe, the exact remainder V w - t q in 64-bit integers (IMAD on
+// the FMA pipe), the butterfly adds back in FP64 -- moves ~half of the FP64 work to the idle integer pipes.
+__device__ __forceinline__ void bfly_hyb(double& U, double& V, long long wi, double wq, long long qi) {
+    const double M = 6755399441055744.0;
+    const long long Mb = 0x4338000000000000ll;
+    const long long ti = __double_as_longlong(fma(V, wq, M)) - Mb;       // rint(V w / q) as an integer
+    const long long vi = __double_as_longlong(V + M) - Mb;               // V as an integer (|V| < 2^51)
+    const long long ri = vi * wi - ti * qi;                               // exact in 64 bits (|r| < 2^62)
+    const double r = __longlong_as_double(Mb + ri) - M;
+    U = U + r;
+    V = U - 2.0 * r;
+}
+
 template <int MODE>
 __global__ void k_bench(uint64_t* io, const TW* tw, uint64_t q, int passes, int check) {
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,6 +66,37 @@ __global__ void k_bench(uint64_t* io, const TW* tw, uint64_t q, int passes, int 
             for (int k = 0; k < 16; k++) { uint64_t x = v[k] >= q2 ? v[k] - q2 : v[k]; v[k] = x >= q2 ? x - q2 : x; }
         }
         for (int k = 0; k < 16; k++) { uint64_t x = v[k] % q; io[tid * 16 + k] = x; }
+    } else if (MODE == 2) {
+        // alternate stages: pure FP64 on even k-groups, hybrid on odd (both kinds of work in flight)
+        double v[16];
+        const double qd = (double)q, qinv = 1.0 / qd, M = 6755399441055744.0;
+        long long wi[8];
+        for (int i = 0; i < 8; i++) wi[i] = (long long)T.wd[i];
+        for (int k = 0; k < 16; k++) v[k] = (double)io[tid * 16 + k];
+        for (int p = 0; p < passes; p++) {
+#pragma unroll
+            for (int rep = 0; rep < 2; rep++)
+#pragma unroll
+                for (int s = 0; s < 4; s++) {
+                    const int span = 8 >> s;
+#pragma unroll
+                    for (int k = 0; k < 16; k++)
+                        if (!(k & span)) {
+                            const int ti = (s + 4 * rep + k) & 7;
+                            if (k & 1) bfly_hyb(v[k], v[k + span], wi[ti], T.wq[ti], (long long)q);
+                            else bfly_fp(v[k], v[k + span], T.wd[ti], T.wq[ti], qd);
+                        }
+                }
+#pragma unroll
+            for (int k = 0; k < 16; k++) { double t = fma(v[k], qinv, M) - M; v[k] = fma(-t, qd, v[k]); }
+        }
+        for (int k = 0; k < 16; k++) {
+            double x = v[k];
+            long long xi = (long long)x;
+            long long r = xi % (long long)q;
+            if (r < 0) r += q;
+            io[tid * 16 + k] = (uint64_t)r;
+        }
     } else {
         double v[16];
         const double qd = (double)q, qinv = 1.0 / qd, M = 6755399441055744.0;
@@ -132,20 +176,34 @@ int main() {
         for (int k = 0; k < 16; k++) badh += v[k] != a[k];
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         const int passes = 64;
-        float ms[2];
-        for (int mode = 0; mode < 2; mode++) {
+        float ms[3];
+        {   // hybrid correctness (2 passes) against the FP64 variant
+            uint64_t* d2; CK(cudaMalloc(&d2, h.size() * 8));
+            CK(cudaMemcpy(d2, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+            k_bench<2><<<threads / 256, 256>>>(d2, dt, q, 2, 1);
+            CK(cudaDeviceSynchronize());
+            std::vector<uint64_t> c(h.size());
+            CK(cudaMemcpy(c.data(), d2, h.size() * 8, cudaMemcpyDeviceToHost));
+            size_t bad2 = 0;
+            for (size_t i = 0; i < c.size(); i++) bad2 += c[i] != b[i];
+            printf("hybrid vs fp64 mismatches: %zu\n", bad2);
+            cudaFree(d2);
+        }
+        for (int mode = 0; mode < 3; mode++) {
             for (int it = 0; it < 2; it++) {
                 cudaEventRecord(e0);
                 if (mode == 0) k_bench<0><<<threads / 256, 256>>>(d0, dt, q, passes, 0);
-                else k_bench<1><<<threads / 256, 256>>>(d1, dt, q, passes, 0);
+                else if (mode == 1) k_bench<1><<<threads / 256, 256>>>(d1, dt, q, passes, 0);
+                else k_bench<2><<<threads / 256, 256>>>(d1, dt, q, passes, 0);
                 cudaEventRecord(e1);
                 CK(cudaEventSynchronize(e1));
                 cudaEventElapsedTime(&ms[mode], e0, e1);
             }
         }
         double bfly = (double)threads * passes * 8 * 8;
-        printf("q=%llu (%d-bit): mismatches int-vs-fp %zu, int-vs-host %zu | int %.3f ms %.1f Gbfly/s | fp64 %.3f ms %.1f Gbfly/s\n",
-               (unsigned long long)q, pi ? 50 : 40, bad, badh, ms[0], bfly / ms[0] / 1e6, ms[1], bfly / ms[1] / 1e6);
+        printf("q=%llu (%d-bit): mismatches int-vs-fp %zu, int-vs-host %zu | int %.3f ms %.1f Gbfly/s | fp64 %.3f ms %.1f Gbfly/s | hybrid %.3f ms %.1f Gbfly/s\n",
+               (unsigned long long)q, pi ? 50 : 40, bad, badh, ms[0], bfly / ms[0] / 1e6, ms[1], bfly / ms[1] / 1e6,
+               ms[2], bfly / ms[2] / 1e6);
         cudaFree(d0); cudaFree(d1); cudaFree(dt);
     }
     return 0;

@@ -223,3 +223,38 @@ def test_fused_gather_through_cuda_ipc_from_another_process(torch_cuda):
     assert (h[:row0] == 0x5A).all() and (h[row0 + m:] == 0x5A).all()
     assert int(flags[1]) == 7 and int(flags[0]) == 0
     del pad
+
+
+def test_fused_gather_error_paths(torch_cuda):
+    """ensi_pcmm_ternary_compact_gather / ensi_ipc_* / ensi_peer_* validate before touching the device: too many or
+    NULL destinations, a destination aliasing x, an unknown pointer for ipc_close, flag counts out of range."""
+    torch = torch_cuda
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_EINVAL
+    o, ctx, x, W, xc = _c1_compact(torch, 93, 8, 4)
+    w = ctx.weights(W)
+    wb = ctx.wire_bytes(3)
+    buf = torch.zeros((8, wb), dtype=torch.uint8, device="cuda")
+    for dsts in ([buf] * 9, [0]):
+        with pytest.raises(EnsiError) as e:
+            ctx.pcmm_ternary_compact_gather(xc, w, dsts, 8, 0, 3)
+        assert e.value.code == ENSI_EINVAL
+    with pytest.raises(EnsiError) as e:                          # the destination is x itself
+        ctx.pcmm_ternary_compact_gather(xc, w, [xc.data_ptr()], 8, 0, 3)
+    assert e.value.code == ENSI_EINVAL
+    with pytest.raises(EnsiError) as e:
+        ctx.ipc_close(buf.data_ptr())
+    assert e.value.code == ENSI_EINVAL
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(EnsiError) as e:
+        ctx.peer_signal([flags] * 9, 0, 1)
+    assert e.value.code == ENSI_EINVAL
+    with pytest.raises(EnsiError) as e:
+        ctx.peer_wait(flags, 0, 1)
+    assert e.value.code == ENSI_EINVAL
+    ctx.peer_signal([flags], 2, 5)                              # a valid signal / wait pair on one GPU
+    flags[0] = 5
+    flags[1] = 5
+    flags[3] = 5
+    ctx.peer_wait(flags, 4, 5)
+    torch.cuda.synchronize()
+    assert flags.tolist() == [5, 5, 5, 5]

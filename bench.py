@@ -419,7 +419,8 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         # projection on its default plan (G = 2: one giant rotation per output, lazy == eager) and the C2 layer with
         # B = 64 (G = 4: three giant steps per output summed over Q_l u P, one ModDown instead of three)
         lz = {}
-        for name, (dd, mm, bb) in (("C3_down_3072x768_default", (3072, 768, 0)), ("C2_768x768_B64", (768, 768, 64))):
+        for name, (dd, mm, bb) in (("C3_down_3072x768_default", (3072, 768, 0)), ("C2_768x768_B64", (768, 768, 64)),
+                                   ("C2_768x768_B32", (768, 768, 32))):
             kk, nin, B, G, rots = layout_b_plan(n, s, dd, mm, bb)
             gkb = sorted({pow(5, s * b, 2 * n) for b in range(1, B)} | {pow(5, s * B * g, 2 * n) for g in range(1, G)})
             keys = _random_keys(ctx, gkb, cfg, n)

@@ -490,7 +490,9 @@ __global__ void __launch_bounds__(kT, 4) k_kip_fpt2(const uint64_t* __restrict__
                                                     uint64_t* __restrict__ acc, GBatch gb, uint32_t log_n,
                                                     uint32_t level, uint32_t L, uint32_t A, uint32_t dnum, ModTab tab,
                                                     uint64_t ext_stride, uint32_t perm, uint32_t limb_major,
-                                                    const uint64_t* __restrict__ c1p, uint64_t in_stride) {
+                                                    const uint64_t* __restrict__ c1p, uint64_t in_stride,
+                                                    uint32_t accum_out) {
+    // accum_out (R19 lazy ModDown): acc already holds canonical partial sums over Q_l u P; add them (in place)
     const uint32_t n = 1u << log_n, E = level + A, T = L + A;
     const uint32_t e = limb_major ? blockIdx.z : blockIdx.y, gi = limb_major ? blockIdx.y : blockIdx.z;
     const uint32_t li = e < level ? e : L + (e - level);
@@ -526,6 +528,11 @@ __global__ void __launch_bounds__(kT, 4) k_kip_fpt2(const uint64_t* __restrict__
             s1a += kip_mul(da, k1a[t], qd, qinv);
             s0b += kip_mul(db, k0b[t], qd, qinv);
             s1b += kip_mul(db, k1b[t], qd, qinv);
+        }
+        if (accum_out) {
+            const ulonglong2 p0 = *reinterpret_cast<const ulonglong2*>(o), p1 = *reinterpret_cast<const ulonglong2*>(o + en);
+            s0a += nttfp::i2d((long long)p0.x), s0b += nttfp::i2d((long long)p0.y);
+            s1a += nttfp::i2d((long long)p1.x), s1b += nttfp::i2d((long long)p1.y);
         }
         *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(nttfp::canon(nttfp::red(s0a, qd, qinv), q),
                                                              nttfp::canon(nttfp::red(s0b, qd, qinv), q));
@@ -827,15 +834,18 @@ __global__ void __launch_bounds__(kT) k_lazy_accum(const uint64_t* __restrict__ 
                                                    const uint64_t* __restrict__ ct, uint64_t* out,
                                                    const uint64_t* add_src, uint64_t add_stride, GBatch gb,
                                                    uint32_t log_n, uint32_t level, uint32_t A, uint32_t L, ModTab tab,
-                                                   uint32_t init) {
+                                                   uint32_t init, uint32_t c0_only) {
+    // c0_only: the key inner product already summed into la (k_kip_fpt2 accum_out); only the sigma_g(c0) add is left
     const uint32_t n = 1u << log_n, E = level + A;
     const uint32_t e = blockIdx.y, gj = blockIdx.z, j = gj & 1, c = gj >> 1;
     const uint32_t k = blockIdx.x * kT + threadIdx.x;
     const uint64_t r = tab.q[e < level ? e : L + (e - level)];
     const size_t o = ((size_t)gj * E + e) * n + k;
-    uint64_t v = acc[o];
-    if (!init) v = add_mod(v, la[o], r);
-    la[o] = v;
+    if (!c0_only) {
+        uint64_t v = acc[o];
+        if (!init) v = add_mod(v, la[o], r);
+        la[o] = v;
+    }
     if (j == 0 && e < level) {
         const uint64_t s = ct[c * gb.in_stride + (size_t)e * n + galois_src_index(k, gb.g[0], log_n)];
         const uint64_t* ab = (add_src ? add_src + c * add_stride : ct + c * gb.in_stride) + (size_t)e * n;
@@ -1163,6 +1173,15 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
         gb.out_c_stride = out_c_stride;
         gb.in_stride = in_stride;
         const uint32_t nr = n_ct * cnt;   // rotations in this batch
+        // R19: the two-position FP64 key inner product sums straight into the lazy accumulator (read-add-write), so
+        // the batch's acc is never written and re-read; other KIP kernels keep acc and k_lazy_accum adds it
+        const bool kip_lazy = ko.lazy_acc != nullptr;
+        uint64_t* kip_out = kip_lazy ? ko.lazy_acc : acc;
+        const uint32_t kip_accum = kip_lazy && !ko.lazy_init ? 1u : 0u;
+        bool kip_fused_lazy = false;
+        if (kip_lazy && !(ctx->ntt_fp_ok && beta <= 4 && n >= 2 * kT)) {
+            kip_out = acc;                 // the k_kip_fpt2 path is not taken: unfused lazy accumulate below
+        }
         {
             dim3 g(n / kT, E, cnt);
             if (ctx->ntt_fp_ok && beta <= 8) {
@@ -1175,8 +1194,9 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
     case B:                                                                                                            \
         if (n >= 2 * kT) {                                                                                             \
             dim3 g2(gk.x / 2, gk.y, gk.z);                                                                             \
-            k_kip_fpt2<B><<<g2, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,         \
-                                             ctx->tab, w_ext1, pm, lm, c1p, in_stride);                                \
+            k_kip_fpt2<B><<<g2, kT, 0, st>>>(ext, keys_base, kip_out, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,     \
+                                             ctx->tab, w_ext1, pm, lm, c1p, in_stride, kip_accum);                     \
+            kip_fused_lazy = kip_lazy;                                                                                 \
         } else {                                                                                                       \
             k_kip_fpt<B><<<gk, kT, 0, st>>>(ext, keys_base, acc, gb, ctx->log_n, level, ctx->L, A, ctx->dnum,          \
                                             ctx->tab, w_ext1, pm, lm, c1p, in_stride);                                 \
@@ -1198,11 +1218,12 @@ int rotate_hoisted_multi(ensi_ctx* ctx, const uint64_t* ct, uint32_t n_ct, uint6
             ENSI_LAUNCH_CHECK(ctx);
         }
         if (ko.lazy_acc) {
-            // R19: sum this giant step's key inner product into the lazy accumulator (Q_l u P) and add
-            // (sigma_g(c0), 0) to the output now; the one ModDown per output runs in lazy_moddown
-            dim3 g(n / kT, E, nr * 2);
+            // R19: sum this giant step's key inner product into the lazy accumulator (Q_l u P) -- done by the KIP
+            // itself when kip_fused_lazy -- and add (sigma_g(c0), 0) to the output now; the one ModDown per output
+            // runs in lazy_moddown
+            dim3 g(n / kT, kip_fused_lazy ? level : E, nr * 2);
             k_lazy_accum<<<g, kT, 0, st>>>(acc, ko.lazy_acc, ct, out, ko.add_src, ko.add_stride, gb, ctx->log_n, level,
-                                          A, ctx->L, ctx->tab, ko.lazy_init ? 1u : 0u);
+                                          A, ctx->L, ctx->tab, ko.lazy_init ? 1u : 0u, kip_fused_lazy ? 1u : 0u);
             ENSI_LAUNCH_CHECK(ctx);
             continue;
         }

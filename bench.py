@@ -465,6 +465,9 @@ def bench_secondary(ctx_cls, cfg, steps: int, warmup: int, peaks, layout_b: bool
         sweep[name] = {"ms_per_layer": ms, "tensor_TOPS": ops / (ms * 1e-3) / 1e12,
                        "tensor_frac": ops / (ms * 1e-3) / 1e12 / (2.0 * peaks["bf16_tflops"]),
                        "hbm_GBps": (dd + mm) * ctb / (ms * 1e-3) / 1e9}
+        if ctb == wb:
+            cp, kc = ctx.last_compact_plan()
+            sweep[name]["launch"] = {"cluster_pairs": cp, "clusters": kc, "sms": 2 * cp * kc}
         if name.endswith("_cudacore"):
             # the CUDA-core path (north star's literal kernel): one exact DFMA per dense term-word on the FP64 pipe
             # (64 lanes/clk/SM, B300_MICROARCH / ntt_fp.cuh), so its floor is d m (2 l N') / (64 x 148 x f_max)
@@ -810,6 +813,9 @@ def main():
     roofline = accum_roofline(ctx, d_k, m_k, int(np.count_nonzero(sh._W_np)), L, ms_kernel, peaks, peak_src, layout, kernel_name, args.config)
     roofline["launches_per_step"] = launches / args.steps
     roofline["ms_per_launch"] = ms_kernel
+    if layout == "compact":
+        cp, kc = ctx.last_compact_plan()
+        roofline["launch"] = {"cluster_pairs": cp, "clusters": kc, "sms": 2 * cp * kc}
 
     out = {"metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",

@@ -16,6 +16,9 @@
 // w planes of each word (64-bit Barrett for w = 5, 128-bit otherwise), pack the canonical words back to w bytes,
 // and stage one [32 outputs][N bytes] row block that a single TMA store writes.
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "tc_ptx.cuh"
 
@@ -180,7 +183,8 @@ template <bool A_RES, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_accum_tcc(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 const __grid_constant__ StoreMaps maps, const __grid_constant__ Tiles tl, uint32_t kblocks,
-                uint32_t pgroups, uint32_t per_group, uint32_t ntiles, ModTab tab, tc::EpiConst ec, uint32_t cpairs) {
+                uint32_t ntiles, uint32_t nsg, uint32_t tmajor, uint32_t nclust, ModTab tab, tc::EpiConst ec,
+                uint32_t cpairs) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages * kABox;
@@ -193,16 +197,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = bars + 2 * kStages;      // [2]        (per CTA, multicast commits)
     uint64_t* tempty = tfull + 2;              // [2]        (leader's: 16 arrivals)
     uint64_t* afull = tempty + 2;              // [1]        (leader's)
-    uint32_t* tmem_slot = (uint32_t*)(afull + 1);
+    uint64_t* adone = afull + 1;               // [1]        (per CTA: the MMAs reading the resident A completed)
+    uint32_t* tmem_slot = (uint32_t*)(adone + 1);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
     const uint32_t rank = crank & 1;
     const uint32_t lead = crank & ~1u;
-    const uint32_t pair = blockIdx.x >> 1;
-    const uint32_t pg = pair % pgroups;
-    const uint32_t p = pair / pgroups;
-    const uint32_t g = pg * 2 + rank;
+    // Work items (super-group sg, word tile t): super-group sg = the cpairs consecutive pair groups
+    // [sg cpairs, (sg + 1) cpairs) of 256 outputs each (one per pair of the cluster; groups past the padded W^T are
+    // TMA zero fill, their stores clipped).  Cluster kc takes items kc, kc + K, kc + 2K, ... of the list ordered
+    // tile-major (tmajor: item = t nsg + sg -- every super-group's clusters read the same X tiles at about the same
+    // time, so each is fetched from DRAM once; a resident W^T needs K to be a multiple of nsg) or super-group-major
+    // (item = sg ntiles + t: a cluster's super-group changes at most nsg - 1 times, its resident W^T reloaded then).
+    // Either way the K clusters of a round take K consecutive items: neighbouring tiles, DRAM-page friendly.
+    const uint32_t pin = crank >> 1;
+    const uint32_t kc = blockIdx.x / (2 * cpairs);
+    const uint32_t nitems = nsg * ntiles;
+    auto decode = [&](uint32_t it, uint32_t& sg, uint32_t& t) {
+        if (tmajor) {
+            t = it / nsg;
+            sg = it - t * nsg;
+        } else {
+            sg = it / ntiles;
+            t = it - sg * ntiles;
+        }
+    };
+    auto grp = [&](uint32_t sg) -> uint32_t { return (sg * cpairs + pin) * 2 + rank; };   // 128-row block
     const uint16_t pair_mask = (uint16_t)(0x3u << lead);
     const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * cpairs)) - 1) : pair_mask;
 
@@ -216,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tempty[a], 16);
         }
         mbar_init(afull, 1);
+        mbar_init(adone, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -230,13 +252,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
-            if (A_RES) {
-                if (rank == 0) mbar_expect_tx(afull, 2 * kblocks * kABox);
-                for (uint32_t kb = 0; kb < kblocks; kb++)
-                    tma_load_2d_2sm(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
-            }
-            uint32_t s = 0, ph = 0, sl = 0;
-            for (uint32_t t = p; t < ntiles; t += per_group) {
+            uint32_t s = 0, ph = 0, sl = 0, cur = ~0u, adph = 0;
+            for (uint32_t it = kc; it < nitems; it += nclust) {
+                uint32_t sg, t;
+                decode(it, sg, t);
+                const uint32_t g = grp(sg);
+                if (sg != cur) {
+                    if (!tmajor) sl = 0;
+                    if (A_RES) {
+                        if (cur != ~0u) {       // every MMA on the previous W^T has completed (MMA issuer's commit)
+                            mbar_wait(adone, adph);
+                            adph ^= 1;
+                        }
+                        if (rank == 0) mbar_expect_tx(afull, 2 * kblocks * kABox);
+                        for (uint32_t kb = 0; kb < kblocks; kb++)
+                            tma_load_2d_2sm(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+                    }
+                    cur = sg;
+                }
                 const TileInfo ti = tile_info(tl, t, sl);
                 const int32_t x0 = (int32_t)(ti.byte + rank * ((ti.n >> 1) & ~15u));   // this CTA's half (half_cols)
                 for (uint32_t kb = 0; kb < kblocks; kb++) {
@@ -262,14 +295,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer (leader CTA only)
         if (rank == 0) {
-            if (A_RES) mbar_wait(afull, 0);
             const uint64_t adesc0 = umma_desc(smem_u32(sA), 16, 1024);
             const uint64_t bdesc0 = umma_desc(smem_u32(sB), kBStage, 1024);
-            uint32_t s = 0, ph = 0, it = 0, sl = 0;
-            for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+            uint32_t s = 0, ph = 0, sl = 0, cur = ~0u, aph = 0, j = 0;
+            for (uint32_t it = kc; it < nitems; it += nclust, j++) {
+                uint32_t sg, t;
+                decode(it, sg, t);
+                if (sg != cur) {
+                    if (!tmajor) sl = 0;
+                    if (A_RES) {
+                        if (cur != ~0u) {       // release the resident W^T once the MMAs issued on it complete
+                            if (elect_one()) mma_commit_2sm_mc(adone, pair_mask);
+                            __syncwarp();
+                        }
+                        mbar_wait(afull, aph);
+                        aph ^= 1;
+                        tc_fence_after();
+                    }
+                    cur = sg;
+                }
                 const TileInfo ti = tile_info(tl, t, sl);
                 const uint32_t idesc = idesc_i8(256, 2 * half_cols(ti.n >> 1));   // see half_cols
-                const uint32_t acc = it & 1, use = it >> 1;
+                const uint32_t acc = j & 1, use = j >> 1;
                 mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * 256;
@@ -301,10 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t half = e >> 2;
         uint8_t* ys = sY + quarter * kYQuarter;
         const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), lead);
-        uint32_t it = 0, sl = 0;
-        for (uint32_t t = p; t < ntiles; t += per_group, it++) {
+        uint32_t sl = 0, cur = ~0u, j = 0;
+        for (uint32_t it = kc; it < nitems; it += nclust, j++) {
+            uint32_t sg, t;
+            decode(it, sg, t);
+            if (sg != cur && !tmajor) sl = 0;
+            cur = sg;
+            const uint32_t g = grp(sg);
             const TileInfo ti = tile_info(tl, t, sl);
-            const uint32_t acc = it & 1, use = it >> 1;
+            const uint32_t acc = j & 1, use = j >> 1;
             EpiArgs ea;
             ea.br = tab.br(ti.limb);
             ea.off_lo = ec.off_lo[ti.limb];
@@ -381,6 +433,72 @@ static PFN_encodeTiledC get_encode_c() {
     return fn;
 }
 
+namespace tcc {
+typedef void (*KernFn)(CUtensorMap, CUtensorMap, StoreMaps, Tiles, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                       ModTab, tc::EpiConst, uint32_t);
+
+// Relative per-SM rate of a cluster of c pairs sharing every X sub-box by multicast (c = 1: plain pairs, each
+// X tile read through L2 by every pair) -- measured at 2048x2048 with every c forced (tools/bench_cluster.py,
+// profiles/r02_tcc_ablations.md).
+static constexpr double kFeed[5] = {0, 0.52, 0.85, 0.90, 1.0};
+
+// Co-resident clusters of c pairs (cudaOccupancyMaxActiveClusters; cached per device, kernel and smem size).
+static int max_clusters(int dev, KernFn k, size_t smem, uint32_t c) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, void*, size_t, uint32_t>, int> cache;
+    const auto key = std::make_tuple(dev, (void*)k, smem, c);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2 * c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(2 * c * 64, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = n;
+    return n;
+}
+
+// Cluster shape: c pairs per cluster (2c CTAs, c <= 4) and K co-resident clusters, minimising the estimated time
+// ceil(I_c / K_c) / kFeed[c] with I_c = ceil(pgroups / c) word-tile items (a super-group that overhangs the padded
+// W^T computes zero rows); force = 1..4 takes that c (ensi_pcmm_opts.cluster_pairs).
+static int plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, KernFn kmc, KernFn kpl, size_t smem,
+                         uint32_t force, uint32_t* cpairs, uint32_t* nclust) {
+    for (KernFn k : {kmc, kpl}) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_err(ctx, e, "accum_tcc smem attribute");
+    }
+    double best = 0;
+    for (uint32_t c = force ? force : 1; c <= (force ? force : 4); c++) {
+        const int kc = max_clusters(ctx->device, c == 1 ? kpl : kmc, smem, c);
+        if (kc < 1) continue;
+        const uint64_t items = (uint64_t)((pgroups + c - 1) / c) * ntiles;
+        const double est = (double)((items + kc - 1) / kc) / kFeed[c];
+        if (best == 0 || est < best * 0.999) {
+            best = est;
+            *cpairs = c;
+            *nclust = (uint32_t)kc;
+        }
+    }
+    if (best == 0) return set_err(ctx, ENSI_ECUDA, "accum_tcc: no cluster shape fits on this device");
+    return ENSI_OK;
+}
+}  // namespace tcc
+
 int build_wt8(ensi_ctx* ctx, ensi_weights* w);
 void fill_epi_const(const ensi_ctx* ctx, const ensi_weights* w, tc::EpiConst* ec);
 
@@ -389,7 +507,7 @@ void fill_epi_const(const ensi_ctx* ctx, const ensi_weights* w, tc::EpiConst* ec
 // y_dst[0..n_dst): output buffers, each [m][ct_bytes] from its pointer on (one for the plain call; every GPU's
 // gathered buffer, offset to this rank's rows, for the fused gather epilogue) -- every tile is TMA-stored to each.
 int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* const* y_dst,
-                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb) {
+                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb, uint32_t cluster_pairs) {
     if (n_dst < 1 || n_dst > tcc::kMaxPeers) return set_err(ctx, ENSI_EINVAL, "1..8 output destinations");
     if (d != w->d) return set_err(ctx, ENSI_EDIM, "d mismatch");
     if (!tcc_supported(ctx, level)) return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable");
@@ -441,13 +559,21 @@ int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weig
             return set_err(ctx, ENSI_ECUDA, "tensor map A");
     }
     const uint32_t pgroups = w->wt_mpad / 256;
-    uint32_t cpairs = 1;
-    for (uint32_t c = 4; c >= 2; c--)
-        if (pgroups % c == 0) {
-            cpairs = c;
-            break;
-        }
+    tc::EpiConst ec;
+    fill_epi_const(ctx, w, &ec);
+    if (!ec.narrow_ok) return set_err(ctx, ENSI_EINVAL, "d too large for the compact tensor-core epilogue");
+    const uint32_t kblocks = w->wt_dpad / 128;
+    const bool ares = (size_t)kblocks * tcc::kABox <= tcc::kAResMax;
+    const size_t a_bytes = ares ? (size_t)kblocks * tcc::kABox : (size_t)tcc::kStages * tcc::kABox;
+    const size_t smem = 1024 + a_bytes + tcc::kStages * tcc::kBStage + 4 * tcc::kYQuarter + 256;
+    const uint32_t ntiles = (uint32_t)tiles;
+    tcc::KernFn kmc = ares ? tcc::k_accum_tcc<true, true> : tcc::k_accum_tcc<false, true>;
+    tcc::KernFn kpl = ares ? tcc::k_accum_tcc<true, false> : tcc::k_accum_tcc<false, false>;
+    uint32_t cpairs = 1, nclust = 1;
+    rc = tcc::plan_clusters(ctx, pgroups, ntiles, kmc, kpl, smem, cluster_pairs, &cpairs, &nclust);
+    if (rc) return rc;
     const bool mc = cpairs >= 2;
+    const tcc::KernFn kern = mc ? kmc : kpl;
     {   // B = compact ciphertext bytes [d][ct_bytes], box 128 bytes x 32 (multicast sub-boxes) or 128 rows
         cuuint64_t dims[2] = {ct_bytes, d};
         cuuint64_t strides[1] = {ct_bytes};
@@ -468,58 +594,35 @@ int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weig
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
                 return set_err(ctx, ENSI_ECUDA, "tensor map Y (compact)");
         }
-    tc::EpiConst ec;
-    fill_epi_const(ctx, w, &ec);
-    if (!ec.narrow_ok) return set_err(ctx, ENSI_EINVAL, "d too large for the compact tensor-core epilogue");
-    const uint32_t kblocks = w->wt_dpad / 128;
-    const bool ares = (size_t)kblocks * tcc::kABox <= tcc::kAResMax;
-    const uint32_t csize = mc ? 2 * cpairs : 2;
-    const size_t a_bytes = ares ? (size_t)kblocks * tcc::kABox : (size_t)tcc::kStages * tcc::kABox;
-    const size_t smem = 1024 + a_bytes + tcc::kStages * tcc::kBStage + 4 * tcc::kYQuarter + 256;
-    void (*kern)(CUtensorMap, CUtensorMap, tcc::StoreMaps, tcc::Tiles, uint32_t, uint32_t, uint32_t, uint32_t, ModTab,
-                 tc::EpiConst, uint32_t);
-    if (ares) kern = mc ? tcc::k_accum_tcc<true, true> : tcc::k_accum_tcc<true, false>;
-    else kern = mc ? tcc::k_accum_tcc<false, true> : tcc::k_accum_tcc<false, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_err(ctx, e, "accum_tcc smem attribute");
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const uint32_t nsg = (pgroups + cpairs - 1) / cpairs;
+    nclust = std::min(nclust, nsg * ntiles);
+    // tile-major unless a resident W^T would be reloaded at every item (K not a multiple of the super-groups)
+    const uint32_t tmajor = (!ares || nclust % nsg == 0) ? 1u : 0u;
+    ctx->tcc_cpairs = cpairs;
+    ctx->tcc_nclust = nclust;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.x = 2 * cpairs;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(2 * cpairs * nclust, 1, 1);
     cfg.blockDim = dim3(tcc::kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const uint32_t ntiles = (uint32_t)tiles;
-    uint32_t per_group;
-    if (mc) {
-        cfg.gridDim = dim3(csize * 64, 1, 1);
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg) != cudaSuccess || nclusters < 1) {
-            cudaGetLastError();
-            nclusters = std::max(1, sms / (int)csize);
-        }
-        per_group = std::max<uint32_t>(1, (uint32_t)nclusters / (pgroups / cpairs));
-    } else {
-        per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
-    }
-    per_group = std::min(per_group, ntiles);
-    cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
-    e = cudaLaunchKernelEx(&cfg, kern, ma, mb, maps, tl, kblocks, pgroups, per_group, ntiles, ctx->tab, ec, cpairs);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, maps, tl, kblocks, ntiles, nsg, tmajor, nclust, ctx->tab,
+                                       ec, cpairs);
     ENSI_LAUNCH_CHECK(ctx);
     if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tcc launch");
 }
 
 int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
-                      cudaStream_t st, int slice_limb) {
+                      cudaStream_t st, int slice_limb, uint32_t cluster_pairs) {
     uint8_t* dst[1] = {y};
-    return accum_ternary_tcc_dst(ctx, x, d, w, dst, 1, level, st, slice_limb);
+    return accum_ternary_tcc_dst(ctx, x, d, w, dst, 1, level, st, slice_limb, cluster_pairs);
 }
 
 // ---------------------------------------------------------------------------------------------- peer signalling

@@ -293,6 +293,13 @@ const char* ensi_last_error(const ensi_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 uint64_t ensi_launch_count(const ensi_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ensi_last_compact_plan(const ensi_ctx* ctx, uint32_t* cluster_pairs, uint32_t* clusters) {
+    if (!ctx || !cluster_pairs || !clusters) return ENSI_EINVAL;
+    *cluster_pairs = ctx->tcc_cpairs;
+    *clusters = ctx->tcc_nclust;
+    return ENSI_OK;
+}
+
 uint32_t ensi_pcmm_kernel(const ensi_ctx* ctx, uint32_t level, uint32_t requested) {
     if (!ctx) return 0;
     const bool tc = tc_supported(ctx, level);
@@ -823,6 +830,7 @@ int check_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights*
     if (o.rescale_out) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: no rescale epilogue");
     if (o.moddown_lazy) return set_err(ctx, ENSI_EINVAL, "moddown_lazy: Layout B only");
     if (o.kernel != 0 && o.kernel != 2) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: kernel must be 0 or 2");
+    if (o.cluster_pairs > 4) return set_err(ctx, ENSI_EINVAL, "cluster_pairs must be 0..4");
     if (x->count != wc->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
     if (!tcc_supported(ctx, x->level) || wc->d >= (1u << 22))
         return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable (sm_100a, 5..8-byte words, N' >= 256)");
@@ -844,7 +852,8 @@ int ensi_pcmm_ternary_compact(ensi_ctx* ctx, const ensi_compact_view* x, const e
     const uint8_t *x0 = x->data, *x1 = x0 + (size_t)x->count * cb, *y0 = y->data, *y1 = y0 + (size_t)y->count * cb;
     if (x0 < y1 && y0 < x1) return set_err(ctx, ENSI_EINVAL, "y aliases x");
     DeviceGuard g(ctx->device);
-    rc = accum_ternary_tcc(ctx, x->data, w->d, w, y->data, x->level, (cudaStream_t)stream);
+    rc = accum_ternary_tcc(ctx, x->data, w->d, w, y->data, x->level, (cudaStream_t)stream, -1,
+                           opts ? opts->cluster_pairs : 0);
     if (!rc) y->log2_scale = x->log2_scale;
     return rc;
 }
@@ -869,7 +878,8 @@ int ensi_pcmm_ternary_compact_gather(ensi_ctx* ctx, const ensi_compact_view* x, 
         dst[p] = y_dst[p] + (size_t)row0 * cb;       // this rank's rows of destination p
     }
     DeviceGuard g(ctx->device);
-    return accum_ternary_tcc_dst(ctx, x->data, w->d, w, dst, n_dst, x->level, (cudaStream_t)stream);
+    return accum_ternary_tcc_dst(ctx, x->data, w->d, w, dst, n_dst, x->level, (cudaStream_t)stream, -1,
+                                 opts ? opts->cluster_pairs : 0);
 }
 
 typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);

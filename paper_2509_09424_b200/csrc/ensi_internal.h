@@ -116,6 +116,7 @@ struct ensi_ctx {
     std::map<void*, void*> ipc_bases;        // ensi_ipc_open: returned pointer -> opened allocation base
     std::string err;
     uint64_t launches = 0;
+    uint32_t tcc_cpairs = 0, tcc_nclust = 0;   // last compact accumulate launch shape
 };
 
 namespace ensi {
@@ -179,9 +180,10 @@ struct PeerFlags {
 __global__ void k_peer_signal(PeerFlags pf, uint32_t slot, uint32_t epoch);
 __global__ void k_peer_wait(const uint32_t* flags, uint32_t n, uint32_t epoch);
 int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* const* y_dst,
-                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb = -1);
+                          uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb = -1,
+                          uint32_t cluster_pairs = 0);
 int accum_ternary_tcc(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* y, uint32_t level,
-                      cudaStream_t st, int slice_limb = -1);
+                      cudaStream_t st, int slice_limb = -1, uint32_t cluster_pairs = 0);
 
 // key switching (keyswitch.cu)
 int conv_tables(ensi_ctx* ctx, uint32_t level, ConvTables** out);

@@ -28,7 +28,7 @@ KERNEL_DEFAULT, KERNEL_CUDA_CORE, KERNEL_TCGEN05, KERNEL_TCGEN05_1CTA, KERNEL_TC
 EXPORTS = ["ensi_abi_version", "ensi_ctx_create", "ensi_ctx_destroy", "ensi_last_error", "ensi_ctx_moduli",
            "ensi_load_keys", "ensi_weights_pack", "ensi_weights_destroy", "ensi_pcmm_ternary_packed",
            "ensi_pcmm_ternary", "ensi_pcmm_ternary_host", "ensi_ntt", "ensi_rotate_hoisted", "ensi_rotate_batch",
-           "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_pcmm_kernel", "ensi_load_relin_key",
+           "ensi_rescale", "ensi_decrypt_debug", "ensi_launch_count", "ensi_last_compact_plan", "ensi_pcmm_kernel", "ensi_load_relin_key",
            "ensi_mul_plain", "ensi_mul_relin", "ensi_ccmm", "ensi_wire_bytes", "ensi_pcmm_ternary_host_wire",
            "ensi_wire_pack", "ensi_wire_unpack", "ensi_pcmm_ternary_compact", "ensi_pcmm_ternary_compact_gather",
            "ensi_ipc_get_handle", "ensi_ipc_open", "ensi_ipc_close", "ensi_peer_signal", "ensi_peer_wait"]
@@ -64,7 +64,7 @@ class IpcHandle(C.Structure):
 
 class PcmmOpts(C.Structure):
     _fields_ = [("layout", C.c_uint32), ("block_s", C.c_uint32), ("baby", C.c_uint32), ("rescale_out", C.c_uint32),
-                ("kernel", C.c_uint32), ("moddown_lazy", C.c_uint32)]
+                ("kernel", C.c_uint32), ("moddown_lazy", C.c_uint32), ("cluster_pairs", C.c_uint32)]
 
 
 _LIB = None
@@ -125,6 +125,7 @@ def lib():
                                 C.POINTER(CcmmOpts), vp]
         L.ensi_launch_count.restype = u64
         L.ensi_pcmm_kernel.argtypes = [vp, u32, u32]
+        L.ensi_last_compact_plan.argtypes = [vp, C.POINTER(u32), C.POINTER(u32)]
         L.ensi_pcmm_kernel.restype = u32
         _LIB = L
     return _LIB
@@ -215,6 +216,12 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().ensi_launch_count(self.h))
 
+    def last_compact_plan(self) -> tuple:
+        """(CTA pairs per multicast cluster, clusters launched) of the most recent compact accumulate."""
+        c, k = C.c_uint32(), C.c_uint32()
+        self._check(lib().ensi_last_compact_plan(self.h, C.byref(c), C.byref(k)))
+        return int(c.value), int(k.value)
+
     def view(self, t, level: int, log2_scale: float = 40.0) -> CtView:
         """torch 64-bit CUDA tensor [count][2][level][N'] on this context's device -> ensi_ct_view."""
         if not (t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 8):
@@ -293,16 +300,17 @@ class Context:
         return CompactView(t.data_ptr(), t.shape[0], level, log2_scale)
 
     def pcmm_ternary_compact(self, x, w: "Weights", y, level: int, kernel: int = 0, stream=None,
-                             log2_scale: float = 40.0) -> float:
-        """y = x (x) W on compact ciphertexts (Layout A); returns y's log2 scale."""
+                             log2_scale: float = 40.0, cluster_pairs: int = 0) -> float:
+        """y = x (x) W on compact ciphertexts (Layout A); returns y's log2 scale.  cluster_pairs: 0 = launch shape
+        chosen per layer, 1..4 = that many CTA pairs per multicast cluster (same words)."""
         xv, yv = self.compact_view(x, level, log2_scale), self.compact_view(y, level)
-        opts = PcmmOpts(0, 0, 0, 0, kernel, 0)
+        opts = PcmmOpts(0, 0, 0, 0, kernel, 0, cluster_pairs)
         self._check(lib().ensi_pcmm_ternary_compact(self.h, C.byref(xv), w.h, C.byref(yv), C.byref(opts),
                                                     _stream_ptr(stream)))
         return yv.log2_scale
 
     def pcmm_ternary_compact_gather(self, x, w: "Weights", dsts, rows_total: int, row0: int, level: int,
-                                    kernel: int = 0, stream=None, log2_scale: float = 40.0):
+                                    kernel: int = 0, stream=None, log2_scale: float = 40.0, cluster_pairs: int = 0):
         """NEXT #4 fused gather: y_i of this call stored into rows row0 + i of every destination (device pointers or
         contiguous uint8 CUDA tensors of rows_total x wire_bytes -- this GPU's gathered buffer and the peers')."""
         xv = self.compact_view(x, level, log2_scale)
@@ -317,7 +325,7 @@ class Context:
             else:
                 ptrs.append(int(dbuf))
         arr = (C.c_void_p * len(ptrs))(*ptrs)
-        opts = PcmmOpts(0, 0, 0, 0, kernel, 0)
+        opts = PcmmOpts(0, 0, 0, 0, kernel, 0, cluster_pairs)
         self._check(lib().ensi_pcmm_ternary_compact_gather(self.h, C.byref(xv), w.h, arr, len(ptrs), rows_total, row0,
                                                            C.byref(opts), _stream_ptr(stream)))
 

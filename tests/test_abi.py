@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_binding_lists_every_symbol(libpath):
     from paper_2509_09424_b200 import ensi
     assert sorted(ensi.EXPORTS) == _declared()
-    assert ensi.lib().ensi_abi_version() == 4
+    assert ensi.lib().ensi_abi_version() == 5
 
 
 def test_sm100a_code_in_library(libpath):

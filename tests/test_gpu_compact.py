@@ -81,6 +81,35 @@ def test_compact_ragged(c1, torch_cuda, d, m, level):
     assert (_run(torch, ctx, x, W, level) == o.pcmm_a(x, W, nthreads=4)).all()
 
 
+@pytest.mark.parametrize("d,m,level", [(200, 1200, 3), (900, 3000, 2), (768, 3100, 1)])
+def test_compact_every_cluster_shape(c1, torch_cuda, d, m, level):
+    """The launch shape (opts.cluster_pairs = 1..4 CTA pairs per multicast cluster, and 0 = the per-layer choice):
+    every co-resident cluster takes a contiguous run of (super-group, word tile) items, so runs cross super-groups
+    (resident W^T reloaded mid-kernel: d <= 768) and super-groups overhang the padded W^T (5 / 12 / 13 pair groups
+    in clusters of 2..4 pairs) -- the outputs are the same words as the oracle's Algorithm 1 for every shape.
+    Resident (d = 200, 768) and streamed (d = 900) W^T."""
+    from paper_2509_09424_b200.ensi import wire_unpack_host
+    o, sk, pk, ctx = c1
+    torch = torch_cuda
+    x = synth.gen_words(d * 77 + m + level, o.q, d, level, o.n)
+    W = synth.gen_W(d + 3 * m + level, d, m)
+    cols = sorted({0, 1, 255, 256, 511, 767, 1023, 1200 - 1, m // 2, m - 257, m - 2, m - 1} & set(range(m)))
+    want = o.pcmm_a(x, W, cols=cols, nthreads=NTH)
+    xc = _compact_dev(torch, ctx, x, level)
+    w = ctx.weights(W)
+    shapes = set()
+    for cp in (0, 1, 2, 3, 4):
+        yc = torch.full((m, ctx.wire_bytes(level)), 0xA5, dtype=torch.uint8, device="cuda")
+        ctx.pcmm_ternary_compact(xc, w, yc, level=level, cluster_pairs=cp)
+        torch.cuda.synchronize()
+        c, k = ctx.last_compact_plan()
+        assert 1 <= c <= 4 and k >= 1 and (cp == 0 or c == cp)
+        shapes.add((c, k))
+        got = wire_unpack_host(yc[cols].cpu().numpy(), ctx.wire_widths(level), level, ctx.n)
+        assert (got == want).all(), (cp, c, k)
+    assert len(shapes) >= 4
+
+
 @pytest.mark.parametrize("kind", ["zero", "identity", "neg_identity", "permutation", "plus", "minus", "toy"])
 def test_compact_edge_weights(c1, torch_cuda, kind):
     o, sk, pk, ctx = c1
@@ -203,13 +232,16 @@ def test_compact_errors(c1, torch_cuda):
     with pytest.raises(EnsiError) as e:
         ctx.pcmm_ternary_compact(x[:2], ctx.weights(synth.gen_W(2, 2, 2)), x[1:3], level=3)
     assert e.value.code == ENSI_EINVAL
+    with pytest.raises(EnsiError) as e:
+        ctx.pcmm_ternary_compact(x, w, y, level=3, cluster_pairs=5)
+    assert e.value.code == ENSI_EINVAL
 
 
 @pytest.mark.parametrize("d,m", [(768, 3072), (3072, 768), (2048, 2048), (2048, 5504), (5504, 2048), (2048, 6144)])
 def test_compact_bench_shapes_sampled_columns(torch_cuda, d, m):
     """Every C3-C5 shape bench.py times on the compact layout (layout_a_shapes) at full size, in the launch
-    configuration it times (one ensi_pcmm_ternary_compact call): 768->3072 (4 pairs per cluster, resident W^T),
-    3072->768 and 5504->2048 (streamed W^T, 24 / 43 K blocks), 2048^2, 2048->5504 (2 pairs per cluster) and the fused
+    configuration it times (one ensi_pcmm_ternary_compact call, the per-layer launch shape): 768->3072 (resident
+    W^T, 12 pair groups), 3072->768 and 5504->2048 (streamed W^T, 24 / 43 K blocks), 2048^2, 2048->5504 and the fused
     Q/K/V 2048->6144 -- sampled output columns == the oracle's Algorithm 1, word for word."""
     from paper_2509_09424_b200 import Context
     from paper_2509_09424_b200.ensi import wire_unpack_host

@@ -225,17 +225,19 @@ static constexpr uint32_t kIdesc2 = (2u << 4) | (1u << 7) | (0u << 10) | (0u << 
 
 // MC = false: clusters of one pair (2 CTAs), each pair loads its own X tiles; the pairs of the pgroups output
 //             groups that share a word tile meet only in L2.
-// MC = true:  clusters of cpairs pairs (cpairs | pgroups, 2*cpairs <= 8 CTAs; cpairs == pgroups when m <= 1024).
-//             The cpairs pairs of a cluster cover consecutive output groups of the same word tile in lockstep;
-//             every X sub-box (32 K-rows x 128 bytes) is loaded once by one pair and multicast to the same N-half
-//             of every pair of the cluster, so each X byte leaves L2/HBM once per cluster (once per layer when
-//             cpairs == pgroups).  The stage ring is released only when all cpairs MMA issuers have consumed it.
+// MC = true:  clusters of cpairs pairs (2*cpairs <= 8 CTAs).  The cpairs pairs of a cluster cover consecutive
+//             output groups (a super-group) of the same word tile in lockstep; every X sub-box (32 K-rows x 128
+//             bytes) is loaded once by one pair and multicast to the same N-half of every pair of the cluster, so
+//             each X byte leaves L2/HBM once per cluster.  The stage ring is released only when all cpairs MMA
+//             issuers have consumed it.
+// Work items (super-group, word tile) are dealt round-robin to the nclust co-resident clusters, in the order and
+// with the resident-W^T reloads of k_accum_tcc (accum_tcc.cu); tc_plan_clusters picks cpairs and nclust.
 template <bool A_RES, bool MC>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_accum_tc2(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t pgroups, uint32_t per_group,
-                uint32_t ntiles, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab, EpiConst ec,
-                uint32_t cpairs) {
+                const __grid_constant__ CUtensorMap map_y, uint32_t kblocks, uint32_t ntiles, uint32_t nsg,
+                uint32_t tmajor, uint32_t nclust, uint32_t log_n, uint32_t level, uint32_t limb0, ModTab tab,
+                EpiConst ec, uint32_t cpairs) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t a_bytes = A_RES ? kblocks * kABox : kStages2 * kABox;
@@ -248,16 +250,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
     uint64_t* tfull = bars + 2 * kStages2;     // [2]         (per CTA, multicast commits)
     uint64_t* tempty = tfull + 2;              // [2]         (leader's: 16 arrivals)
     uint64_t* afull = tempty + 2;              // [1]         (leader's)
-    uint32_t* tmem_slot = (uint32_t*)(afull + 1);
+    uint64_t* adone = afull + 1;               // [1]         (per CTA: the MMAs reading the resident A completed)
+    uint32_t* tmem_slot = (uint32_t*)(adone + 1);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = cluster_rank();
     const uint32_t rank = crank & 1;           // rank inside the CTA pair (0 = leader, issues the MMAs)
     const uint32_t lead = crank & ~1u;         // cluster rank of this pair's leader
-    const uint32_t pair = blockIdx.x >> 1;
-    const uint32_t pg = pair % pgroups;        // pair group: outputs [256 pg, 256 pg + 256)
-    const uint32_t p = pair / pgroups;
-    const uint32_t g = pg * 2 + rank;          // this CTA's 128-output group
+    const uint32_t pin = crank >> 1;           // pair inside the cluster
+    const uint32_t kc = blockIdx.x / (2 * cpairs);
+    // pair group (sg cpairs + pin): outputs [256 pg, 256 pg + 256); this CTA's 128-output group
+    auto grp = [&](uint32_t sg) -> uint32_t { return (sg * cpairs + pin) * 2 + rank; };
     const uint16_t pair_mask = (uint16_t)(0x3u << lead);
     const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * cpairs)) - 1) : pair_mask;
 
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&tempty[a], 16);
         }
         mbar_init(afull, 1);
+        mbar_init(adone, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -285,13 +289,20 @@ __global__ void __launch_bounds__(kThreads2, 1)
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
-            if (A_RES) {
-                if (rank == 0) mbar_expect_tx(afull, 2 * kblocks * kABox);
-                for (uint32_t kb = 0; kb < kblocks; kb++)
-                    tma_load_2d_2sm(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
-            }
-            uint32_t s = 0, ph = 0;
-            for (uint32_t t = p; t < ntiles; t += per_group) {
+            uint32_t s = 0, ph = 0, cur = ~0u, adph = 0;
+            for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next()) {
+                const uint32_t sg = wi.sg, t = wi.t;
+                const uint32_t g = grp(sg);
+                if (A_RES && sg != cur) {
+                    if (cur != ~0u) {           // every MMA on the previous W^T has completed (MMA issuer's commit)
+                        mbar_wait(adone, adph);
+                        adph ^= 1;
+                    }
+                    if (rank == 0) mbar_expect_tx(afull, 2 * kblocks * kABox);
+                    for (uint32_t kb = 0; kb < kblocks; kb++)
+                        tma_load_2d_2sm(sA + kb * kABox, &map_a, afull, (int32_t)(kb * kBoxK), (int32_t)(g * 128));
+                    cur = sg;
+                }
                 for (uint32_t kb = 0; kb < kblocks; kb++) {
                     mbar_wait(&empty[s], ph ^ 1);
                     if (rank == 0) mbar_expect_tx(&full[s], 2 * (kBStage2 + (A_RES ? 0 : kABox)));
@@ -322,12 +333,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
         // A single-lane loop made the compiler rebuild every descriptor through an ELECT/R2UR.BROADCAST loop
         // (~23 instructions per MMA), and the issuer warp was busy 94% of its samples.
         if (rank == 0) {
-            if (A_RES) mbar_wait(afull, 0);
             const uint64_t adesc0 = umma_desc(smem_u32(sA), 16, 1024);
             const uint64_t bdesc0 = umma_desc(smem_u32(sB), kBStage2, 1024);
-            uint32_t s = 0, ph = 0, it = 0;
-            for (uint32_t t = p; t < ntiles; t += per_group, it++) {
-                const uint32_t acc = it & 1, use = it >> 1;
+            uint32_t s = 0, ph = 0, j = 0, cur = ~0u, aph = 0;
+            for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next(), j++) {
+                const uint32_t sg = wi.sg, t = wi.t;
+                if (A_RES && sg != cur) {
+                    if (cur != ~0u) {           // release the resident W^T once the MMAs issued on it complete
+                        if (elect_one()) mma_commit_2sm_mc(adone, pair_mask);
+                        __syncwarp();
+                    }
+                    mbar_wait(afull, aph);
+                    aph ^= 1;
+                    tc_fence_after();
+                    cur = sg;
+                }
+                const uint32_t acc = j & 1, use = j >> 1;
                 mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * 256;
@@ -365,9 +386,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
         const uint32_t row = lane;
         const uint32_t words_per_limb = 1u << log_n;
         const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), lead);
-        uint32_t it = 0;
-        for (uint32_t t = p; t < ntiles; t += per_group, it++) {
-            const uint32_t acc = it & 1, use = it >> 1;
+        uint32_t j = 0;
+        for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next(), j++) {
+            const uint32_t sg = wi.sg, t = wi.t;
+            const uint32_t g = grp(sg);
+            const uint32_t acc = j & 1, use = j >> 1;
             const uint32_t word0 = t * 32;
             const uint32_t limb = (limb0 + word0 / words_per_limb) % level;
             const Barrett br = tab.br(limb);
@@ -544,14 +567,25 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
             return set_err(ctx, ENSI_ECUDA, "tensor map A");
     }
     const uint32_t pgroups = w->wt_mpad / 256;
-    uint32_t cpairs = 1;                       // pairs per multicast cluster: largest divisor of pgroups <= 4
-    for (uint32_t c = 4; c >= 2; c--)
-        if (pgroups % c == 0) {
-            cpairs = c;
-            break;
-        }
-    if (variant == TC_AUTO) variant = cpairs >= 2 ? TC_PAIR_MC : TC_PAIR;
-    if (variant == TC_PAIR_MC && cpairs < 2) variant = TC_PAIR;
+    tc::EpiConst ec;
+    fill_epi_const(ctx, w, &ec);
+    const uint32_t kblocks = w->wt_dpad / 128;
+    const uint32_t ntiles = (uint32_t)(ctw / 32);
+    const bool ares = (size_t)kblocks * tc::kABox <= tc::kAResMax;
+    typedef void (*Kern2)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                          uint32_t, uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t);
+    const Kern2 kmc = ares ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<false, true>;
+    const Kern2 kpl = ares ? tc::k_accum_tc2<true, false> : tc::k_accum_tc2<false, false>;
+    const size_t smem2 = 1024 + (ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox) +
+                         tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
+    uint32_t cpairs = 1, nclust = 1;           // pairs per multicast cluster, co-resident clusters
+    if (variant != TC_ONE_CTA) {
+        // TC_AUTO / TC_PAIR_MC: the per-layer launch shape; TC_PAIR: plain pairs (no multicast)
+        rc = tc_plan_clusters(ctx, pgroups, ntiles, (const void*)kmc, (const void*)kpl, smem2, tc::kThreads2,
+                              variant == TC_PAIR ? 1u : 0u, &cpairs, &nclust);
+        if (rc) return rc;
+        variant = cpairs >= 2 ? TC_PAIR_MC : TC_PAIR;
+    }
     {   // B = raw ciphertext bytes [d][ctw*8], box 128 bytes x 128 rows (x 32 rows: multicast sub-boxes)
         cuuint64_t dims[2] = {ctw * 8, d};
         cuuint64_t strides[1] = {ctw * 8};
@@ -570,54 +604,28 @@ int accum_ternary_tc(ensi_ctx* ctx, const uint64_t* x, uint32_t d, ensi_weights*
                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return set_err(ctx, ENSI_ECUDA, "tensor map Y");
     }
-    tc::EpiConst ec;
-    fill_epi_const(ctx, w, &ec);
-    const uint32_t kblocks = w->wt_dpad / 128;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    const uint32_t ntiles = (uint32_t)(ctw / 32);
-    const bool ares = (size_t)kblocks * tc::kABox <= tc::kAResMax;
     cudaError_t e;
     if (variant != TC_ONE_CTA) {
-        // CTA pairs (cta_group::2): pair group pg covers outputs [256 pg, 256 pg + 256)
-        const bool mc = variant == TC_PAIR_MC;
-        const uint32_t csize = mc ? 2 * cpairs : 2;
-        const size_t a_bytes = ares ? (size_t)kblocks * tc::kABox : (size_t)tc::kStages2 * tc::kABox;
-        const size_t smem = 1024 + a_bytes + tc::kStages2 * tc::kBStage2 + 8 * tc::kYWarp + 256;
-        void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                     uint32_t, uint32_t, ModTab, tc::EpiConst, uint32_t);
-        if (ares) kern = mc ? tc::k_accum_tc2<true, true> : tc::k_accum_tc2<true, false>;
-        else kern = mc ? tc::k_accum_tc2<false, true> : tc::k_accum_tc2<false, false>;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_err(ctx, e, "accum_tc2 smem attribute");
+        // CTA pairs (cta_group::2) in clusters of cpairs pairs, items dealt round-robin (see k_accum_tc2)
+        const uint32_t nsg = (pgroups + cpairs - 1) / cpairs;
+        nclust = std::min(nclust, nsg * ntiles);
+        const uint32_t tmajor = (!ares || nclust % nsg == 0) ? 1u : 0u;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.x = 2 * cpairs;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * cpairs * nclust, 1, 1);
         cfg.blockDim = dim3(tc::kThreads2, 1, 1);
-        cfg.dynamicSmemBytes = smem;
+        cfg.dynamicSmemBytes = smem2;
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        // persistent: as many clusters as can be co-resident (each cluster = pgroups/(csize/2) ... pairs)
-        uint32_t per_group;
-        if (mc) {
-            cfg.gridDim = dim3(csize * 64, 1, 1);
-            int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg) != cudaSuccess || nclusters < 1) {
-                cudaGetLastError();
-                nclusters = std::max(1, sms / (int)csize);
-            }
-            per_group = std::max<uint32_t>(1, (uint32_t)nclusters / (pgroups / cpairs));
-        } else {
-            per_group = std::max<uint32_t>(1, (uint32_t)sms / (2 * pgroups));
-        }
-        per_group = std::min(per_group, ntiles);
-        cfg.gridDim = dim3(2 * pgroups * per_group, 1, 1);
-        e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, kblocks, pgroups, per_group, ntiles, ctx->log_n, level, limb0,
-                               ctx->tab, ec, cpairs);
+        e = cudaLaunchKernelEx(&cfg, cpairs >= 2 ? kmc : kpl, ma, mb, my, kblocks, ntiles, nsg, tmajor, nclust,
+                               ctx->log_n, level, limb0, ctx->tab, ec, cpairs);
         ENSI_LAUNCH_CHECK(ctx);
         if (e == cudaSuccess) e = cudaGetLastError();
         return e == cudaSuccess ? ENSI_OK : cuda_err(ctx, e, "accum_tc2 launch");

@@ -213,16 +213,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Either way the K clusters of a round take K consecutive items: neighbouring tiles, DRAM-page friendly.
     const uint32_t pin = crank >> 1;
     const uint32_t kc = blockIdx.x / (2 * cpairs);
-    const uint32_t nitems = nsg * ntiles;
-    auto decode = [&](uint32_t it, uint32_t& sg, uint32_t& t) {
-        if (tmajor) {
-            t = it / nsg;
-            sg = it - t * nsg;
-        } else {
-            sg = it / ntiles;
-            t = it - sg * ntiles;
-        }
-    };
     auto grp = [&](uint32_t sg) -> uint32_t { return (sg * cpairs + pin) * 2 + rank; };   // 128-row block
     const uint16_t pair_mask = (uint16_t)(0x3u << lead);
     const uint16_t all_mask = MC ? (uint16_t)((1u << (2 * cpairs)) - 1) : pair_mask;
@@ -253,9 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             uint32_t s = 0, ph = 0, sl = 0, cur = ~0u, adph = 0;
-            for (uint32_t it = kc; it < nitems; it += nclust) {
-                uint32_t sg, t;
-                decode(it, sg, t);
+            for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next()) {
+                const uint32_t sg = wi.sg, t = wi.t;
                 const uint32_t g = grp(sg);
                 if (sg != cur) {
                     if (!tmajor) sl = 0;
@@ -298,9 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t adesc0 = umma_desc(smem_u32(sA), 16, 1024);
             const uint64_t bdesc0 = umma_desc(smem_u32(sB), kBStage, 1024);
             uint32_t s = 0, ph = 0, sl = 0, cur = ~0u, aph = 0, j = 0;
-            for (uint32_t it = kc; it < nitems; it += nclust, j++) {
-                uint32_t sg, t;
-                decode(it, sg, t);
+            for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next(), j++) {
+                const uint32_t sg = wi.sg, t = wi.t;
                 if (sg != cur) {
                     if (!tmajor) sl = 0;
                     if (A_RES) {
@@ -349,9 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* ys = sY + quarter * kYQuarter;
         const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), lead);
         uint32_t sl = 0, cur = ~0u, j = 0;
-        for (uint32_t it = kc; it < nitems; it += nclust, j++) {
-            uint32_t sg, t;
-            decode(it, sg, t);
+        for (WorkIter wi(kc, nclust, nsg, ntiles, tmajor); wi.valid(); wi.next(), j++) {
+            const uint32_t sg = wi.sg, t = wi.t;
             if (sg != cur && !tmajor) sl = 0;
             cur = sg;
             const uint32_t g = grp(sg);
@@ -443,10 +430,10 @@ typedef void (*KernFn)(CUtensorMap, CUtensorMap, StoreMaps, Tiles, uint32_t, uin
 static constexpr double kFeed[5] = {0, 0.52, 0.85, 0.90, 1.0};
 
 // Co-resident clusters of c pairs (cudaOccupancyMaxActiveClusters; cached per device, kernel and smem size).
-static int max_clusters(int dev, KernFn k, size_t smem, uint32_t c) {
+static int max_clusters(int dev, const void* k, size_t smem, uint32_t threads, uint32_t c) {
     static std::mutex mu;
-    static std::map<std::tuple<int, void*, size_t, uint32_t>, int> cache;
-    const auto key = std::make_tuple(dev, (void*)k, smem, c);
+    static std::map<std::tuple<int, const void*, size_t, uint32_t>, int> cache;
+    const auto key = std::make_tuple(dev, k, smem, c);
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -459,7 +446,7 @@ static int max_clusters(int dev, KernFn k, size_t smem, uint32_t c) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(2 * c * 64, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -475,29 +462,31 @@ static int max_clusters(int dev, KernFn k, size_t smem, uint32_t c) {
 
 // Cluster shape: c pairs per cluster (2c CTAs, c <= 4) and K co-resident clusters, minimising the estimated time
 // ceil(I_c / K_c) / kFeed[c] with I_c = ceil(pgroups / c) word-tile items (a super-group that overhangs the padded
-// W^T computes zero rows); force = 1..4 takes that c (ensi_pcmm_opts.cluster_pairs).
-static int plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, KernFn kmc, KernFn kpl, size_t smem,
-                         uint32_t force, uint32_t* cpairs, uint32_t* nclust) {
-    for (KernFn k : {kmc, kpl}) {
+// W^T computes zero rows); force = 1..4 takes that c (ensi_pcmm_opts.cluster_pairs).  Shared by the compact
+// (k_accum_tcc) and the uint64-word (k_accum_tc2) pair kernels: kmc / kpl are the multicast / plain-pair variants.
+}  // namespace tcc
+
+int tc_plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, const void* kmc, const void* kpl, size_t smem,
+                     uint32_t threads, uint32_t force, uint32_t* cpairs, uint32_t* nclust) {
+    for (const void* k : {kmc, kpl}) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_err(ctx, e, "accum_tcc smem attribute");
+        if (e != cudaSuccess) return cuda_err(ctx, e, "accumulate smem attribute");
     }
     double best = 0;
     for (uint32_t c = force ? force : 1; c <= (force ? force : 4); c++) {
-        const int kc = max_clusters(ctx->device, c == 1 ? kpl : kmc, smem, c);
+        const int kc = tcc::max_clusters(ctx->device, c == 1 ? kpl : kmc, smem, threads, c);
         if (kc < 1) continue;
         const uint64_t items = (uint64_t)((pgroups + c - 1) / c) * ntiles;
-        const double est = (double)((items + kc - 1) / kc) / kFeed[c];
+        const double est = (double)((items + kc - 1) / kc) / tcc::kFeed[c];
         if (best == 0 || est < best * 0.999) {
             best = est;
             *cpairs = c;
             *nclust = (uint32_t)kc;
         }
     }
-    if (best == 0) return set_err(ctx, ENSI_ECUDA, "accum_tcc: no cluster shape fits on this device");
+    if (best == 0) return set_err(ctx, ENSI_ECUDA, "tensor-core accumulate: no cluster shape fits on this device");
     return ENSI_OK;
 }
-}  // namespace tcc
 
 int build_wt8(ensi_ctx* ctx, ensi_weights* w);
 void fill_epi_const(const ensi_ctx* ctx, const ensi_weights* w, tc::EpiConst* ec);
@@ -570,7 +559,8 @@ int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weig
     tcc::KernFn kmc = ares ? tcc::k_accum_tcc<true, true> : tcc::k_accum_tcc<false, true>;
     tcc::KernFn kpl = ares ? tcc::k_accum_tcc<true, false> : tcc::k_accum_tcc<false, false>;
     uint32_t cpairs = 1, nclust = 1;
-    rc = tcc::plan_clusters(ctx, pgroups, ntiles, kmc, kpl, smem, cluster_pairs, &cpairs, &nclust);
+    rc = tc_plan_clusters(ctx, pgroups, ntiles, (const void*)kmc, (const void*)kpl, smem, tcc::kThreads, cluster_pairs,
+                          &cpairs, &nclust);
     if (rc) return rc;
     const bool mc = cpairs >= 2;
     const tcc::KernFn kern = mc ? kmc : kpl;

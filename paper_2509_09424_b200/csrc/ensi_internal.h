@@ -179,6 +179,9 @@ struct PeerFlags {
 };
 __global__ void k_peer_signal(PeerFlags pf, uint32_t slot, uint32_t epoch);
 __global__ void k_peer_wait(const uint32_t* flags, uint32_t n, uint32_t epoch);
+// launch shape of the tensor-core pair kernels (accum_tcc.cu): c pairs per multicast cluster, K clusters
+int tc_plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, const void* kmc, const void* kpl, size_t smem,
+                     uint32_t threads, uint32_t force, uint32_t* cpairs, uint32_t* nclust);
 int accum_ternary_tcc_dst(ensi_ctx* ctx, const uint8_t* x, uint32_t d, ensi_weights* w, uint8_t* const* y_dst,
                           uint32_t n_dst, uint32_t level, cudaStream_t st, int slice_limb = -1,
                           uint32_t cluster_pairs = 0);

@@ -190,5 +190,40 @@ __device__ __forceinline__ uint64_t combine_word5(const uint32_t* r, uint64_t q,
     return rr >= q ? rr - q : rr;
 }
 
+// One cluster's walk over the (super-group sg, word tile t) work items of the pair kernels: items kc, kc + K,
+// kc + 2K, ... of the list ordered tile-major (item = t nsg + sg) or super-group-major (item = sg ntiles + t),
+// stepped without divisions (k_accum_tcc / k_accum_tc2).
+struct WorkIter {
+    uint32_t sg, t, dsg, dt, nsg, ntiles, tmajor;
+    __device__ __forceinline__ WorkIter(uint32_t kc, uint32_t nclust, uint32_t nsg_, uint32_t ntiles_, uint32_t tmajor_)
+        : nsg(nsg_), ntiles(ntiles_), tmajor(tmajor_) {
+        if (tmajor) {
+            t = kc / nsg;
+            sg = kc % nsg;
+            dt = nclust / nsg;
+            dsg = nclust % nsg;
+        } else {
+            sg = kc / ntiles;
+            t = kc % ntiles;
+            dsg = nclust / ntiles;
+            dt = nclust % ntiles;
+        }
+    }
+    __device__ __forceinline__ bool valid() const { return tmajor ? t < ntiles : sg < nsg; }
+    __device__ __forceinline__ void next() {
+        sg += dsg;
+        t += dt;
+        if (tmajor) {
+            if (sg >= nsg) {
+                sg -= nsg;
+                t++;
+            }
+        } else if (t >= ntiles) {
+            t -= ntiles;
+            sg++;
+        }
+    }
+};
+
 }  // namespace tc
 }  // namespace ensi

@@ -612,10 +612,12 @@ def test_rotate_hoisted_n16_reduced_limbs(torch_cuda, L, alpha, dnum, level):
 
 
 @pytest.mark.parametrize("kernel", [2, 4, 1])
-@pytest.mark.parametrize("d,m", [(2048, 1200), (300, 2100), (3072, 96)])
+@pytest.mark.parametrize("d,m", [(2048, 1200), (300, 2100), (3072, 96), (200, 1200), (768, 3100)])
 def test_pcmm_a_block_shapes_streamed_a(torch_cuda, kernel, d, m):
     """C3-C5-like shapes at a small ring: d > 768 streams W^T per stage (no resident A), m > 1024 has more than
-    four pair groups (no cluster multicast); sampled output columns against the oracle."""
+    four pair groups -- the (super-group, word tile) items dealt round-robin to every co-resident cluster, super-groups
+    overhanging the padded W^T, resident W^T (d <= 768) reloaded where a cluster's items cross super-groups;
+    sampled output columns against the oracle."""
     from paper_2509_09424_b200 import Context
     torch = torch_cuda
     o = oracle.Oracle(12, 2, 1, 2)

@@ -427,7 +427,7 @@ typedef void (*KernFn)(CUtensorMap, CUtensorMap, StoreMaps, Tiles, uint32_t, uin
 // Relative per-SM rate of a cluster of c pairs sharing every X sub-box by multicast (c = 1: plain pairs, each
 // X tile read through L2 by every pair) -- measured at 2048x2048 with every c forced (tools/bench_cluster.py,
 // profiles/r02_tcc_ablations.md).
-static constexpr double kFeed[5] = {0, 0.52, 0.85, 0.90, 1.0};
+static constexpr double kFeed[9] = {0, 0.52, 0.85, 0.90, 1.0, 1.0, 1.0, 1.0, 1.0};
 
 // Co-resident clusters of c pairs (cudaOccupancyMaxActiveClusters; cached per device, kernel and smem size).
 static int max_clusters(int dev, const void* k, size_t smem, uint32_t threads, uint32_t c) {
@@ -460,9 +460,9 @@ static int max_clusters(int dev, const void* k, size_t smem, uint32_t threads, u
     return n;
 }
 
-// Cluster shape: c pairs per cluster (2c CTAs, c <= 4) and K co-resident clusters, minimising the estimated time
+// Cluster shape: c pairs per cluster (2c CTAs, c <= 8) and K co-resident clusters, minimising the estimated time
 // ceil(I_c / K_c) / kFeed[c] with I_c = ceil(pgroups / c) word-tile items (a super-group that overhangs the padded
-// W^T computes zero rows); force = 1..4 takes that c (ensi_pcmm_opts.cluster_pairs).  Shared by the compact
+// W^T computes zero rows); force = 1..8 takes that c (ensi_pcmm_opts.cluster_pairs).  Shared by the compact
 // (k_accum_tcc) and the uint64-word (k_accum_tc2) pair kernels: kmc / kpl are the multicast / plain-pair variants.
 }  // namespace tcc
 
@@ -472,8 +472,13 @@ int tc_plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, const voi
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_err(ctx, e, "accumulate smem attribute");
     }
+    // clusters of up to 16 CTAs (8 pairs) are a non-portable size
+    const bool big = cudaFuncSetAttribute(kmc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+    if (!big) cudaGetLastError();
+    const uint32_t cmax = big ? 8 : 4;
+    if (force > cmax) return set_err(ctx, ENSI_EINVAL, "cluster_pairs larger than this device allows");
     double best = 0;
-    for (uint32_t c = force ? force : 1; c <= (force ? force : 4); c++) {
+    for (uint32_t c = force ? force : 1; c <= (force ? force : cmax); c++) {
         const int kc = tcc::max_clusters(ctx->device, c == 1 ? kpl : kmc, smem, threads, c);
         if (kc < 1) continue;
         const uint64_t items = (uint64_t)((pgroups + c - 1) / c) * ntiles;

@@ -830,7 +830,7 @@ int check_compact(ensi_ctx* ctx, const ensi_compact_view* x, const ensi_weights*
     if (o.rescale_out) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: no rescale epilogue");
     if (o.moddown_lazy) return set_err(ctx, ENSI_EINVAL, "moddown_lazy: Layout B only");
     if (o.kernel != 0 && o.kernel != 2) return set_err(ctx, ENSI_EINVAL, "compact ciphertexts: kernel must be 0 or 2");
-    if (o.cluster_pairs > 4) return set_err(ctx, ENSI_EINVAL, "cluster_pairs must be 0..4");
+    if (o.cluster_pairs > 8) return set_err(ctx, ENSI_EINVAL, "cluster_pairs must be 0..8");
     if (x->count != wc->d) return set_err(ctx, ENSI_EDIM, "x.count must equal d");
     if (!tcc_supported(ctx, x->level) || wc->d >= (1u << 22))
         return set_err(ctx, ENSI_EINVAL, "compact tensor-core accumulate unavailable (sm_100a, 5..8-byte words, N' >= 256)");

@@ -83,7 +83,8 @@ def test_compact_ragged(c1, torch_cuda, d, m, level):
 
 @pytest.mark.parametrize("d,m,level", [(200, 1200, 3), (900, 3000, 2), (768, 3100, 1)])
 def test_compact_every_cluster_shape(c1, torch_cuda, d, m, level):
-    """The launch shape (opts.cluster_pairs = 1..4 CTA pairs per multicast cluster, and 0 = the per-layer choice):
+    """The launch shape (opts.cluster_pairs = 1..4 and 8 CTA pairs per multicast cluster -- 16 CTAs is a non-portable
+    cluster size -- and 0 = the per-layer choice):
     every co-resident cluster takes a contiguous run of (super-group, word tile) items, so runs cross super-groups
     (resident W^T reloaded mid-kernel: d <= 768) and super-groups overhang the padded W^T (5 / 12 / 13 pair groups
     in clusters of 2..4 pairs) -- the outputs are the same words as the oracle's Algorithm 1 for every shape.
@@ -98,12 +99,12 @@ def test_compact_every_cluster_shape(c1, torch_cuda, d, m, level):
     xc = _compact_dev(torch, ctx, x, level)
     w = ctx.weights(W)
     shapes = set()
-    for cp in (0, 1, 2, 3, 4):
+    for cp in (0, 1, 2, 3, 4, 8):
         yc = torch.full((m, ctx.wire_bytes(level)), 0xA5, dtype=torch.uint8, device="cuda")
         ctx.pcmm_ternary_compact(xc, w, yc, level=level, cluster_pairs=cp)
         torch.cuda.synchronize()
         c, k = ctx.last_compact_plan()
-        assert 1 <= c <= 4 and k >= 1 and (cp == 0 or c == cp)
+        assert 1 <= c <= 8 and k >= 1 and (cp == 0 or c == cp)
         shapes.add((c, k))
         got = wire_unpack_host(yc[cols].cpu().numpy(), ctx.wire_widths(level), level, ctx.n)
         assert (got == want).all(), (cp, c, k)
@@ -233,7 +234,7 @@ def test_compact_errors(c1, torch_cuda):
         ctx.pcmm_ternary_compact(x[:2], ctx.weights(synth.gen_W(2, 2, 2)), x[1:3], level=3)
     assert e.value.code == ENSI_EINVAL
     with pytest.raises(EnsiError) as e:
-        ctx.pcmm_ternary_compact(x, w, y, level=3, cluster_pairs=5)
+        ctx.pcmm_ternary_compact(x, w, y, level=3, cluster_pairs=9)
     assert e.value.code == ENSI_EINVAL
 
 

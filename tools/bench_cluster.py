@@ -35,7 +35,7 @@ def main():
         xc = torch.randint(0, 256, (d, wb), dtype=torch.uint8, device="cuda")   # timing only: any bytes
         yc = torch.empty((m, wb), dtype=torch.uint8, device="cuda")
         row = {}
-        for cp in (0, 1, 2, 3, 4):
+        for cp in (0, 1, 2, 3, 4, 5, 6, 8):
             try:
                 ms = t(lambda: ctx.pcmm_ternary_compact(xc, w, yc, level=L, cluster_pairs=cp))
             except Exception as ex:  # a cluster size that cannot be resident

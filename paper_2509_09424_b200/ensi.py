@@ -239,6 +239,9 @@ class Context:
         ga = np.ascontiguousarray(galois if galois is not None else [], np.uint64)
         mem, kp = MEM_HOST, None
         if rot_keys is not None:
+            words = ga.shape[0] * self.dnum * 2 * (self.L + self.A) * self.n
+            if (rot_keys.size if isinstance(rot_keys, np.ndarray) else rot_keys.numel()) != words:
+                raise ValueError(f"rotation keys must hold n_rot x dnum x 2 x (num_q + num_p) x N' = {words} words")
             if isinstance(rot_keys, np.ndarray):
                 rk = np.ascontiguousarray(rot_keys, np.uint64)
                 kp = rk.ctypes.data
@@ -421,6 +424,9 @@ class Context:
     # ---- CCMM (R18)
     def load_relin_key(self, key):
         """key [dnum][2][num_q+num_p][N']: numpy (host, copied) or torch CUDA tensor (device, referenced)."""
+        words = self.dnum * 2 * (self.L + self.A) * self.n
+        if (key.size if isinstance(key, np.ndarray) else key.numel()) != words:
+            raise ValueError(f"relinearisation key must hold dnum x 2 x (num_q + num_p) x N' = {words} words")
         if isinstance(key, np.ndarray):
             k = np.ascontiguousarray(key, np.uint64)
             self._check(lib().ensi_load_relin_key(self.h, k.ctypes.data, MEM_HOST))

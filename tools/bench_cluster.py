@@ -30,7 +30,10 @@ def main():
     L = 12
     wb = ctx.wire_bytes(L)
     out = {}
-    for d, m in [(768, 768), (768, 3072), (3072, 768), (2048, 2048), (2048, 5504), (5504, 2048), (2048, 6144)]:
+    shapes = [(768, 768), (768, 3072), (3072, 768), (2048, 2048), (2048, 5504), (5504, 2048), (2048, 6144), (2048, 11008)]
+    if len(sys.argv) > 1:
+        shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]]
+    for d, m in shapes:
         w = ctx.weights(synth.gen_W(synth.SEED_BASE + d + m, d, m))
         xc = torch.randint(0, 256, (d, wb), dtype=torch.uint8, device="cuda")   # timing only: any bytes
         yc = torch.empty((m, wb), dtype=torch.uint8, device="cuda")

@@ -460,11 +460,12 @@ static int max_clusters(int dev, const void* k, size_t smem, uint32_t threads, u
     return n;
 }
 
+}  // namespace tcc
+
 // Cluster shape: c pairs per cluster (2c CTAs, c <= 8) and K co-resident clusters, minimising the estimated time
 // ceil(I_c / K_c) / kFeed[c] with I_c = ceil(pgroups / c) word-tile items (a super-group that overhangs the padded
 // W^T computes zero rows); force = 1..8 takes that c (ensi_pcmm_opts.cluster_pairs).  Shared by the compact
 // (k_accum_tcc) and the uint64-word (k_accum_tc2) pair kernels: kmc / kpl are the multicast / plain-pair variants.
-}  // namespace tcc
 
 int tc_plan_clusters(ensi_ctx* ctx, uint32_t pgroups, uint32_t ntiles, const void* kmc, const void* kpl, size_t smem,
                      uint32_t threads, uint32_t force, uint32_t* cpairs, uint32_t* nclust) {

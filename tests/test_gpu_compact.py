@@ -99,9 +99,14 @@ def test_compact_every_cluster_shape(c1, torch_cuda, d, m, level):
     xc = _compact_dev(torch, ctx, x, level)
     w = ctx.weights(W)
     shapes = set()
+    from paper_2509_09424_b200.ensi import EnsiError, ENSI_ECUDA
     for cp in (0, 1, 2, 3, 4, 8):
         yc = torch.full((m, ctx.wire_bytes(level)), 0xA5, dtype=torch.uint8, device="cuda")
-        ctx.pcmm_ternary_compact(xc, w, yc, level=level, cluster_pairs=cp)
+        try:
+            ctx.pcmm_ternary_compact(xc, w, yc, level=level, cluster_pairs=cp)
+        except EnsiError as ex:     # a non-portable 16-CTA cluster that this device cannot make resident
+            assert cp == 8 and ex.code == ENSI_ECUDA
+            continue
         torch.cuda.synchronize()
         c, k = ctx.last_compact_plan()
         assert 1 <= c <= 8 and k >= 1 and (cp == 0 or c == cp)

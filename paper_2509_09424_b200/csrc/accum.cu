@@ -24,18 +24,29 @@
 
 namespace ensi {
 
-static constexpr int AO = 8;          // outputs per warp
+#ifndef ENSI_ACC_AO
+#define ENSI_ACC_AO 8
+#endif
+#ifndef ENSI_ACC_RUNROLL
+#define ENSI_ACC_RUNROLL 4
+#endif
+static constexpr int AO = ENSI_ACC_AO;  // outputs per warp
+// FP64 path: rows of a stage unrolled (the next row's shared loads issue under this row's DFMAs; measured
+// C2 88.0 / 86.6 / 85.5 ms at 1 / 2 / 4; 16 outputs per warp: 86.0-86.5 / 85.5 ms at 1 / 2 (224 registers))
+static constexpr int kRunroll = ENSI_ACC_RUNROLL;
 static constexpr int AP = ENSI_ACC_AP;  // positions per lane
 static constexpr int AW = 8;          // warps per CTA
 static constexpr int ATI = AO * AW;   // 64 outputs per CTA
 static constexpr int ATW = 32 * AP;   // 256 positions per CTA
+static constexpr int NPW = ATI / 32;  // sign-plane words per sign and row of the CTA's output tile
 #ifndef ENSI_ACC_AKC
 #define ENSI_ACC_AKC 32
 #endif
 static constexpr int AKC = ENSI_ACC_AKC;   // x rows per pipeline stage (32: 160 KB of dynamic shared memory, 1 CTA/SM; measured 86 ms vs 89 at 16 and 94 at 8 rows)
 
-// dynamic shared memory layout: sx [2][AKC][ATW] uint64 | swd [2][AKC][ATI] double | ssg [2][AKC][4] uint32
-static constexpr size_t kAccSmem = (size_t)2 * AKC * ATW * 8 + (size_t)2 * AKC * ATI * 8 + (size_t)2 * AKC * 4 * 4;
+// dynamic shared memory layout: sx [2][AKC][ATW] uint64 | swd [2][AKC][ATI] double | ssg [2][AKC][2 NPW] uint32
+static constexpr size_t kAccSmem =
+    (size_t)2 * AKC * ATW * 8 + (size_t)2 * AKC * ATI * 8 + (size_t)2 * AKC * 2 * NPW * 4;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -69,22 +80,23 @@ __device__ __forceinline__ uint64_t acc_canon(double v, uint64_t q, double qd, d
 }
 
 // planes: [d][2][mw] uint32 (pos bits, neg bits); bit (i % 32) of word i / 32; mw even, zero padded.
-__global__ void __launch_bounds__(256, 8 / AP)
+__global__ void __launch_bounds__(256, AO * AP > 32 ? 1 : 8 / AP)
     k_accum_ternary(const uint64_t* __restrict__ x, uint32_t d, uint64_t ctw, const uint32_t* __restrict__ planes,
                     uint32_t mw, uint32_t m, uint64_t* __restrict__ y, uint32_t log_n, uint32_t level, uint32_t limb0,
                     ModTab tab, uint32_t ared) {
     extern __shared__ __align__(16) uint8_t acc_smem[];
     uint64_t (*sx)[AKC][ATW] = reinterpret_cast<uint64_t (*)[AKC][ATW]>(acc_smem);
     double (*swd)[AKC][ATI] = reinterpret_cast<double (*)[AKC][ATI]>(acc_smem + (size_t)2 * AKC * ATW * 8);
-    uint32_t (*ssg)[AKC][4] = reinterpret_cast<uint32_t (*)[AKC][4]>(acc_smem + (size_t)2 * AKC * ATW * 8 +
-                                                                     (size_t)2 * AKC * ATI * 8);   // pos lo/hi, neg lo/hi
+    // sign words of the tile: pos [0, NPW), neg [NPW, 2 NPW)
+    uint32_t (*ssg)[AKC][2 * NPW] = reinterpret_cast<uint32_t (*)[AKC][2 * NPW]>(
+        acc_smem + (size_t)2 * AKC * ATW * 8 + (size_t)2 * AKC * ATI * 8);
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t i0 = blockIdx.x * ATI;
     const uint64_t pos0 = (uint64_t)blockIdx.y * ATW;
     const uint32_t limb = (uint32_t)((limb0 + (pos0 >> log_n)) % level);
     const Barrett br = tab.br(limb);
-    const uint32_t wsel = warp >> 2, wsh = (warp & 3) * 8;
-    const uint32_t pw0 = i0 >> 5;   // first plane word of this output tile (even)
+    const uint32_t wsel = (warp * AO) >> 5, wsh = (warp * AO) & 31;   // this warp's AO sign bits
+    const uint32_t pw0 = i0 >> 5;   // first plane word of this output tile
 
     int64_t acc[AO][AP];
 #pragma unroll
@@ -104,10 +116,11 @@ __global__ void __launch_bounds__(256, 8 / AP)
             uint32_t j = j0 + r;
             if (j < d) cp_async16(&sx[buf][r][col], x + (uint64_t)j * ctw + pos0 + col);
         }
-        if (tid < AKC * 4) {
-            uint32_t r = tid >> 2, which = tid & 3, j = j0 + r;
-            if (j < d) {
-                const uint32_t* src = planes + ((uint64_t)j * 2 + (which >> 1)) * mw + pw0 + (which & 1);
+        if (tid < AKC * 2 * NPW) {
+            const uint32_t r = tid / (2 * NPW), which = tid % (2 * NPW), j = j0 + r;
+            const uint32_t sign = which / NPW, word = pw0 + which % NPW;
+            if (j < d && word < mw) {
+                const uint32_t* src = planes + ((uint64_t)j * 2 + sign) * mw + word;
                 cp_async4(&ssg[buf][r][which], src);
             } else {
                 ssg[buf][r][which] = 0;
@@ -150,12 +163,12 @@ __global__ void __launch_bounds__(256, 8 / AP)
 #pragma unroll
                 for (int c = 0; c < AKC * ATI / 256; c++) {
                     const uint32_t e = tid + 256 * c, r = e / ATI, o = e % ATI;
-                    const uint32_t pw = ssg[buf][r][o >> 5], nw = ssg[buf][r][2 + (o >> 5)];
+                    const uint32_t pw = ssg[buf][r][o >> 5], nw = ssg[buf][r][NPW + (o >> 5)];
                     swd[buf][r][o] = (double)(int)((pw >> (o & 31)) & 1u) - (double)(int)((nw >> (o & 31)) & 1u);
                 }
             }
             __syncthreads();
-#pragma unroll 1
+#pragma unroll kRunroll
             for (int r = 0; r < AKC; r++) {
                 if (sincef == ared_fp) {   // |acd| <= (ared_fp + 1/2) q < 2^53 between reductions
 #pragma unroll
@@ -217,8 +230,9 @@ __global__ void __launch_bounds__(256, 8 / AP)
                 since = 0;
             }
             since++;
-            const uint32_t pb = (ssg[buf][r][wsel] >> wsh) & 0xFFu;
-            const uint32_t nb = (ssg[buf][r][2 + wsel] >> wsh) & 0xFFu;
+            constexpr uint32_t omask = AO >= 32 ? 0xFFFFFFFFu : (1u << AO) - 1;
+            const uint32_t pb = (ssg[buf][r][wsel] >> wsh) & omask;
+            const uint32_t nb = (ssg[buf][r][NPW + wsel] >> wsh) & omask;
             if ((pb | nb) == 0) continue;
             int64_t xv[AP];
 #pragma unroll

@@ -189,6 +189,20 @@ def test_compact_paper_ring_n14(torch_cuda, L, alpha):
     assert (_run(torch, ctx, x, W, L) == o.pcmm_a(x, W, nthreads=4)).all()
 
 
+@pytest.mark.parametrize("log_n", [8, 13, 15])
+def test_compact_other_rings(torch_cuda, log_n):
+    """N' = 2^8 (the smallest compact ring: 5 full 48-word tiles and a 16-word tail per 40-bit slice), 2^13 and 2^15
+    (32-word tails after 170 / 682 full tiles) at the C1 prime rule -- every word == the oracle."""
+    from paper_2509_09424_b200 import Context
+    torch = torch_cuda
+    o = oracle.Oracle(log_n, 3, 1, 3)
+    ctx = Context(log_n, 3, 1, 3)
+    x = synth.gen_words(14900 + log_n, o.q, 140, 3, o.n)
+    x[3, :, :, :9] = np.uint64(0)
+    W = synth.gen_W(14901 + log_n, 140, 300)
+    assert (_run(torch, ctx, x, W, 3) == o.pcmm_a(x, W, nthreads=4)).all()
+
+
 def test_compact_c2_full_size_bench_launch(torch_cuda):
     """C2 (BASELINE configs[1]) exactly as bench.py times it: 768 compact input ciphertexts (8.1 MB each) -> 768
     outputs in one launch; three whole output columns == the oracle, and the uint64 tensor-core path agrees on

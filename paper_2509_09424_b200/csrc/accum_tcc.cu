@@ -109,68 +109,70 @@ struct EpiArgs {
     uint32_t mu32;
 };
 
-// One warp: HW consecutive words (W bytes each) of the tile for its 32 outputs.  Drains the TMEM columns, releases
-// the accumulator, recombines and packs into u[] (HW*W/8 little-endian u64 of the compact row segment).
-template <uint32_t W, uint32_t HW>
-__device__ __forceinline__ void epi_words(uint32_t tcol, uint32_t release_addr, uint32_t lane, const EpiArgs& ea,
-                                          uint64_t* u) {
-    constexpr uint32_t NC = W * HW;
-    static_assert(NC % 8 == 0, "TMEM pieces are 8 columns");
-    uint32_t r[NC];
+// CW words (W bytes each) of one output row from their TMEM planes r[0, CW W) -> canonical words, packed into
+// CW W / 8 little-endian u64 and written to the staging row at dst.
+template <uint32_t W, uint32_t CW>
+__device__ __forceinline__ void epi_chunk(const uint32_t* r, const EpiArgs& ea, uint8_t* dst) {
+    static_assert((CW * W) % 8 == 0, "a chunk ends on a u64");
+    uint64_t u[CW * W / 8];
 #pragma unroll
-    for (uint32_t c = 0; c < NC; c += 8) TMEM_LD_X8(tcol + c, r + c);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_remote(release_addr);
-    uint64_t v[HW];
+    for (uint32_t j = 0; j < CW * W / 8; j++) u[j] = 0;
 #pragma unroll
-    for (uint32_t i = 0; i < HW; i++) {
+    for (uint32_t i = 0; i < CW; i++) {
+        uint64_t v;
 #ifdef ENSI_ABL_NOCOMBINE   // timing-only ablation build (wrong words; profiles/r02_tcc_ablations.md)
-        v[i] = r[W * i];
+        v = r[W * i];
 #else
-        if constexpr (W == 5) v[i] = combine_word5(r + 5 * i, ea.br.q, ea.mu32, ea.off64);
-        else v[i] = combine_w<W>(r + W * i, ea.br, ea.off_lo, ea.off_hi);
+        if constexpr (W == 5) v = combine_word5(r + 5 * i, ea.br.q, ea.mu32, ea.off64);
+        else v = combine_w<W>(r + W * i, ea.br, ea.off_lo, ea.off_hi);
 #endif
-    }
-#pragma unroll
-    for (uint32_t j = 0; j < NC / 8; j++) u[j] = 0;
-#pragma unroll
-    for (uint32_t i = 0; i < HW; i++) {
         constexpr uint32_t bits = 8 * W;
         const uint32_t bit = i * bits, j = bit / 64, sh = bit % 64;
-        u[j] |= v[i] << sh;
-        if (sh + bits > 64) u[j + 1] |= v[i] >> (64 - sh);
+        u[j] |= v << sh;
+        if (sh + bits > 64) u[j + 1] |= v >> (64 - sh);
     }
+#pragma unroll
+    for (uint32_t j = 0; j < CW * W / 8; j++)
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(smem_u32(dst + 8 * j)), "l"(u[j]) : "memory");
 }
 
-// The whole epilogue of one tile for a warp (quarter q, half h): both warps of the quarter stage their halves into
-// one [32][N] block, the half-0 warp issues the TMA store.
+// The whole epilogue of one tile for a warp (quarter q, half h): drain this warp's HW words (W TMEM columns each) and
+// hand the accumulator back, then both warps of the quarter stage their halves of one [32][N] row block -- in chunks
+// of 8 words, each written as soon as it is combined (staging everything after the last combine measured 2-7 %
+// slower: the burst of shared-memory writes stalls the MMA operand reads) -- and the half-0 warp issues the TMA store.
 template <uint32_t W, uint32_t HW>
 __device__ __forceinline__ void epi_tile(uint32_t tbase_q, uint32_t release_addr, uint32_t lane, uint32_t half,
                                          uint32_t quarter, uint8_t* ys, const EpiArgs& ea, const CUtensorMap* map,
                                          uint32_t byte, uint32_t row0, uint32_t n_dst) {
-    constexpr uint32_t NB = W * HW;             // bytes of this warp's half row segment
+    constexpr uint32_t NB = W * HW;             // bytes (and TMEM columns) of this warp's half row segment
+    constexpr uint32_t CH = 8;                  // words per staged chunk
+    static_assert(NB % 8 == 0, "TMEM pieces are 8 columns");
 #ifdef ENSI_ABL_NOEPI       // timing-only ablation build (no outputs): release the accumulator at once
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_remote(release_addr);
     return;
 #endif
-    uint64_t u[NB / 8];
-    epi_words<W, HW>(tbase_q + half * half1_col(NB), release_addr, lane, ea, u);
-#ifdef ENSI_ABL_NOSTS       // timing-only ablation build (no outputs): words computed and kept alive, not staged
+    uint32_t r[NB];
 #pragma unroll
-    for (uint32_t j = 0; j < NB / 8; j++) asm volatile("" ::"l"(u[j]));
-    return;
-#endif
+    for (uint32_t c = 0; c < NB; c += 8) TMEM_LD_X8(tbase_q + half * half1_col(NB) + c, r + c);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_remote(release_addr);
     // staging free: the previous TMA store of this quarter has read it
     if (half == 0 && lane == 0) tma_store_wait_read0();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     uint8_t* dst = ys + lane * (2 * NB) + half * NB;
 #pragma unroll
-    for (uint32_t j = 0; j < NB / 8; j++)
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(smem_u32(dst + 8 * j)), "l"(u[j]) : "memory");
+    for (uint32_t c0 = 0; c0 < HW; c0 += CH) {
+        if constexpr (HW % CH == 0) {
+            epi_chunk<W, CH>(r + W * c0, ea, dst + W * c0);
+        } else {
+            if (c0 + CH <= HW) epi_chunk<W, CH>(r + W * c0, ea, dst + W * c0);
+            else epi_chunk<W, (HW % CH)>(r + W * c0, ea, dst + W * c0);
+        }
+    }
     fence_proxy_async();
     asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     if (half == 0 && lane == 0) {

@@ -128,27 +128,49 @@ class FusedGatherPCMM:
 
             def alloc(shape, dt):
                 return torch.zeros(shape, dtype=getattr(torch, dt), device="cuda")
-        self.y_all = alloc((self.S * world, self.wb), "uint8")
-        self.flags = alloc((world,), "int32")
-        mine = (ctx.ipc_handle(self.y_all), ctx.ipc_handle(self.flags))
-        if world > 1:
-            import torch.distributed as dist
-            handles = [None] * world
-            dist.all_gather_object(handles, mine, group=group)
-        else:
-            handles = [mine]
+        # Collectively consistent setup: every rank reaches both exchanges even when a local step fails, and all ranks
+        # raise together (a rank left behind would otherwise hang its peers in the exchange or in peer_wait).
+        err = None
+        try:
+            self.y_all = alloc((self.S * world, self.wb), "uint8")
+            self.flags = alloc((world,), "int32")
+            mine = (ctx.ipc_handle(self.y_all), ctx.ipc_handle(self.flags))
+        except Exception as e:  # noqa: BLE001 -- reported to every rank below
+            mine, err = None, f"rank {rank}: {e!r}"
+        handles = self._exchange((err, mine), group)
+        errs = [h[0] for h in handles if h[0]]
+        if errs:
+            raise RuntimeError("fused gather setup failed: " + "; ".join(errs))
         self._opened = []
         self.dst, self.flag_dst = [], []
-        for r in range(world):
-            if r == rank:
-                self.dst.append(self.y_all)
-                self.flag_dst.append(self.flags)
-            else:
-                py, pf = ctx.ipc_open(handles[r][0]), ctx.ipc_open(handles[r][1])
-                self._opened += [py, pf]
-                self.dst.append(py)
-                self.flag_dst.append(pf)
+        try:
+            for r in range(world):
+                if r == rank:
+                    self.dst.append(self.y_all)
+                    self.flag_dst.append(self.flags)
+                else:
+                    py = ctx.ipc_open(handles[r][1][0])
+                    self._opened.append(py)
+                    pf = ctx.ipc_open(handles[r][1][1])
+                    self._opened.append(pf)
+                    self.dst.append(py)
+                    self.flag_dst.append(pf)
+            err = None
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank}: {e!r}"
+        errs = [e for e in self._exchange(err, group) if e]
+        if errs:
+            self.close()
+            raise RuntimeError("fused gather peer mapping failed: " + "; ".join(errs))
         self.epoch = 0
+
+    def _exchange(self, obj, group):
+        if self.world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=group)
+        return out
 
     def __call__(self, x, stream=None):
         self.ctx.pcmm_ternary_compact_gather(x, self.w_local, self.dst, self.S * self.world, self.rank * self.S,

@@ -251,3 +251,52 @@ def test_fused_gather_protocol_world2_ragged():
     o = oracle.Oracle(12, 2, 1, 2)
     want = o.pcmm_a(synth.gen_words(57, o.q, d, 1, o.n), synth.gen_W(58, d, m))
     assert (got == want).all()
+
+
+class _FailOpenCtx(_ShmCtx):
+    """The stand-in with a peer mapping that fails on one rank (e.g. a GPU pair without peer access)."""
+
+    def __init__(self, o, level, fail):
+        super().__init__(o, level)
+        self.fail = fail
+
+    def ipc_open(self, h):
+        if self.fail:
+            raise OSError("peer mapping refused")
+        return super().ipc_open(h)
+
+
+def _fused_fail_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    import oracle
+    import synth
+    from paper_2509_09424_b200.dist import FusedGatherPCMM
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    o = oracle.Oracle(12, 2, 1, 2)
+    ctx = _FailOpenCtx(o, 1, fail=(rank == 1))
+    try:
+        FusedGatherPCMM(ctx, synth.gen_W(58, 5, 7), world, rank, 1, alloc=ctx.alloc)
+        out_q.put((rank, "no error"))
+    except RuntimeError as e:
+        out_q.put((rank, str(e)))
+    dist.barrier()                                              # both ranks still in step after the failure
+    dist.destroy_process_group()
+
+
+def test_fused_gather_setup_fails_on_every_rank_together():
+    """A peer mapping that fails on rank 1 makes FusedGatherPCMM raise on BOTH ranks (no rank is left waiting in the
+    handle exchange or in peer_wait) -- the bench's N > 1 fused-gather leg relies on it to skip cleanly."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_fail_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert "peer mapping failed" in got[r] and "rank 1" in got[r], got
